@@ -1,0 +1,203 @@
+/*
+ * bmg_cuda.h -- C ABI of libbmgcuda.so, the B200 (sm_100a) implementation of
+ * the multilevel V-cycle application path of arXiv 2509.06744 (`blockmg`).
+ *
+ * Each entry point replaces one piece of the reference's C++ hot-path API
+ * (paths relative to /root/reference/proj); INTEGRATION.md shows the C++
+ * facade (include/bmg/blockmg.hpp) and the ctypes binding that sit on top.
+ *
+ *   reference                                         C ABI here
+ *   ------------------------------------------------  ---------------------------------
+ *   BlockSparseMatrix (block_matrix.hpp:26-70)        bmg_bsr_create / _download
+ *   spmv (kernels.hpp:15, kernels.cpp:39-47)          bmg_spmv
+ *   spmv_transpose (kernels.hpp:19, kernels.cpp:56-64) bmg_spmv_t
+ *   r = b - A x (chebyshev.hpp:55-56,61-62;
+ *                multilevel.cpp:91-93)                bmg_residual
+ *   galerkin_coarsen (multilevel.hpp:50,
+ *                     multilevel.cpp:11-28)           bmg_galerkin
+ *   build_fsai / adaptive_build / nested_build
+ *     (fsai.hpp:25,50,68; fsai.cpp:72-253)            bmg_fsai_build
+ *   NestedFsai::apply (fsai.hpp:62, fsai.cpp:200-217) bmg_fsai_apply   (M = G^T G)
+ *   NestedFsai::apply_transformed (fsai.cpp:219-241)  bmg_fsai_apply_transformed
+ *   cheb_fourth_apply (chebyshev.hpp:48-69)           bmg_cheb4_apply
+ *   lanczos_lambda_max (multilevel.hpp:53-54,
+ *                       multilevel.cpp:30-34,
+ *                       lanczos.hpp:16-58)            bmg_lanczos_lambda_max
+ *   setup (multilevel.hpp:59-60, multilevel.cpp:36-75) bmg_hier_setup
+ *   v_cycle (multilevel.hpp:65, multilevel.cpp:77-103) bmg_vcycle / bmg_vcycle_host
+ *   measure_rates loop (experiments.cpp:15-67)        bmg_solve (residual history)
+ *
+ * Conventions
+ *   - Every entry returns BMG_OK (0) or a negative status; the message of the
+ *     last failure on the calling thread is bmg_last_error(), and for
+ *     BMG_ENOTSPD the failing 0-based pivot is bmg_last_pivot().  Status codes
+ *     map 1:1 onto the reference's exception types (see below).
+ *   - Host buffers are caller-owned, read or written synchronously before the
+ *     call returns.  Device objects are owned by their handle.  A context and
+ *     its objects are single-threaded unless externally synchronised (the
+ *     reference's objects are immutable after setup).
+ *   - Block values cross the ABI row-major, unpadded, in row_ptr/col_idx order
+ *     (the reference's DenseBlock is row-major, types.hpp:9).  Column indices
+ *     within a row must be strictly ascending (the reference's std::map order).
+ *   - FP64 everywhere.  There is no CPU fallback: without a CUDA device every
+ *     compute entry returns BMG_ECUDA.
+ */
+#pragma once
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  BMG_OK = 0,
+  BMG_EINVAL = -1,   /* std::invalid_argument */
+  BMG_ERANGE = -2,   /* std::out_of_range */
+  BMG_ENOTSPD = -3,  /* bmg::NotPositiveDefinite{pivot} (small_cholesky.hpp:10-13) */
+  BMG_ERUNTIME = -4, /* std::runtime_error (e.g. multilevel.cpp:72-73) */
+  BMG_ECUDA = -5,    /* CUDA runtime / cuSOLVER failure or no device */
+  BMG_ENCCL = -6,    /* NCCL failure (multi-GPU contexts) */
+};
+
+/* bmg_bsr_create flags */
+enum {
+  BMG_SYMMETRIC = 1, /* validation contract, as BlockSparseMatrix::symmetric() */
+};
+
+/* bmg_fsai_build kinds */
+enum {
+  BMG_FSAI_STATIC_LOWER = 0, /* build_fsai(A, LowerPattern::from_matrix(A)) */
+  BMG_FSAI_DIAGONAL = 1,     /* build_fsai(A, LowerPattern::diagonal(n))   */
+  BMG_FSAI_ADAPTIVE = 3,     /* nested_build(A, t_max, tau, nest)          */
+};
+
+typedef struct bmg_ctx bmg_ctx;
+typedef struct bmg_bsr bmg_bsr;
+typedef struct bmg_vec bmg_vec;
+typedef struct bmg_fsai bmg_fsai;
+typedef struct bmg_hier bmg_hier;
+
+/* SetupParams (multilevel.hpp:35-47); only the fourth-kind smoother is on the
+ * device path (SmootherKind::ChebFourth, the reference default). */
+typedef struct bmg_setup_params {
+  int t_max;          /* 4 in the reference; 1 for the BASELINE configs */
+  double tau;         /* 1.0 */
+  int nest;           /* 0 */
+  int fsai_kind;      /* BMG_FSAI_ADAPTIVE (reference setup) or BMG_FSAI_STATIC_LOWER */
+  int lanczos_iters;  /* 100 */
+  double lanczos_safety; /* 1.01 */
+  uint64_t seed;      /* 42 */
+  int coarse_dim_cap; /* 5000 */
+} bmg_setup_params;
+
+const char* bmg_last_error(void);
+int bmg_last_pivot(void);
+const char* bmg_version(void);
+void bmg_setup_params_default(bmg_setup_params* p);
+
+/* ---- context ---------------------------------------------------------- */
+int bmg_ctx_create(int device, bmg_ctx** out);
+int bmg_ctx_destroy(bmg_ctx* ctx);
+/* launch on an external stream (e.g. torch's current stream); NULL = own */
+int bmg_ctx_set_stream(bmg_ctx* ctx, void* cuda_stream);
+int bmg_ctx_sync(bmg_ctx* ctx);
+/* kernels launched by this context since creation (all are libbmgcuda's own) */
+int64_t bmg_ctx_launch_count(const bmg_ctx* ctx);
+
+/* ---- block-sparse matrices --------------------------------------------- */
+int bmg_bsr_create(bmg_ctx* ctx, int nbr, const int32_t* row_sizes, int nbc,
+                   const int32_t* col_sizes, const int64_t* row_ptr, const int32_t* col_idx,
+                   const double* vals, int flags, bmg_bsr** out);
+int bmg_bsr_destroy(bmg_bsr* a);
+/* device bytes held (values + indices + plan) and algorithmic bytes of one
+ * streaming pass (nnzb * (8 m_r m_c + 4)) */
+int bmg_bsr_info(const bmg_bsr* a, int* nbr, int* nbc, int64_t* nnzb, int* dim_r, int* dim_c,
+                 int64_t* device_bytes, int64_t* pass_bytes);
+int bmg_bsr_download(const bmg_bsr* a, int64_t* row_ptr, int32_t* col_idx, double* vals);
+/* device-built transpose (values transposed per block) */
+int bmg_bsr_transpose(const bmg_bsr* a, bmg_bsr** out);
+
+/* ---- vectors ------------------------------------------------------------ */
+int bmg_vec_create(bmg_ctx* ctx, int64_t n, bmg_vec** out);
+int bmg_vec_destroy(bmg_vec* v);
+int bmg_vec_upload(bmg_vec* v, const double* host);
+int bmg_vec_download(const bmg_vec* v, double* host);
+int bmg_vec_fill(bmg_vec* v, double value);
+void* bmg_vec_device_ptr(bmg_vec* v);
+int64_t bmg_vec_size(const bmg_vec* v);
+
+/* ---- kernels (kernels.cpp) --------------------------------------------- */
+int bmg_spmv(const bmg_bsr* a, const bmg_vec* x, bmg_vec* y);
+int bmg_spmv_t(const bmg_bsr* a, const bmg_vec* x, bmg_vec* y);
+int bmg_residual(const bmg_bsr* a, const bmg_vec* b, const bmg_vec* x, bmg_vec* r);
+int bmg_dot(const bmg_vec* a, const bmg_vec* b, double* out);
+int bmg_galerkin(const bmg_bsr* a, const bmg_bsr* p, bmg_bsr** out);
+
+/* ---- block-FSAI (fsai.cpp) ---------------------------------------------- */
+int bmg_fsai_build(const bmg_bsr* a, int kind, int t_max, double tau, int nest, bmg_fsai** out);
+/* inject reference-built factors of a one-factor chain: F (unit-diagonal
+ * lower BSR) and the row-major Cholesky factors of S-hat packed per block row */
+int bmg_fsai_from_factors(bmg_ctx* ctx, const bmg_bsr* F, const double* shat_l_packed,
+                          bmg_fsai** out);
+int bmg_fsai_destroy(bmg_fsai* m);
+int bmg_fsai_apply(const bmg_fsai* m, const bmg_vec* r, bmg_vec* z);
+int bmg_fsai_apply_transformed(const bmg_fsai* m, const bmg_bsr* a, const bmg_vec* x,
+                               bmg_vec* y);
+/* borrowed handle of the device factor G (M = G^T G) */
+int bmg_fsai_G(const bmg_fsai* m, const bmg_bsr** g);
+
+/* ---- smoother / spectral bound ------------------------------------------ */
+int bmg_cheb4_apply(const bmg_bsr* a, const bmg_fsai* m, const bmg_vec* b, bmg_vec* x,
+                    double beta, int k);
+int bmg_lanczos_lambda_max(const bmg_bsr* a, const bmg_fsai* m, int iters, double safety,
+                           uint64_t seed, double* beta);
+
+/* ---- multilevel --------------------------------------------------------- */
+/* transfers[l-1] prolongates level l-1 to level l (multilevel.hpp:56-60) */
+int bmg_hier_setup(const bmg_bsr* a_finest, int ntransfers, const bmg_bsr* const* transfers,
+                   const bmg_setup_params* params, bmg_hier** out);
+/* inject a hierarchy built elsewhere (apply-phase parity):
+ * A[0..L-1] (level 0 coarsest), P[1..L-1] (P[0] ignored), M[1..L-1], beta[1..L-1] */
+int bmg_hier_create(bmg_ctx* ctx, int nlevels, const bmg_bsr* const* A, const bmg_bsr* const* P,
+                    const bmg_fsai* const* M, const double* beta, int coarse_dim_cap,
+                    bmg_hier** out);
+int bmg_hier_destroy(bmg_hier* h);
+int bmg_hier_info(const bmg_hier* h, int* nlevels, int64_t* device_bytes);
+int bmg_hier_beta(const bmg_hier* h, int level, double* beta);
+int bmg_hier_level(const bmg_hier* h, int level, const bmg_bsr** a, const bmg_bsr** p,
+                   const bmg_fsai** m);
+/* algorithmic HBM bytes of one V(k_pre,k_post) cycle on the finest level */
+int bmg_hier_cycle_bytes(const bmg_hier* h, int k_pre, int k_post, int64_t* bytes);
+/* 1 (default) = replay each cycle from a captured CUDA graph */
+int bmg_hier_use_graph(bmg_hier* h, int on);
+int bmg_vcycle(bmg_hier* h, int k_pre, int k_post, const bmg_vec* b, bmg_vec* x);
+/* end-to-end: host b, host x (in/out); H2D + cycle + D2H inside the call */
+int bmg_vcycle_host(bmg_hier* h, int k_pre, int k_post, const double* b, double* x);
+int bmg_solve(bmg_hier* h, int k_pre, int k_post, const bmg_vec* b, bmg_vec* x, double tol,
+              int max_iter, double* hist, int* iters, int* status);
+
+/* ---- profiling helpers (bench.py) --------------------------------------- */
+/* time `reps` back-to-back launches of the residual pass r = b - A x on the
+ * context stream with CUDA events; returns the average ms per launch */
+int bmg_time_residual(const bmg_bsr* a, const bmg_vec* b, const bmg_vec* x, bmg_vec* r, int reps,
+                      double* ms);
+
+/* symmetric tridiagonal eigenvalues (ascending), the host step of Lanczos */
+int bmg_tridiag_eigs(int n, const double* d, const double* e, double* out);
+
+/* ---- synthetic BASELINE problems (host generator) -------- */
+/* S_p = L_D^p block stencil on an n^dim patch grid (dim 2 or 3), blocks
+ * A_ij = S_ij C (+ reg D_i on the diagonal).  Two calls: arrays NULL to query
+ * nnzb, then filled. */
+int bmg_gen_stencil(int dim, int n, int power, int m, uint64_t seed, double reg, int64_t* nnzb,
+                    int64_t* row_ptr, int32_t* col_idx, double* vals);
+/* prolongation from an (n/2)^dim coarse grid to the n^dim fine grid */
+int bmg_gen_prolongation(int dim, int n_fine, int m, uint64_t seed, int level, int64_t* nnzb,
+                         int64_t* row_ptr, int32_t* col_idx, double* vals);
+/* N(0,1) vector (Box-Muller on the counter RNG), stream `tag` */
+int bmg_gen_normal(uint64_t seed, uint64_t tag, int64_t n, double* out);
+
+#ifdef __cplusplus
+}
+#endif

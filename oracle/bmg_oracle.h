@@ -1,0 +1,129 @@
+/*
+ * bmg_oracle.h -- C API of the CPU ORACLE (test infrastructure only).
+ *
+ * THIS IS NOT THE PRODUCT.  The oracle is a plain-C++ CPU restatement of the
+ * reference's hot-path algorithms (arXiv 2509.06744, `blockmg` 0.1.0, under
+ * /root/reference/proj).  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load it, and only as the checker or
+ * the CPU baseline.  The product (libbmgcuda.so) never links or calls it.
+ *
+ * Parity status: the reference cannot be compiled here (Eigen3 and vendor/ are
+ * absent), and it ships no golden vectors.  The
+ * restatement is pinned against every known-answer and property test the
+ * reference holds for this path (tests/test_oracle_pins.py citing
+ * proj/tests/ sources  line by line).
+ *
+ * Handles are opaque; every entry returns 0 on success or a negative status
+ * (see ORC_E*), with the message available from orc_last_error().
+ */
+#pragma once
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  ORC_OK = 0,
+  ORC_EINVAL = -1,      /* std::invalid_argument */
+  ORC_ERANGE = -2,      /* std::out_of_range */
+  ORC_ENOTSPD = -3,     /* NotPositiveDefinite (pivot in orc_last_pivot) */
+  ORC_ERUNTIME = -4,    /* std::runtime_error */
+};
+
+typedef struct orc_mat orc_mat;
+typedef struct orc_fsai orc_fsai;
+typedef struct orc_hier orc_hier;
+
+const char* orc_last_error(void);
+int orc_last_pivot(void);
+int orc_set_threads(int n);
+int orc_get_threads(void);
+
+/* ---- block-sparse matrices (block_matrix.hpp:26-70) ---- */
+int orc_mat_create(int nbr, const int32_t* row_sizes, int nbc, const int32_t* col_sizes,
+                   const int64_t* row_ptr, const int32_t* col_idx, const double* vals,
+                   int symmetric, orc_mat** out);
+void orc_mat_destroy(orc_mat* a);
+/* sizes of the export arrays: nnzb, total scalars */
+int orc_mat_info(const orc_mat* a, int* nbr, int* nbc, int64_t* nnzb, int64_t* nvals, int* dim_r,
+                 int* dim_c);
+int orc_mat_export(const orc_mat* a, int64_t* row_ptr, int32_t* col_idx, double* vals);
+
+/* ---- kernels (kernels.cpp) ---- */
+int orc_spmv(const orc_mat* a, const double* x, double* y);
+int orc_spmv_t(const orc_mat* a, const double* x, double* y);
+int orc_multiply(const orc_mat* a, const orc_mat* b, orc_mat** out);
+int orc_transpose_multiply(const orc_mat* p, const orc_mat* b, orc_mat** out);
+int orc_triple_product(const orc_mat* f, const orc_mat* a, orc_mat** out);
+int orc_galerkin(const orc_mat* a, const orc_mat* p, orc_mat** out);
+
+/* ---- SmallCholesky (small_cholesky.cpp:12-47), dense row-major n x n ---- */
+int orc_cholesky(int n, const double* b, double* l_out, double* logdet);
+int orc_chol_solve(int n, const double* l, const double* rhs, double* x);
+
+/* ---- FSAI (fsai.cpp) ---- */
+/* kind 0: build_fsai with LowerPattern::from_matrix(A) (static lower(P(A)))
+ * kind 1: build_fsai with LowerPattern::diagonal (block Jacobi)
+ * kind 2: build_fsai with LowerPattern::full
+ * kind 3: nested_build(A, t_max, tau, nest)                                  */
+int orc_fsai_build(const orc_mat* a, int kind, int t_max, double tau, int nest, orc_fsai** out);
+void orc_fsai_destroy(orc_fsai* f);
+int orc_fsai_apply(const orc_fsai* f, const double* r, double* out);
+int orc_fsai_apply_transformed(const orc_fsai* f, const orc_mat* a, const double* x, double* out);
+/* number of chain factors; F_k export (unit-diagonal lower) and S-hat Cholesky
+ * factors of the last factor (n blocks, row-major m_i x m_i each, packed) */
+int orc_fsai_chain_len(const orc_fsai* f);
+int orc_fsai_factor(const orc_fsai* f, int k, orc_mat** F_out);
+int orc_fsai_shat(const orc_fsai* f, double* l_packed);
+/* G = L-hat^{-1} F-hat of a one-factor chain as a BSR (the product's M = G^T G) */
+int orc_fsai_G(const orc_fsai* f, orc_mat** G_out);
+
+/* ---- Lanczos (lanczos.hpp:16-58) ---- */
+int orc_lanczos_lambda_max(const orc_mat* a, const orc_fsai* f, int iters, double safety,
+                           uint64_t seed, double* beta);
+/* diagonal operator, for the reference's own known-spectrum pins */
+int orc_lanczos_diag(int n, const double* lam, int iters, double safety, uint64_t seed,
+                     int smallest, double* out);
+int orc_tridiag_eigs(int n, const double* d, const double* e, double* eig_sorted);
+
+/* ---- Chebyshev / smoothers (chebyshev.hpp, chebyshev.cpp) ---- */
+/* kind: 0 Richardson(param=omega), 1 first kind(alpha=param), 2 fourth kind */
+int orc_smoother_apply(const orc_mat* a, const orc_fsai* f, int kind, double alpha, double beta,
+                       double omega, int k, const double* b, double* x);
+/* diag(lam) operator with identity preconditioner (test_chebyshev.cpp fixtures) */
+int orc_smoother_apply_diag(int n, const double* lam, int kind, double alpha, double beta,
+                            double omega, int k, const double* b, double* x);
+/* ChebKind: 0 FirstT, 1 FourthW, 2 ScaledFirst, 3 ScaledFourth */
+int orc_poly_eval(int kind, int degree, double alpha, double beta, double t, double* out);
+double orc_fourth_kind_mu(int n);
+
+/* ---- multilevel (multilevel.cpp) ---- */
+/* transfers[l-1] prolongates level l-1 to level l; levels = ntransfers + 1.
+ * fsai_kind: 3 = nested_build(t_max, tau, nest) as reference setup();
+ *            0 = static lower(P(A)) per level (lower-level API, config 1)     */
+int orc_setup(const orc_mat* a_finest, int ntransfers, const orc_mat* const* transfers,
+              int t_max, double tau, int nest, int fsai_kind, int lanczos_iters,
+              double lanczos_safety, uint64_t seed, int coarse_dim_cap, int smallest_ritz_probe,
+              orc_hier** out);
+void orc_hier_destroy(orc_hier* h);
+int orc_hier_levels(const orc_hier* h);
+int orc_hier_level_A(const orc_hier* h, int l, const orc_mat** a);
+int orc_hier_level_P(const orc_hier* h, int l, const orc_mat** p);
+int orc_hier_level_fsai(const orc_hier* h, int l, const orc_fsai** f);
+int orc_hier_beta(const orc_hier* h, int l, double* beta);
+int orc_hier_coarse_l(const orc_hier* h, double* l_dense);   /* N0 x N0 row-major */
+int orc_vcycle(const orc_hier* h, int k_pre, int k_post, int level, const double* b, double* x);
+/* residual-history driver modelled on measure_rates (experiments.cpp:15-67):
+ * hist[0] = ||b - A x0||, hist[n] after n cycles; stops when
+ * hist[n]/hist[0] < tol; status 0 converged, 1 max_iter, 2 diverged. */
+int orc_solve(const orc_hier* h, int k_pre, int k_post, const double* b, double* x, double tol,
+              int max_iter, double* hist, int* iters, int* status);
+
+/* ---- RNG (rng.hpp:12-57) ---- */
+uint64_t orc_mix64(uint64_t z);
+double orc_rng_uniform(uint64_t seed, uint64_t i);
+
+#ifdef __cplusplus
+}
+#endif

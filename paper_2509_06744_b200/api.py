@@ -1,0 +1,382 @@
+"""Python mirror of the reference's hot-path interface over the C ABI.
+
+Names follow /root/reference/proj/include/blockmg: BlockSparseMatrix
+(block_matrix.hpp:26-70), spmv / spmv_transpose (kernels.hpp:15,19),
+galerkin_coarsen (multilevel.hpp:50), build_fsai / nested_build (fsai.hpp:25,68),
+cheb_fourth_apply (chebyshev.hpp:48), lanczos_lambda_max (multilevel.hpp:53),
+setup / v_cycle (multilevel.hpp:59,65) and the measure_rates-style solve loop
+(experiments.cpp:15-67).  Every object lives on the GPU; host data crosses the
+boundary only in the explicit upload/download calls.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import native as N
+from .native import check, dptr, i32ptr, i64ptr, lib
+
+
+@dataclass
+class HostBsr:
+    """Host block-CSR: row-major unpadded blocks in row_ptr/col_idx order."""
+
+    row_sizes: np.ndarray
+    col_sizes: np.ndarray
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    vals: np.ndarray
+    symmetric: bool = False
+
+    def __post_init__(self):
+        self.row_sizes = np.ascontiguousarray(self.row_sizes, dtype=np.int32)
+        self.col_sizes = np.ascontiguousarray(self.col_sizes, dtype=np.int32)
+        self.row_ptr = np.ascontiguousarray(self.row_ptr, dtype=np.int64)
+        self.col_idx = np.ascontiguousarray(self.col_idx, dtype=np.int32)
+        self.vals = np.ascontiguousarray(self.vals, dtype=np.float64)
+
+    @property
+    def nbr(self):
+        return len(self.row_sizes)
+
+    @property
+    def nbc(self):
+        return len(self.col_sizes)
+
+    @property
+    def nnzb(self):
+        return int(self.row_ptr[-1])
+
+    @property
+    def dim_r(self):
+        return int(self.row_sizes.sum())
+
+    @property
+    def dim_c(self):
+        return int(self.col_sizes.sum())
+
+    def to_dense(self) -> np.ndarray:
+        ro = np.concatenate([[0], np.cumsum(self.row_sizes)])
+        co = np.concatenate([[0], np.cumsum(self.col_sizes)])
+        out = np.zeros((ro[-1], co[-1]))
+        v = 0
+        for i in range(self.nbr):
+            for p in range(self.row_ptr[i], self.row_ptr[i + 1]):
+                j = self.col_idx[p]
+                mi, mj = self.row_sizes[i], self.col_sizes[j]
+                out[ro[i]:ro[i] + mi, co[j]:co[j] + mj] = self.vals[v:v + mi * mj].reshape(mi, mj)
+                v += mi * mj
+        return out
+
+
+class Context:
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(lib().bmg_ctx_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def set_stream(self, stream_ptr: int | None):
+        check(lib().bmg_ctx_set_stream(self.h, C.c_void_p(stream_ptr or 0)))
+
+    def sync(self):
+        check(lib().bmg_ctx_sync(self.h))
+
+    @property
+    def launch_count(self) -> int:
+        return int(lib().bmg_ctx_launch_count(self.h))
+
+    def close(self):
+        if self.h:
+            check(lib().bmg_ctx_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class BlockSparseMatrix:
+    """Device BSR (reference BlockSparseMatrix, block_matrix.hpp:26-70)."""
+
+    def __init__(self, ctx: Context, host: HostBsr | None = None, _handle=None, _owned=True):
+        self.ctx = ctx
+        self._owned = _owned
+        if _handle is not None:
+            self.h = _handle
+            return
+        h = C.c_void_p()
+        check(lib().bmg_bsr_create(ctx.h, host.nbr, i32ptr(host.row_sizes), host.nbc, i32ptr(host.col_sizes),
+                                   i64ptr(host.row_ptr), i32ptr(host.col_idx), dptr(host.vals),
+                                   N.BMG_SYMMETRIC if host.symmetric else 0, C.byref(h)))
+        self.h = h
+
+    def info(self) -> dict:
+        a, b, d, e = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        nnzb, dev, pb = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib().bmg_bsr_info(self.h, C.byref(a), C.byref(b), C.byref(nnzb), C.byref(d), C.byref(e),
+                                 C.byref(dev), C.byref(pb)))
+        return dict(nbr=a.value, nbc=b.value, nnzb=nnzb.value, dim_r=d.value, dim_c=e.value,
+                    device_bytes=dev.value, pass_bytes=pb.value)
+
+    def download(self, row_sizes, col_sizes, symmetric=False) -> HostBsr:
+        inf = self.info()
+        rp = np.zeros(inf["nbr"] + 1, np.int64)
+        ci = np.zeros(max(inf["nnzb"], 1), np.int32)
+        rs = np.asarray(row_sizes, np.int64)
+        cs = np.asarray(col_sizes, np.int64)
+        check(lib().bmg_bsr_download(self.h, i64ptr(rp), i32ptr(ci), None))
+        nvals = int(sum(rs[i] * cs[ci[p]] for i in range(inf["nbr"]) for p in range(rp[i], rp[i + 1]))) \
+            if not (np.all(rs == rs[0]) and np.all(cs == cs[0])) else int(inf["nnzb"] * rs[0] * cs[0])
+        vals = np.zeros(max(nvals, 1))
+        check(lib().bmg_bsr_download(self.h, i64ptr(rp), i32ptr(ci), dptr(vals)))
+        return HostBsr(row_sizes, col_sizes, rp, ci[:inf["nnzb"]], vals[:nvals], symmetric)
+
+    def transpose(self) -> "BlockSparseMatrix":
+        h = C.c_void_p()
+        check(lib().bmg_bsr_transpose(self.h, C.byref(h)))
+        return BlockSparseMatrix(self.ctx, _handle=h)
+
+    def close(self):
+        if self.h and self._owned:
+            check(lib().bmg_bsr_destroy(self.h))
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Vector:
+    def __init__(self, ctx: Context, n_or_array):
+        self.ctx = ctx
+        if isinstance(n_or_array, (int, np.integer)):
+            n = int(n_or_array)
+            data = None
+        else:
+            data = np.ascontiguousarray(n_or_array, dtype=np.float64)
+            n = data.size
+        h = C.c_void_p()
+        check(lib().bmg_vec_create(ctx.h, n, C.byref(h)))
+        self.h = h
+        self.n = n
+        if data is not None:
+            self.upload(data)
+
+    def upload(self, a: np.ndarray):
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        assert a.size == self.n
+        check(lib().bmg_vec_upload(self.h, dptr(a)))
+
+    def download(self) -> np.ndarray:
+        out = np.empty(self.n)
+        check(lib().bmg_vec_download(self.h, dptr(out)))
+        return out
+
+    def fill(self, v: float):
+        check(lib().bmg_vec_fill(self.h, v))
+
+    @property
+    def device_ptr(self) -> int:
+        return lib().bmg_vec_device_ptr(self.h)
+
+    def close(self):
+        if self.h:
+            check(lib().bmg_vec_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def spmv(a: BlockSparseMatrix, x: Vector, y: Vector):
+    check(lib().bmg_spmv(a.h, x.h, y.h))
+
+
+def spmv_transpose(a: BlockSparseMatrix, x: Vector, y: Vector):
+    check(lib().bmg_spmv_t(a.h, x.h, y.h))
+
+
+def residual(a: BlockSparseMatrix, b: Vector, x: Vector, r: Vector):
+    check(lib().bmg_residual(a.h, b.h, x.h, r.h))
+
+
+def dot(a: Vector, b: Vector) -> float:
+    out = C.c_double()
+    check(lib().bmg_dot(a.h, b.h, C.byref(out)))
+    return out.value
+
+
+def galerkin_coarsen(a: BlockSparseMatrix, p: BlockSparseMatrix) -> BlockSparseMatrix:
+    h = C.c_void_p()
+    check(lib().bmg_galerkin(a.h, p.h, C.byref(h)))
+    return BlockSparseMatrix(a.ctx, _handle=h)
+
+
+class Fsai:
+    """Device block-FSAI, M = G^T G (NestedFsai, fsai.hpp:56-66)."""
+
+    def __init__(self, ctx, handle, owned=True):
+        self.ctx = ctx
+        self.h = handle
+        self._owned = owned
+
+    @classmethod
+    def build(cls, a: BlockSparseMatrix, kind=N.FSAI_ADAPTIVE, t_max=1, tau=1.0, nest=0) -> "Fsai":
+        h = C.c_void_p()
+        check(lib().bmg_fsai_build(a.h, kind, t_max, tau, nest, C.byref(h)))
+        return cls(a.ctx, h)
+
+    @classmethod
+    def from_factors(cls, ctx: Context, F: BlockSparseMatrix, shat_l_packed: np.ndarray) -> "Fsai":
+        h = C.c_void_p()
+        s = np.ascontiguousarray(shat_l_packed, np.float64)
+        check(lib().bmg_fsai_from_factors(ctx.h, F.h, dptr(s), C.byref(h)))
+        return cls(ctx, h)
+
+    def apply(self, r: Vector, z: Vector):
+        check(lib().bmg_fsai_apply(self.h, r.h, z.h))
+
+    def apply_transformed(self, a: BlockSparseMatrix, x: Vector, y: Vector):
+        check(lib().bmg_fsai_apply_transformed(self.h, a.h, x.h, y.h))
+
+    @property
+    def G(self) -> BlockSparseMatrix:
+        h = C.c_void_p()
+        check(lib().bmg_fsai_G(self.h, C.byref(h)))
+        return BlockSparseMatrix(self.ctx, _handle=h, _owned=False)
+
+    def close(self):
+        if self.h and self._owned:
+            check(lib().bmg_fsai_destroy(self.h))
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def cheb_fourth_apply(a: BlockSparseMatrix, m: Fsai, b: Vector, x: Vector, beta: float, k: int):
+    """x <- cheb_fourth_apply(A, M, b, x, beta, k) (chebyshev.hpp:48-69), in place."""
+    check(lib().bmg_cheb4_apply(a.h, m.h, b.h, x.h, beta, k))
+
+
+def lanczos_lambda_max(a: BlockSparseMatrix, m: Fsai, iters=100, safety=1.01, seed=42) -> float:
+    out = C.c_double()
+    check(lib().bmg_lanczos_lambda_max(a.h, m.h, iters, safety, seed, C.byref(out)))
+    return out.value
+
+
+def default_params(**kw) -> N.SetupParams:
+    p = N.SetupParams()
+    lib().bmg_setup_params_default(C.byref(p))
+    for k, v in kw.items():
+        setattr(p, k, v)
+    return p
+
+
+class Hierarchy:
+    """Device multigrid hierarchy (Hierarchy, multilevel.hpp:28-33)."""
+
+    def __init__(self, ctx, handle, keep=()):
+        self.ctx = ctx
+        self.h = handle
+        self._keep = list(keep)
+
+    @classmethod
+    def setup(cls, a_finest: BlockSparseMatrix, transfers, params: N.SetupParams | None = None) -> "Hierarchy":
+        arr = (C.c_void_p * max(len(transfers), 1))(*[t.h.value for t in transfers])
+        h = C.c_void_p()
+        check(lib().bmg_hier_setup(a_finest.h, len(transfers), arr,
+                                   C.byref(params) if params is not None else None, C.byref(h)))
+        return cls(a_finest.ctx, h, keep=[a_finest, *transfers])
+
+    @classmethod
+    def create(cls, ctx, A, P, M, beta, coarse_dim_cap=1 << 30) -> "Hierarchy":
+        L = len(A)
+        aa = (C.c_void_p * L)(*[a.h.value for a in A])
+        pp = (C.c_void_p * L)(*[(p.h.value if p is not None else None) for p in P])
+        mm = (C.c_void_p * L)(*[(m.h.value if m is not None else None) for m in M])
+        bb = np.ascontiguousarray(beta, np.float64)
+        h = C.c_void_p()
+        check(lib().bmg_hier_create(ctx.h, L, aa, pp, mm, dptr(bb), coarse_dim_cap, C.byref(h)))
+        return cls(ctx, h, keep=[*A, *P, *M])
+
+    @property
+    def levels(self) -> int:
+        n = C.c_int()
+        check(lib().bmg_hier_info(self.h, C.byref(n), None))
+        return n.value
+
+    @property
+    def device_bytes(self) -> int:
+        b = C.c_int64()
+        check(lib().bmg_hier_info(self.h, None, C.byref(b)))
+        return b.value
+
+    def beta(self, level: int) -> float:
+        out = C.c_double()
+        check(lib().bmg_hier_beta(self.h, level, C.byref(out)))
+        return out.value
+
+    def level(self, l: int):
+        a, p, m = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        check(lib().bmg_hier_level(self.h, l, C.byref(a), C.byref(p), C.byref(m)))
+        A = BlockSparseMatrix(self.ctx, _handle=a, _owned=False)
+        P = BlockSparseMatrix(self.ctx, _handle=p, _owned=False) if p.value else None
+        M = Fsai(self.ctx, m, owned=False) if m.value else None
+        return A, P, M
+
+    def cycle_bytes(self, k_pre, k_post) -> int:
+        out = C.c_int64()
+        check(lib().bmg_hier_cycle_bytes(self.h, k_pre, k_post, C.byref(out)))
+        return out.value
+
+    def use_graph(self, on: bool):
+        check(lib().bmg_hier_use_graph(self.h, 1 if on else 0))
+
+    def v_cycle(self, k_pre, k_post, b: Vector, x: Vector):
+        check(lib().bmg_vcycle(self.h, k_pre, k_post, b.h, x.h))
+
+    def v_cycle_host(self, k_pre, k_post, b: np.ndarray, x: np.ndarray):
+        check(lib().bmg_vcycle_host(self.h, k_pre, k_post, dptr(b), dptr(x)))
+
+    def v_cycle_host_ptr(self, k_pre, k_post, b_ptr: int, x_ptr: int):
+        check(lib().bmg_vcycle_host(self.h, k_pre, k_post, C.cast(b_ptr, N._PD), C.cast(x_ptr, N._PD)))
+
+    def solve(self, k_pre, k_post, b: Vector, x: Vector, tol=1e-8, max_iter=50):
+        hist = np.zeros(max_iter + 1)
+        it, st = C.c_int(), C.c_int()
+        check(lib().bmg_solve(self.h, k_pre, k_post, b.h, x.h, tol, max_iter, dptr(hist), C.byref(it),
+                              C.byref(st)))
+        return hist[:it.value + 1], it.value, st.value
+
+    def close(self):
+        if self.h:
+            check(lib().bmg_hier_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def tridiag_eigs(d, e) -> np.ndarray:
+    d = np.ascontiguousarray(d, np.float64)
+    e = np.ascontiguousarray(e, np.float64)
+    out = np.zeros(len(d))
+    check(lib().bmg_tridiag_eigs(len(d), dptr(d), dptr(e) if len(e) else None, dptr(out)))
+    return out

@@ -1,0 +1,699 @@
+// bmg_core.cu -- context, device BSR storage + streaming plans, vectors, the
+// streaming-kernel launchers, reductions and the corresponding C ABI.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
+#include "bmg_abi.h"
+#include "bmg_internal.h"
+#include "bsr_stream.cuh"
+
+namespace bmg {
+
+// ============================================================================ errors
+[[noreturn]] void fail(int status, const std::string& msg, int pivot) { throw Error(status, msg, pivot); }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(BMG_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+thread_local std::string g_last_error;
+thread_local int g_last_pivot = -1;
+
+// ============================================================================ context
+Ctx::~Ctx() {
+  if (solver) cusolverDnDestroy(solver);
+  if (h_red) cudaFreeHost(h_red);
+  if (own) cudaStreamDestroy(own);
+}
+
+cusolverDnHandle_t Ctx::cusolver() {
+  if (!solver) {
+    if (cusolverDnCreate(&solver) != CUSOLVER_STATUS_SUCCESS) fail(BMG_ECUDA, "cusolverDnCreate failed");
+  }
+  cusolverDnSetStream(solver, stream);
+  return solver;
+}
+
+// ============================================================================ kernels
+namespace kern {
+
+__global__ void fill_kernel(double* p, int64_t n, double v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+__global__ void copy_kernel(double* __restrict__ d, const double* __restrict__ s, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    d[i] = s[i];
+}
+
+constexpr int kDotBlocks = 592;
+constexpr int kDotThreads = 256;
+
+// deterministic two-stage dot: fixed segments per block, fixed tree order
+__global__ void __launch_bounds__(kDotThreads) dot_stage1(const double* __restrict__ a,
+                                                          const double* __restrict__ b, int64_t n,
+                                                          double* partial) {
+  __shared__ double sh[kDotThreads];
+  const int64_t seg = (n + kDotBlocks - 1) / kDotBlocks;
+  const int64_t lo = blockIdx.x * seg;
+  const int64_t hi = min(n, lo + seg);
+  double s = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += kDotThreads) s = __fma_rn(a[i], b[i], s);
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = kDotThreads / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+__global__ void __launch_bounds__(1024) dot_stage2(const double* partial, double* out) {
+  __shared__ double sh[1024];
+  sh[threadIdx.x] = threadIdx.x < kDotBlocks ? partial[threadIdx.x] : 0.0;
+  __syncthreads();
+  for (int w = 512; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = sh[0];
+}
+
+// per-block transpose through a permutation of blocks (uniform layouts)
+__global__ void transpose_uniform_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                                         const int64_t* __restrict__ perm, int64_t nnzb, int mr,
+                                         int mc, int bs_src, int bs_dst) {
+  const int64_t total = nnzb * (int64_t)(mr * mc);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = e / (mr * mc);
+    const int q = (int)(e - t * (mr * mc));
+    const int r = q / mr, c = q - r * mr;  // dst block is mc x mr: (r, c) = src (c, r)
+    dst[t * bs_dst + q] = src[perm[t] * bs_src + (int64_t)c * mc + r];
+  }
+}
+__global__ void transpose_var_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                                     const int64_t* __restrict__ perm,
+                                     const int64_t* __restrict__ voff_src,
+                                     const int64_t* __restrict__ voff_dst,
+                                     const int* __restrict__ trow_of, const int* __restrict__ tcol,
+                                     const int* __restrict__ tsz_r, const int* __restrict__ tsz_c,
+                                     int64_t nnzb) {
+  for (int64_t t = blockIdx.x; t < nnzb; t += gridDim.x) {
+    const int mr = tsz_r[trow_of[t]], mc = tsz_c[tcol[t]];  // dst block mr x mc
+    const int64_t s0 = voff_src[perm[t]], d0 = voff_dst[t];
+    for (int q = threadIdx.x; q < mr * mc; q += blockDim.x) {
+      const int r = q / mc, c = q - r * mc;
+      dst[d0 + q] = src[s0 + (int64_t)c * mr + r];
+    }
+  }
+}
+
+}  // namespace kern
+
+static int grid_for(int64_t n, int threads = 256) {
+  int64_t g = (n + threads - 1) / threads;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16));
+}
+
+void fill(Ctx* ctx, double* p, int64_t n, double v) {
+  if (n <= 0) return;
+  kern::fill_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(p, n, v);
+  ctx->count();
+  BMG_CUDA(cudaGetLastError());
+}
+void copy(Ctx* ctx, double* dst, const double* src, int64_t n) {
+  if (n <= 0 || dst == src) return;
+  kern::copy_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(dst, src, n);
+  ctx->count();
+  BMG_CUDA(cudaGetLastError());
+}
+
+double dot(Ctx* ctx, const double* a, const double* b, int64_t n) {
+  if (ctx->red.n < (size_t)kern::kDotBlocks + 8) ctx->red.alloc(kern::kDotBlocks + 8);
+  if (!ctx->h_red) BMG_CUDA(cudaMallocHost(&ctx->h_red, 8 * sizeof(double)));
+  kern::dot_stage1<<<kern::kDotBlocks, kern::kDotThreads, 0, ctx->stream>>>(a, b, n, ctx->red.p);
+  kern::dot_stage2<<<1, 1024, 0, ctx->stream>>>(ctx->red.p, ctx->red.p + kern::kDotBlocks);
+  ctx->count(2);
+  BMG_CUDA(cudaGetLastError());
+  BMG_CUDA(cudaMemcpyAsync(ctx->h_red, ctx->red.p + kern::kDotBlocks, sizeof(double),
+                           cudaMemcpyDeviceToHost, ctx->stream));
+  BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+  return ctx->h_red[0];
+}
+
+// ============================================================================ BSR
+int64_t Bsr::pass_bytes() const {
+  // algorithmic bytes of one streaming pass: every block's values + its column index
+  int64_t v = 0;
+  if (uniform)
+    v = nnzb * ((int64_t)mr * mc * 8 + 4);
+  else
+    for (int i = 0; i < nbr; ++i)
+      for (int64_t p = h_row_ptr[i]; p < h_row_ptr[i + 1]; ++p) v += (int64_t)rsz[i] * csz[h_col[p]] * 8 + 4;
+  return v;
+}
+int64_t Bsr::device_bytes() const {
+  return (int64_t)(row_ptr.bytes() + col.bytes() + vals.bytes() + voff.bytes() + d_roff.bytes() +
+                   d_coff.bytes() + d_rsz.bytes() + d_csz.bytes() + plan.chunks.bytes() +
+                   plan.cta_chunk.bytes());
+}
+
+static bool stream_supported(int mr, int mc) {
+  return mr == mc && (mr == 10 || mr == 15 || mr == 20 || mr == 21);
+}
+
+static int chunk_target_bytes() {
+  static int v = [] {
+    const char* e = std::getenv("BMG_CHUNK_KB");
+    int kb = e ? std::atoi(e) : 16;
+    if (kb < 2) kb = 2;
+    if (kb > 48) kb = 48;
+    return kb * 1024;
+  }();
+  return v;
+}
+
+template <int MR, int MC>
+static int stream_occupancy(size_t smem) {
+  auto kfn = kern::bsr_stream_kernel<MR, MC, kern::EpiStore>;
+  BMG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  BMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kern::kThreads, smem));
+  return std::max(occ, 1);
+}
+
+static int occupancy_for(int mr, int mc, size_t smem) {
+  switch (mr) {
+    case 10: return stream_occupancy<10, 10>(smem);
+    case 15: return stream_occupancy<15, 15>(smem);
+    case 20: return stream_occupancy<20, 20>(smem);
+    case 21: return stream_occupancy<21, 21>(smem);
+  }
+  return 1;
+}
+
+// Partition block rows into per-CTA ranges balanced by blocks; cut each
+// range's contiguous block span into chunks of cb_max blocks (bsr_stream.cuh).
+void build_plan(Bsr& a) {
+  Plan& P = a.plan;
+  P = Plan();
+  if (!(a.uniform && stream_supported(a.mr, a.mc)) || a.nbr == 0) return;
+  const int block_bytes = a.bs * 8;
+  P.cb_max = std::max(1, chunk_target_bytes() / block_bytes);
+  const auto& rp = a.h_row_ptr;
+  // chunk list per CTA range
+  std::vector<int4> chunks;
+  std::vector<int> cta;
+  int rmax = 1;
+  // first pass with a provisional rmax to size smem and query occupancy
+  const size_t smem0 = kern::SmemLayout(a.bs, P.cb_max, P.cb_max + 2, a.mr).total;
+  const int occ = occupancy_for(a.mr, a.mc, smem0);
+  const int64_t gmax = (int64_t)a.ctx->sms * occ;
+  const int64_t per = std::max<int64_t>(1, (a.nnzb + gmax - 1) / gmax);
+  int row = 0;
+  while (row < a.nbr) {
+    const int rlo = row;
+    const int64_t b0 = rp[rlo];
+    while (row < a.nbr && rp[row + 1] - b0 < per) ++row;
+    if (row < a.nbr) ++row;  // include the row that reaches the target
+    // rows that are empty right after the cut stay with this CTA
+    while (row < a.nbr && rp[row + 1] == rp[row]) ++row;
+    const int rhi = row;
+    const int64_t B0 = rp[rlo], B1 = rp[rhi];
+    cta.push_back((int)chunks.size());
+    int r = rlo;
+    int64_t clo = B0;
+    do {
+      const int64_t chi = std::min(B1, clo + P.cb_max);
+      const int row_lo = r;
+      while (r < rhi && rp[r + 1] <= chi) ++r;
+      const bool cout = (r < rhi && rp[r] < chi);
+      const int row_hi = cout ? r + 1 : r;
+      const bool cin = rp[row_lo] < clo;
+      const int nrows = row_hi - row_lo;
+      if (nrows >= (int)kern::kRowMask) fail(BMG_EINVAL, "plan: too many rows in a chunk");
+      unsigned w = (unsigned)nrows | (cin ? kern::kCarryIn : 0u) | (cout ? kern::kCarryOut : 0u);
+      chunks.push_back(make_int4((int)clo, (int)(chi - clo), row_lo, (int)w));
+      rmax = std::max(rmax, nrows);
+      clo = chi;
+    } while (clo < B1);
+    if (r != rhi) fail(BMG_ERUNTIME, "plan: row bookkeeping mismatch");
+  }
+  cta.push_back((int)chunks.size());
+  P.rmax = rmax;
+  P.nctas = (int)cta.size() - 1;
+  P.nchunks = (int)chunks.size();
+  P.smem = kern::SmemLayout(a.bs, P.cb_max, P.rmax, a.mr).total;
+  if (P.smem > 227 * 1024) fail(BMG_EINVAL, "plan: chunk does not fit in shared memory");
+  occupancy_for(a.mr, a.mc, P.smem);  // sets the dynamic smem attribute
+  P.chunks.alloc(chunks.size());
+  P.cta_chunk.alloc(cta.size());
+  BMG_CUDA(cudaMemcpy(P.chunks.p, chunks.data(), chunks.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  BMG_CUDA(cudaMemcpy(P.cta_chunk.p, cta.data(), cta.size() * sizeof(int), cudaMemcpyHostToDevice));
+}
+
+static void finish_layouts(Bsr& a, int nbr, const int* rsz, int nbc, const int* csz) {
+  a.nbr = nbr;
+  a.nbc = nbc;
+  a.rsz.assign(rsz, rsz + nbr);
+  a.csz.assign(csz, csz + nbc);
+  a.roff.resize(nbr);
+  a.coff.resize(nbc);
+  int d = 0;
+  for (int i = 0; i < nbr; ++i) {
+    if (rsz[i] < 1) fail(BMG_EINVAL, "BlockLayout: block sizes must be >= 1");
+    a.roff[i] = d;
+    d += rsz[i];
+  }
+  a.dim_r = d;
+  d = 0;
+  for (int j = 0; j < nbc; ++j) {
+    if (csz[j] < 1) fail(BMG_EINVAL, "BlockLayout: block sizes must be >= 1");
+    a.coff[j] = d;
+    d += csz[j];
+  }
+  a.dim_c = d;
+  a.uniform = nbr > 0 && nbc > 0;
+  for (int i = 1; i < nbr && a.uniform; ++i) a.uniform = rsz[i] == rsz[0];
+  for (int j = 1; j < nbc && a.uniform; ++j) a.uniform = csz[j] == csz[0];
+  a.mr = a.uniform ? rsz[0] : 0;
+  a.mc = a.uniform ? csz[0] : 0;
+  a.bs = a.uniform ? ((a.mr * a.mc + 1) & ~1) : 0;
+}
+
+static void upload_structure(Bsr& a) {
+  a.nnzb = a.h_row_ptr.empty() ? 0 : a.h_row_ptr.back();
+  if (a.nnzb >= ((int64_t)1 << 31)) fail(BMG_EINVAL, "bsr: more than 2^31 blocks");
+  a.row_ptr.alloc(a.nbr + 1);
+  BMG_CUDA(cudaMemcpy(a.row_ptr.p, a.h_row_ptr.data(), (a.nbr + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+  a.col.alloc(a.nnzb + 8);
+  BMG_CUDA(cudaMemset(a.col.p, 0, (a.nnzb + 8) * sizeof(int32_t)));
+  if (a.nnzb)
+    BMG_CUDA(cudaMemcpy(a.col.p, a.h_col.data(), a.nnzb * sizeof(int32_t), cudaMemcpyHostToDevice));
+  // value offsets
+  a.h_voff.resize(a.nnzb + 1);
+  int64_t v = 0;
+  for (int i = 0; i < a.nbr; ++i)
+    for (int64_t p = a.h_row_ptr[i]; p < a.h_row_ptr[i + 1]; ++p) {
+      a.h_voff[p] = v;
+      v += a.uniform ? a.bs : (int64_t)a.rsz[i] * a.csz[a.h_col[p]];
+    }
+  a.h_voff[a.nnzb] = v;
+  const bool streamed = a.uniform && stream_supported(a.mr, a.mc);
+  if (!streamed) {
+    a.voff.alloc(a.nnzb + 1);
+    BMG_CUDA(cudaMemcpy(a.voff.p, a.h_voff.data(), (a.nnzb + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+    a.d_roff.alloc(a.nbr);
+    a.d_rsz.alloc(a.nbr);
+    a.d_coff.alloc(a.nbc);
+    a.d_csz.alloc(a.nbc);
+    BMG_CUDA(cudaMemcpy(a.d_roff.p, a.roff.data(), a.nbr * sizeof(int), cudaMemcpyHostToDevice));
+    BMG_CUDA(cudaMemcpy(a.d_rsz.p, a.rsz.data(), a.nbr * sizeof(int), cudaMemcpyHostToDevice));
+    BMG_CUDA(cudaMemcpy(a.d_coff.p, a.coff.data(), a.nbc * sizeof(int), cudaMemcpyHostToDevice));
+    BMG_CUDA(cudaMemcpy(a.d_csz.p, a.csz.data(), a.nbc * sizeof(int), cudaMemcpyHostToDevice));
+  }
+  a.vals.alloc(std::max<int64_t>(v, 2));
+  build_plan(a);
+}
+
+static void validate_structure(int nbr, int nbc, const int64_t* row_ptr, const int32_t* col) {
+  if (nbr < 0 || nbc < 0) fail(BMG_EINVAL, "bsr: negative dimensions");
+  if (row_ptr[0] != 0) fail(BMG_EINVAL, "bsr: row_ptr[0] must be 0");
+  for (int i = 0; i < nbr; ++i) {
+    if (row_ptr[i + 1] < row_ptr[i]) fail(BMG_EINVAL, "bsr: row_ptr must be non-decreasing");
+    for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
+      if (col[p] < 0 || col[p] >= nbc) fail(BMG_ERANGE, "BlockSparseMatrix: block index out of range");
+      if (p > row_ptr[i] && col[p] <= col[p - 1])
+        fail(BMG_EINVAL, "bsr: column indices must be strictly ascending within a row");
+    }
+  }
+}
+
+std::unique_ptr<Bsr> make_bsr_structure(Ctx* ctx, int nbr, const int* rsz, int nbc, const int* csz,
+                                        std::vector<int64_t> row_ptr, std::vector<int32_t> col,
+                                        bool sym) {
+  auto a = std::make_unique<Bsr>();
+  a->ctx = ctx;
+  finish_layouts(*a, nbr, rsz, nbc, csz);
+  if (sym && !(a->rsz == a->csz)) fail(BMG_EINVAL, "BlockSparseMatrix: symmetric matrix must be square");
+  a->sym = sym;
+  a->h_row_ptr = std::move(row_ptr);
+  a->h_col = std::move(col);
+  upload_structure(*a);
+  return a;
+}
+
+std::unique_ptr<Bsr> make_bsr(Ctx* ctx, int nbr, const int* rsz, int nbc, const int* csz,
+                              const int64_t* row_ptr, const int32_t* col, const double* vals,
+                              bool sym, bool vals_on_device) {
+  validate_structure(nbr, nbc, row_ptr, col);
+  const int64_t nnzb = row_ptr[nbr];
+  auto a = make_bsr_structure(ctx, nbr, rsz, nbc, csz,
+                              std::vector<int64_t>(row_ptr, row_ptr + nbr + 1),
+                              std::vector<int32_t>(col, col + nnzb), sym);
+  if (nnzb == 0) return a;
+  const auto kind = vals_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  if (!a->uniform || a->bs == a->mr * a->mc) {
+    BMG_CUDA(cudaMemcpy(a->vals.p, vals, a->h_voff[nnzb] * sizeof(double), kind));
+  } else {
+    // pad each block to the even stride (16-byte aligned blocks)
+    const size_t src = (size_t)a->mr * a->mc * sizeof(double), dst = (size_t)a->bs * sizeof(double);
+    BMG_CUDA(cudaMemset(a->vals.p, 0, a->vals.bytes()));
+    BMG_CUDA(cudaMemcpy2D(a->vals.p, dst, vals, src, src, nnzb, kind));
+  }
+  return a;
+}
+
+std::unique_ptr<Bsr> bsr_transpose(const Bsr& a) {
+  // structure on the host (integer counting sort: transposed rows ascending),
+  // values transposed on the device through the block permutation
+  std::vector<int64_t> trp(a.nbc + 1, 0);
+  for (int64_t p = 0; p < a.nnzb; ++p) trp[a.h_col[p] + 1]++;
+  for (int j = 0; j < a.nbc; ++j) trp[j + 1] += trp[j];
+  std::vector<int32_t> tcol(a.nnzb);
+  std::vector<int64_t> perm(a.nnzb);
+  std::vector<int64_t> fillp(trp.begin(), trp.end() - 1);
+  for (int i = 0; i < a.nbr; ++i)
+    for (int64_t p = a.h_row_ptr[i]; p < a.h_row_ptr[i + 1]; ++p) {
+      const int64_t q = fillp[a.h_col[p]]++;
+      tcol[q] = i;
+      perm[q] = p;
+    }
+  auto t = make_bsr_structure(a.ctx, a.nbc, a.csz.data(), a.nbr, a.rsz.data(), std::move(trp),
+                              std::move(tcol), a.sym);
+  if (a.nnzb == 0) return t;
+  DBuf<int64_t> dperm(a.nnzb);
+  BMG_CUDA(cudaMemcpy(dperm.p, perm.data(), a.nnzb * sizeof(int64_t), cudaMemcpyHostToDevice));
+  Ctx* ctx = a.ctx;
+  if (a.uniform) {
+    kern::transpose_uniform_kernel<<<grid_for(a.nnzb * a.mr * a.mc), 256, 0, ctx->stream>>>(
+        a.vals.p, t->vals.p, dperm.p, a.nnzb, a.mr, a.mc, a.bs, t->bs);
+  } else {
+    std::vector<int> trow_of(a.nnzb);
+    for (int j = 0; j < t->nbr; ++j)
+      for (int64_t q = t->h_row_ptr[j]; q < t->h_row_ptr[j + 1]; ++q) trow_of[q] = j;
+    DBuf<int64_t> vsrc(a.nnzb + 1), vdst(a.nnzb + 1);
+    DBuf<int> drow(a.nnzb), dcol(a.nnzb), dr(t->nbr), dc(t->nbc);
+    BMG_CUDA(cudaMemcpy(vsrc.p, a.h_voff.data(), (a.nnzb + 1) * 8, cudaMemcpyHostToDevice));
+    BMG_CUDA(cudaMemcpy(vdst.p, t->h_voff.data(), (a.nnzb + 1) * 8, cudaMemcpyHostToDevice));
+    BMG_CUDA(cudaMemcpy(drow.p, trow_of.data(), a.nnzb * 4, cudaMemcpyHostToDevice));
+    BMG_CUDA(cudaMemcpy(dcol.p, t->h_col.data(), a.nnzb * 4, cudaMemcpyHostToDevice));
+    BMG_CUDA(cudaMemcpy(dr.p, t->rsz.data(), t->nbr * 4, cudaMemcpyHostToDevice));
+    BMG_CUDA(cudaMemcpy(dc.p, t->csz.data(), t->nbc * 4, cudaMemcpyHostToDevice));
+    kern::transpose_var_kernel<<<grid_for(a.nnzb * 32, 256), 256, 0, ctx->stream>>>(
+        a.vals.p, t->vals.p, dperm.p, vsrc.p, vdst.p, drow.p, dcol.p, dr.p, dc.p, a.nnzb);
+    BMG_CUDA(cudaGetLastError());
+    BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  ctx->count();
+  BMG_CUDA(cudaGetLastError());
+  BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+  return t;
+}
+
+// ============================================================================ launches
+template <int MR, int MC, class Epi>
+static void launch_stream_t(const Bsr& a, const double* x, Epi epi) {
+  kern::StreamArgs s;
+  s.vals = a.vals.p;
+  s.col = a.col.p;
+  s.row_ptr = a.row_ptr.p;
+  s.chunks = a.plan.chunks.p;
+  s.cta_chunk = a.plan.cta_chunk.p;
+  s.x = x;
+  s.bs = a.bs;
+  s.cb_max = a.plan.cb_max;
+  s.rmax = a.plan.rmax;
+  kern::bsr_stream_kernel<MR, MC, Epi><<<a.plan.nctas, kern::kThreads, a.plan.smem, a.ctx->stream>>>(s, epi);
+  a.ctx->count();
+  BMG_CUDA(cudaGetLastError());
+}
+
+template <class Epi>
+static void launch(const Bsr& a, const double* x, Epi epi) {
+  if (a.nbr == 0) return;
+  if (a.uniform && stream_supported(a.mr, a.mc)) {
+    // make sure the dynamic smem attribute covers this epilogue's instantiation
+    auto set = [&](auto kfn) {
+      static thread_local size_t done = 0;
+      if (done < a.plan.smem) {
+        BMG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        done = 227 * 1024;
+      }
+    };
+    switch (a.mr) {
+      case 10: set(kern::bsr_stream_kernel<10, 10, Epi>); return launch_stream_t<10, 10>(a, x, epi);
+      case 15: set(kern::bsr_stream_kernel<15, 15, Epi>); return launch_stream_t<15, 15>(a, x, epi);
+      case 20: set(kern::bsr_stream_kernel<20, 20, Epi>); return launch_stream_t<20, 20>(a, x, epi);
+      case 21: set(kern::bsr_stream_kernel<21, 21, Epi>); return launch_stream_t<21, 21>(a, x, epi);
+    }
+  }
+  kern::VarArgs s;
+  s.vals = a.vals.p;
+  s.col = a.col.p;
+  s.row_ptr = a.row_ptr.p;
+  s.voff = a.voff.p;
+  s.roff = a.d_roff.p;
+  s.rsz = a.d_rsz.p;
+  s.coff = a.d_coff.p;
+  s.csz = a.d_csz.p;
+  s.x = x;
+  s.nbr = a.nbr;
+  const int blocks = (int)(((int64_t)a.nbr * 32 + 255) / 256);
+  kern::bsr_var_kernel<Epi><<<blocks, 256, 0, a.ctx->stream>>>(s, epi);
+  a.ctx->count();
+  BMG_CUDA(cudaGetLastError());
+}
+
+void spmv(const Bsr& a, const double* x, double* y) { launch(a, x, kern::EpiStore{y}); }
+void residual(const Bsr& a, const double* b, const double* x, double* r) {
+  launch(a, x, kern::EpiResidual{b, r});
+}
+void prolong_add(const Bsr& a, const double* e, double* x) { launch(a, e, kern::EpiAdd{x}); }
+void gt_cheb(const Bsr& gt, const double* w, double* p, double* x, double mu2, double dmu,
+             bool first, bool xzero) {
+  launch(gt, w, kern::EpiCheb{p, x, mu2, dmu, first ? 1 : 0, xzero ? 1 : 0});
+}
+
+}  // namespace bmg
+
+// ============================================================================ C ABI
+using namespace bmg;
+
+extern "C" {
+
+const char* bmg_last_error(void) { return g_last_error.c_str(); }
+int bmg_last_pivot(void) { return g_last_pivot; }
+const char* bmg_version(void) { return "blockmg-b200 0.1.0 (reference blockmg 0.1.0)"; }
+
+int bmg_ctx_create(int device, bmg_ctx** out) {
+  return guard([&] {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) fail(BMG_ECUDA, "no CUDA device available");
+    if (device < 0 || device >= n) fail(BMG_ERANGE, "bmg_ctx_create: device out of range");
+    auto c = std::make_unique<Ctx>();
+    c->device = device;
+    BMG_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    BMG_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) fail(BMG_ECUDA, "libbmgcuda requires an sm_100 (Blackwell) device");
+    c->sms = prop.multiProcessorCount;
+    BMG_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+    c->stream = c->own;
+    *out = reinterpret_cast<bmg_ctx*>(c.release());
+  });
+}
+int bmg_ctx_destroy(bmg_ctx* ctx) {
+  return guard([&] { delete reinterpret_cast<Ctx*>(ctx); });
+}
+int bmg_ctx_set_stream(bmg_ctx* ctx, void* s) {
+  return guard([&] {
+    Ctx* c = reinterpret_cast<Ctx*>(ctx);
+    c->stream = s ? static_cast<cudaStream_t>(s) : c->own;
+  });
+}
+int bmg_ctx_sync(bmg_ctx* ctx) {
+  return guard([&] { BMG_CUDA(cudaStreamSynchronize(reinterpret_cast<Ctx*>(ctx)->stream)); });
+}
+int64_t bmg_ctx_launch_count(const bmg_ctx* ctx) { return reinterpret_cast<const Ctx*>(ctx)->launches; }
+
+int bmg_bsr_create(bmg_ctx* ctx, int nbr, const int32_t* row_sizes, int nbc, const int32_t* col_sizes,
+                   const int64_t* row_ptr, const int32_t* col_idx, const double* vals, int flags,
+                   bmg_bsr** out) {
+  return guard([&] {
+    Ctx* c = reinterpret_cast<Ctx*>(ctx);
+    c->activate();
+    auto a = make_bsr(c, nbr, row_sizes, nbc, col_sizes, row_ptr, col_idx, vals, (flags & BMG_SYMMETRIC) != 0);
+    *out = reinterpret_cast<bmg_bsr*>(a.release());
+  });
+}
+int bmg_bsr_destroy(bmg_bsr* a) {
+  return guard([&] { delete reinterpret_cast<Bsr*>(a); });
+}
+int bmg_bsr_info(const bmg_bsr* ah, int* nbr, int* nbc, int64_t* nnzb, int* dim_r, int* dim_c,
+                 int64_t* device_bytes, int64_t* pass_bytes) {
+  return guard([&] {
+    const Bsr* a = reinterpret_cast<const Bsr*>(ah);
+    if (nbr) *nbr = a->nbr;
+    if (nbc) *nbc = a->nbc;
+    if (nnzb) *nnzb = a->nnzb;
+    if (dim_r) *dim_r = a->dim_r;
+    if (dim_c) *dim_c = a->dim_c;
+    if (device_bytes) *device_bytes = a->device_bytes();
+    if (pass_bytes) *pass_bytes = a->pass_bytes();
+  });
+}
+int bmg_bsr_download(const bmg_bsr* ah, int64_t* row_ptr, int32_t* col_idx, double* vals) {
+  return guard([&] {
+    const Bsr* a = reinterpret_cast<const Bsr*>(ah);
+    a->ctx->activate();
+    BMG_CUDA(cudaStreamSynchronize(a->ctx->stream));
+    if (row_ptr) std::memcpy(row_ptr, a->h_row_ptr.data(), (a->nbr + 1) * sizeof(int64_t));
+    if (col_idx && a->nnzb) std::memcpy(col_idx, a->h_col.data(), a->nnzb * sizeof(int32_t));
+    if (vals && a->nnzb) {
+      if (!a->uniform || a->bs == a->mr * a->mc) {
+        BMG_CUDA(cudaMemcpy(vals, a->vals.p, a->h_voff[a->nnzb] * sizeof(double), cudaMemcpyDeviceToHost));
+      } else {
+        const size_t w = (size_t)a->mr * a->mc * sizeof(double);
+        BMG_CUDA(cudaMemcpy2D(vals, w, a->vals.p, (size_t)a->bs * sizeof(double), w, a->nnzb,
+                              cudaMemcpyDeviceToHost));
+      }
+    }
+  });
+}
+int bmg_bsr_transpose(const bmg_bsr* ah, bmg_bsr** out) {
+  return guard([&] {
+    const Bsr* a = reinterpret_cast<const Bsr*>(ah);
+    a->ctx->activate();
+    *out = reinterpret_cast<bmg_bsr*>(bsr_transpose(*a).release());
+  });
+}
+
+int bmg_vec_create(bmg_ctx* ctx, int64_t n, bmg_vec** out) {
+  return guard([&] {
+    if (n < 0) fail(BMG_EINVAL, "bmg_vec_create: negative length");
+    Ctx* c = reinterpret_cast<Ctx*>(ctx);
+    c->activate();
+    auto v = std::make_unique<Vec>();
+    v->ctx = c;
+    v->n = n;
+    v->d.alloc(std::max<int64_t>(n, 1));
+    BMG_CUDA(cudaMemsetAsync(v->d.p, 0, v->d.bytes(), c->stream));
+    *out = reinterpret_cast<bmg_vec*>(v.release());
+  });
+}
+int bmg_vec_destroy(bmg_vec* v) {
+  return guard([&] { delete reinterpret_cast<Vec*>(v); });
+}
+int bmg_vec_upload(bmg_vec* vh, const double* host) {
+  return guard([&] {
+    Vec* v = reinterpret_cast<Vec*>(vh);
+    BMG_CUDA(cudaMemcpyAsync(v->d.p, host, v->n * sizeof(double), cudaMemcpyHostToDevice, v->ctx->stream));
+    BMG_CUDA(cudaStreamSynchronize(v->ctx->stream));
+  });
+}
+int bmg_vec_download(const bmg_vec* vh, double* host) {
+  return guard([&] {
+    const Vec* v = reinterpret_cast<const Vec*>(vh);
+    BMG_CUDA(cudaMemcpyAsync(host, v->d.p, v->n * sizeof(double), cudaMemcpyDeviceToHost, v->ctx->stream));
+    BMG_CUDA(cudaStreamSynchronize(v->ctx->stream));
+  });
+}
+int bmg_vec_fill(bmg_vec* vh, double value) {
+  return guard([&] {
+    Vec* v = reinterpret_cast<Vec*>(vh);
+    fill(v->ctx, v->d.p, v->n, value);
+  });
+}
+void* bmg_vec_device_ptr(bmg_vec* v) { return reinterpret_cast<Vec*>(v)->d.p; }
+int64_t bmg_vec_size(const bmg_vec* v) { return reinterpret_cast<const Vec*>(v)->n; }
+
+static void check_len(const Vec* v, int64_t n, const char* what) {
+  if (v->n != n) fail(BMG_EINVAL, std::string(what) + ": vector length does not match layout");
+}
+
+int bmg_spmv(const bmg_bsr* ah, const bmg_vec* xh, bmg_vec* yh) {
+  return guard([&] {
+    const Bsr* a = reinterpret_cast<const Bsr*>(ah);
+    const Vec* x = reinterpret_cast<const Vec*>(xh);
+    Vec* y = reinterpret_cast<Vec*>(yh);
+    check_len(x, a->dim_c, "spmv");
+    check_len(y, a->dim_r, "spmv");
+    spmv(*a, x->d.p, y->d.p);
+  });
+}
+int bmg_spmv_t(const bmg_bsr* ah, const bmg_vec* xh, bmg_vec* yh) {
+  return guard([&] {
+    const Bsr* a = reinterpret_cast<const Bsr*>(ah);
+    const Vec* x = reinterpret_cast<const Vec*>(xh);
+    Vec* y = reinterpret_cast<Vec*>(yh);
+    check_len(x, a->dim_r, "spmv_transpose");
+    check_len(y, a->dim_c, "spmv_transpose");
+    Bsr* mut = const_cast<Bsr*>(a);
+    if (!mut->tcache) mut->tcache = bsr_transpose(*a);
+    spmv(*mut->tcache, x->d.p, y->d.p);
+  });
+}
+int bmg_residual(const bmg_bsr* ah, const bmg_vec* bh, const bmg_vec* xh, bmg_vec* rh) {
+  return guard([&] {
+    const Bsr* a = reinterpret_cast<const Bsr*>(ah);
+    const Vec* b = reinterpret_cast<const Vec*>(bh);
+    const Vec* x = reinterpret_cast<const Vec*>(xh);
+    Vec* r = reinterpret_cast<Vec*>(rh);
+    check_len(x, a->dim_c, "residual");
+    check_len(b, a->dim_r, "residual");
+    check_len(r, a->dim_r, "residual");
+    residual(*a, b->d.p, x->d.p, r->d.p);
+  });
+}
+int bmg_dot(const bmg_vec* ah, const bmg_vec* bh, double* out) {
+  return guard([&] {
+    const Vec* a = reinterpret_cast<const Vec*>(ah);
+    const Vec* b = reinterpret_cast<const Vec*>(bh);
+    if (a->n != b->n) fail(BMG_EINVAL, "dot: length mismatch");
+    *out = dot(a->ctx, a->d.p, b->d.p, a->n);
+  });
+}
+
+int bmg_time_residual(const bmg_bsr* ah, const bmg_vec* bh, const bmg_vec* xh, bmg_vec* rh, int reps,
+                      double* ms) {
+  return guard([&] {
+    const Bsr* a = reinterpret_cast<const Bsr*>(ah);
+    const Vec* b = reinterpret_cast<const Vec*>(bh);
+    const Vec* x = reinterpret_cast<const Vec*>(xh);
+    Vec* r = reinterpret_cast<Vec*>(rh);
+    Ctx* c = a->ctx;
+    cudaEvent_t e0, e1;
+    BMG_CUDA(cudaEventCreate(&e0));
+    BMG_CUDA(cudaEventCreate(&e1));
+    residual(*a, b->d.p, x->d.p, r->d.p);  // warm
+    BMG_CUDA(cudaEventRecord(e0, c->stream));
+    for (int i = 0; i < reps; ++i) residual(*a, b->d.p, x->d.p, r->d.p);
+    BMG_CUDA(cudaEventRecord(e1, c->stream));
+    BMG_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    BMG_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    *ms = (double)t / std::max(reps, 1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  });
+}
+
+int bmg_gen_stencil(int dim, int n, int power, int m, uint64_t seed, double reg, int64_t* nnzb,
+                    int64_t* row_ptr, int32_t* col_idx, double* vals) {
+  return guard([&] { *nnzb = gen_stencil(dim, n, power, m, seed, reg, row_ptr, col_idx, vals); });
+}
+int bmg_gen_prolongation(int dim, int n_fine, int m, uint64_t seed, int level, int64_t* nnzb,
+                         int64_t* row_ptr, int32_t* col_idx, double* vals) {
+  return guard([&] { *nnzb = gen_prolongation(dim, n_fine, m, seed, level, row_ptr, col_idx, vals); });
+}
+int bmg_gen_normal(uint64_t seed, uint64_t tag, int64_t n, double* out) {
+  return guard([&] { gen_normal(seed, tag, n, out); });
+}
+
+}  // extern "C"

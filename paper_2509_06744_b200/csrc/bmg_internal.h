@@ -1,0 +1,162 @@
+// bmg_internal.h -- host-side object model behind the C ABI (include/bmg_cuda.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/bmg_cuda.h"
+
+namespace bmg {
+
+// ---- errors: C++ exceptions inside, status codes at the ABI -----------------
+struct Error : std::runtime_error {
+  int status;
+  int pivot;
+  Error(int s, const std::string& m, int p = -1) : std::runtime_error(m), status(s), pivot(p) {}
+};
+[[noreturn]] void fail(int status, const std::string& msg, int pivot = -1);
+void cuda_check(cudaError_t e, const char* what);
+#define BMG_CUDA(x) ::bmg::cuda_check((x), #x)
+
+// ---- device memory ------------------------------------------------------------
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  explicit DBuf(size_t count) { alloc(count); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) BMG_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+// ---- context ------------------------------------------------------------------
+struct Ctx {
+  int device = 0;
+  int sms = 148;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;
+  cusolverDnHandle_t solver = nullptr;
+  DBuf<double> red;          // reduction partials
+  double* h_red = nullptr;   // pinned result slot(s)
+  void activate() const { BMG_CUDA(cudaSetDevice(device)); }
+  void count(int n = 1) { launches += n; }
+  cusolverDnHandle_t cusolver();
+  ~Ctx();
+};
+
+// ---- streaming plan (see bsr_stream.cuh) --------------------------------------
+struct Plan {
+  int cb_max = 0;        // blocks per chunk
+  int rmax = 0;          // max rows per chunk
+  int nctas = 0;
+  int nchunks = 0;
+  size_t smem = 0;
+  DBuf<int4> chunks;     // {blk_lo, nblk, row_lo, nrows | carry flags}
+  DBuf<int> cta_chunk;   // [nctas + 1]
+};
+
+// ---- block-sparse matrix on the device ----------------------------------------
+// Uniform layouts (every block m_r x m_c) store blocks row-major with a padded
+// stride bs = m_r*m_c rounded up to even (16-byte aligned blocks), streamed by
+// the sm_100a bulk-copy kernel.  Variable layouts use per-block value offsets
+// and a warp-per-block-row kernel.
+struct Bsr {
+  Ctx* ctx = nullptr;
+  int nbr = 0, nbc = 0;
+  std::vector<int> rsz, csz, roff, coff;  // host layouts
+  int dim_r = 0, dim_c = 0;
+  bool uniform = false;
+  int mr = 0, mc = 0, bs = 0;  // uniform sizes / padded stride (doubles)
+  int64_t nnzb = 0;
+  bool sym = false;
+  std::vector<int64_t> h_row_ptr;
+  std::vector<int32_t> h_col;
+  std::vector<int64_t> h_voff;  // value offsets (unpadded for variable; padded for uniform)
+  DBuf<int64_t> row_ptr;
+  DBuf<int32_t> col;            // nnzb + 4 (bulk-copy padding)
+  DBuf<double> vals;
+  DBuf<int64_t> voff;           // variable layouts only
+  DBuf<int> d_roff, d_coff, d_rsz, d_csz;
+  Plan plan;
+  std::unique_ptr<Bsr> tcache;  // device transpose (spmv_t)
+  int64_t pass_bytes() const;
+  int64_t device_bytes() const;
+};
+
+struct Vec {
+  Ctx* ctx = nullptr;
+  int64_t n = 0;
+  DBuf<double> d;
+};
+
+// M = G^T G with G = L-hat^{-1} F-hat; `fwd` holds the forward factors applied
+// in order (one for nest = 0: G itself), `bwd` their transposes (reverse order).
+struct Fsai {
+  Ctx* ctx = nullptr;
+  int dim = 0;
+  std::vector<std::unique_ptr<Bsr>> fwd, bwd;
+  const Bsr& G() const { return *fwd.back(); }
+};
+
+// ---- uploads / construction -------------------------------------------------
+std::unique_ptr<Bsr> make_bsr(Ctx* ctx, int nbr, const int* rsz, int nbc, const int* csz,
+                              const int64_t* row_ptr, const int32_t* col, const double* vals,
+                              bool sym, bool vals_on_device = false);
+// same structure, values already on the device in padded layout
+std::unique_ptr<Bsr> make_bsr_structure(Ctx* ctx, int nbr, const int* rsz, int nbc, const int* csz,
+                                        std::vector<int64_t> row_ptr, std::vector<int32_t> col,
+                                        bool sym);
+std::unique_ptr<Bsr> bsr_transpose(const Bsr& a);
+void build_plan(Bsr& a);
+
+// ---- device operations (all enqueue on ctx->stream) --------------------------
+void spmv(const Bsr& a, const double* x, double* y);
+void residual(const Bsr& a, const double* b, const double* x, double* r);
+void prolong_add(const Bsr& a, const double* e, double* x);
+// z = G^T w fused with the fourth-kind update: p = first ? z : mu2 p + z;
+// x = (xzero ? 0 : x) + dmu p
+void gt_cheb(const Bsr& gt, const double* w, double* p, double* x, double mu2, double dmu,
+             bool first, bool xzero);
+double dot(Ctx* ctx, const double* a, const double* b, int64_t n);
+void fill(Ctx* ctx, double* p, int64_t n, double v);
+void copy(Ctx* ctx, double* dst, const double* src, int64_t n);
+void fsai_apply(const Fsai& m, const double* r, double* z, double* tmp1, double* tmp2);
+std::unique_ptr<Fsai> fsai_build(const Bsr& a, int kind, int t_max, double tau, int nest);
+std::unique_ptr<Fsai> fsai_from_factors(Ctx* ctx, const Bsr& F, const double* shat_l_packed);
+double lanczos_lambda_max(const Bsr& a, const Fsai& m, int iters, double safety, uint64_t seed);
+std::unique_ptr<Bsr> galerkin(const Bsr& a, const Bsr& p);
+
+// host helpers
+std::vector<double> tridiag_eigenvalues(std::vector<double> d, std::vector<double> e);
+
+// generator (generator.cpp)
+int64_t gen_stencil(int dim, int n, int power, int m, uint64_t seed, double reg, int64_t* row_ptr,
+                    int32_t* col_idx, double* vals);
+int64_t gen_prolongation(int dim, int n_fine, int m, uint64_t seed, int level, int64_t* row_ptr,
+                         int32_t* col_idx, double* vals);
+void gen_normal(uint64_t seed, uint64_t tag, int64_t n, double* out);
+
+}  // namespace bmg

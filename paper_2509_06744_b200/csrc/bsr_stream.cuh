@@ -1,0 +1,305 @@
+// bsr_stream.cuh -- the sm_100a block-sparse streaming kernel and its epilogues.
+//
+// One kernel shape serves every pass of the V-cycle:
+//   y = A x                      spmv            (kernels.cpp:39-47)
+//   r = b - A x                  residual        (chebyshev.hpp:55-56, multilevel.cpp:91-93)
+//   w = G r                      FSAI first half (fsai.cpp:203-211, with S-hat folded into G)
+//   z = G^T w; p, x update       FSAI second half + Chebyshev (fsai.cpp:212-215,
+//                                                   chebyshev.hpp:57-59,63-66)
+//   rc = R r  (R = P^T)          restriction     (multilevel.cpp:95)
+//   x += P e                     prolongation    (multilevel.cpp:98-100)
+//
+// Design (uniform block sizes, the BASELINE configs):
+//   * The host plan (build_plan) gives each CTA a contiguous range of block rows
+//     balanced by blocks; the rows' value span is contiguous in HBM and is cut
+//     into chunks of cb_max blocks (rows may straddle chunks; a per-CTA carry
+//     holds the partial row sum).
+//   * One producer thread streams chunks into a 4-stage shared-memory ring with
+//     cp.async.bulk (TMA bulk copy, mbarrier complete_tx): values and the
+//     chunk's column indices.  HBM sees large sequential transfers; nothing is
+//     re-read.
+//   * Consumers (4 warps) compute per-(block, scalar row) dot products from
+//     shared memory against x gathered through L2 (phase A), release the
+//     stage, then sum each row's partials in ascending block order and run the
+//     fused epilogue with coalesced vector traffic (phase B).
+//   * Arithmetic order matches the oracle exactly: t = fma-chain over columns
+//     from 0.0, then y += t per block in ascending column order, so results
+//     are bitwise identical to oracle/bmg_oracle.cpp spmv.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace bmg {
+namespace kern {
+
+constexpr int kStages = 4;
+constexpr int kConsumerWarps = 4;
+constexpr int kConsumers = kConsumerWarps * 32;
+constexpr int kThreads = kConsumers + 32;
+constexpr unsigned kCarryIn = 1u << 30;
+constexpr unsigned kCarryOut = 1u << 31;
+constexpr unsigned kRowMask = kCarryIn - 1;
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void consumer_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+}
+
+// ---------------------------------------------------------------- epilogues
+// Each epilogue receives the scalar output index and the finished row sum y.
+struct EpiStore {
+  double* y;
+  __device__ __forceinline__ void operator()(int64_t i, double v) const { y[i] = v; }
+};
+struct EpiResidual {  // r = b - A x
+  const double* b;
+  double* r;
+  __device__ __forceinline__ void operator()(int64_t i, double v) const { r[i] = __dsub_rn(b[i], v); }
+};
+struct EpiAdd {  // x += P e
+  double* x;
+  __device__ __forceinline__ void operator()(int64_t i, double v) const { x[i] = __dadd_rn(x[i], v); }
+};
+// z = G^T w; p = first ? z : (mu*mu) p + z; x += (d*mu) p   (chebyshev.hpp:57-59,63-66)
+struct EpiCheb {
+  double* p;
+  double* x;
+  double mu2, dmu;
+  int first, xzero;
+  __device__ __forceinline__ void operator()(int64_t i, double z) const {
+    const double pn = first ? z : __dadd_rn(__dmul_rn(mu2, p[i]), z);
+    p[i] = pn;
+    const double inc = __dmul_rn(dmu, pn);
+    x[i] = xzero ? inc : __dadd_rn(x[i], inc);
+  }
+};
+
+struct StreamArgs {
+  const double* vals;
+  const int32_t* col;
+  const int64_t* row_ptr;
+  const int4* chunks;
+  const int* cta_chunk;
+  const double* x;
+  int bs;      // padded block stride (doubles)
+  int cb_max;  // blocks per chunk
+  int rmax;    // rows per chunk
+};
+
+struct SmemLayout {
+  uint32_t vals, cols, part, rp, carry, bars, total;
+  __host__ __device__ SmemLayout(int bs, int cb_max, int rmax, int mr) {
+    uint32_t o = 0;
+    auto al = [](uint32_t v, uint32_t a) { return (v + a - 1) / a * a; };
+    vals = o;
+    o += al((uint32_t)kStages * cb_max * bs * 8, 128);
+    cols = o;
+    o += al((uint32_t)kStages * (cb_max + 8) * 4, 128);
+    part = o;
+    o += al((uint32_t)cb_max * mr * 8, 16);
+    rp = o;
+    o += al((uint32_t)(rmax + 1) * 8, 16);
+    carry = o;
+    o += al((uint32_t)mr * 8, 16);
+    bars = o;
+    o += 2 * kStages * 8;
+    total = al(o, 128);
+  }
+};
+
+template <int MR, int MC, class Epi>
+__global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi epi) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const SmemLayout L(s.bs, s.cb_max, s.rmax, MR);
+  double* vals_s = reinterpret_cast<double*>(smem + L.vals);
+  int* cols_s = reinterpret_cast<int*>(smem + L.cols);
+  double* part = reinterpret_cast<double*>(smem + L.part);
+  int64_t* rp_s = reinterpret_cast<int64_t*>(smem + L.rp);
+  double* carry = reinterpret_cast<double*>(smem + L.carry);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
+  uint64_t* empty = full + kStages;
+
+  const int c0 = s.cta_chunk[blockIdx.x];
+  const int c1 = s.cta_chunk[blockIdx.x + 1];
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  const int stage_vals = s.cb_max * s.bs;
+  const int stage_cols = s.cb_max + 8;
+
+  if (tid >= kConsumers) {
+    // ------------------------------------------------------------ producer
+    if (tid == kConsumers) {
+      for (int c = c0, it = 0; c < c1; ++c, ++it) {
+        const int st = it % kStages;
+        if (it >= kStages) mbar_wait(&empty[st], ((it / kStages) - 1) & 1);
+        const int4 d = s.chunks[c];
+        if (d.y == 0) {
+          mbar_arrive_expect_tx(&full[st], 0);
+          continue;
+        }
+        const uint32_t vbytes = (uint32_t)d.y * (uint32_t)s.bs * 8u;
+        const int cl = d.x & ~3;
+        const int ch = (d.x + d.y + 3) & ~3;
+        const uint32_t cbytes = (uint32_t)(ch - cl) * 4u;
+        mbar_arrive_expect_tx(&full[st], vbytes + cbytes);
+        bulk_g2s(vals_s + (size_t)st * stage_vals, s.vals + (int64_t)d.x * s.bs, vbytes, &full[st]);
+        bulk_g2s(cols_s + st * stage_cols, s.col + cl, cbytes, &full[st]);
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  for (int c = c0, it = 0; c < c1; ++c, ++it) {
+    const int st = it % kStages;
+    const int4 d = s.chunks[c];
+    const int nrows = (int)((unsigned)d.w & kRowMask);
+    const bool cin = ((unsigned)d.w & kCarryIn) != 0;
+    const bool cout = ((unsigned)d.w & kCarryOut) != 0;
+    if (tid <= nrows) rp_s[tid] = s.row_ptr[d.z + tid];
+    mbar_wait(&full[st], (it / kStages) & 1);
+
+    // phase A: partial dot products per (block, scalar row)
+    const double* vs = vals_s + (size_t)st * stage_vals;
+    const int* cs = cols_s + st * stage_cols + (d.x & 3);
+    const int items = d.y * MR;
+    for (int item = tid; item < items; item += kConsumers) {
+      const int b = item / MR;
+      const int r = item - b * MR;
+      const int j = cs[b];
+      const double* __restrict__ xj = s.x + (int64_t)j * MC;
+      const double* a = vs + b * s.bs + r * MC;
+      double xv[MC];
+      if constexpr (MC % 2 == 0) {
+#pragma unroll
+        for (int q = 0; q < MC / 2; ++q) {
+          const double2 t2 = __ldg(reinterpret_cast<const double2*>(xj) + q);
+          xv[2 * q] = t2.x;
+          xv[2 * q + 1] = t2.y;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < MC; ++q) xv[q] = __ldg(xj + q);
+      }
+      double t = 0.0;
+      if constexpr (MC % 2 == 0) {
+#pragma unroll
+        for (int q = 0; q < MC / 2; ++q) {
+          const double2 a2 = reinterpret_cast<const double2*>(a)[q];
+          t = __fma_rn(a2.x, xv[2 * q], t);
+          t = __fma_rn(a2.y, xv[2 * q + 1], t);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < MC; ++q) t = __fma_rn(a[q], xv[q], t);
+      }
+      part[item] = t;
+    }
+    consumer_bar();
+    if (tid == 0) mbar_arrive(&empty[st]);
+
+    // phase B: ordered row sums + fused epilogue
+    const int ritems = nrows * MR;
+    for (int item = tid; item < ritems; item += kConsumers) {
+      const int rr = item / MR;
+      const int r = item - rr * MR;
+      const int64_t lo = max(rp_s[rr], (int64_t)d.x);
+      const int64_t hi = min(rp_s[rr + 1], (int64_t)(d.x + d.y));
+      double acc = (rr == 0 && cin) ? carry[r] : 0.0;
+      for (int64_t b = lo; b < hi; ++b) acc = __dadd_rn(acc, part[(int)(b - d.x) * MR + r]);
+      if (rr == nrows - 1 && cout)
+        carry[r] = acc;
+      else
+        epi((int64_t)(d.z + rr) * MR + r, acc);
+    }
+    consumer_bar();
+  }
+}
+
+// ------------------------------------------------------ variable block sizes
+// Warp per block row, lane per scalar row (looping for m_i > 32); same
+// arithmetic order as the streaming kernel and the oracle.
+struct VarArgs {
+  const double* vals;
+  const int32_t* col;
+  const int64_t* row_ptr;
+  const int64_t* voff;
+  const int* roff;
+  const int* rsz;
+  const int* coff;
+  const int* csz;
+  const double* x;
+  int nbr;
+};
+
+template <class Epi>
+__global__ void __launch_bounds__(256) bsr_var_kernel(VarArgs s, Epi epi) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= s.nbr) return;
+  const int mi = s.rsz[warp];
+  const int64_t b0 = s.row_ptr[warp], b1 = s.row_ptr[warp + 1];
+  for (int r0 = 0; r0 < mi; r0 += 32) {
+    const int r = r0 + lane;
+    double acc = 0.0;
+    for (int64_t b = b0; b < b1; ++b) {
+      const int j = s.col[b];
+      const int mj = s.csz[j];
+      const double* xj = s.x + s.coff[j];
+      const double* a = s.vals + s.voff[b];
+      if (r < mi) {
+        double t = 0.0;
+        for (int q = 0; q < mj; ++q) t = __fma_rn(a[(int64_t)r * mj + q], __ldg(xj + q), t);
+        acc = __dadd_rn(acc, t);
+      }
+    }
+    if (r < mi) epi((int64_t)s.roff[warp] + r, acc);
+  }
+}
+
+}  // namespace kern
+}  // namespace bmg

@@ -1,0 +1,94 @@
+"""Synthetic BASELINE problems (BASELINE.json configs).
+
+The generator itself is host C++ inside libbmgcuda.so (csrc/generator.cpp); this
+module only sizes the arrays and names the configs.  Inputs are data, not the
+solver path: the reference's PUM discretiser is out of scope.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .api import HostBsr
+from .native import check, dptr, i32ptr, i64ptr, lib
+
+
+@dataclass
+class Config:
+    name: str
+    dim: int
+    n: int          # patches per direction on the finest grid
+    power: int      # S_p = L_D^p
+    m: int          # block size
+    levels: int     # hierarchy depth (1 = single level)
+    fsai: str       # "static" | "adaptive" | "nested"
+    k: int          # Chebyshev degree per smoothing
+    nest: int = 0
+    seed: int = 0
+    reg: float = 0.01
+    tol: float = 1e-8
+    notes: str = ""
+    extra: dict = field(default_factory=dict)
+
+    def scaled(self, n: int, levels: int | None = None) -> "Config":
+        return Config(self.name + f"@{n}", self.dim, n, self.power, self.m,
+                      self.levels if levels is None else levels, self.fsai, self.k, self.nest,
+                      self.seed, self.reg, self.tol, self.notes)
+
+    @property
+    def unit(self) -> str:
+        return "smoother applications/s" if self.levels == 1 else "V-cycles/s"
+
+
+CONFIGS = {
+    "C1": Config("C1", 2, 64, 2, 10, 1, "static", 3, notes="single-level smoothing, 13-pt"),
+    "C2": Config("C2", 2, 256, 2, 10, 4, "adaptive", 3, notes="4-level V(3,3)"),
+    "C3": Config("C3", 2, 1024, 3, 21, 5, "nested", 4, nest=1, notes="25-pt triharmonic, V(4,4)"),
+    "C4": Config("C4", 3, 64, 2, 20, 4, "adaptive", 3, notes="3-D 25-pt, V(3,3)"),
+    "C5": Config("C5", 2, 2048, 2, 15, 6, "adaptive", 3, notes="strong scaling, V(3,3)"),
+}
+
+
+def stencil_matrix(dim: int, n: int, power: int, m: int, seed: int = 0, reg: float = 0.01) -> HostBsr:
+    """A = S_p (x) C + reg blockdiag(D_i) on an n^dim patch grid."""
+    nnzb = C.c_int64()
+    check(lib().bmg_gen_stencil(dim, n, power, m, seed, reg, C.byref(nnzb), None, None, None))
+    nodes = n ** dim
+    rp = np.zeros(nodes + 1, np.int64)
+    ci = np.zeros(nnzb.value, np.int32)
+    vals = np.zeros(nnzb.value * m * m)
+    check(lib().bmg_gen_stencil(dim, n, power, m, seed, reg, C.byref(nnzb), i64ptr(rp), i32ptr(ci), dptr(vals)))
+    sizes = np.full(nodes, m, np.int32)
+    return HostBsr(sizes, sizes, rp, ci, vals, symmetric=True)
+
+
+def prolongation(dim: int, n_fine: int, m: int, seed: int = 0, level: int = 1) -> HostBsr:
+    nnzb = C.c_int64()
+    check(lib().bmg_gen_prolongation(dim, n_fine, m, seed, level, C.byref(nnzb), None, None, None))
+    nf = n_fine ** dim
+    nc = (n_fine // 2) ** dim
+    rp = np.zeros(nf + 1, np.int64)
+    ci = np.zeros(nnzb.value, np.int32)
+    vals = np.zeros(nnzb.value * m * m)
+    check(lib().bmg_gen_prolongation(dim, n_fine, m, seed, level, C.byref(nnzb), i64ptr(rp), i32ptr(ci),
+                                     dptr(vals)))
+    return HostBsr(np.full(nf, m, np.int32), np.full(nc, m, np.int32), rp, ci, vals, symmetric=False)
+
+
+def normal_vector(n: int, seed: int = 0, tag: int = 0) -> np.ndarray:
+    out = np.zeros(n)
+    check(lib().bmg_gen_normal(seed, tag, n, dptr(out)))
+    return out
+
+
+def make_problem(cfg: Config):
+    """Finest A, transfers (transfers[l-1] prolongates level l-1 -> l) and b."""
+    A = stencil_matrix(cfg.dim, cfg.n, cfg.power, cfg.m, cfg.seed, cfg.reg)
+    transfers = []
+    for l in range(1, cfg.levels):
+        n_l = cfg.n >> (cfg.levels - 1 - l)
+        transfers.append(prolongation(cfg.dim, n_l, cfg.m, cfg.seed, l))
+    b = normal_vector(A.dim_r, cfg.seed, 0)
+    return A, transfers, b
