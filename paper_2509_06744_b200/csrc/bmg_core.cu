@@ -21,6 +21,18 @@ void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) fail(BMG_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+void debug_sync(cudaStream_t s, const char* what) {
+  static const bool on = [] {
+    const char* e = std::getenv("BMG_DEBUG_SYNC");
+    return e && e[0] == '1';
+  }();
+  cuda_check(cudaGetLastError(), what);
+  if (!on) return;
+  cudaStreamCaptureStatus cs;
+  if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) return;
+  cuda_check(cudaStreamSynchronize(s), what);
+}
+
 thread_local std::string g_last_error;
 thread_local int g_last_pivot = -1;
 
@@ -429,28 +441,27 @@ static void launch_stream_t(const Bsr& a, const double* x, Epi epi) {
   s.bs = a.bs;
   s.cb_max = a.plan.cb_max;
   s.rmax = a.plan.rmax;
+  // one attribute per template instantiation (covers the largest plan)
+  static bool attr_set = false;
+  if (!attr_set) {
+    BMG_CUDA(cudaFuncSetAttribute(kern::bsr_stream_kernel<MR, MC, Epi>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr_set = true;
+  }
   kern::bsr_stream_kernel<MR, MC, Epi><<<a.plan.nctas, kern::kThreads, a.plan.smem, a.ctx->stream>>>(s, epi);
   a.ctx->count();
-  BMG_CUDA(cudaGetLastError());
+  BMG_LAUNCHED(a.ctx->stream, "bsr_stream_kernel");
 }
 
 template <class Epi>
 static void launch(const Bsr& a, const double* x, Epi epi) {
   if (a.nbr == 0) return;
   if (a.uniform && stream_supported(a.mr, a.mc)) {
-    // make sure the dynamic smem attribute covers this epilogue's instantiation
-    auto set = [&](auto kfn) {
-      static thread_local size_t done = 0;
-      if (done < a.plan.smem) {
-        BMG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        done = 227 * 1024;
-      }
-    };
     switch (a.mr) {
-      case 10: set(kern::bsr_stream_kernel<10, 10, Epi>); return launch_stream_t<10, 10>(a, x, epi);
-      case 15: set(kern::bsr_stream_kernel<15, 15, Epi>); return launch_stream_t<15, 15>(a, x, epi);
-      case 20: set(kern::bsr_stream_kernel<20, 20, Epi>); return launch_stream_t<20, 20>(a, x, epi);
-      case 21: set(kern::bsr_stream_kernel<21, 21, Epi>); return launch_stream_t<21, 21>(a, x, epi);
+      case 10: return launch_stream_t<10, 10>(a, x, epi);
+      case 15: return launch_stream_t<15, 15>(a, x, epi);
+      case 20: return launch_stream_t<20, 20>(a, x, epi);
+      case 21: return launch_stream_t<21, 21>(a, x, epi);
     }
   }
   kern::VarArgs s;
@@ -467,7 +478,7 @@ static void launch(const Bsr& a, const double* x, Epi epi) {
   const int blocks = (int)(((int64_t)a.nbr * 32 + 255) / 256);
   kern::bsr_var_kernel<Epi><<<blocks, 256, 0, a.ctx->stream>>>(s, epi);
   a.ctx->count();
-  BMG_CUDA(cudaGetLastError());
+  BMG_LAUNCHED(a.ctx->stream, "bsr_var_kernel");
 }
 
 void spmv(const Bsr& a, const double* x, double* y) { launch(a, x, kern::EpiStore{y}); }
@@ -503,13 +514,19 @@ int bmg_ctx_create(int device, bmg_ctx** out) {
     BMG_CUDA(cudaGetDeviceProperties(&prop, device));
     if (prop.major < 10) fail(BMG_ECUDA, "libbmgcuda requires an sm_100 (Blackwell) device");
     c->sms = prop.multiProcessorCount;
-    BMG_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+    // a blocking stream: setup-time cudaMemcpy/cudaMemset on the legacy stream are
+    // ordered with the kernels launched here
+    BMG_CUDA(cudaStreamCreate(&c->own));
     c->stream = c->own;
     *out = reinterpret_cast<bmg_ctx*>(c.release());
   });
 }
 int bmg_ctx_destroy(bmg_ctx* ctx) {
-  return guard([&] { delete reinterpret_cast<Ctx*>(ctx); });
+  return guard([&] {
+    Ctx* c = reinterpret_cast<Ctx*>(ctx);
+    if (c) BMG_CUDA(cudaStreamSynchronize(c->stream));
+    delete c;
+  });
 }
 int bmg_ctx_set_stream(bmg_ctx* ctx, void* s) {
   return guard([&] {
@@ -532,8 +549,14 @@ int bmg_bsr_create(bmg_ctx* ctx, int nbr, const int32_t* row_sizes, int nbc, con
     *out = reinterpret_cast<bmg_bsr*>(a.release());
   });
 }
+// destroying an object first drains its context stream: queued work may still
+// reference it (device objects follow CUDA's asynchronous semantics)
 int bmg_bsr_destroy(bmg_bsr* a) {
-  return guard([&] { delete reinterpret_cast<Bsr*>(a); });
+  return guard([&] {
+    Bsr* m = reinterpret_cast<Bsr*>(a);
+    if (m) BMG_CUDA(cudaStreamSynchronize(m->ctx->stream));
+    delete m;
+  });
 }
 int bmg_bsr_info(const bmg_bsr* ah, int* nbr, int* nbc, int64_t* nnzb, int* dim_r, int* dim_c,
                  int64_t* device_bytes, int64_t* pass_bytes) {
@@ -588,7 +611,11 @@ int bmg_vec_create(bmg_ctx* ctx, int64_t n, bmg_vec** out) {
   });
 }
 int bmg_vec_destroy(bmg_vec* v) {
-  return guard([&] { delete reinterpret_cast<Vec*>(v); });
+  return guard([&] {
+    Vec* p = reinterpret_cast<Vec*>(v);
+    if (p) BMG_CUDA(cudaStreamSynchronize(p->ctx->stream));
+    delete p;
+  });
 }
 int bmg_vec_upload(bmg_vec* vh, const double* host) {
   return guard([&] {

@@ -22,6 +22,9 @@ struct Error : std::runtime_error {
 [[noreturn]] void fail(int status, const std::string& msg, int pivot = -1);
 void cuda_check(cudaError_t e, const char* what);
 #define BMG_CUDA(x) ::bmg::cuda_check((x), #x)
+// BMG_DEBUG_SYNC=1: synchronise and check after every launch (fault localisation)
+void debug_sync(cudaStream_t s, const char* what);
+#define BMG_LAUNCHED(stream, what) ::bmg::debug_sync((stream), (what))
 
 // ---- device memory ------------------------------------------------------------
 template <class T>

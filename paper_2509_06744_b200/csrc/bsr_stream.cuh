@@ -122,6 +122,10 @@ struct StreamArgs {
   int rmax;    // rows per chunk
 };
 
+// column-index slots per stage: cb_max + 8, rounded to 16 bytes (bulk-copy
+// destinations must be 16-byte aligned)
+__host__ __device__ inline int stage_cols_of(int cb_max) { return (cb_max + 8 + 3) & ~3; }
+
 struct SmemLayout {
   uint32_t vals, cols, part, rp, carry, bars, total;
   __host__ __device__ SmemLayout(int bs, int cb_max, int rmax, int mr) {
@@ -130,7 +134,7 @@ struct SmemLayout {
     vals = o;
     o += al((uint32_t)kStages * cb_max * bs * 8, 128);
     cols = o;
-    o += al((uint32_t)kStages * (cb_max + 8) * 4, 128);
+    o += al((uint32_t)kStages * stage_cols_of(cb_max) * 4, 128);
     part = o;
     o += al((uint32_t)cb_max * mr * 8, 16);
     rp = o;
@@ -168,7 +172,7 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
   __syncthreads();
 
   const int stage_vals = s.cb_max * s.bs;
-  const int stage_cols = s.cb_max + 8;
+  const int stage_cols = stage_cols_of(s.cb_max);
 
   if (tid >= kConsumers) {
     // ------------------------------------------------------------ producer

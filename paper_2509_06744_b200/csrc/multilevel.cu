@@ -549,7 +549,7 @@ static void enqueue_vcycle(Hier& h, int kpre, int kpost, const double* bf, doubl
     const int64_t N = h.n0;
     kern::gemv_kernel<<<(int)((N * 32 + 255) / 256), 256, 0, ctx->stream>>>(h.ainv.p, B[0], X[0], N);
     ctx->count();
-    BMG_CUDA(cudaGetLastError());
+    BMG_LAUNCHED(ctx->stream, "gemv_kernel");
   }
   for (int l = 1; l <= top; ++l) {
     Level& L = h.lv[l];
@@ -650,7 +650,11 @@ int bmg_fsai_from_factors(bmg_ctx* ctx, const bmg_bsr* F, const double* shat, bm
   });
 }
 int bmg_fsai_destroy(bmg_fsai* m) {
-  return guard([&] { delete reinterpret_cast<Fsai*>(m); });
+  return guard([&] {
+    Fsai* f = reinterpret_cast<Fsai*>(m);
+    if (f) BMG_CUDA(cudaStreamSynchronize(f->ctx->stream));
+    delete f;
+  });
 }
 int bmg_fsai_apply(const bmg_fsai* mh, const bmg_vec* r, bmg_vec* z) {
   return guard([&] {
@@ -772,7 +776,11 @@ int bmg_hier_create(bmg_ctx* ctx, int nlevels, const bmg_bsr* const* A, const bm
 }
 
 int bmg_hier_destroy(bmg_hier* h) {
-  return guard([&] { delete reinterpret_cast<Hier*>(h); });
+  return guard([&] {
+    Hier* p = reinterpret_cast<Hier*>(h);
+    if (p) BMG_CUDA(cudaStreamSynchronize(p->ctx->stream));
+    delete p;
+  });
 }
 int bmg_hier_info(const bmg_hier* hh, int* nlevels, int64_t* device_bytes) {
   return guard([&] {
