@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""Benchmark: V-cycle application of the multilevel Chebyshev(4th kind) + block-FSAI
+solver (arXiv 2509.06744 hot path) on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+A step is one V(k,k) cycle on the finest level of the config's hierarchy with the
+inputs (hierarchy, b, x) resident in HBM.  Workload: config C2 (BASELINE.json
+configs[1]: 256^2 patches, m = 10, 4 levels, V(3,3), adaptive block-FSAI), the
+configs[1] case that fits one GPU; its per-cycle traffic (14+ GB) exceeds L2, so
+no explicit flush is needed between cycles.  For N > 1 every rank runs its own
+replica (weak scaling, no data-path collective yet).
+
+One JSON line is printed by rank 0.  `--impl reference` times the CPU oracle
+(the restatement of the reference, which cannot be built here) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+HBM_FALLBACK = 6650.0
+
+
+def hbm_peak():
+    try:
+        with open(MEASURED_PEAKS) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK, "fallback"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        smax = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        under_load = [s for s in sm if s > 0.5 * (max(sm) if sm else 1)]
+        return {"sm_mhz": statistics.median(under_load) if under_load else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_info():
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return model
+
+
+# ------------------------------------------------------------------ CPU oracle arm
+def oracle_vcycles(cfg, steps, warmup, threads):
+    """Time V-cycles of the CPU oracle (restatement of the reference) on `threads`
+    host threads: setup untimed, then warmup + `steps` cycles timed by wall clock."""
+    from oracle import pyoracle as O
+    from paper_2509_06744_b200 import problems as pr
+
+    O.set_threads(threads)
+    A, T, b = pr.make_problem(cfg)
+    t0 = time.perf_counter()
+    H = O.Hierarchy(O.Mat(A), [O.Mat(p) for p in T], t_max=1, tau=1.0, nest=cfg.nest,
+                    fsai_kind=0 if cfg.fsai == "static" else 3, coarse_dim_cap=1 << 30, probe=False)
+    setup_s = time.perf_counter() - t0
+    x = np.zeros_like(b)
+    for _ in range(warmup):
+        x = H.v_cycle(cfg.k, cfg.k, b, x)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        x = H.v_cycle(cfg.k, cfg.k, b, x)
+    dt = time.perf_counter() - t0
+    return steps / dt, setup_s, dt
+
+
+def run_reference(args, cfg):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    steps = max(1, args.steps)
+    warm = max(0, min(args.warmup, 3))
+    rate, setup_s, dt = oracle_vcycles(cfg, steps, warm, threads)
+    unit = "V-cycles/s"
+    line = {
+        "impl": "reference",
+        "metric": f"V-cycles/s ({cfg.name}, V({cfg.k},{cfg.k}))",
+        "value": rate, "unit": unit, "n_gpus": args.gpus, "steps": steps, "warmup": warm,
+        "ms_per_step": 1e3 * dt / steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE.md §3 generator, seed 0)",
+        "config": {"workload": f"{cfg.name}: {cfg.n}^{cfg.dim} patches, m={cfg.m}, {cfg.levels} levels, "
+                               f"V({cfg.k},{cfg.k}), {cfg.fsai} block-FSAI t_max=1"},
+        "cpu_baseline": {"value": rate, "unit": unit, "cores": threads, "kind": "port",
+                         "sample": f"{steps} V-cycles of the C++ oracle (reference restatement; the reference "
+                                   f"itself needs Eigen3, absent) after {setup_s:.0f}s untimed setup; "
+                                   f"CPU {cpu_info()}"},
+        "e2e": {"value": rate, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2509_06744_b200 import BlockSparseMatrix, Context, Hierarchy, Vector, default_params, residual
+    from paper_2509_06744_b200 import problems as pr
+
+    ctx = Context(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+
+    A, T, b = pr.make_problem(cfg)
+    dA = BlockSparseMatrix(ctx, A)
+    dT = [BlockSparseMatrix(ctx, p) for p in T]
+    t0 = time.perf_counter()
+    params = default_params(t_max=1, tau=1.0, nest=cfg.nest, coarse_dim_cap=1 << 30,
+                            fsai_kind=0 if cfg.fsai == "static" else 3)
+    H = Hierarchy.setup(dA, dT, params)
+    ctx.sync()
+    setup_s = time.perf_counter() - t0
+    n = A.dim_r
+    bv = Vector(ctx, b)
+    xv = Vector(ctx, n)
+    k = cfg.k
+
+    for _ in range(max(args.warmup, 3)):
+        H.v_cycle(k, k, bv, xv)
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.launch_count
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        H.v_cycle(k, k, bv, xv)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    launches = ctx.launch_count - launches0
+    ms = e0.elapsed_time(e1)
+    if ws > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per = ms / args.steps
+    rate = ws * args.steps / (ms / 1e3)
+    cycle_bytes = H.cycle_bytes(k, k)
+    peak, peak_kind = hbm_peak()
+    eff_gbs = cycle_bytes / (ms_per / 1e3) / 1e9
+
+    # ---- dominant kernel: finest-level residual pass r = b - A x (2k+1 per cycle)
+    Af, _, _ = H.level(H.levels - 1)
+    rv = Vector(ctx, n)
+    reps = 20
+    residual(Af, bv, xv, rv)
+    torch.cuda.synchronize()
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k0.record(stream)
+    for _ in range(reps):
+        residual(Af, bv, xv, rv)
+    k1.record(stream)
+    torch.cuda.synchronize()
+    kern_ms = k0.elapsed_time(k1) / reps
+    inf = Af.info()
+    kern_bytes = inf["pass_bytes"] + 24 * n
+    achieved = kern_bytes / (kern_ms / 1e3) / 1e9
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "latest_traffic.json")
+    if os.path.exists(tfile):
+        try:
+            with open(tfile) as f:
+                traffic = json.load(f).get("residual_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- e2e through the public C ABI with pinned host buffers
+    hb = torch.from_numpy(b).pin_memory()
+    hx = torch.zeros(n, dtype=torch.float64).pin_memory()
+    for _ in range(2):
+        H.v_cycle_host_ptr(k, k, hb.data_ptr(), hx.data_ptr())
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    q0.record(stream)
+    for _ in range(args.steps):
+        H.v_cycle_host_ptr(k, k, hb.data_ptr(), hx.data_ptr())
+    q1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = q0.elapsed_time(q1)
+    if ws > 1:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_rate = ws * args.steps / (e2e_ms / 1e3)
+
+    # ---- CPU baseline (rank 0, N = 1 only): bounded oracle sample
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        crate, csetup, cdt = oracle_vcycles(cfg, 2, 0, threads)
+        cpu = {"value": crate, "unit": "V-cycles/s", "cores": threads, "kind": "port",
+               "sample": f"2 V-cycles of the C++ oracle (reference restatement) on {cfg.name} after "
+                         f"{csetup:.0f}s untimed setup, {threads} OpenMP threads, CPU {cpu_info()}"}
+
+    if rank == 0:
+        line = {
+            "metric": f"V-cycles/s ({cfg.name}, V({k},{k}))",
+            "value": rate,
+            "unit": "V-cycles/s",
+            "n_gpus": ws,
+            "steps": args.steps,
+            "warmup": max(args.warmup, 3),
+            "ms_per_step": ms_per,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (BASELINE.md §3 generator, seed 0; random-init hierarchy built on the device)",
+            "config": {"workload": f"{cfg.name}: {cfg.n}^{cfg.dim} patches, m={cfg.m}, {cfg.levels} levels, "
+                                   f"V({k},{k}), {cfg.fsai} block-FSAI t_max=1",
+                       "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (>= 14 GB streamed per cycle)",
+                       "setup_s": round(setup_s, 2)},
+            "effective_gbs": eff_gbs,
+            "cycle_bytes": cycle_bytes,
+            "frac_of_roofline_cycle": eff_gbs / peak,
+            "roofline": {"bound": "hbm", "kernel": "bsr_stream_kernel<10,10,EpiResidual> (finest A, r = b - A x)",
+                         "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "bytes_per_launch": kern_bytes, "ms_per_launch": kern_ms},
+            "clocks": clocks,
+            "e2e": {"value": e2e_rate, "unit": "V-cycles/s", "h2d_bytes_per_step": 2 * 8 * n,
+                    "d2h_bytes_per_step": 8 * n},
+            "gpu_launches": launches,
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    from paper_2509_06744_b200 import problems as pr
+
+    cfg = pr.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -179,15 +179,19 @@ static bool stream_supported(int mr, int mc) {
   return mr == mc && (mr == 10 || mr == 15 || mr == 20 || mr == 21);
 }
 
-static int chunk_target_bytes() {
-  static int v = [] {
+// chunk size: about one phase-A item per consumer thread, capped by bytes so two
+// CTAs (4 stages each) fit per SM; BMG_CHUNK_KB overrides the byte cap
+static int chunk_blocks(int mr, int bs) {
+  static int cap = [] {
     const char* e = std::getenv("BMG_CHUNK_KB");
-    int kb = e ? std::atoi(e) : 16;
+    int kb = e ? std::atoi(e) : 24;
     if (kb < 2) kb = 2;
     if (kb > 48) kb = 48;
     return kb * 1024;
   }();
-  return v;
+  const int by_items = std::max(1, kern::kConsumers / mr);
+  const int by_bytes = std::max(1, cap / (bs * 8));
+  return std::min(by_items, by_bytes);
 }
 
 template <int MR, int MC>
@@ -215,8 +219,7 @@ void build_plan(Bsr& a) {
   Plan& P = a.plan;
   P = Plan();
   if (!(a.uniform && stream_supported(a.mr, a.mc)) || a.nbr == 0) return;
-  const int block_bytes = a.bs * 8;
-  P.cb_max = std::max(1, chunk_target_bytes() / block_bytes);
+  P.cb_max = chunk_blocks(a.mr, a.bs);
   const auto& rp = a.h_row_ptr;
   // chunk list per CTA range
   std::vector<int4> chunks;

@@ -34,7 +34,7 @@ namespace bmg {
 namespace kern {
 
 constexpr int kStages = 4;
-constexpr int kConsumerWarps = 4;
+constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = kConsumerWarps * 32;
 constexpr int kThreads = kConsumers + 32;
 constexpr unsigned kCarryIn = 1u << 30;
@@ -83,18 +83,30 @@ __device__ __forceinline__ void consumer_bar() {
 
 // ---------------------------------------------------------------- epilogues
 // Each epilogue receives the scalar output index and the finished row sum y.
+// load() issues the epilogue's own vector reads early (before the chunk's
+// matrix data has landed) so their latency hides behind phase A.
 struct EpiStore {
   double* y;
-  __device__ __forceinline__ void operator()(int64_t i, double v) const { y[i] = v; }
+  struct Pre {};
+  __device__ __forceinline__ Pre load(int64_t) const { return {}; }
+  __device__ __forceinline__ void store(int64_t i, double v, const Pre&) const { y[i] = v; }
 };
 struct EpiResidual {  // r = b - A x
   const double* b;
   double* r;
-  __device__ __forceinline__ void operator()(int64_t i, double v) const { r[i] = __dsub_rn(b[i], v); }
+  struct Pre {
+    double b;
+  };
+  __device__ __forceinline__ Pre load(int64_t i) const { return {__ldg(b + i)}; }
+  __device__ __forceinline__ void store(int64_t i, double v, const Pre& p) const { r[i] = __dsub_rn(p.b, v); }
 };
 struct EpiAdd {  // x += P e
   double* x;
-  __device__ __forceinline__ void operator()(int64_t i, double v) const { x[i] = __dadd_rn(x[i], v); }
+  struct Pre {
+    double x;
+  };
+  __device__ __forceinline__ Pre load(int64_t i) const { return {x[i]}; }
+  __device__ __forceinline__ void store(int64_t i, double v, const Pre& p) const { x[i] = __dadd_rn(p.x, v); }
 };
 // z = G^T w; p = first ? z : (mu*mu) p + z; x += (d*mu) p   (chebyshev.hpp:57-59,63-66)
 struct EpiCheb {
@@ -102,11 +114,17 @@ struct EpiCheb {
   double* x;
   double mu2, dmu;
   int first, xzero;
-  __device__ __forceinline__ void operator()(int64_t i, double z) const {
-    const double pn = first ? z : __dadd_rn(__dmul_rn(mu2, p[i]), z);
+  struct Pre {
+    double p, x;
+  };
+  __device__ __forceinline__ Pre load(int64_t i) const {
+    return {first ? 0.0 : p[i], xzero ? 0.0 : x[i]};
+  }
+  __device__ __forceinline__ void store(int64_t i, double z, const Pre& q) const {
+    const double pn = first ? z : __dadd_rn(__dmul_rn(mu2, q.p), z);
     p[i] = pn;
     const double inc = __dmul_rn(dmu, pn);
-    x[i] = xzero ? inc : __dadd_rn(x[i], inc);
+    x[i] = xzero ? inc : __dadd_rn(q.x, inc);
   }
 };
 
@@ -127,20 +145,19 @@ struct StreamArgs {
 __host__ __device__ inline int stage_cols_of(int cb_max) { return (cb_max + 8 + 3) & ~3; }
 
 struct SmemLayout {
-  uint32_t vals, cols, part, rp, carry, bars, total;
+  uint32_t vals, cols, part, carry, bars, total;
   __host__ __device__ SmemLayout(int bs, int cb_max, int rmax, int mr) {
     uint32_t o = 0;
     auto al = [](uint32_t v, uint32_t a) { return (v + a - 1) / a * a; };
+    (void)rmax;
     vals = o;
     o += al((uint32_t)kStages * cb_max * bs * 8, 128);
     cols = o;
     o += al((uint32_t)kStages * stage_cols_of(cb_max) * 4, 128);
-    part = o;
-    o += al((uint32_t)cb_max * mr * 8, 16);
-    rp = o;
-    o += al((uint32_t)(rmax + 1) * 8, 16);
-    carry = o;
-    o += al((uint32_t)mr * 8, 16);
+    part = o;  // double-buffered partial sums
+    o += al((uint32_t)2 * cb_max * mr * 8, 16);
+    carry = o;  // double-buffered row carry
+    o += al((uint32_t)2 * mr * 8, 16);
     bars = o;
     o += 2 * kStages * 8;
     total = al(o, 128);
@@ -153,9 +170,8 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
   const SmemLayout L(s.bs, s.cb_max, s.rmax, MR);
   double* vals_s = reinterpret_cast<double*>(smem + L.vals);
   int* cols_s = reinterpret_cast<int*>(smem + L.cols);
-  double* part = reinterpret_cast<double*>(smem + L.part);
-  int64_t* rp_s = reinterpret_cast<int64_t*>(smem + L.rp);
-  double* carry = reinterpret_cast<double*>(smem + L.carry);
+  double* part_s = reinterpret_cast<double*>(smem + L.part);
+  double* carry_s = reinterpret_cast<double*>(smem + L.carry);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
   uint64_t* empty = full + kStages;
 
@@ -198,13 +214,27 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
   }
 
   // -------------------------------------------------------------- consumers
+  // One named barrier per chunk: partial sums and the row carry are double
+  // buffered, so phase B of chunk c overlaps phase A of chunk c+1.
   for (int c = c0, it = 0; c < c1; ++c, ++it) {
     const int st = it % kStages;
+    const int pb = it & 1;
     const int4 d = s.chunks[c];
     const int nrows = (int)((unsigned)d.w & kRowMask);
     const bool cin = ((unsigned)d.w & kCarryIn) != 0;
     const bool cout = ((unsigned)d.w & kCarryOut) != 0;
-    if (tid <= nrows) rp_s[tid] = s.row_ptr[d.z + tid];
+    double* part = part_s + pb * s.cb_max * MR;
+
+    // early loads for this thread's first phase-B item (row bounds + epilogue inputs)
+    const int ritems = nrows * MR;
+    int64_t rlo0 = 0, rhi0 = 0;
+    typename Epi::Pre pre0{};
+    if (tid < ritems) {
+      const int rr = tid / MR;
+      rlo0 = __ldg(s.row_ptr + d.z + rr);
+      rhi0 = __ldg(s.row_ptr + d.z + rr + 1);
+      pre0 = epi.load((int64_t)(d.z + rr) * MR + (tid - rr * MR));
+    }
     mbar_wait(&full[st], (it / kStages) & 1);
 
     // phase A: partial dot products per (block, scalar row)
@@ -247,20 +277,27 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
     if (tid == 0) mbar_arrive(&empty[st]);
 
     // phase B: ordered row sums + fused epilogue
-    const int ritems = nrows * MR;
+    const double* carry_in = carry_s + (pb ^ 1) * MR;
+    double* carry_out = carry_s + pb * MR;
     for (int item = tid; item < ritems; item += kConsumers) {
       const int rr = item / MR;
       const int r = item - rr * MR;
-      const int64_t lo = max(rp_s[rr], (int64_t)d.x);
-      const int64_t hi = min(rp_s[rr + 1], (int64_t)(d.x + d.y));
-      double acc = (rr == 0 && cin) ? carry[r] : 0.0;
-      for (int64_t b = lo; b < hi; ++b) acc = __dadd_rn(acc, part[(int)(b - d.x) * MR + r]);
+      int64_t rlo = rlo0, rhi = rhi0;
+      typename Epi::Pre pre = pre0;
+      if (item != tid) {
+        rlo = __ldg(s.row_ptr + d.z + rr);
+        rhi = __ldg(s.row_ptr + d.z + rr + 1);
+        pre = epi.load((int64_t)(d.z + rr) * MR + r);
+      }
+      const int lo = (int)(max(rlo, (int64_t)d.x) - d.x);
+      const int hi = (int)(min(rhi, (int64_t)(d.x + d.y)) - d.x);
+      double acc = (rr == 0 && cin) ? carry_in[r] : 0.0;
+      for (int b = lo; b < hi; ++b) acc = __dadd_rn(acc, part[b * MR + r]);
       if (rr == nrows - 1 && cout)
-        carry[r] = acc;
+        carry_out[r] = acc;
       else
-        epi((int64_t)(d.z + rr) * MR + r, acc);
+        epi.store((int64_t)(d.z + rr) * MR + r, acc, pre);
     }
-    consumer_bar();
   }
 }
 
@@ -301,7 +338,10 @@ __global__ void __launch_bounds__(256) bsr_var_kernel(VarArgs s, Epi epi) {
         acc = __dadd_rn(acc, t);
       }
     }
-    if (r < mi) epi((int64_t)s.roff[warp] + r, acc);
+    if (r < mi) {
+      const int64_t i = (int64_t)s.roff[warp] + r;
+      epi.store(i, acc, epi.load(i));
+    }
   }
 }
 
