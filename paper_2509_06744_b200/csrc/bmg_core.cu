@@ -179,6 +179,15 @@ static bool stream_supported(int mr, int mc) {
   return mr == mc && (mr == 10 || mr == 15 || mr == 20 || mr == 21);
 }
 
+static int ring_stages() {
+  static int v = [] {
+    const char* e = std::getenv("BMG_STAGES");
+    int st = e ? std::atoi(e) : 2;
+    return std::max(2, std::min(st, kern::kMaxStages));
+  }();
+  return v;
+}
+
 // chunk size: about one phase-A item per consumer thread, capped by bytes so two
 // CTAs (4 stages each) fit per SM; BMG_CHUNK_KB overrides the byte cap
 static int chunk_blocks(int mr, int bs) {
@@ -220,13 +229,14 @@ void build_plan(Bsr& a) {
   P = Plan();
   if (!(a.uniform && stream_supported(a.mr, a.mc)) || a.nbr == 0) return;
   P.cb_max = chunk_blocks(a.mr, a.bs);
+  P.stages = ring_stages();
   const auto& rp = a.h_row_ptr;
   // chunk list per CTA range
   std::vector<int4> chunks;
   std::vector<int> cta;
   int rmax = 1;
   // first pass with a provisional rmax to size smem and query occupancy
-  const size_t smem0 = kern::SmemLayout(a.bs, P.cb_max, P.cb_max + 2, a.mr).total;
+  const size_t smem0 = kern::SmemLayout(a.bs, P.cb_max, P.cb_max + 2, a.mr, P.stages).total;
   const int occ = occupancy_for(a.mr, a.mc, smem0);
   const int64_t gmax = (int64_t)a.ctx->sms * occ;
   const int64_t per = std::max<int64_t>(1, (a.nnzb + gmax - 1) / gmax);
@@ -263,7 +273,7 @@ void build_plan(Bsr& a) {
   P.rmax = rmax;
   P.nctas = (int)cta.size() - 1;
   P.nchunks = (int)chunks.size();
-  P.smem = kern::SmemLayout(a.bs, P.cb_max, P.rmax, a.mr).total;
+  P.smem = kern::SmemLayout(a.bs, P.cb_max, P.rmax, a.mr, P.stages).total;
   if (P.smem > 227 * 1024) fail(BMG_EINVAL, "plan: chunk does not fit in shared memory");
   occupancy_for(a.mr, a.mc, P.smem);  // sets the dynamic smem attribute
   P.chunks.alloc(chunks.size());
@@ -444,6 +454,7 @@ static void launch_stream_t(const Bsr& a, const double* x, Epi epi) {
   s.bs = a.bs;
   s.cb_max = a.plan.cb_max;
   s.rmax = a.plan.rmax;
+  s.stages = a.plan.stages;
   // one attribute per template instantiation (covers the largest plan)
   static bool attr_set = false;
   if (!attr_set) {

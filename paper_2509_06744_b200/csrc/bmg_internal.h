@@ -74,6 +74,7 @@ struct Ctx {
 struct Plan {
   int cb_max = 0;        // blocks per chunk
   int rmax = 0;          // max rows per chunk
+  int stages = 4;        // shared-memory ring depth
   int nctas = 0;
   int nchunks = 0;
   size_t smem = 0;

@@ -33,7 +33,7 @@
 namespace bmg {
 namespace kern {
 
-constexpr int kStages = 4;
+constexpr int kMaxStages = 8;
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = kConsumerWarps * 32;
 constexpr int kThreads = kConsumers + 32;
@@ -138,6 +138,7 @@ struct StreamArgs {
   int bs;      // padded block stride (doubles)
   int cb_max;  // blocks per chunk
   int rmax;    // rows per chunk
+  int stages;  // shared-memory ring depth (<= kMaxStages)
 };
 
 // column-index slots per stage: cb_max + 8, rounded to 16 bytes (bulk-copy
@@ -146,7 +147,7 @@ __host__ __device__ inline int stage_cols_of(int cb_max) { return (cb_max + 8 + 
 
 struct SmemLayout {
   uint32_t vals, cols, part, carry, bars, total;
-  __host__ __device__ SmemLayout(int bs, int cb_max, int rmax, int mr) {
+  __host__ __device__ SmemLayout(int bs, int cb_max, int rmax, int mr, int kStages) {
     uint32_t o = 0;
     auto al = [](uint32_t v, uint32_t a) { return (v + a - 1) / a * a; };
     (void)rmax;
@@ -167,7 +168,8 @@ struct SmemLayout {
 template <int MR, int MC, class Epi>
 __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi epi) {
   extern __shared__ __align__(128) unsigned char smem[];
-  const SmemLayout L(s.bs, s.cb_max, s.rmax, MR);
+  const int kStages = s.stages;
+  const SmemLayout L(s.bs, s.cb_max, s.rmax, MR, kStages);
   double* vals_s = reinterpret_cast<double*>(smem + L.vals);
   int* cols_s = reinterpret_cast<int*>(smem + L.cols);
   double* part_s = reinterpret_cast<double*>(smem + L.part);
