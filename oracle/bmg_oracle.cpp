@@ -1269,6 +1269,35 @@ int orc_fsai_build(const orc_mat* a, int kind, int t_max, double tau, int nest, 
     *out = new orc_fsai{std::move(f)};
   });
 }
+static LowerPattern pattern_from_csr(int n, const int64_t* pp, const int32_t* pc) {
+  LowerPattern p = LowerPattern::diagonal(n);
+  for (int i = 0; i < n; ++i)
+    for (int64_t q = pp[i]; q < pp[i + 1]; ++q) p.add(i, pc[q]);
+  return p;
+}
+int orc_fsai_build_pattern(const orc_mat* a, const int64_t* pat_ptr, const int32_t* pat_col,
+                           orc_fsai** out) {
+  return guard([&] {
+    Nested f;
+    f.layout = a->m.rl;
+    f.chain.push_back(build_fsai(a->m, pattern_from_csr(a->m.nbr(), pat_ptr, pat_col)));
+    *out = new orc_fsai{std::move(f)};
+  });
+}
+int orc_delta_ratio(const orc_mat* a, const int64_t* pat_ptr, const int32_t* pat_col, int k, int c,
+                    double* out) {
+  return guard([&] {
+    check_spd_inputs(a->m);
+    const LowerPattern p = pattern_from_csr(a->m.nbr(), pat_ptr, pat_col);
+    RowMap frow;
+    Chol s, gram;
+    build_row(a->m, p, k, frow, s, gram);  // make_adaptive_state, fsai.cpp:90-104
+    const RowMap h = build_h_row(a->m, frow, k);
+    auto it = h.find(c);
+    if (it == h.end()) throw std::invalid_argument("delta_ratio: H_kc not stored");
+    *out = delta_ratio(a->m, p, gram, s, k, c, it->second);
+  });
+}
 void orc_fsai_destroy(orc_fsai* f) { delete f; }
 int orc_fsai_apply(const orc_fsai* f, const double* r, double* out) {
   return guard([&] { nested_apply(f->f, r, out); });

@@ -68,6 +68,12 @@ int orc_chol_solve(int n, const double* l, const double* rhs, double* x);
  * kind 2: build_fsai with LowerPattern::full
  * kind 3: nested_build(A, t_max, tau, nest)                                  */
 int orc_fsai_build(const orc_mat* a, int kind, int t_max, double tau, int nest, orc_fsai** out);
+/* build_fsai(A, p) for an explicit strict-lower pattern (CSR over block rows) */
+int orc_fsai_build_pattern(const orc_mat* a, const int64_t* pat_ptr, const int32_t* pat_col,
+                           orc_fsai** out);
+/* delta_ratio(state(A, p), A, k, c) (fsai.cpp:106-130) for pattern p */
+int orc_delta_ratio(const orc_mat* a, const int64_t* pat_ptr, const int32_t* pat_col, int k, int c,
+                    double* out);
 void orc_fsai_destroy(orc_fsai* f);
 int orc_fsai_apply(const orc_fsai* f, const double* r, double* out);
 int orc_fsai_apply_transformed(const orc_fsai* f, const orc_mat* a, const double* x, double* out);

@@ -43,6 +43,8 @@ _SIGS = {
     "orc_chol_solve": (_I, [_I, _PD, _PD, _PD]),
     "orc_fsai_build": (_I, [_P, _I, _I, _D, _I, _PP]),
     "orc_fsai_destroy": (None, [_P]),
+    "orc_fsai_build_pattern": (_I, [_P, _PI64, _PI32, _PP]),
+    "orc_delta_ratio": (_I, [_P, _PI64, _PI32, _I, _I, _PD]),
     "orc_fsai_apply": (_I, [_P, _PD, _PD]),
     "orc_fsai_apply_transformed": (_I, [_P, _P, _PD, _PD]),
     "orc_fsai_chain_len": (_I, [_P]),
@@ -251,6 +253,34 @@ class Fsai:
                 lib().orc_fsai_destroy(self.h)
         except Exception:
             pass
+
+
+def _pattern_csr(n, pattern):
+    """pattern: list of strict-lower column lists per block row."""
+    pp = np.zeros(n + 1, np.int64)
+    cols = []
+    for i in range(n):
+        cols.extend(sorted(pattern[i]))
+        pp[i + 1] = len(cols)
+    return pp, np.asarray(cols if cols else [0], np.int32)
+
+
+def fsai_with_pattern(a, pattern):
+    n = a.info()["nbr"]
+    pp, pc = _pattern_csr(n, pattern)
+    h = C.c_void_p()
+    check(lib().orc_fsai_build_pattern(a.h, _i64(pp), _i32(pc), C.byref(h)))
+    f = Fsai(None, 0, _handle=h)
+    f.row_sizes = a.row_sizes
+    return f
+
+
+def delta_ratio(a, pattern, k, c):
+    n = a.info()["nbr"]
+    pp, pc = _pattern_csr(n, pattern)
+    out = C.c_double()
+    check(lib().orc_delta_ratio(a.h, _i64(pp), _i32(pc), k, c, C.byref(out)))
+    return out.value
 
 
 def lanczos_lambda_max(a, f, iters=100, safety=1.01, seed=42):
