@@ -1,0 +1,292 @@
+// blockmg.hpp -- header-only C++ facade over the C ABI (include/bmg_cuda.h).
+//
+// Mirrors the reference's hot-path interface (/root/reference/proj/include/blockmg):
+// the same function names, argument meaning and exception types, so a caller of
+// the reference's spmv / nested_build / cheb_fourth_apply / lanczos_lambda_max /
+// setup / v_cycle can switch by replacing the matrix type with a device handle.
+//   BlockLayout              block_layout.hpp:8-28
+//   NotPositiveDefinite      small_cholesky.hpp:10-13
+//   spmv / spmv_transpose    kernels.hpp:15,19
+//   galerkin_coarsen         multilevel.hpp:50
+//   nested_build             fsai.hpp:68   (NestedFsai::apply fsai.hpp:62)
+//   cheb_fourth_apply        chebyshev.hpp:48
+//   lanczos_lambda_max       multilevel.hpp:53
+//   SetupParams / CycleSpec  multilevel.hpp:13-19, 35-47
+//   setup / v_cycle          multilevel.hpp:59-65
+// Values are FP64; every object lives on one B200 (sm_100a).  No CPU fallback.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../bmg_cuda.h"
+
+namespace bmg {
+
+struct NotPositiveDefinite : std::runtime_error {
+  int pivot;
+  NotPositiveDefinite(int p, const std::string& msg) : std::runtime_error(msg), pivot(p) {}
+};
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void check(int status) {
+  if (status == BMG_OK) return;
+  const std::string msg = bmg_last_error();
+  switch (status) {
+    case BMG_EINVAL: throw std::invalid_argument(msg);
+    case BMG_ERANGE: throw std::out_of_range(msg);
+    case BMG_ENOTSPD: throw NotPositiveDefinite(bmg_last_pivot(), msg);
+    case BMG_ECUDA: throw CudaError(msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+
+// Partition of {0..N-1} into blocks of sizes m_i >= 1 (block_layout.hpp:8-28).
+class BlockLayout {
+ public:
+  BlockLayout() = default;
+  explicit BlockLayout(std::vector<int> sizes) : sizes_(std::move(sizes)) {
+    for (int m : sizes_) {
+      if (m < 1) throw std::invalid_argument("BlockLayout: block sizes must be >= 1");
+      offsets_.push_back(dim_);
+      dim_ += m;
+    }
+  }
+  static BlockLayout scalar(int n) { return uniform(n, 1); }
+  static BlockLayout uniform(int n, int m) { return BlockLayout(std::vector<int>((size_t)n, m)); }
+  int blocks() const { return (int)sizes_.size(); }
+  int dim() const { return dim_; }
+  int size(int i) const { return sizes_[(size_t)i]; }
+  int offset(int i) const { return offsets_[(size_t)i]; }
+  const std::vector<int>& sizes() const { return sizes_; }
+  bool operator==(const BlockLayout& o) const { return sizes_ == o.sizes_; }
+
+ private:
+  std::vector<int> sizes_, offsets_;
+  int dim_ = 0;
+};
+
+class Context {
+ public:
+  explicit Context(int device = 0) { check(bmg_ctx_create(device, &h_)); }
+  ~Context() {
+    if (h_) bmg_ctx_destroy(h_);
+  }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+  bmg_ctx* get() const { return h_; }
+  void set_stream(void* s) { check(bmg_ctx_set_stream(h_, s)); }
+  void sync() { check(bmg_ctx_sync(h_)); }
+
+ private:
+  bmg_ctx* h_ = nullptr;
+};
+
+// Block-CSR host arrays: rows ascending, columns strictly ascending per row,
+// blocks row-major (the reference's DenseBlock, types.hpp:9).
+struct HostBsr {
+  BlockLayout rows, cols;
+  std::vector<int64_t> row_ptr{0};
+  std::vector<int32_t> col_idx;
+  std::vector<double> vals;
+  bool symmetric = false;
+};
+
+class DeviceMatrix {
+ public:
+  DeviceMatrix(Context& ctx, const HostBsr& h) : rows_(h.rows), cols_(h.cols) {
+    check(bmg_bsr_create(ctx.get(), h.rows.blocks(), h.rows.sizes().data(), h.cols.blocks(),
+                         h.cols.sizes().data(), h.row_ptr.data(), h.col_idx.data(), h.vals.data(),
+                         h.symmetric ? BMG_SYMMETRIC : 0, &h_));
+  }
+  DeviceMatrix(bmg_bsr* borrowed, BlockLayout r, BlockLayout c)
+      : h_(borrowed), rows_(std::move(r)), cols_(std::move(c)), owned_(false) {}
+  ~DeviceMatrix() {
+    if (h_ && owned_) bmg_bsr_destroy(h_);
+  }
+  DeviceMatrix(DeviceMatrix&& o) noexcept : h_(o.h_), rows_(o.rows_), cols_(o.cols_), owned_(o.owned_) {
+    o.h_ = nullptr;
+  }
+  DeviceMatrix(const DeviceMatrix&) = delete;
+  const bmg_bsr* get() const { return h_; }
+  const BlockLayout& row_layout() const { return rows_; }
+  const BlockLayout& col_layout() const { return cols_; }
+
+ private:
+  friend DeviceMatrix galerkin_coarsen(const DeviceMatrix&, const DeviceMatrix&);
+  bmg_bsr* h_ = nullptr;
+  BlockLayout rows_, cols_;
+  bool owned_ = true;
+};
+
+class DeviceVector {
+ public:
+  DeviceVector(Context& ctx, int64_t n) { check(bmg_vec_create(ctx.get(), n, &h_)); }
+  DeviceVector(Context& ctx, const std::vector<double>& v) : DeviceVector(ctx, (int64_t)v.size()) { upload(v); }
+  ~DeviceVector() {
+    if (h_) bmg_vec_destroy(h_);
+  }
+  DeviceVector(const DeviceVector&) = delete;
+  void upload(const std::vector<double>& v) { check(bmg_vec_upload(h_, v.data())); }
+  std::vector<double> download() const {
+    std::vector<double> out((size_t)bmg_vec_size(h_));
+    check(bmg_vec_download(h_, out.data()));
+    return out;
+  }
+  bmg_vec* get() const { return h_; }
+
+ private:
+  bmg_vec* h_ = nullptr;
+};
+
+// y = A x (kernels.hpp:15); y = A^T x (kernels.hpp:19)
+inline void spmv(const DeviceMatrix& a, const DeviceVector& x, DeviceVector& y) {
+  check(bmg_spmv(a.get(), x.get(), y.get()));
+}
+inline void spmv_transpose(const DeviceMatrix& a, const DeviceVector& x, DeviceVector& y) {
+  check(bmg_spmv_t(a.get(), x.get(), y.get()));
+}
+
+// P^T A P, symmetrised (multilevel.hpp:50)
+inline DeviceMatrix galerkin_coarsen(const DeviceMatrix& a, const DeviceMatrix& p) {
+  bmg_bsr* out = nullptr;
+  check(bmg_galerkin(a.get(), p.get(), &out));
+  DeviceMatrix m(out, p.col_layout(), p.col_layout());
+  m.owned_ = true;
+  return m;
+}
+
+// Block-FSAI, M = G^T G on the device (NestedFsai, fsai.hpp:56-66)
+class NestedFsai {
+ public:
+  explicit NestedFsai(bmg_fsai* h) : h_(h) {}
+  ~NestedFsai() {
+    if (h_) bmg_fsai_destroy(h_);
+  }
+  NestedFsai(NestedFsai&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
+  NestedFsai(const NestedFsai&) = delete;
+  void apply(const DeviceVector& r, DeviceVector& z) const { check(bmg_fsai_apply(h_, r.get(), z.get())); }
+  const bmg_fsai* get() const { return h_; }
+
+ private:
+  bmg_fsai* h_ = nullptr;
+};
+
+inline NestedFsai nested_build(const DeviceMatrix& a, int t_max, double tau, int n_levels) {
+  bmg_fsai* out = nullptr;
+  check(bmg_fsai_build(a.get(), BMG_FSAI_ADAPTIVE, t_max, tau, n_levels, &out));
+  return NestedFsai(out);
+}
+inline NestedFsai build_fsai_static(const DeviceMatrix& a) {  // build_fsai(A, LowerPattern::from_matrix(A))
+  bmg_fsai* out = nullptr;
+  check(bmg_fsai_build(a.get(), BMG_FSAI_STATIC_LOWER, 1, 1.0, 0, &out));
+  return NestedFsai(out);
+}
+
+// x <- cheb_fourth_apply(A, M, b, x, beta, k) (chebyshev.hpp:48-69), in place
+inline void cheb_fourth_apply(const DeviceMatrix& a, const NestedFsai& m, const DeviceVector& b, DeviceVector& x,
+                              double beta, int k) {
+  check(bmg_cheb4_apply(a.get(), m.get(), b.get(), x.get(), beta, k));
+}
+
+inline double lanczos_lambda_max(const DeviceMatrix& a, const NestedFsai& m, int iters = 100,
+                                 double safety = 1.01, uint64_t seed = 42) {
+  double beta = 0.0;
+  check(bmg_lanczos_lambda_max(a.get(), m.get(), iters, safety, seed, &beta));
+  return beta;
+}
+
+struct CycleSpec {  // multilevel.hpp:13-19
+  int k_pre = 1;
+  int k_post = 1;
+  static CycleSpec vkk(int k) { return {k, k}; }
+  static CycleSpec v2k0(int k) { return {2 * k, 0}; }
+};
+
+struct SetupParams {  // multilevel.hpp:35-47 (fourth-kind smoothing)
+  int t_max = 4;
+  double tau = 1.0;
+  int nest = 0;
+  int lanczos_iters = 100;
+  double lanczos_safety = 1.01;
+  uint64_t seed = 42;
+  int coarse_dim_cap = 5000;
+  bool static_pattern = false;  // lower(P(A)) instead of the adaptive chain
+};
+
+class Hierarchy {
+ public:
+  explicit Hierarchy(bmg_hier* h) : h_(h) {}
+  ~Hierarchy() {
+    if (h_) bmg_hier_destroy(h_);
+  }
+  Hierarchy(Hierarchy&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
+  Hierarchy(const Hierarchy&) = delete;
+  bmg_hier* get() const { return h_; }
+  int levels() const {
+    int n = 0;
+    check(bmg_hier_info(h_, &n, nullptr));
+    return n;
+  }
+  int finest() const { return levels() - 1; }
+  double beta(int level) const {
+    double b = 0.0;
+    check(bmg_hier_beta(h_, level, &b));
+    return b;
+  }
+
+ private:
+  bmg_hier* h_ = nullptr;
+};
+
+// setup (multilevel.hpp:59-60): transfers[l-1] prolongates level l-1 to l
+inline Hierarchy setup(const DeviceMatrix& a_finest, const std::vector<const DeviceMatrix*>& transfers,
+                       const SetupParams& p) {
+  bmg_setup_params c;
+  bmg_setup_params_default(&c);
+  c.t_max = p.t_max;
+  c.tau = p.tau;
+  c.nest = p.nest;
+  c.fsai_kind = p.static_pattern ? BMG_FSAI_STATIC_LOWER : BMG_FSAI_ADAPTIVE;
+  c.lanczos_iters = p.lanczos_iters;
+  c.lanczos_safety = p.lanczos_safety;
+  c.seed = p.seed;
+  c.coarse_dim_cap = p.coarse_dim_cap;
+  std::vector<const bmg_bsr*> t;
+  for (auto* m : transfers) t.push_back(m->get());
+  bmg_hier* h = nullptr;
+  check(bmg_hier_setup(a_finest.get(), (int)t.size(), t.data(), &c, &h));
+  return Hierarchy(h);
+}
+
+// v_cycle on the finest level (multilevel.hpp:65); x is updated in place
+inline void v_cycle(const Hierarchy& h, const CycleSpec& spec, const DeviceVector& b, DeviceVector& x) {
+  check(bmg_vcycle(h.get(), spec.k_pre, spec.k_post, b.get(), x.get()));
+}
+inline void v_cycle(const Hierarchy& h, const CycleSpec& spec, const std::vector<double>& b,
+                    std::vector<double>& x) {
+  check(bmg_vcycle_host(h.get(), spec.k_pre, spec.k_post, b.data(), x.data()));
+}
+
+struct SolveReport {  // residual-history analogue of RateReport (experiments.hpp:17-27)
+  std::vector<double> residual;
+  int iterations = 0;
+  int status = 0;  // 0 converged, 1 max_iter, 2 diverged
+};
+inline SolveReport solve(const Hierarchy& h, const CycleSpec& spec, const DeviceVector& b, DeviceVector& x,
+                         double tol, int max_iter) {
+  SolveReport r;
+  r.residual.assign((size_t)max_iter + 1, 0.0);
+  check(bmg_solve(h.get(), spec.k_pre, spec.k_post, b.get(), x.get(), tol, max_iter, r.residual.data(),
+                  &r.iterations, &r.status));
+  r.residual.resize((size_t)r.iterations + 1);
+  return r;
+}
+
+}  // namespace bmg
