@@ -442,6 +442,14 @@ std::unique_ptr<Bsr> bsr_transpose(const Bsr& a) {
 }
 
 // ============================================================================ launches
+static bool pdl_enabled() {
+  static bool on = [] {
+    const char* e = std::getenv("BMG_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <int MR, int MC, class Epi>
 static void launch_stream_t(const Bsr& a, const double* x, Epi epi) {
   kern::StreamArgs s;
@@ -462,7 +470,17 @@ static void launch_stream_t(const Bsr& a, const double* x, Epi epi) {
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set = true;
   }
-  kern::bsr_stream_kernel<MR, MC, Epi><<<a.plan.nctas, kern::kThreads, a.plan.smem, a.ctx->stream>>>(s, epi);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.plan.nctas);
+  cfg.blockDim = dim3(kern::kThreads);
+  cfg.dynamicSmemBytes = a.plan.smem;
+  cfg.stream = a.ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  BMG_CUDA(cudaLaunchKernelEx(&cfg, kern::bsr_stream_kernel<MR, MC, Epi>, s, epi));
   a.ctx->count();
   BMG_LAUNCHED(a.ctx->stream, "bsr_stream_kernel");
 }

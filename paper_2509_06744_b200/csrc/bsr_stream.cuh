@@ -77,6 +77,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// Programmatic dependent launch (sm_90+): the next pass may start streaming its
+// matrix while this one drains; vector reads/writes wait for the predecessor.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 __device__ __forceinline__ void consumer_bar() {
   asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
 }
@@ -180,6 +186,9 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
   const int c0 = s.cta_chunk[blockIdx.x];
   const int c1 = s.cta_chunk[blockIdx.x + 1];
   const int tid = threadIdx.x;
+  // single-wave persistent grid: every CTA is resident, so the dependent pass can
+  // be scheduled as soon as SMs free up
+  pdl_launch_dependents();
   if (tid == 0) {
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&full[i], 1);
@@ -216,6 +225,7 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
   }
 
   // -------------------------------------------------------------- consumers
+  pdl_wait();  // vectors (x, b, p, outputs) belong to the predecessor pass
   // One named barrier per chunk: partial sums and the row carry are double
   // buffered, so phase B of chunk c overlaps phase A of chunk c+1.
   for (int c = c0, it = 0; c < c1; ++c, ++it) {

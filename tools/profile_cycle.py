@@ -31,6 +31,18 @@ if mode == "cycle":
         H.v_cycle(cfg.k, cfg.k, bv, xv)
     torch.cuda.synchronize()
     torch.cuda.profiler.stop()
+elif mode in ("gpass", "gtpass"):
+    from paper_2509_06744_b200 import spmv
+    Af, _, Mf = H.level(H.levels - 1)
+    G = Mf.G if mode == "gpass" else Mf.G.transpose()
+    rv = Vector(ctx, A.dim_r)
+    spmv(G, bv, rv)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
+    for _ in range(3):
+        spmv(G, bv, rv)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
 else:
     rv = Vector(ctx, A.dim_r)
     Af, _, _ = H.level(H.levels - 1)
