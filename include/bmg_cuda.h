@@ -177,6 +177,28 @@ int bmg_vcycle_host(bmg_hier* h, int k_pre, int k_post, const double* b, double*
 int bmg_solve(bmg_hier* h, int k_pre, int k_post, const bmg_vec* b, bmg_vec* x, double tol,
               int max_iter, double* hist, int* iters, int* status);
 
+/* ---- multi-GPU (row-partitioned V-cycle) ---------------
+ * Every rank builds the same hierarchy (setup is deterministic), then keeps its
+ * row strip of every level: contiguous block-row ranges balanced by blocks with
+ * boundaries on multiples of granule[l] rows (a grid row in 2-D, a plane in
+ * 3-D), the `agglomerate` coarsest levels on rank 0.  Halo exchanges are NCCL
+ * send/recv of contiguous slices inside the captured V-cycle graph.  After the
+ * partition bmg_vcycle / bmg_solve take this rank's own rows of b and x.
+ * rank = -1 on a plain context emulates all `world` ranks in this process
+ * (virtual ranks, device copies for the halos; b, x stay global): results are
+ * bitwise equal to the unpartitioned cycle. */
+int bmg_nccl_unique_id(unsigned char* id128);
+int bmg_ctx_create_nccl(int device, int rank, int world, const unsigned char* id128, bmg_ctx** out);
+int bmg_hier_partition(bmg_hier* h, int world, int rank, const int32_t* granule, int agglomerate);
+/* own rows [lo, hi) and vector window [wlo, whi) of `rank` on `level` */
+int bmg_hier_part_info(const bmg_hier* h, int level, int rank, int32_t* lo, int32_t* hi, int32_t* wlo,
+                       int32_t* whi);
+/* host planning (no device needed): balanced contiguous row ranges; column hull */
+int bmg_partition_rows(int nbr, const int64_t* row_ptr, int world, int granule, int agglomerate,
+                       int32_t* bounds);
+int bmg_row_window(const int64_t* row_ptr, const int32_t* col, int lo, int hi, int clo, int chi,
+                   int32_t* ext_lo, int32_t* ext_hi);
+
 /* ---- profiling helpers (bench.py) --------------------------------------- */
 /* time `reps` back-to-back launches of the residual pass r = b - A x on the
  * context stream with CUDA events; returns the average ms per launch */

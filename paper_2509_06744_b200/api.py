@@ -72,11 +72,23 @@ class HostBsr:
 
 
 class Context:
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, nccl: tuple | None = None):
+        """nccl = (rank, world, unique_id_bytes) for a multi-GPU context."""
         h = C.c_void_p()
-        check(lib().bmg_ctx_create(device, C.byref(h)))
+        if nccl is None:
+            check(lib().bmg_ctx_create(device, C.byref(h)))
+        else:
+            rank, world, uid = nccl
+            check(lib().bmg_ctx_create_nccl(device, rank, world, bytes(uid), C.byref(h)))
         self.h = h
         self.device = device
+        self.rank, self.world = (nccl[0], nccl[1]) if nccl else (0, 1)
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(lib().bmg_nccl_unique_id(buf))
+        return buf.raw
 
     def set_stream(self, stream_ptr: int | None):
         check(lib().bmg_ctx_set_stream(self.h, C.c_void_p(stream_ptr or 0)))
@@ -343,6 +355,16 @@ class Hierarchy:
         check(lib().bmg_hier_cycle_bytes(self.h, k_pre, k_post, C.byref(out)))
         return out.value
 
+    def partition(self, world: int, granule, agglomerate: int = 1, rank: int = -1):
+        """Row-partition the hierarchy (rank = -1: emulate all ranks in-process)."""
+        g = np.ascontiguousarray(granule, np.int32)
+        check(lib().bmg_hier_partition(self.h, world, rank, i32ptr(g), agglomerate))
+
+    def part_info(self, level: int, rank: int):
+        lo, hi, wlo, whi = (C.c_int32() for _ in range(4))
+        check(lib().bmg_hier_part_info(self.h, level, rank, C.byref(lo), C.byref(hi), C.byref(wlo), C.byref(whi)))
+        return lo.value, hi.value, wlo.value, whi.value
+
     def use_graph(self, on: bool):
         check(lib().bmg_hier_use_graph(self.h, 1 if on else 0))
 
@@ -372,6 +394,21 @@ class Hierarchy:
             self.close()
         except Exception:
             pass
+
+
+def partition_rows(row_ptr, world: int, granule: int = 1, agglomerate: bool = False) -> np.ndarray:
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    out = np.zeros(world + 1, np.int32)
+    check(lib().bmg_partition_rows(len(rp) - 1, i64ptr(rp), world, granule, 1 if agglomerate else 0, i32ptr(out)))
+    return out
+
+
+def row_window(row_ptr, col_idx, lo: int, hi: int, clo: int, chi: int):
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    ci = np.ascontiguousarray(col_idx if len(col_idx) else [0], np.int32)
+    a, b = C.c_int32(), C.c_int32()
+    check(lib().bmg_row_window(i64ptr(rp), i32ptr(ci), lo, hi, clo, chi, C.byref(a), C.byref(b)))
+    return a.value, b.value
 
 
 def tridiag_eigs(d, e) -> np.ndarray:

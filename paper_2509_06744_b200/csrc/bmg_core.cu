@@ -1,6 +1,7 @@
 // bmg_core.cu -- context, device BSR storage + streaming plans, vectors, the
 // streaming-kernel launchers, reductions and the corresponding C ABI.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -38,6 +39,7 @@ thread_local int g_last_pivot = -1;
 
 // ============================================================================ context
 Ctx::~Ctx() {
+  if (nccl) ncclCommDestroy(static_cast<ncclComm_t>(nccl));
   if (solver) cusolverDnDestroy(solver);
   if (h_red) cudaFreeHost(h_red);
   if (own) cudaStreamDestroy(own);

@@ -62,6 +62,8 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   int64_t launches = 0;
   cusolverDnHandle_t solver = nullptr;
+  void* nccl = nullptr;  // ncclComm_t of a multi-GPU context (bmg_ctx_create_nccl)
+  int rank = 0, world = 1;
   DBuf<double> red;          // reduction partials
   double* h_red = nullptr;   // pinned result slot(s)
   void activate() const { BMG_CUDA(cudaSetDevice(device)); }
@@ -152,6 +154,12 @@ std::unique_ptr<Fsai> fsai_build(const Bsr& a, int kind, int t_max, double tau, 
 std::unique_ptr<Fsai> fsai_from_factors(Ctx* ctx, const Bsr& F, const double* shat_l_packed);
 double lanczos_lambda_max(const Bsr& a, const Fsai& m, int iters, double safety, uint64_t seed);
 std::unique_ptr<Bsr> galerkin(const Bsr& a, const Bsr& p);
+
+// host planning for the partitioned V-cycle (partition.cpp)
+void partition_rows(int nbr, const int64_t* row_ptr, int world, int granule, bool agglomerate,
+                    int32_t* bounds);
+void row_window(const int64_t* row_ptr, const int32_t* col, int lo, int hi, int clo, int chi,
+                int32_t* ext_lo, int32_t* ext_hi);
 
 // host helpers
 std::vector<double> tridiag_eigenvalues(std::vector<double> d, std::vector<double> e);

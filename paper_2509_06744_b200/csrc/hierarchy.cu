@@ -1,0 +1,948 @@
+// hierarchy.cu -- the device-resident multilevel hierarchy, its row partition over
+// ranks (NCCL) or virtual ranks (in-process emulation), the V-cycle (captured as
+// a CUDA graph) and the measure_rates-style solve loop.
+//
+// Reference: setup (multilevel.cpp:36-75), v_cycle (multilevel.cpp:77-103),
+// measure_rates (experiments.cpp:15-67).  Partitioning: SURVEY.md §8(e).
+//
+// Every level of every (virtual) rank keeps its vectors in one contiguous window
+// of global block rows [wlo, whi) that contains its own rows [lo, hi) plus the
+// halo its matrices read; local matrices index columns as `global - wlo`.  A halo
+// exchange therefore moves contiguous slices: rank s sends [max(lo_s, wlo_r),
+// min(hi_s, whi_r)) to rank r.  Per-row arithmetic does not depend on the
+// partition, so partitioned cycles are bitwise equal to the 1-GPU cycle.
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <tuple>
+
+#include "bmg_abi.h"
+#include "bmg_internal.h"
+
+namespace bmg {
+namespace kern {
+
+__global__ void bsr_to_dense_kernel(const double* __restrict__ vals, const int64_t* __restrict__ row_ptr,
+                                    const int32_t* __restrict__ col, int nbr, int m, int bs,
+                                    double* __restrict__ dense, int64_t N) {
+  for (int i = blockIdx.x; i < nbr; i += gridDim.x)
+    for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
+      const int j = col[p];
+      for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+        const int r = e / m, c = e - r * m;
+        dense[((int64_t)i * m + r) * N + (int64_t)j * m + c] = vals[p * bs + e];
+      }
+    }
+}
+
+__global__ void symmetrize_dense_kernel(double* a, int64_t N) {
+  // cuSOLVER potri (column-major lower) leaves the row-major upper triangle
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < N * N; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / N, c = e - r * N;
+    if (r > c) a[e] = a[c * N + r];
+  }
+}
+
+// x = A0^{-1} b (dense, row-major): warp per row, double2 loads
+__global__ void __launch_bounds__(256) gemv_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                                                   double* __restrict__ x, int64_t N) {
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= N) return;
+  const double* ar = a + row * N;
+  double s = 0.0;
+  if ((N & 1) == 0) {
+    const double2* a2 = reinterpret_cast<const double2*>(ar);
+    const double2* b2 = reinterpret_cast<const double2*>(b);
+    for (int64_t q = lane; q < N / 2; q += 32) {
+      const double2 av = __ldg(a2 + q), bv = __ldg(b2 + q);
+      s = __fma_rn(av.x, bv.x, s);
+      s = __fma_rn(av.y, bv.y, s);
+    }
+  } else {
+    for (int64_t q = lane; q < N; q += 32) s = __fma_rn(__ldg(ar + q), __ldg(b + q), s);
+  }
+  for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o));
+  if (lane == 0) x[row] = s;
+}
+
+// Partition-invariant squared norm: one fixed-shape tree per segment of
+// `seg_len` scalars (a segment = one granule of block rows, never split
+// across ranks); segment sums are then added in order on the host.
+__global__ void __launch_bounds__(256) segment_sq_kernel(const double* __restrict__ v, int64_t n, int64_t seg_len,
+                                                         double* __restrict__ out) {
+  __shared__ double sh[256];
+  const int64_t s0 = blockIdx.x * seg_len;
+  const int64_t s1 = min(n, s0 + seg_len);
+  double acc = 0.0;
+  for (int64_t i = s0 + threadIdx.x; i < s1; i += 256) acc = __fma_rn(v[i], v[i], acc);
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = sh[0];
+}
+
+}  // namespace kern
+
+static int grid1d(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)); }
+
+static void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) fail(BMG_ENCCL, std::string(what) + ": " + ncclGetErrorString(r));
+}
+
+// ============================================================================ data model
+enum Which { VB = 0, VX, VR, VW, VP, VT, VNUM };
+
+struct PLevel {  // one (virtual) rank's share of one level
+  int lo = 0, hi = 0;    // own block rows
+  int wlo = 0, whi = 0;  // vector window (block rows)
+  int m = 0;             // uniform block size on this level
+  const Bsr* A = nullptr;
+  const Bsr* R = nullptr;  // restriction to level l-1 (rows: own rows of l-1)
+  const Bsr* P = nullptr;  // prolongation from level l-1 (rows: own rows of l)
+  const Fsai* M = nullptr;
+  std::unique_ptr<Bsr> A_own, R_own, P_own;
+  std::unique_ptr<Fsai> M_own;
+  double beta = 1.0;
+  DBuf<double> v[VNUM];
+  int64_t off() const { return (int64_t)(lo - wlo) * m; }
+  int64_t n_own() const { return (int64_t)(hi - lo) * m; }
+  int64_t n_win() const { return (int64_t)(whi - wlo) * m; }
+  bool active() const { return hi > lo; }
+};
+
+struct Part {
+  int rank = 0;
+  std::vector<PLevel> lv;
+  DBuf<double> ainv;  // dense A_0^{-1} (rank owning level 0)
+};
+
+struct LevelStats {  // global byte model inputs (bmg_hier_cycle_bytes)
+  int64_t n = 0, a_pass = 0, m_pass = 0, r_pass = 0, p_pass = 0;
+};
+
+struct GraphKey {
+  int kpre, kpost;
+  const double* b;
+  double* x;
+  bool operator<(const GraphKey& o) const { return std::tie(kpre, kpost, b, x) < std::tie(o.kpre, o.kpost, o.b, o.x); }
+};
+
+struct Hier {
+  Ctx* ctx = nullptr;
+  int world = 1;          // ranks the rows are split over
+  bool emulated = false;  // all virtual ranks live in this process
+  std::vector<Part> parts;
+  std::vector<int> nbr, msz;                  // per level
+  std::vector<std::vector<int32_t>> bounds;   // per level: world + 1
+  std::vector<std::vector<int32_t>> wlo, whi; // per level, per rank
+  int granule_top = 1;                        // block rows per norm segment (top level)
+  int64_t n0 = 0;
+  std::vector<LevelStats> stats;
+  bool use_graph = true;
+  struct Captured {
+    cudaGraphExec_t exec;
+    int64_t kernels;
+  };
+  std::map<GraphKey, Captured> graphs;
+  DBuf<double> io_b, io_x, seg;
+  const double* user_b = nullptr;
+  double* user_x = nullptr;
+  ~Hier() {
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
+  }
+  int finest() const { return (int)nbr.size() - 1; }
+  bool whole() const { return world == 1; }
+  void drop_graphs() {
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
+    graphs.clear();
+  }
+};
+
+// vector of level l on part p; the unpartitioned top level uses the caller's b, x
+static double* vec(Hier& h, Part& p, int l, Which w) {
+  if (h.whole() && l == h.finest()) {
+    if (w == VB) return const_cast<double*>(h.user_b);
+    if (w == VX) return h.user_x;
+  }
+  return p.lv[l].v[w].p;
+}
+
+// ============================================================================ halo exchange
+static void exchange(Hier& h, int l, Which w) {
+  if (h.world == 1) return;
+  Ctx* ctx = h.ctx;
+  const int m = h.msz[l];
+  const auto& B = h.bounds[l];
+  if (h.emulated) {
+    for (Part& dst : h.parts)
+      for (Part& src : h.parts) {
+        if (&dst == &src) continue;
+        const int r = dst.rank, s = src.rank;
+        const int g0 = std::max(B[s], h.wlo[l][r]), g1 = std::min(B[s + 1], h.whi[l][r]);
+        if (g1 <= g0) continue;
+        double* d = vec(h, dst, l, w) + (int64_t)(g0 - h.wlo[l][r]) * m;
+        const double* sp = vec(h, src, l, w) + (int64_t)(g0 - h.wlo[l][s]) * m;
+        BMG_CUDA(cudaMemcpyAsync(d, sp, (size_t)(g1 - g0) * m * sizeof(double), cudaMemcpyDeviceToDevice,
+                                 ctx->stream));
+      }
+    return;
+  }
+  Part& me = h.parts[0];
+  const int r = me.rank;
+  double* base = vec(h, me, l, w);
+  ncclComm_t comm = static_cast<ncclComm_t>(ctx->nccl);
+  nccl_check(ncclGroupStart(), "ncclGroupStart");
+  for (int s = 0; s < h.world; ++s) {
+    if (s == r) continue;
+    // send my own rows inside s's window
+    const int a0 = std::max(B[r], h.wlo[l][s]), a1 = std::min(B[r + 1], h.whi[l][s]);
+    if (a1 > a0)
+      nccl_check(ncclSend(base + (int64_t)(a0 - h.wlo[l][r]) * m, (size_t)(a1 - a0) * m, ncclDouble, s, comm,
+                          ctx->stream),
+                 "ncclSend");
+    // receive s's own rows inside my window
+    const int b0 = std::max(B[s], h.wlo[l][r]), b1 = std::min(B[s + 1], h.whi[l][r]);
+    if (b1 > b0)
+      nccl_check(ncclRecv(base + (int64_t)(b0 - h.wlo[l][r]) * m, (size_t)(b1 - b0) * m, ncclDouble, s, comm,
+                          ctx->stream),
+                 "ncclRecv");
+  }
+  nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+}
+
+// ============================================================================ V-cycle
+// one fourth-kind smoothing application on level l, all parts (chebyshev.hpp:48-69)
+static void smooth(Hier& h, int l, int k, bool xzero) {
+  if (k < 1) return;
+  for (int s = 1; s <= k; ++s) {
+    Which src;
+    if (s == 1 && xzero) {
+      src = VB;  // A * 0 = 0: r = b exactly
+    } else {
+      exchange(h, l, VX);
+      for (Part& p : h.parts) {
+        PLevel& L = p.lv[l];
+        if (!L.active()) continue;
+        residual(*L.A, vec(h, p, l, VB) + L.off(), vec(h, p, l, VX), vec(h, p, l, VR) + L.off());
+      }
+      src = VR;
+    }
+    // forward chain w = F_n ... F_0 r (nest = 0: w = G r), then all but the last transpose
+    Which cur = src;
+    Which nxt = VW;
+    const Fsai* M0 = nullptr;
+    for (Part& p : h.parts)
+      if (p.lv[l].active()) M0 = p.lv[l].M;
+    const size_t nf = M0 ? M0->fwd.size() : 1, nb = M0 ? M0->bwd.size() : 1;
+    for (size_t q = 0; q < nf + nb - 1; ++q) {
+      exchange(h, l, cur);
+      for (Part& p : h.parts) {
+        PLevel& L = p.lv[l];
+        if (!L.active()) continue;
+        const Bsr& f = q < nf ? *L.M->fwd[q] : *L.M->bwd[nb - 1 - (q - nf)];
+        spmv(f, vec(h, p, l, cur), vec(h, p, l, nxt) + L.off());
+      }
+      cur = nxt;
+      nxt = (nxt == VW) ? VT : VW;
+    }
+    exchange(h, l, cur);
+    for (Part& p : h.parts) {
+      PLevel& L = p.lv[l];
+      if (!L.active()) continue;
+      const double d = 4.0 / L.beta;
+      double* P = vec(h, p, l, VP) + L.off();
+      double* X = vec(h, p, l, VX) + L.off();
+      if (s == 1) {
+        const double dmu = d * ((2.0 * 0 + 1.0) / (2.0 * 0 + 3.0));
+        gt_cheb(*L.M->bwd[0], vec(h, p, l, cur), P, X, 0.0, dmu, true, xzero);
+      } else {
+        const double mu_prev = (2.0 * (s - 2) + 1.0) / (2.0 * (s - 2) + 3.0);
+        const double mu = (2.0 * (s - 1) + 1.0) / (2.0 * (s - 1) + 3.0);
+        gt_cheb(*L.M->bwd[0], vec(h, p, l, cur), P, X, mu_prev * mu_prev, d * mu, false, false);
+      }
+    }
+  }
+}
+
+static void coarse_solve(Hier& h) {
+  for (Part& p : h.parts) {
+    PLevel& L = p.lv[0];
+    if (!L.active()) continue;
+    const int64_t N = h.n0;
+    kern::gemv_kernel<<<(int)((N * 32 + 255) / 256), 256, 0, h.ctx->stream>>>(p.ainv.p, vec(h, p, 0, VB) + L.off(),
+                                                                              vec(h, p, 0, VX) + L.off(), N);
+    h.ctx->count();
+    BMG_LAUNCHED(h.ctx->stream, "gemv_kernel");
+  }
+}
+
+// v_cycle (multilevel.cpp:77-103), recursion unrolled: down, coarse solve, up
+static void enqueue_vcycle(Hier& h, int kpre, int kpost) {
+  const int top = h.finest();
+  for (int l = top; l >= 1; --l) {
+    const bool xzero = l < top;
+    Which r = VR;
+    if (kpre > 0) {
+      smooth(h, l, kpre, xzero);
+    } else if (xzero) {
+      for (Part& p : h.parts)
+        if (p.lv[l].active()) fill(h.ctx, vec(h, p, l, VX) + p.lv[l].off(), p.lv[l].n_own(), 0.0);
+      r = VB;
+    }
+    if (r == VR) {
+      exchange(h, l, VX);
+      for (Part& p : h.parts) {
+        PLevel& L = p.lv[l];
+        if (!L.active()) continue;
+        residual(*L.A, vec(h, p, l, VB) + L.off(), vec(h, p, l, VX), vec(h, p, l, VR) + L.off());
+      }
+    }
+    exchange(h, l, r);
+    for (Part& p : h.parts) {  // rc = P^T r  (multilevel.cpp:95)
+      PLevel& C = p.lv[l - 1];
+      if (!C.active()) continue;
+      spmv(*p.lv[l].R, vec(h, p, l, r), vec(h, p, l - 1, VB) + C.off());
+    }
+  }
+  coarse_solve(h);
+  for (int l = 1; l <= top; ++l) {
+    exchange(h, l - 1, VX);
+    for (Part& p : h.parts) {  // x += P ec  (multilevel.cpp:98-100)
+      PLevel& L = p.lv[l];
+      if (!L.active()) continue;
+      prolong_add(*L.P, vec(h, p, l - 1, VX), vec(h, p, l, VX) + L.off());
+    }
+    smooth(h, l, kpost, false);
+  }
+}
+
+// copy the caller's finest-level b, x into the partitioned buffers (and back);
+// emulated: global vectors; NCCL: this rank's own rows
+static void stage_in(Hier& h, const double* b, const double* x) {
+  if (h.whole()) return;
+  const int top = h.finest();
+  for (Part& p : h.parts) {
+    PLevel& L = p.lv[top];
+    if (!L.active()) continue;
+    const int64_t src = h.emulated ? (int64_t)L.lo * L.m : 0;
+    copy(h.ctx, L.v[VB].p + L.off(), b + src, L.n_own());
+    copy(h.ctx, L.v[VX].p + L.off(), x + src, L.n_own());
+  }
+}
+static void stage_out(Hier& h, double* x) {
+  if (h.whole()) return;
+  const int top = h.finest();
+  for (Part& p : h.parts) {
+    PLevel& L = p.lv[top];
+    if (!L.active()) continue;
+    const int64_t dst = h.emulated ? (int64_t)L.lo * L.m : 0;
+    copy(h.ctx, x + dst, L.v[VX].p + L.off(), L.n_own());
+  }
+}
+
+static void run_vcycle(Hier& h, int kpre, int kpost, const double* bf, double* xf) {
+  if (kpre + kpost < 1) fail(BMG_EINVAL, "v_cycle: cycle needs at least one smoothing step");
+  Ctx* ctx = h.ctx;
+  h.user_b = bf;
+  h.user_x = xf;
+  if (h.finest() == 0) {
+    stage_in(h, bf, xf);
+    coarse_solve(h);
+    stage_out(h, xf);
+    return;
+  }
+  if (!h.use_graph) {
+    stage_in(h, bf, xf);
+    enqueue_vcycle(h, kpre, kpost);
+    stage_out(h, xf);
+    return;
+  }
+  GraphKey key{kpre, kpost, bf, xf};
+  auto it = h.graphs.find(key);
+  if (it == h.graphs.end()) {
+    cudaStream_t user = ctx->stream;
+    ctx->stream = ctx->own;
+    const int64_t before = ctx->launches;
+    BMG_CUDA(cudaStreamBeginCapture(ctx->own, cudaStreamCaptureModeThreadLocal));
+    try {
+      stage_in(h, bf, xf);
+      enqueue_vcycle(h, kpre, kpost);
+      stage_out(h, xf);
+    } catch (...) {
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(ctx->own, &g);
+      if (g) cudaGraphDestroy(g);
+      ctx->stream = user;
+      ctx->launches = before;
+      throw;
+    }
+    cudaGraph_t g;
+    BMG_CUDA(cudaStreamEndCapture(ctx->own, &g));
+    ctx->stream = user;
+    cudaGraphExec_t ex;
+    BMG_CUDA(cudaGraphInstantiate(&ex, g, 0));
+    cudaGraphDestroy(g);
+    it = h.graphs.emplace(key, Hier::Captured{ex, ctx->launches - before}).first;
+    ctx->launches = before;
+  }
+  BMG_CUDA(cudaGraphLaunch(it->second.exec, ctx->stream));
+  ctx->launches += it->second.kernels;
+}
+
+// ============================================================================ construction
+static void coarse_factor(Hier& h, Part& p) {
+  Ctx* ctx = h.ctx;
+  const Bsr& a0 = *p.lv[0].A;
+  if (!(a0.uniform && a0.mr == a0.mc)) fail(BMG_EINVAL, "coarse solve: uniform block sizes required");
+  const int64_t N = a0.dim_r;
+  h.n0 = N;
+  p.ainv.alloc(std::max<int64_t>(N * N, 1));
+  BMG_CUDA(cudaMemsetAsync(p.ainv.p, 0, p.ainv.bytes(), ctx->stream));
+  kern::bsr_to_dense_kernel<<<std::max(1, std::min(a0.nbr, ctx->sms * 8)), 128, 0, ctx->stream>>>(
+      a0.vals.p, a0.row_ptr.p, a0.col.p, a0.nbr, a0.mr, a0.bs, p.ainv.p, N);
+  ctx->count();
+  BMG_CUDA(cudaGetLastError());
+  cusolverDnHandle_t s = ctx->cusolver();
+  int lwork = 0, lwork2 = 0;
+  if (cusolverDnDpotrf_bufferSize(s, CUBLAS_FILL_MODE_LOWER, (int)N, p.ainv.p, (int)N, &lwork) != CUSOLVER_STATUS_SUCCESS)
+    fail(BMG_ECUDA, "cusolverDnDpotrf_bufferSize failed");
+  if (cusolverDnDpotri_bufferSize(s, CUBLAS_FILL_MODE_LOWER, (int)N, p.ainv.p, (int)N, &lwork2) != CUSOLVER_STATUS_SUCCESS)
+    fail(BMG_ECUDA, "cusolverDnDpotri_bufferSize failed");
+  DBuf<double> work(std::max(std::max(lwork, lwork2), 1));
+  DBuf<int> info(1);
+  if (cusolverDnDpotrf(s, CUBLAS_FILL_MODE_LOWER, (int)N, p.ainv.p, (int)N, work.p, lwork, info.p) != CUSOLVER_STATUS_SUCCESS)
+    fail(BMG_ECUDA, "cusolverDnDpotrf failed");
+  int hinfo = 0;
+  BMG_CUDA(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (hinfo != 0) fail(BMG_ERUNTIME, "setup: coarsest operator is not positive definite");
+  if (cusolverDnDpotri(s, CUBLAS_FILL_MODE_LOWER, (int)N, p.ainv.p, (int)N, work.p, lwork2, info.p) != CUSOLVER_STATUS_SUCCESS)
+    fail(BMG_ECUDA, "cusolverDnDpotri failed");
+  BMG_CUDA(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (hinfo != 0) fail(BMG_ERUNTIME, "setup: coarse inverse failed");
+  kern::symmetrize_dense_kernel<<<grid1d(N * N), 256, 0, ctx->stream>>>(p.ainv.p, N);
+  ctx->count();
+  BMG_CUDA(cudaGetLastError());
+  BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+static void alloc_vectors(Hier& h, PLevel& L, bool top) {
+  for (int w = 0; w < VNUM; ++w) {
+    if (h.whole() && top && (w == VB || w == VX)) continue;  // caller's vectors
+    L.v[w].alloc(std::max<int64_t>(L.n_win(), 1));
+    BMG_CUDA(cudaMemsetAsync(L.v[w].p, 0, L.v[w].bytes(), h.ctx->stream));
+  }
+}
+
+static void record_stats(Hier& h) {
+  Part& p = h.parts[0];
+  h.stats.assign(h.finest() + 1, LevelStats());
+  for (int l = 0; l <= h.finest(); ++l) {
+    LevelStats& s = h.stats[l];
+    const PLevel& L = p.lv[l];
+    s.n = L.A->dim_r;
+    s.a_pass = L.A->pass_bytes();
+    if (l >= 1) {
+      for (auto& f : L.M->fwd) s.m_pass += f->pass_bytes();
+      for (auto& f : L.M->bwd) s.m_pass += f->pass_bytes();
+      s.r_pass = L.R->pass_bytes();
+      s.p_pass = L.P->pass_bytes();
+    }
+  }
+}
+
+// common tail of setup / create: whole-level layout, vectors, coarse factor
+static void finish_whole(Hier& h, int cap) {
+  Part& p = h.parts[0];
+  const int L = (int)p.lv.size();
+  h.nbr.assign(L, 0);
+  h.msz.assign(L, 0);
+  for (int l = 0; l < L; ++l) {
+    PLevel& lv = p.lv[l];
+    if (!(lv.A->uniform && lv.A->mr == lv.A->mc)) fail(BMG_EINVAL, "hierarchy: uniform square blocks required");
+    h.nbr[l] = lv.A->nbr;
+    h.msz[l] = lv.A->mr;
+    lv.lo = lv.wlo = 0;
+    lv.hi = lv.whi = lv.A->nbr;
+    lv.m = lv.A->mr;
+  }
+  const int64_t n0 = p.lv[0].A->dim_r;
+  if (n0 > cap) fail(BMG_EINVAL, "setup: coarsest level exceeds the dense-solve cap");
+  for (int l = 0; l < L; ++l) alloc_vectors(h, p.lv[l], l == L - 1);
+  h.bounds.assign(L, std::vector<int32_t>{0, 0});
+  h.wlo.assign(L, std::vector<int32_t>{0});
+  h.whi.assign(L, std::vector<int32_t>{0});
+  for (int l = 0; l < L; ++l) {
+    h.bounds[l][1] = h.nbr[l];
+    h.whi[l][0] = h.nbr[l];
+  }
+  h.granule_top = 1;
+  coarse_factor(h, p);
+  record_stats(h);
+}
+
+// rows [lo, hi) of g with columns shifted by -col_lo into a window of ncols blocks
+static std::unique_ptr<Bsr> slice_rows(const Bsr& g, int lo, int hi, int col_lo, int ncols) {
+  if (hi <= lo) return nullptr;
+  const int64_t p0 = g.h_row_ptr[lo], p1 = g.h_row_ptr[hi];
+  std::vector<int64_t> rp(hi - lo + 1);
+  for (int i = lo; i <= hi; ++i) rp[i - lo] = g.h_row_ptr[i] - p0;
+  std::vector<int32_t> col(p1 - p0);
+  for (int64_t q = p0; q < p1; ++q) {
+    const int c = g.h_col[q] - col_lo;
+    if (c < 0 || c >= ncols) fail(BMG_ERUNTIME, "partition: column outside the window");
+    col[q - p0] = c;
+  }
+  auto out = make_bsr_structure(g.ctx, hi - lo, g.rsz.data() + lo, ncols, g.csz.data() + col_lo, std::move(rp),
+                                std::move(col), false);
+  const int64_t v0 = g.h_voff[p0], v1 = g.h_voff[p1];
+  if (v1 > v0)
+    BMG_CUDA(cudaMemcpyAsync(out->vals.p, g.vals.p + v0, (v1 - v0) * sizeof(double), cudaMemcpyDeviceToDevice,
+                             g.ctx->stream));
+  return out;
+}
+
+// Split the (identically built) whole hierarchy into row strips.  rank < 0:
+// every virtual rank in this process (emulation); else only this rank's share
+// and the context's NCCL communicator moves the halos.
+static void partition(Hier& h, int world, int rank, const int32_t* granule, int agglomerate) {
+  if (!h.whole()) fail(BMG_EINVAL, "partition: hierarchy is already partitioned");
+  if (world < 1) fail(BMG_EINVAL, "partition: world must be >= 1");
+  if (world == 1) {  // nothing to split; record the norm segmentation so 1-rank
+                     // and N-rank residual norms are summed identically
+    h.granule_top = granule ? std::max(1, granule[h.finest()]) : 1;
+    return;
+  }
+  if (rank >= 0 && (!h.ctx->nccl || h.ctx->world != world || h.ctx->rank != rank))
+    fail(BMG_EINVAL, "partition: context is not an NCCL context of this rank/world");
+  Ctx* ctx = h.ctx;
+  BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+  const int L = h.finest() + 1;
+  agglomerate = std::max(1, agglomerate);  // level 0 (dense solve) always on rank 0
+  Part& G = h.parts[0];
+  std::vector<std::vector<int32_t>> B(L, std::vector<int32_t>(world + 1));
+  for (int l = 0; l < L; ++l)
+    partition_rows(h.nbr[l], G.lv[l].A->h_row_ptr.data(), world, granule ? granule[l] : 1, l < agglomerate,
+                   B[l].data());
+  // windows: hull over everything that reads level-l vectors
+  std::vector<std::vector<int32_t>> WL(L, std::vector<int32_t>(world)), WH(L, std::vector<int32_t>(world));
+  for (int l = 0; l < L; ++l)
+    for (int r = 0; r < world; ++r) {
+      int a = B[l][r], b = B[l][r + 1];
+      auto join = [&](const Bsr& m, int lo, int hi, int clo, int chi) {
+        if (hi <= lo) return;
+        int32_t e0, e1;
+        row_window(m.h_row_ptr.data(), m.h_col.data(), lo, hi, clo, chi, &e0, &e1);
+        if (a >= b) {
+          a = e0;
+          b = e1;
+        } else if (e1 > e0) {
+          a = std::min(a, e0);
+          b = std::max(b, e1);
+        }
+      };
+      const PLevel& lv = G.lv[l];
+      join(*lv.A, B[l][r], B[l][r + 1], B[l][r], B[l][r + 1]);
+      if (l >= 1) {
+        for (auto& f : lv.M->fwd) join(*f, B[l][r], B[l][r + 1], B[l][r], B[l][r + 1]);
+        for (auto& f : lv.M->bwd) join(*f, B[l][r], B[l][r + 1], B[l][r], B[l][r + 1]);
+        join(*lv.R, B[l - 1][r], B[l - 1][r + 1], B[l][r], B[l][r + 1]);
+      }
+      if (l + 1 < L) join(*G.lv[l + 1].P, B[l + 1][r], B[l + 1][r + 1], B[l][r], B[l][r + 1]);
+      if (a >= b) a = b = 0;
+      WL[l][r] = a;
+      WH[l][r] = b;
+    }
+  // build the parts
+  std::vector<Part> parts;
+  for (int r = 0; r < world; ++r) {
+    if (rank >= 0 && r != rank) continue;
+    Part p;
+    p.rank = r;
+    p.lv.resize(L);
+    for (int l = 0; l < L; ++l) {
+      PLevel& d = p.lv[l];
+      const PLevel& s = G.lv[l];
+      d.lo = B[l][r];
+      d.hi = B[l][r + 1];
+      d.wlo = WL[l][r];
+      d.whi = WH[l][r];
+      d.m = h.msz[l];
+      d.beta = s.beta;
+      const int nwin = d.whi - d.wlo;
+      d.A_own = slice_rows(*s.A, d.lo, d.hi, d.wlo, nwin);
+      d.A = d.A_own.get();
+      if (l >= 1) {
+        if (d.hi > d.lo) {
+          d.M_own = std::make_unique<Fsai>();
+          d.M_own->ctx = ctx;
+          d.M_own->dim = (int)d.n_own();
+          for (auto& f : s.M->fwd) d.M_own->fwd.push_back(slice_rows(*f, d.lo, d.hi, d.wlo, nwin));
+          for (auto& f : s.M->bwd) d.M_own->bwd.push_back(slice_rows(*f, d.lo, d.hi, d.wlo, nwin));
+          d.M = d.M_own.get();
+        }
+        d.P_own = slice_rows(*s.P, d.lo, d.hi, WL[l - 1][r], WH[l - 1][r] - WL[l - 1][r]);
+        d.P = d.P_own.get();
+        d.R_own = slice_rows(*s.R, B[l - 1][r], B[l - 1][r + 1], d.wlo, nwin);
+        d.R = d.R_own.get();
+      }
+      alloc_vectors(h, d, false);
+    }
+    if (r == 0) p.ainv = std::move(G.ainv);
+    parts.push_back(std::move(p));
+  }
+  BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+  h.drop_graphs();
+  h.parts = std::move(parts);  // frees the whole-level objects
+  h.world = world;
+  h.emulated = rank < 0;
+  h.bounds = B;
+  h.wlo = WL;
+  h.whi = WH;
+  h.granule_top = granule ? std::max(1, granule[L - 1]) : 1;
+}
+
+// partition-invariant ||r||_2 of the finest level (segments = granules)
+static double finest_norm(Hier& h, const double* r_whole) {
+  Ctx* ctx = h.ctx;
+  const int top = h.finest();
+  const int m = h.msz[top];
+  const int gran = h.granule_top;
+  const int nseg = (h.nbr[top] + gran - 1) / gran;
+  if (h.seg.n < (size_t)nseg) h.seg.alloc(nseg);
+  BMG_CUDA(cudaMemsetAsync(h.seg.p, 0, nseg * sizeof(double), ctx->stream));
+  for (Part& p : h.parts) {
+    PLevel& L = p.lv[top];
+    if (!L.active()) continue;
+    const double* r = h.whole() ? r_whole : L.v[VR].p + L.off();
+    const int s0 = L.lo / gran;
+    const int ns = (L.hi - L.lo + gran - 1) / gran;
+    kern::segment_sq_kernel<<<ns, 256, 0, ctx->stream>>>(r, L.n_own(), (int64_t)gran * m, h.seg.p + s0);
+    ctx->count();
+    BMG_CUDA(cudaGetLastError());
+  }
+  if (!h.whole() && !h.emulated) {
+    // one rank owns each segment; the others contribute exact zeros
+    nccl_check(ncclAllReduce(h.seg.p, h.seg.p, nseg, ncclDouble, ncclSum, static_cast<ncclComm_t>(ctx->nccl),
+                             ctx->stream),
+               "ncclAllReduce");
+  }
+  std::vector<double> hs(nseg);
+  BMG_CUDA(cudaMemcpyAsync(hs.data(), h.seg.p, nseg * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+  double s = 0.0;
+  for (double v : hs) s += v;
+  return std::sqrt(s);
+}
+
+static void finest_residual(Hier& h, const double* b, double* x, double* rtmp) {
+  const int top = h.finest();
+  if (h.whole()) {
+    residual(*h.parts[0].lv[top].A, b, x, rtmp);
+    return;
+  }
+  h.user_b = b;
+  h.user_x = x;
+  stage_in(h, b, x);
+  exchange(h, top, VX);
+  for (Part& p : h.parts) {
+    PLevel& L = p.lv[top];
+    if (!L.active()) continue;
+    residual(*L.A, L.v[VB].p + L.off(), L.v[VX].p, L.v[VR].p + L.off());
+  }
+}
+
+}  // namespace bmg
+
+// ============================================================================ C ABI
+using namespace bmg;
+
+namespace {
+const Bsr* B_(const bmg_bsr* a) { return reinterpret_cast<const Bsr*>(a); }
+const Vec* V_(const bmg_vec* v) { return reinterpret_cast<const Vec*>(v); }
+Vec* V_(bmg_vec* v) { return reinterpret_cast<Vec*>(v); }
+const Fsai* M_(const bmg_fsai* m) { return reinterpret_cast<const Fsai*>(m); }
+Hier* H_(bmg_hier* h) { return reinterpret_cast<Hier*>(h); }
+const Hier* H_(const bmg_hier* h) { return reinterpret_cast<const Hier*>(h); }
+void need_len(const Vec* v, int64_t n, const char* what) {
+  if (v->n != n) fail(BMG_EINVAL, std::string(what) + ": vector length does not match layout");
+}
+// length of the finest-level vectors the caller passes
+int64_t finest_len(const Hier& h) {
+  const int top = h.finest();
+  if (h.whole() || h.emulated) return (int64_t)h.nbr[top] * h.msz[top];
+  return h.parts[0].lv[top].n_own();
+}
+}  // namespace
+
+extern "C" {
+
+// setup (multilevel.cpp:36-75) with every step on the device
+int bmg_hier_setup(const bmg_bsr* a_finest, int ntransfers, const bmg_bsr* const* transfers,
+                   const bmg_setup_params* params, bmg_hier** out) {
+  return guard([&] {
+    bmg_setup_params prm;
+    if (params)
+      prm = *params;
+    else
+      bmg_setup_params_default(&prm);
+    const Bsr* af = B_(a_finest);
+    Ctx* ctx = af->ctx;
+    ctx->activate();
+    if (ntransfers < 0) fail(BMG_EINVAL, "setup: negative transfer count");
+    auto h = std::make_unique<Hier>();
+    h->ctx = ctx;
+    h->parts.resize(1);
+    Part& p = h->parts[0];
+    const int depth = ntransfers;
+    p.lv.resize(depth + 1);
+    p.lv[depth].A = af;
+    for (int l = depth; l >= 1; --l) {
+      PLevel& L = p.lv[l];
+      L.P = B_(transfers[l - 1]);
+      L.R_own = bsr_transpose(*L.P);
+      L.R = L.R_own.get();
+      p.lv[l - 1].A_own = galerkin(*L.A, *L.P);
+      p.lv[l - 1].A = p.lv[l - 1].A_own.get();
+    }
+    for (int l = 1; l <= depth; ++l) {
+      PLevel& L = p.lv[l];
+      L.M_own = fsai_build(*L.A, prm.fsai_kind, prm.t_max, prm.tau, prm.nest);
+      L.M = L.M_own.get();
+      L.beta = lanczos_lambda_max(*L.A, *L.M, prm.lanczos_iters, prm.lanczos_safety, prm.seed);
+    }
+    finish_whole(*h, prm.coarse_dim_cap);
+    *out = reinterpret_cast<bmg_hier*>(h.release());
+  });
+}
+
+int bmg_hier_create(bmg_ctx* ctx, int nlevels, const bmg_bsr* const* A, const bmg_bsr* const* P,
+                    const bmg_fsai* const* Mh, const double* beta, int coarse_dim_cap, bmg_hier** out) {
+  return guard([&] {
+    Ctx* c = reinterpret_cast<Ctx*>(ctx);
+    c->activate();
+    if (nlevels < 1) fail(BMG_EINVAL, "hierarchy needs at least one level");
+    auto h = std::make_unique<Hier>();
+    h->ctx = c;
+    h->parts.resize(1);
+    Part& p = h->parts[0];
+    p.lv.resize(nlevels);
+    for (int l = 0; l < nlevels; ++l) {
+      PLevel& L = p.lv[l];
+      L.A = B_(A[l]);
+      if (l >= 1) {
+        L.P = B_(P[l]);
+        if (L.P->dim_r != L.A->dim_r || L.P->dim_c != B_(A[l - 1])->dim_r)
+          fail(BMG_EINVAL, "hierarchy: prolongation shape does not match the levels");
+        L.R_own = bsr_transpose(*L.P);
+        L.R = L.R_own.get();
+        L.M = M_(Mh[l]);
+        L.beta = beta[l];
+        if (!(L.beta > 0.0)) fail(BMG_EINVAL, "cheb_fourth_apply: beta must be positive");
+      }
+    }
+    finish_whole(*h, coarse_dim_cap);
+    *out = reinterpret_cast<bmg_hier*>(h.release());
+  });
+}
+
+int bmg_hier_partition(bmg_hier* hh, int world, int rank, const int32_t* granule, int agglomerate) {
+  return guard([&] {
+    Hier* h = H_(hh);
+    h->ctx->activate();
+    partition(*h, world, rank, granule, agglomerate);
+  });
+}
+
+int bmg_hier_part_info(const bmg_hier* hh, int level, int rank, int32_t* lo, int32_t* hi, int32_t* wlo,
+                       int32_t* whi) {
+  return guard([&] {
+    const Hier* h = H_(hh);
+    if (level < 0 || level > h->finest()) fail(BMG_ERANGE, "hierarchy: level out of range");
+    if (rank < 0 || rank >= h->world) fail(BMG_ERANGE, "hierarchy: rank out of range");
+    *lo = h->bounds[level][rank];
+    *hi = h->bounds[level][rank + 1];
+    *wlo = h->wlo[level][h->world == 1 ? 0 : rank];
+    *whi = h->whi[level][h->world == 1 ? 0 : rank];
+  });
+}
+
+int bmg_hier_destroy(bmg_hier* h) {
+  return guard([&] {
+    Hier* p = H_(h);
+    if (p) BMG_CUDA(cudaStreamSynchronize(p->ctx->stream));
+    delete p;
+  });
+}
+
+int bmg_hier_info(const bmg_hier* hh, int* nlevels, int64_t* device_bytes) {
+  return guard([&] {
+    const Hier* h = H_(hh);
+    if (nlevels) *nlevels = h->finest() + 1;
+    if (device_bytes) {
+      int64_t b = 0;
+      for (const Part& p : h->parts) {
+        b += (int64_t)p.ainv.bytes();
+        for (const auto& L : p.lv) {
+          if (L.A_own) b += L.A_own->device_bytes();
+          if (L.R_own) b += L.R_own->device_bytes();
+          if (L.P_own) b += L.P_own->device_bytes();
+          if (L.M_own) {
+            for (auto& f : L.M_own->fwd) b += f->device_bytes();
+            for (auto& f : L.M_own->bwd) b += f->device_bytes();
+          }
+          for (int w = 0; w < VNUM; ++w) b += (int64_t)L.v[w].bytes();
+        }
+      }
+      *device_bytes = b;
+    }
+  });
+}
+
+int bmg_hier_beta(const bmg_hier* hh, int level, double* beta) {
+  return guard([&] {
+    const Hier* h = H_(hh);
+    if (level < 1 || level > h->finest()) fail(BMG_ERANGE, "hierarchy: level out of range");
+    *beta = h->parts[0].lv[level].beta;
+  });
+}
+
+int bmg_hier_level(const bmg_hier* hh, int level, const bmg_bsr** a, const bmg_bsr** p, const bmg_fsai** m) {
+  return guard([&] {
+    const Hier* h = H_(hh);
+    if (level < 0 || level > h->finest()) fail(BMG_ERANGE, "hierarchy: level out of range");
+    const PLevel& L = h->parts[0].lv[level];
+    if (a) *a = reinterpret_cast<const bmg_bsr*>(L.A);
+    if (p) *p = reinterpret_cast<const bmg_bsr*>(L.P);
+    if (m) *m = reinterpret_cast<const bmg_fsai*>(L.M);
+  });
+}
+
+// algorithmic HBM bytes of one V(k_pre, k_post) cycle over all ranks (BASELINE.md
+// §3 byte model, with the exact A*0 skip on coarse levels)
+int bmg_hier_cycle_bytes(const bmg_hier* hh, int kpre, int kpost, int64_t* bytes) {
+  return guard([&] {
+    const Hier* h = H_(hh);
+    int64_t tot = 0;
+    const int top = h->finest();
+    for (int l = 1; l <= top; ++l) {
+      const LevelStats& s = h->stats[l];
+      const int64_t n = s.n, nc = h->stats[l - 1].n;
+      const int64_t apass = s.a_pass + 24 * n;  // x, b read; r write
+      const int64_t gvec = 16 * n + 40 * n;     // G: r, w; G^T+cheb: w, p rw, x rw
+      const int steps = kpre + kpost;
+      int64_t lvl = steps * (apass + s.m_pass + gvec);
+      if (l < top && kpre > 0) lvl -= apass + 8 * n;  // first coarse pre-step: A*0 skipped, x not read
+      lvl += apass;                                   // residual before restriction
+      lvl += s.r_pass + 8 * n + 8 * nc;               // restriction
+      lvl += s.p_pass + 8 * nc + 16 * n;              // prolongation x += P e
+      tot += lvl;
+    }
+    tot += h->n0 * h->n0 * 8 + 16 * h->n0;  // dense coarse solve
+    *bytes = tot;
+  });
+}
+
+int bmg_hier_use_graph(bmg_hier* hh, int on) {
+  return guard([&] { H_(hh)->use_graph = on != 0; });
+}
+
+int bmg_vcycle(bmg_hier* hh, int kpre, int kpost, const bmg_vec* b, bmg_vec* x) {
+  return guard([&] {
+    Hier* h = H_(hh);
+    const int64_t n = finest_len(*h);
+    need_len(V_(b), n, "v_cycle");
+    need_len(V_(x), n, "v_cycle");
+    run_vcycle(*h, kpre, kpost, V_(b)->d.p, V_(x)->d.p);
+  });
+}
+
+int bmg_vcycle_host(bmg_hier* hh, int kpre, int kpost, const double* b, double* x) {
+  return guard([&] {
+    Hier* h = H_(hh);
+    Ctx* ctx = h->ctx;
+    const int64_t n = finest_len(*h);
+    if (h->io_b.n < (size_t)n) {
+      h->io_b.alloc(std::max<int64_t>(n, 1));
+      h->io_x.alloc(std::max<int64_t>(n, 1));
+    }
+    BMG_CUDA(cudaMemcpyAsync(h->io_b.p, b, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    BMG_CUDA(cudaMemcpyAsync(h->io_x.p, x, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    run_vcycle(*h, kpre, kpost, h->io_b.p, h->io_x.p);
+    BMG_CUDA(cudaMemcpyAsync(x, h->io_x.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+// residual-history driver modelled on measure_rates (experiments.cpp:15-67)
+int bmg_solve(bmg_hier* hh, int kpre, int kpost, const bmg_vec* bh, bmg_vec* xh, double tol, int max_iter,
+              double* hist, int* iters, int* status) {
+  return guard([&] {
+    Hier* h = H_(hh);
+    const int64_t n = finest_len(*h);
+    need_len(V_(bh), n, "solve");
+    need_len(V_(xh), n, "solve");
+    const double* b = V_(bh)->d.p;
+    double* x = V_(xh)->d.p;
+    PLevel& F = h->parts[0].lv[h->finest()];
+    auto resid = [&]() {
+      finest_residual(*h, b, x, F.v[VR].p);
+      return finest_norm(*h, F.v[VR].p);
+    };
+    hist[0] = resid();
+    int it = 0, st = 1;
+    if (hist[0] == 0.0) st = 0;
+    while (st == 1 && it < max_iter) {
+      run_vcycle(*h, kpre, kpost, b, x);
+      ++it;
+      hist[it] = resid();
+      const double growth = hist[it] / std::max(hist[it - 1], 1e-300);
+      if (!std::isfinite(hist[it]) || growth > 1e6) {
+        st = 2;
+        break;
+      }
+      if (hist[it] / hist[0] < tol) st = 0;
+    }
+    *iters = it;
+    *status = st;
+  });
+}
+
+int bmg_ctx_create_nccl(int device, int rank, int world, const unsigned char* id128, bmg_ctx** out) {
+  return guard([&] {
+    bmg_ctx* c = nullptr;
+    const int st = bmg_ctx_create(device, &c);
+    if (st != BMG_OK) fail(st, bmg_last_error());
+    Ctx* ctx = reinterpret_cast<Ctx*>(c);
+    std::unique_ptr<Ctx> own(ctx);
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    ncclComm_t comm;
+    nccl_check(ncclCommInitRank(&comm, world, id, rank), "ncclCommInitRank");
+    ctx->nccl = comm;
+    ctx->rank = rank;
+    ctx->world = world;
+    *out = reinterpret_cast<bmg_ctx*>(own.release());
+  });
+}
+
+int bmg_nccl_unique_id(unsigned char* id128) {
+  return guard([&] {
+    ncclUniqueId id;
+    nccl_check(ncclGetUniqueId(&id), "ncclGetUniqueId");
+    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(id128, &id, sizeof(id));
+  });
+}
+
+}  // extern "C"

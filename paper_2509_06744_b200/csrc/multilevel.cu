@@ -53,50 +53,6 @@ __global__ void symmetrize_kernel(const double* __restrict__ C, const int64_t* _
   }
 }
 
-__global__ void bsr_to_dense_kernel(const double* __restrict__ vals, const int64_t* __restrict__ row_ptr,
-                                    const int32_t* __restrict__ col, int nbr, int m, int bs,
-                                    double* __restrict__ dense, int64_t N) {
-  for (int i = blockIdx.x; i < nbr; i += gridDim.x)
-    for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
-      const int j = col[p];
-      for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-        const int r = e / m, c = e - r * m;
-        dense[((int64_t)i * m + r) * N + (int64_t)j * m + c] = vals[p * bs + e];
-      }
-    }
-}
-
-__global__ void symmetrize_dense_kernel(double* a, int64_t N) {
-  // cuSOLVER potri (column-major lower) leaves the row-major upper triangle
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < N * N; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e / N, c = e - r * N;
-    if (r > c) a[e] = a[c * N + r];
-  }
-}
-
-// x = Ainv b (dense, row-major): warp per row, double2 loads
-__global__ void __launch_bounds__(256) gemv_kernel(const double* __restrict__ a, const double* __restrict__ b,
-                                                   double* __restrict__ x, int64_t N) {
-  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (row >= N) return;
-  const double* ar = a + row * N;
-  double s = 0.0;
-  if ((N & 1) == 0) {
-    const double2* a2 = reinterpret_cast<const double2*>(ar);
-    const double2* b2 = reinterpret_cast<const double2*>(b);
-    for (int64_t q = lane; q < N / 2; q += 32) {
-      const double2 av = __ldg(a2 + q), bv = __ldg(b2 + q);
-      s = __fma_rn(av.x, bv.x, s);
-      s = __fma_rn(av.y, bv.y, s);
-    }
-  } else {
-    for (int64_t q = lane; q < N; q += 32) s = __fma_rn(__ldg(ar + q), __ldg(b + q), s);
-  }
-  for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o));
-  if (lane == 0) x[row] = s;
-}
-
 __global__ void rng_symmetric_kernel(double* v, int64_t n, uint64_t seed) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     uint64_t z = seed + (uint64_t)(i + 1) * 0x9e3779b97f4a7c15ULL;  // rng.hpp:22-24
@@ -386,219 +342,35 @@ double lanczos_lambda_max(const Bsr& a, const Fsai& m, int iters, double safety,
   return safety * ev.back();
 }
 
-// ============================================================================ hierarchy
-struct Level {
-  const Bsr* A = nullptr;
-  const Bsr* P = nullptr;  // prolongation from level-1 (unset at 0)
-  const Bsr* R = nullptr;  // P^T
-  const Fsai* M = nullptr;
-  double beta = 1.0;
-  std::unique_ptr<Bsr> A_own, P_own, R_own;
-  std::unique_ptr<Fsai> M_own;
-  DBuf<double> b, x, r, w, p, t;
-  int64_t n = 0;
-};
-
-struct GraphKey {
-  int kpre, kpost;
-  const double* b;
-  double* x;
-  bool operator<(const GraphKey& o) const { return std::tie(kpre, kpost, b, x) < std::tie(o.kpre, o.kpost, o.b, o.x); }
-};
-
-struct Hier {
-  Ctx* ctx = nullptr;
-  std::vector<Level> lv;  // 0 = coarsest
-  DBuf<double> ainv;      // dense A_0^{-1}
-  int64_t n0 = 0;
-  bool use_graph = true;
-  struct Captured {
-    cudaGraphExec_t exec;
-    int64_t kernels;
-  };
-  std::map<GraphKey, Captured> graphs;
-  DBuf<double> io_b, io_x;  // e2e staging
-  ~Hier() {
-    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
-  }
-  int finest() const { return (int)lv.size() - 1; }
-};
-
-static void alloc_level_vectors(Level& L, bool finest) {
-  L.n = L.A->dim_r;
-  if (!finest) {
-    L.b.alloc(L.n);
-    L.x.alloc(L.n);
-  }
-  L.r.alloc(L.n);
-  L.w.alloc(L.n);
-  L.p.alloc(L.n);
-  L.t.alloc(L.n);
-}
-
-static void coarse_factor(Hier& h) {
-  Ctx* ctx = h.ctx;
-  const Bsr& a0 = *h.lv[0].A;
-  if (!(a0.uniform && a0.mr == a0.mc)) fail(BMG_EINVAL, "coarse solve: uniform block sizes required");
-  const int64_t N = a0.dim_r;
-  h.n0 = N;
-  h.ainv.alloc(std::max<int64_t>(N * N, 1));
-  BMG_CUDA(cudaMemsetAsync(h.ainv.p, 0, h.ainv.bytes(), ctx->stream));
-  kern::bsr_to_dense_kernel<<<std::max(1, std::min(a0.nbr, ctx->sms * 8)), 128, 0, ctx->stream>>>(
-      a0.vals.p, a0.row_ptr.p, a0.col.p, a0.nbr, a0.mr, a0.bs, h.ainv.p, N);
-  ctx->count();
-  BMG_CUDA(cudaGetLastError());
-  cusolverDnHandle_t s = ctx->cusolver();
-  int lwork = 0, lwork2 = 0;
-  if (cusolverDnDpotrf_bufferSize(s, CUBLAS_FILL_MODE_LOWER, (int)N, h.ainv.p, (int)N, &lwork) != CUSOLVER_STATUS_SUCCESS)
-    fail(BMG_ECUDA, "cusolverDnDpotrf_bufferSize failed");
-  if (cusolverDnDpotri_bufferSize(s, CUBLAS_FILL_MODE_LOWER, (int)N, h.ainv.p, (int)N, &lwork2) != CUSOLVER_STATUS_SUCCESS)
-    fail(BMG_ECUDA, "cusolverDnDpotri_bufferSize failed");
-  DBuf<double> work(std::max(std::max(lwork, lwork2), 1));
-  DBuf<int> info(1);
-  if (cusolverDnDpotrf(s, CUBLAS_FILL_MODE_LOWER, (int)N, h.ainv.p, (int)N, work.p, lwork, info.p) != CUSOLVER_STATUS_SUCCESS)
-    fail(BMG_ECUDA, "cusolverDnDpotrf failed");
-  int hinfo = 0;
-  BMG_CUDA(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-  BMG_CUDA(cudaStreamSynchronize(ctx->stream));
-  if (hinfo != 0) fail(BMG_ERUNTIME, "setup: coarsest operator is not positive definite");
-  if (cusolverDnDpotri(s, CUBLAS_FILL_MODE_LOWER, (int)N, h.ainv.p, (int)N, work.p, lwork2, info.p) != CUSOLVER_STATUS_SUCCESS)
-    fail(BMG_ECUDA, "cusolverDnDpotri failed");
-  BMG_CUDA(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-  BMG_CUDA(cudaStreamSynchronize(ctx->stream));
-  if (hinfo != 0) fail(BMG_ERUNTIME, "setup: coarse inverse failed");
-  kern::symmetrize_dense_kernel<<<grid1d(N * N), 256, 0, ctx->stream>>>(h.ainv.p, N);
-  ctx->count();
-  BMG_CUDA(cudaGetLastError());
-  BMG_CUDA(cudaStreamSynchronize(ctx->stream));
-}
-
-static void finish_hier(Hier& h, int cap) {
-  const int64_t n0 = h.lv[0].A->dim_r;
-  if (n0 > cap) fail(BMG_EINVAL, "setup: coarsest level exceeds the dense-solve cap");
-  for (int l = 0; l <= h.finest(); ++l) alloc_level_vectors(h.lv[l], l == h.finest());
-  coarse_factor(h);
-}
-
-// one fourth-kind smoothing application (chebyshev.hpp:48-69) on level l
-static void smooth(Level& L, int k, const double* b, double* x, bool xzero) {
-  if (k < 1) return;
-  const double d = 4.0 / L.beta;
-  const Fsai& M = *L.M;
+// ============================================================================ standalone smoother
+// cheb_fourth_apply (chebyshev.hpp:48-69) on one device: r = b - A x; M r as the
+// forward passes then the transposes, the last transpose fused with the update.
+static void smooth_single(const Bsr& A, const Fsai& M, double beta, int k, const double* b, double* x, double* r,
+                          double* w, double* t, double* p) {
+  const double d = 4.0 / beta;
   for (int s = 1; s <= k; ++s) {
-    const double* rsrc;
-    if (s == 1 && xzero) {
-      rsrc = b;  // A * 0 = 0: r = b exactly
-    } else {
-      residual(*L.A, b, x, L.r.p);
-      rsrc = L.r.p;
-    }
-    // forward chain: w = F_n ... F_0 r  (nest = 0: w = G r)
-    const double* cur = rsrc;
-    double* bufs[2] = {L.w.p, L.t.p};
-    int wsel = 0;
+    residual(A, b, x, r);
+    const double* cur = r;
+    double* bufs[2] = {w, t};
+    int sel = 0;
     for (const auto& f : M.fwd) {
-      spmv(*f, cur, bufs[wsel]);
-      cur = bufs[wsel];
-      wsel ^= 1;
+      spmv(*f, cur, bufs[sel]);
+      cur = bufs[sel];
+      sel ^= 1;
     }
     for (size_t i = M.bwd.size(); i-- > 1;) {
-      spmv(*M.bwd[i], cur, bufs[wsel]);
-      cur = bufs[wsel];
-      wsel ^= 1;
+      spmv(*M.bwd[i], cur, bufs[sel]);
+      cur = bufs[sel];
+      sel ^= 1;
     }
     if (s == 1) {
-      const double dmu = d * ((2.0 * 0 + 1.0) / (2.0 * 0 + 3.0));
-      gt_cheb(*M.bwd[0], cur, L.p.p, x, 0.0, dmu, true, xzero);
+      gt_cheb(*M.bwd[0], cur, p, x, 0.0, d * ((2.0 * 0 + 1.0) / (2.0 * 0 + 3.0)), true, false);
     } else {
       const double mu_prev = (2.0 * (s - 2) + 1.0) / (2.0 * (s - 2) + 3.0);
       const double mu = (2.0 * (s - 1) + 1.0) / (2.0 * (s - 1) + 3.0);
-      gt_cheb(*M.bwd[0], cur, L.p.p, x, mu_prev * mu_prev, d * mu, false, false);
+      gt_cheb(*M.bwd[0], cur, p, x, mu_prev * mu_prev, d * mu, false, false);
     }
   }
-}
-
-// v_cycle (multilevel.cpp:77-103), recursion unrolled: down, coarse solve, up
-static void enqueue_vcycle(Hier& h, int kpre, int kpost, const double* bf, double* xf) {
-  Ctx* ctx = h.ctx;
-  const int top = h.finest();
-  std::vector<const double*> B(top + 1);
-  std::vector<double*> X(top + 1);
-  for (int l = 0; l <= top; ++l) {
-    B[l] = l == top ? bf : h.lv[l].b.p;
-    X[l] = l == top ? xf : h.lv[l].x.p;
-  }
-  for (int l = top; l >= 1; --l) {
-    Level& L = h.lv[l];
-    const bool xzero = l < top;
-    const double* r;
-    if (kpre > 0) {
-      smooth(L, kpre, B[l], X[l], xzero);
-      residual(*L.A, B[l], X[l], L.r.p);
-      r = L.r.p;
-    } else if (xzero) {
-      fill(ctx, X[l], L.n, 0.0);
-      r = B[l];
-    } else {
-      residual(*L.A, B[l], X[l], L.r.p);
-      r = L.r.p;
-    }
-    spmv(*L.R, r, h.lv[l - 1].b.p);  // rc = P^T r
-  }
-  {
-    const int64_t N = h.n0;
-    kern::gemv_kernel<<<(int)((N * 32 + 255) / 256), 256, 0, ctx->stream>>>(h.ainv.p, B[0], X[0], N);
-    ctx->count();
-    BMG_LAUNCHED(ctx->stream, "gemv_kernel");
-  }
-  for (int l = 1; l <= top; ++l) {
-    Level& L = h.lv[l];
-    prolong_add(*L.P, X[l - 1], X[l]);  // x += P ec
-    smooth(L, kpost, B[l], X[l], false);
-  }
-}
-
-static void run_vcycle(Hier& h, int kpre, int kpost, const double* bf, double* xf) {
-  if (kpre + kpost < 1) fail(BMG_EINVAL, "v_cycle: cycle needs at least one smoothing step");
-  Ctx* ctx = h.ctx;
-  if (!h.use_graph || h.finest() == 0) {
-    if (h.finest() == 0) {
-      const int64_t N = h.n0;
-      kern::gemv_kernel<<<(int)((N * 32 + 255) / 256), 256, 0, ctx->stream>>>(h.ainv.p, bf, xf, N);
-      ctx->count();
-      BMG_CUDA(cudaGetLastError());
-      return;
-    }
-    enqueue_vcycle(h, kpre, kpost, bf, xf);
-    return;
-  }
-  GraphKey key{kpre, kpost, bf, xf};
-  auto it = h.graphs.find(key);
-  if (it == h.graphs.end()) {
-    cudaStream_t user = ctx->stream;
-    ctx->stream = ctx->own;
-    const int64_t before = ctx->launches;
-    BMG_CUDA(cudaStreamBeginCapture(ctx->own, cudaStreamCaptureModeThreadLocal));
-    try {
-      enqueue_vcycle(h, kpre, kpost, bf, xf);
-    } catch (...) {
-      cudaGraph_t g;
-      cudaStreamEndCapture(ctx->own, &g);
-      if (g) cudaGraphDestroy(g);
-      ctx->stream = user;
-      throw;
-    }
-    cudaGraph_t g;
-    BMG_CUDA(cudaStreamEndCapture(ctx->own, &g));
-    ctx->stream = user;
-    cudaGraphExec_t ex;
-    BMG_CUDA(cudaGraphInstantiate(&ex, g, 0));
-    cudaGraphDestroy(g);
-    it = h.graphs.emplace(key, Hier::Captured{ex, ctx->launches - before}).first;
-    ctx->launches = before;
-  }
-  BMG_CUDA(cudaGraphLaunch(it->second.exec, ctx->stream));
-  ctx->launches += it->second.kernels;
 }
 
 }  // namespace bmg
@@ -688,16 +460,9 @@ int bmg_cheb4_apply(const bmg_bsr* ah, const bmg_fsai* mh, const bmg_vec* b, bmg
     const Bsr* a = B(ah);
     need_len(V(b), a->dim_r, "cheb_fourth_apply");
     need_len(V(x), a->dim_r, "cheb_fourth_apply");
-    Level L;
-    L.A = a;
-    L.M = M(mh);
-    L.beta = beta;
-    L.n = a->dim_r;
-    L.r.alloc(std::max<int64_t>(L.n, 1));
-    L.w.alloc(std::max<int64_t>(L.n, 1));
-    L.p.alloc(std::max<int64_t>(L.n, 1));
-    L.t.alloc(std::max<int64_t>(L.n, 1));
-    smooth(L, k, V(b)->d.p, V(x)->d.p, false);
+    const int64_t n = std::max<int64_t>(a->dim_r, 1);
+    DBuf<double> r(n), w(n), t(n), p(n);
+    smooth_single(*a, *M(mh), beta, k, V(b)->d.p, V(x)->d.p, r.p, w.p, t.p, p.p);
     BMG_CUDA(cudaStreamSynchronize(a->ctx->stream));
   });
 }
@@ -707,210 +472,6 @@ int bmg_lanczos_lambda_max(const bmg_bsr* a, const bmg_fsai* m, int iters, doubl
   return guard([&] {
     B(a)->ctx->activate();
     *beta = lanczos_lambda_max(*B(a), *M(m), iters, safety, seed);
-  });
-}
-
-// setup (multilevel.cpp:36-75) with every step on the device
-int bmg_hier_setup(const bmg_bsr* a_finest, int ntransfers, const bmg_bsr* const* transfers,
-                   const bmg_setup_params* params, bmg_hier** out) {
-  return guard([&] {
-    bmg_setup_params prm;
-    if (params)
-      prm = *params;
-    else
-      bmg_setup_params_default(&prm);
-    const Bsr* af = B(a_finest);
-    Ctx* ctx = af->ctx;
-    ctx->activate();
-    if (ntransfers < 0) fail(BMG_EINVAL, "setup: negative transfer count");
-    auto h = std::make_unique<Hier>();
-    h->ctx = ctx;
-    const int depth = ntransfers;
-    h->lv.resize(depth + 1);
-    h->lv[depth].A = af;
-    for (int l = depth; l >= 1; --l) {
-      Level& L = h->lv[l];
-      L.P = B(transfers[l - 1]);
-      L.R_own = bsr_transpose(*L.P);
-      L.R = L.R_own.get();
-      h->lv[l - 1].A_own = galerkin(*L.A, *L.P);
-      h->lv[l - 1].A = h->lv[l - 1].A_own.get();
-    }
-    for (int l = 1; l <= depth; ++l) {
-      Level& L = h->lv[l];
-      L.M_own = fsai_build(*L.A, prm.fsai_kind, prm.t_max, prm.tau, prm.nest);
-      L.M = L.M_own.get();
-      L.beta = lanczos_lambda_max(*L.A, *L.M, prm.lanczos_iters, prm.lanczos_safety, prm.seed);
-    }
-    finish_hier(*h, prm.coarse_dim_cap);
-    *out = reinterpret_cast<bmg_hier*>(h.release());
-  });
-}
-
-int bmg_hier_create(bmg_ctx* ctx, int nlevels, const bmg_bsr* const* A, const bmg_bsr* const* P,
-                    const bmg_fsai* const* Mh, const double* beta, int coarse_dim_cap, bmg_hier** out) {
-  return guard([&] {
-    Ctx* c = reinterpret_cast<Ctx*>(ctx);
-    c->activate();
-    if (nlevels < 1) fail(BMG_EINVAL, "hierarchy needs at least one level");
-    auto h = std::make_unique<Hier>();
-    h->ctx = c;
-    h->lv.resize(nlevels);
-    for (int l = 0; l < nlevels; ++l) {
-      Level& L = h->lv[l];
-      L.A = B(A[l]);
-      if (l >= 1) {
-        L.P = B(P[l]);
-        if (L.P->dim_r != L.A->dim_r || L.P->dim_c != B(A[l - 1])->dim_r)
-          fail(BMG_EINVAL, "hierarchy: prolongation shape does not match the levels");
-        L.R_own = bsr_transpose(*L.P);
-        L.R = L.R_own.get();
-        L.M = M(Mh[l]);
-        L.beta = beta[l];
-        if (!(L.beta > 0.0)) fail(BMG_EINVAL, "cheb_fourth_apply: beta must be positive");
-      }
-    }
-    finish_hier(*h, coarse_dim_cap);
-    *out = reinterpret_cast<bmg_hier*>(h.release());
-  });
-}
-
-int bmg_hier_destroy(bmg_hier* h) {
-  return guard([&] {
-    Hier* p = reinterpret_cast<Hier*>(h);
-    if (p) BMG_CUDA(cudaStreamSynchronize(p->ctx->stream));
-    delete p;
-  });
-}
-int bmg_hier_info(const bmg_hier* hh, int* nlevels, int64_t* device_bytes) {
-  return guard([&] {
-    const Hier* h = reinterpret_cast<const Hier*>(hh);
-    if (nlevels) *nlevels = (int)h->lv.size();
-    if (device_bytes) {
-      int64_t b = (int64_t)h->ainv.bytes();
-      for (const auto& L : h->lv) {
-        if (L.A_own) b += L.A_own->device_bytes();
-        if (L.R_own) b += L.R_own->device_bytes();
-        if (L.M_own)
-          for (auto& f : L.M_own->fwd) b += f->device_bytes();
-        if (L.M_own)
-          for (auto& f : L.M_own->bwd) b += f->device_bytes();
-        b += (int64_t)(L.b.bytes() + L.x.bytes() + L.r.bytes() + L.w.bytes() + L.p.bytes() + L.t.bytes());
-      }
-      *device_bytes = b;
-    }
-  });
-}
-int bmg_hier_beta(const bmg_hier* hh, int level, double* beta) {
-  return guard([&] {
-    const Hier* h = reinterpret_cast<const Hier*>(hh);
-    if (level < 1 || level > h->finest()) fail(BMG_ERANGE, "hierarchy: level out of range");
-    *beta = h->lv[level].beta;
-  });
-}
-int bmg_hier_level(const bmg_hier* hh, int level, const bmg_bsr** a, const bmg_bsr** p, const bmg_fsai** m) {
-  return guard([&] {
-    const Hier* h = reinterpret_cast<const Hier*>(hh);
-    if (level < 0 || level > h->finest()) fail(BMG_ERANGE, "hierarchy: level out of range");
-    const Level& L = h->lv[level];
-    if (a) *a = reinterpret_cast<const bmg_bsr*>(L.A);
-    if (p) *p = reinterpret_cast<const bmg_bsr*>(L.P);
-    if (m) *m = reinterpret_cast<const bmg_fsai*>(L.M);
-  });
-}
-
-// algorithmic HBM bytes of one V(k_pre, k_post) cycle (BASELINE.md §3 byte
-// model, with the exact A*0 skip on coarse levels)
-int bmg_hier_cycle_bytes(const bmg_hier* hh, int kpre, int kpost, int64_t* bytes) {
-  return guard([&] {
-    const Hier* h = reinterpret_cast<const Hier*>(hh);
-    int64_t tot = 0;
-    const int top = h->finest();
-    for (int l = 1; l <= top; ++l) {
-      const Level& L = h->lv[l];
-      const int64_t n = L.n, nc = h->lv[l - 1].A->dim_r;
-      int64_t gb = 0;
-      for (auto& f : L.M->fwd) gb += f->pass_bytes();
-      for (auto& f : L.M->bwd) gb += f->pass_bytes();
-      const int64_t apass = L.A->pass_bytes() + 24 * n;  // x, b read; r write
-      const int64_t gvec = 16 * n + 40 * n;              // G: r, w; G^T+cheb: w, p rw, x rw
-      const int steps = kpre + kpost;
-      int64_t lvl = steps * (apass + gb + gvec);
-      if (l < top && kpre > 0) lvl -= apass;  // first coarse pre-step: A*0 skipped
-      if (l < top && kpre > 0) lvl -= 8 * n;  // and x not read in that step
-      lvl += apass;                                        // residual before restriction
-      lvl += L.R->pass_bytes() + 8 * n + 8 * nc;           // restriction
-      lvl += L.P->pass_bytes() + 8 * nc + 16 * n;          // prolongation x += P e
-      tot += lvl;
-    }
-    tot += h->n0 * h->n0 * 8 + 16 * h->n0;  // dense coarse solve
-    *bytes = tot;
-  });
-}
-
-int bmg_hier_use_graph(bmg_hier* hh, int on) {
-  return guard([&] { reinterpret_cast<Hier*>(hh)->use_graph = on != 0; });
-}
-
-int bmg_vcycle(bmg_hier* hh, int kpre, int kpost, const bmg_vec* b, bmg_vec* x) {
-  return guard([&] {
-    Hier* h = reinterpret_cast<Hier*>(hh);
-    const int64_t n = h->lv.back().A->dim_r;
-    need_len(V(b), n, "v_cycle");
-    need_len(V(x), n, "v_cycle");
-    run_vcycle(*h, kpre, kpost, V(b)->d.p, V(x)->d.p);
-  });
-}
-
-int bmg_vcycle_host(bmg_hier* hh, int kpre, int kpost, const double* b, double* x) {
-  return guard([&] {
-    Hier* h = reinterpret_cast<Hier*>(hh);
-    Ctx* ctx = h->ctx;
-    const int64_t n = h->lv.back().A->dim_r;
-    if (h->io_b.n < (size_t)n) {
-      h->io_b.alloc(std::max<int64_t>(n, 1));
-      h->io_x.alloc(std::max<int64_t>(n, 1));
-    }
-    BMG_CUDA(cudaMemcpyAsync(h->io_b.p, b, n * 8, cudaMemcpyHostToDevice, ctx->stream));
-    BMG_CUDA(cudaMemcpyAsync(h->io_x.p, x, n * 8, cudaMemcpyHostToDevice, ctx->stream));
-    run_vcycle(*h, kpre, kpost, h->io_b.p, h->io_x.p);
-    BMG_CUDA(cudaMemcpyAsync(x, h->io_x.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
-    BMG_CUDA(cudaStreamSynchronize(ctx->stream));
-  });
-}
-
-// residual-history driver modelled on measure_rates (experiments.cpp:15-67)
-int bmg_solve(bmg_hier* hh, int kpre, int kpost, const bmg_vec* bh, bmg_vec* xh, double tol, int max_iter,
-              double* hist, int* iters, int* status) {
-  return guard([&] {
-    Hier* h = reinterpret_cast<Hier*>(hh);
-    Ctx* ctx = h->ctx;
-    Level& F = h->lv.back();
-    const int64_t n = F.A->dim_r;
-    need_len(V(bh), n, "solve");
-    need_len(V(xh), n, "solve");
-    const double* b = V(bh)->d.p;
-    double* x = V(xh)->d.p;
-    auto resid = [&]() {
-      residual(*F.A, b, x, F.r.p);
-      return std::sqrt(dot(ctx, F.r.p, F.r.p, n));
-    };
-    hist[0] = resid();
-    int it = 0, st = 1;
-    if (hist[0] == 0.0) st = 0;
-    while (st == 1 && it < max_iter) {
-      run_vcycle(*h, kpre, kpost, b, x);
-      ++it;
-      hist[it] = resid();
-      const double growth = hist[it] / std::max(hist[it - 1], 1e-300);
-      if (!std::isfinite(hist[it]) || growth > 1e6) {
-        st = 2;
-        break;
-      }
-      if (hist[it] / hist[0] < tol) st = 0;
-    }
-    *iters = it;
-    *status = st;
   });
 }
 

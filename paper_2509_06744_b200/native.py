@@ -123,6 +123,12 @@ _SIGS = {
     "bmg_vcycle_host": (_I, [_P, _I, _I, _PD, _PD]),
     "bmg_solve": (_I, [_P, _I, _I, _P, _P, _D, _I, _PD, C.POINTER(_I), C.POINTER(_I)]),
     "bmg_time_residual": (_I, [_P, _P, _P, _P, _I, _PD]),
+    "bmg_nccl_unique_id": (_I, [C.c_char_p]),
+    "bmg_ctx_create_nccl": (_I, [_I, _I, _I, C.c_char_p, _PP]),
+    "bmg_hier_partition": (_I, [_P, _I, _I, _PI32, _I]),
+    "bmg_hier_part_info": (_I, [_P, _I, _I, _PI32, _PI32, _PI32, _PI32]),
+    "bmg_partition_rows": (_I, [_I, _PI64, _I, _I, _I, _PI32]),
+    "bmg_row_window": (_I, [_PI64, _PI32, _I, _I, _I, _I, _PI32, _PI32]),
     "bmg_tridiag_eigs": (_I, [_I, _PD, _PD, _PD]),
     "bmg_gen_stencil": (_I, [_I, _I, _I, _I, _U64, _D, _PI64, _PI64, _PI32, _PD]),
     "bmg_gen_prolongation": (_I, [_I, _I, _I, _U64, _I, _PI64, _PI64, _PI32, _PD]),

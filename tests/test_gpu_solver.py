@@ -213,3 +213,34 @@ def test_single_level_hierarchy_direct_solve(ctx):
     dh.v_cycle(2, 2, Vector(ctx, b), xv)
     want = np.linalg.solve(host.to_dense(), b)
     assert np.linalg.norm(xv.download() - want) <= 1e-9 * np.linalg.norm(want)
+
+
+@pytest.mark.parametrize("world,agg", [(2, 1), (3, 2), (4, 1)])
+def test_partitioned_vcycle_bitwise_equal_to_single(ctx, world, agg):
+    # row strips + halo exchange; per-row arithmetic is partition
+    # independent, so emulated ranks (in-process halos) match the 1-GPU cycle bitwise
+    cfg = pr.CONFIGS["C2"].scaled(32, 3)
+    A, T, b = pr.make_problem(cfg)
+    params = default_params(t_max=1, coarse_dim_cap=1 << 30)
+    dA = BlockSparseMatrix(ctx, A)
+    dT = [BlockSparseMatrix(ctx, p) for p in T]
+    h1 = Hierarchy.setup(dA, dT, params)
+    h2 = Hierarchy.setup(dA, dT, params)
+    granule = [cfg.n >> (cfg.levels - 1 - l) for l in range(cfg.levels)]
+    h1.partition(1, granule)  # same residual-norm segmentation (one segment per grid row)
+    h2.partition(world, granule, agglomerate=agg)
+    for l in range(cfg.levels):
+        spans = [h2.part_info(l, r) for r in range(world)]
+        assert spans[0][0] == 0 and spans[-1][1] == A.nbr >> (2 * (cfg.levels - 1 - l))
+        if l < agg:
+            assert all(s[1] == s[0] for s in spans[1:])
+    x1, x2 = Vector(ctx, b.size), Vector(ctx, b.size)
+    bv = Vector(ctx, b)
+    for it in range(3):
+        h1.v_cycle(3, 3, bv, x1)
+        h2.v_cycle(3, 3, bv, x2)
+        assert np.array_equal(x1.download(), x2.download())
+    x1, x2 = Vector(ctx, b.size), Vector(ctx, b.size)
+    hist1, it1, _ = h1.solve(3, 3, bv, x1, 1e-8, 6)
+    hist2, it2, _ = h2.solve(3, 3, bv, x2, 1e-8, 6)
+    assert it1 == it2 and np.array_equal(hist1, hist2)
