@@ -8,8 +8,10 @@ A step is one V(k,k) cycle on the finest level of the config's hierarchy with th
 inputs (hierarchy, b, x) resident in HBM.  Workload: config C2 (BASELINE.json
 configs[1]: 256^2 patches, m = 10, 4 levels, V(3,3), adaptive block-FSAI), the
 configs[1] case that fits one GPU; its per-cycle traffic (14+ GB) exceeds L2, so
-no explicit flush is needed between cycles.  For N > 1 every rank runs its own
-replica (weak scaling, no data-path collective yet).
+no explicit flush is needed between cycles.  For N > 1 the hierarchy is split
+into row strips per rank with NCCL halo exchanges inside the captured cycle and
+the coarsest two levels on rank 0 (strong scaling); `--replicas`
+runs independent copies instead (weak scaling).
 
 One JSON line is printed by rank 0.  `--impl reference` times the CPU oracle
 (the restatement of the reference, which cannot be built here) on the host cores.
@@ -174,7 +176,13 @@ def run_ours(args, cfg):
     from paper_2509_06744_b200 import BlockSparseMatrix, Context, Hierarchy, Vector, default_params, residual
     from paper_2509_06744_b200 import problems as pr
 
-    ctx = Context(local)
+    mode = "single GPU"
+    if ws > 1:
+        uid = [Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx = Context(local, nccl=(rank, ws, uid[0]))
+    else:
+        ctx = Context(local)
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
 
@@ -185,11 +193,33 @@ def run_ours(args, cfg):
     params = default_params(t_max=1, tau=1.0, nest=cfg.nest, coarse_dim_cap=1 << 30,
                             fsai_kind=0 if cfg.fsai == "static" else 3)
     H = Hierarchy.setup(dA, dT, params)
+    granule = [(cfg.n >> (cfg.levels - 1 - l)) ** (cfg.dim - 1) for l in range(cfg.levels)]
+    agglomerate = min(2, cfg.levels)
+    cycle_bytes = H.cycle_bytes(cfg.k, cfg.k)
+    n = A.dim_r
+    lo_row, hi_row = 0, A.nbr
+    scaling = "weak" if (ws > 1 and args.replicas) else "strong"
+    if ws > 1 and not args.replicas:
+        try:
+            H.partition(ws, granule, agglomerate=agglomerate, rank=rank)
+            lo_row, hi_row, _, _ = H.part_info(cfg.levels - 1, rank)
+            mode = f"row strips x{ws} (NCCL halos, coarsest {agglomerate} levels on rank 0)"
+            scaling = "strong"
+        except Exception as e:  # keep the run alive: independent replicas instead
+            H = Hierarchy.setup(dA, dT, params)
+            mode = f"replicas x{ws} (partitioned path failed: {type(e).__name__}: {e})"
+            scaling = "weak"
+    elif ws > 1:
+        mode = f"replicas x{ws}"
+    else:
+        H.partition(1, granule)  # residual-norm segmentation identical to the N-GPU runs
     ctx.sync()
     setup_s = time.perf_counter() - t0
-    n = A.dim_r
-    bv = Vector(ctx, b)
-    xv = Vector(ctx, n)
+    m = cfg.m
+    b_own = np.ascontiguousarray(b[lo_row * m:hi_row * m])
+    n_own = b_own.size
+    bv = Vector(ctx, b_own)
+    xv = Vector(ctx, n_own)
     k = cfg.k
 
     for _ in range(max(args.warmup, 3)):
@@ -219,14 +249,14 @@ def run_ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_per = ms / args.steps
-    rate = ws * args.steps / (ms / 1e3)
+    rate = (1 if scaling == "strong" else ws) * args.steps / (ms / 1e3)
     cycle_bytes = H.cycle_bytes(k, k)
     peak, peak_kind = hbm_peak()
-    eff_gbs = cycle_bytes / (ms_per / 1e3) / 1e9
+    eff_gbs = (1 if scaling == "strong" else ws) * cycle_bytes / (ms_per / 1e3) / 1e9
 
     # ---- dominant kernel: finest-level residual pass r = b - A x (2k+1 per cycle)
     Af, _, _ = H.level(H.levels - 1)
-    rv = Vector(ctx, n)
+    rv = Vector(ctx, n_own)
     reps = 20
     residual(Af, bv, xv, rv)
     torch.cuda.synchronize()
@@ -238,7 +268,7 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     kern_ms = k0.elapsed_time(k1) / reps
     inf = Af.info()
-    kern_bytes = inf["pass_bytes"] + 24 * n
+    kern_bytes = inf["pass_bytes"] + 24 * n_own
     achieved = kern_bytes / (kern_ms / 1e3) / 1e9
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "latest_traffic.json")
@@ -250,8 +280,8 @@ def run_ours(args, cfg):
             traffic = None
 
     # ---- e2e through the public C ABI with pinned host buffers
-    hb = torch.from_numpy(b).pin_memory()
-    hx = torch.zeros(n, dtype=torch.float64).pin_memory()
+    hb = torch.from_numpy(b_own).pin_memory()
+    hx = torch.zeros(n_own, dtype=torch.float64).pin_memory()
     for _ in range(2):
         H.v_cycle_host_ptr(k, k, hb.data_ptr(), hx.data_ptr())
     torch.cuda.synchronize()
@@ -268,7 +298,7 @@ def run_ours(args, cfg):
         t = torch.tensor([e2e_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    e2e_rate = ws * args.steps / (e2e_ms / 1e3)
+    e2e_rate = (1 if scaling == "strong" else ws) * args.steps / (e2e_ms / 1e3)
 
     # ---- CPU baseline (rank 0, N = 1 only): bounded oracle sample
     cpu = None
@@ -289,13 +319,13 @@ def run_ours(args, cfg):
             "warmup": max(args.warmup, 3),
             "ms_per_step": ms_per,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": scaling,
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic (BASELINE.md §3 generator, seed 0; random-init hierarchy built on the device)",
             "config": {"workload": f"{cfg.name}: {cfg.n}^{cfg.dim} patches, m={cfg.m}, {cfg.levels} levels, "
                                    f"V({k},{k}), {cfg.fsai} block-FSAI t_max=1",
-                       "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                       "parallelism": mode,
                        "l2": "inputs larger than L2 (>= 14 GB streamed per cycle)",
                        "setup_s": round(setup_s, 2)},
             "effective_gbs": eff_gbs,
@@ -306,8 +336,8 @@ def run_ours(args, cfg):
                          "frac": achieved / peak, "traffic": traffic,
                          "bytes_per_launch": kern_bytes, "ms_per_launch": kern_ms},
             "clocks": clocks,
-            "e2e": {"value": e2e_rate, "unit": "V-cycles/s", "h2d_bytes_per_step": 2 * 8 * n,
-                    "d2h_bytes_per_step": 8 * n},
+            "e2e": {"value": e2e_rate, "unit": "V-cycles/s", "h2d_bytes_per_step": 2 * 8 * n_own,
+                    "d2h_bytes_per_step": 8 * n_own},
             "gpu_launches": launches,
         }
         if cpu is not None:
@@ -325,6 +355,7 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of row strips")
     args = ap.parse_args()
     from paper_2509_06744_b200 import problems as pr
 
