@@ -133,6 +133,8 @@ int bmg_spmv_t(const bmg_bsr* a, const bmg_vec* x, bmg_vec* y);
 int bmg_residual(const bmg_bsr* a, const bmg_vec* b, const bmg_vec* x, bmg_vec* r);
 int bmg_dot(const bmg_vec* a, const bmg_vec* b, double* out);
 int bmg_galerkin(const bmg_bsr* a, const bmg_bsr* p, bmg_bsr** out);
+/* F A F^T, exactly symmetric, exact-zero blocks dropped (kernels.hpp:29) */
+int bmg_triple_product(const bmg_bsr* f, const bmg_bsr* a, bmg_bsr** out);
 
 /* ---- block-FSAI (fsai.cpp) ---------------------------------------------- */
 int bmg_fsai_build(const bmg_bsr* a, int kind, int t_max, double tau, int nest, bmg_fsai** out);
@@ -144,8 +146,11 @@ int bmg_fsai_destroy(bmg_fsai* m);
 int bmg_fsai_apply(const bmg_fsai* m, const bmg_vec* r, bmg_vec* z);
 int bmg_fsai_apply_transformed(const bmg_fsai* m, const bmg_bsr* a, const bmg_vec* x,
                                bmg_vec* y);
-/* borrowed handle of the device factor G (M = G^T G) */
+/* borrowed handle of the device factor G (M = G^T G; the last factor of a chain) */
 int bmg_fsai_G(const bmg_fsai* m, const bmg_bsr** g);
+/* chain length and borrowed factor k: F_k for k < last, G = L-hat^{-1} F_last */
+int bmg_fsai_chain_len(const bmg_fsai* m);
+int bmg_fsai_factor(const bmg_fsai* m, int k, const bmg_bsr** f);
 
 /* ---- smoother / spectral bound ------------------------------------------ */
 int bmg_cheb4_apply(const bmg_bsr* a, const bmg_fsai* m, const bmg_vec* b, bmg_vec* x,

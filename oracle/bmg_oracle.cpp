@@ -1321,12 +1321,11 @@ int orc_fsai_shat(const orc_fsai* f, double* l_packed) {
     }
   });
 }
-// G = L^{-1} F for a one-factor chain: G_kj = L_k^{-1} F_kj, column-wise
-// forward substitution with the Chol::solve_l order.
+// G = L-hat^{-1} F_last (the last factor of the chain): G_kj = L_k^{-1} F_kj,
+// column-wise forward substitution with the Chol::solve_l order.
 int orc_fsai_G(const orc_fsai* f, orc_mat** G_out) {
   return guard([&] {
-    if (f->f.chain.size() != 1) throw std::invalid_argument("orc_fsai_G: one-factor chain only");
-    const Factors& fac = f->f.chain[0];
+    const Factors& fac = f->f.chain.back();
     const Mat& F = fac.F;
     Mat G = F;
     for (int k = 0; k < F.nbr(); ++k) {

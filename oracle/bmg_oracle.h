@@ -82,7 +82,7 @@ int orc_fsai_apply_transformed(const orc_fsai* f, const orc_mat* a, const double
 int orc_fsai_chain_len(const orc_fsai* f);
 int orc_fsai_factor(const orc_fsai* f, int k, orc_mat** F_out);
 int orc_fsai_shat(const orc_fsai* f, double* l_packed);
-/* G = L-hat^{-1} F-hat of a one-factor chain as a BSR (the product's M = G^T G) */
+/* G = L-hat^{-1} F_last of the chain as a BSR (the product's last device factor) */
 int orc_fsai_G(const orc_fsai* f, orc_mat** G_out);
 
 /* ---- Lanczos (lanczos.hpp:16-58) ---- */

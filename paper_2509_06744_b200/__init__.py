@@ -7,6 +7,7 @@ from .native import (BmgError, CudaError, InvalidArgument, NotPositiveDefinite, 
                      FSAI_ADAPTIVE, FSAI_DIAGONAL, FSAI_STATIC_LOWER, SetupParams, lib)
 from .api import (BlockSparseMatrix, Context, Fsai, Hierarchy, HostBsr, Vector, cheb_fourth_apply,  # noqa: F401
                   default_params, dot, galerkin_coarsen, lanczos_lambda_max, residual, spmv, spmv_transpose,
+                  triple_product,
                   tridiag_eigs)
 from . import problems  # noqa: F401
 

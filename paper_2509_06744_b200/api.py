@@ -234,6 +234,12 @@ def galerkin_coarsen(a: BlockSparseMatrix, p: BlockSparseMatrix) -> BlockSparseM
     return BlockSparseMatrix(a.ctx, _handle=h)
 
 
+def triple_product(f: BlockSparseMatrix, a: BlockSparseMatrix) -> BlockSparseMatrix:
+    h = C.c_void_p()
+    check(lib().bmg_triple_product(f.h, a.h, C.byref(h)))
+    return BlockSparseMatrix(a.ctx, _handle=h)
+
+
 class Fsai:
     """Device block-FSAI, M = G^T G (NestedFsai, fsai.hpp:56-66)."""
 
@@ -260,6 +266,15 @@ class Fsai:
 
     def apply_transformed(self, a: BlockSparseMatrix, x: Vector, y: Vector):
         check(lib().bmg_fsai_apply_transformed(self.h, a.h, x.h, y.h))
+
+    @property
+    def chain_len(self) -> int:
+        return int(lib().bmg_fsai_chain_len(self.h))
+
+    def factor(self, k: int) -> BlockSparseMatrix:
+        h = C.c_void_p()
+        check(lib().bmg_fsai_factor(self.h, k, C.byref(h)))
+        return BlockSparseMatrix(self.ctx, _handle=h, _owned=False)
 
     @property
     def G(self) -> BlockSparseMatrix:

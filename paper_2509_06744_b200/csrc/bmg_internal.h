@@ -154,6 +154,8 @@ std::unique_ptr<Fsai> fsai_build(const Bsr& a, int kind, int t_max, double tau, 
 std::unique_ptr<Fsai> fsai_from_factors(Ctx* ctx, const Bsr& F, const double* shat_l_packed);
 double lanczos_lambda_max(const Bsr& a, const Fsai& m, int iters, double safety, uint64_t seed);
 std::unique_ptr<Bsr> galerkin(const Bsr& a, const Bsr& p);
+// F A F^T, exactly symmetric, exact-zero blocks dropped (kernels.cpp:88-119)
+std::unique_ptr<Bsr> triple_product(const Bsr& f, const Bsr& a);
 
 // host planning for the partitioned V-cycle (partition.cpp)
 void partition_rows(int nbr, const int64_t* row_ptr, int world, int granule, bool agglomerate,

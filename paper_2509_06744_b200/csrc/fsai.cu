@@ -7,10 +7,10 @@
 // passes: w = G r and z = G^T w (G^T stored as its own BSR, no atomics).
 //
 // Setup kernels (one CTA per block row, small dense work in shared memory):
-//   fsai_select_kernel   adaptive_build with P0 = diagonal, t_max = 1
+//   fsai_adaptive_kernel adaptive_build with P0 = diagonal, any t_max
 //                        (fsai.cpp:132-198, delta_ratio fsai.cpp:106-130):
-//                        scores every lower candidate c of H row k = A row k and
-//                        picks argmin rho (ties -> smallest c).
+//                        scores every lower candidate c of H row k = F_k A and
+//                        admits argmin rho (ties -> smallest c) while rho < tau.
 //   fsai_row_kernel      build_row (fsai.cpp:18-43) for an explicit lower
 //                        pattern, then G row k = L_k^{-1} [F_kS, I].
 // Dense arithmetic follows the oracle's fixed order (fma chains ascending), so
@@ -146,185 +146,129 @@ struct MatView {
   const int64_t* diag;  // position of block (i, i) in row i
 };
 
-// adaptive_build, P0 = diagonal, t_max = 1: candidate scoring per row
-__global__ void __launch_bounds__(kFsaiThreads) fsai_select_kernel(MatView A, int n, int mmax,
-                                                                   int* best, double* best_rho,
-                                                                   FsaiErr* err) {
-  extern __shared__ double sm[];
-  const int mm = mmax * mmax;
-  double* Lk = sm;
-  double* W = Lk + mm;
-  double* X = W + mm;
-  double* U = X + mm;
-  double* H = U + mm;
-  __shared__ double s_ldw, s_ldu, s_thr, s_best_rho;
-  __shared__ int s_best, s_skip, s_fail;
-  for (int k = blockIdx.x; k < n; k += gridDim.x) {
-    const int mk = A.rsz[k];
-    const int64_t pk = A.diag[k];
-    cta_load_block(Lk, A.vals + A.voff[pk], mk * mk);
-    if (threadIdx.x == 0) s_thr = 1e-12 * frob_serial(Lk, mk * mk);
-    const int piv = cta_chol(Lk, mk, nullptr);
-    if (piv >= 0) {
-      if (threadIdx.x == 0) atomicCAS(&err->row, -1, k) == -1 ? (err->pivot = piv, err->what = 2) : 0;
-      return;
+// build_row (fsai.cpp:18-43) for row k with the strict lower pattern S (ns
+// blocks, ascending): gram = chol(A[S,S]) (ng x ng), X = gram^{-1} A_kS^T
+// (ng x mk), AKS = A_kS (mk x ng), S_kk = A_kk - A_kS X and Lk = chol(S_kk).
+// Returns 0, or an error code (1 principal submatrix / 2 S row) with *piv.
+__device__ int row_factor(const MatView& A, int k, const int32_t* S, int ns, double* gram, double* X,
+                          double* AKS, double* Lk, int* ng_out, int* piv) {
+  const int mk = A.rsz[k];
+  int ng = 0;
+  for (int q = 0; q < ns; ++q) ng += A.rsz[S[q]];
+  *ng_out = ng;
+  cta_load_block(Lk, A.vals + A.voff[A.diag[k]], mk * mk);
+  if (ns > 0) {
+    for (int e = threadIdx.x; e < ng * ng; e += blockDim.x) gram[e] = 0.0;
+    __syncthreads();
+    int ro = 0;
+    for (int qa = 0; qa < ns; ++qa) {
+      const int ia = S[qa], ma = A.rsz[ia];
+      int co = 0;
+      for (int qb = 0; qb < ns; ++qb) {
+        const int ib = S[qb], mb = A.rsz[ib];
+        const int64_t lo = A.row_ptr[ia], hi = A.row_ptr[ia + 1];
+        const int pos = find_col(A.col, lo, hi, ib);
+        if (pos < hi && A.col[pos] == ib) {
+          const double* blk = A.vals + A.voff[pos];
+          for (int e = threadIdx.x; e < ma * mb; e += blockDim.x) {
+            const int r = e / mb, c = e - r * mb;
+            gram[(ro + r) * ng + co + c] = blk[e];
+          }
+        }
+        co += mb;
+      }
+      ro += ma;
     }
-    if (threadIdx.x == 0) {
-      s_best = -1;
-      s_best_rho = 0.0;
+    int co = 0;
+    for (int q = 0; q < ns; ++q) {
+      const int j = S[q], mj = A.rsz[j];
+      const int64_t lo = A.row_ptr[k], hi = A.row_ptr[k + 1];
+      const int pos = find_col(A.col, lo, hi, j);
+      const bool present = pos < hi && A.col[pos] == j;
+      const double* blk = present ? A.vals + A.voff[pos] : nullptr;
+      for (int e = threadIdx.x; e < mk * mj; e += blockDim.x) {
+        const int r = e / mj, c = e - r * mj;
+        const double v = present ? blk[e] : 0.0;
+        AKS[r * ng + co + c] = v;
+        X[(co + c) * mk + r] = v;
+      }
+      co += mj;
     }
     __syncthreads();
-    for (int64_t p = A.row_ptr[k]; p < A.row_ptr[k + 1]; ++p) {
-      const int c = A.col[p];
-      if (c >= k) break;
-      const int mc = A.rsz[c];
-      cta_load_block(H, A.vals + A.voff[p], mk * mc);
-      if (threadIdx.x == 0) s_skip = frob_serial(H, mk * mc) <= s_thr;
-      __syncthreads();
-      if (s_skip) continue;
-      // W = A_cc (pattern strict part is empty) and its Cholesky
-      const double* acc = A.vals + A.voff[A.diag[c]];
-      cta_load_block(W, acc, mc * mc);
-      const int pw = cta_chol(W, mc, &s_ldw);
-      if (pw >= 0) {
-        if (threadIdx.x == 0) atomicCAS(&err->row, -1, k) == -1 ? (err->pivot = pw, err->what = 3, err->cand = c) : 0;
-        return;
-      }
-      // X = S_k^{-1} H_kc ; U = W - H_kc^T X
-      cta_load_block(X, H, mk * mc);
-      cta_solve(Lk, mk, X, mc);
-      for (int e = threadIdx.x; e < mc * mc; e += blockDim.x) {
-        const int r = e / mc, q = e - r * mc;
-        double t = 0.0;
-        for (int z = 0; z < mk; ++z) t = __fma_rn(H[z * mc + r], X[z * mc + q], t);
-        U[e] = __dsub_rn(acc[e], t);
-      }
-      __syncthreads();
-      const int pu = cta_chol(U, mc, &s_ldu);
-      if (threadIdx.x == 0) {
-        if (pu >= 0) {
-          s_ldu = 0.0;
-          s_fail = 1;
-        } else {
-          s_fail = 0;
-        }
-        const double rho = s_fail ? 0.0 : fmin(exp(__dsub_rn(s_ldu, s_ldw)), 1.0);
-        if (s_best < 0 || rho < s_best_rho) {
-          s_best = c;
-          s_best_rho = rho;
-        }
-      }
-      __syncthreads();
+    const int pg = cta_chol(gram, ng, nullptr);
+    if (pg >= 0) {
+      *piv = pg;
+      return 1;
     }
-    if (threadIdx.x == 0) {
-      best[k] = s_best;
-      best_rho[k] = s_best_rho;
+    cta_solve(gram, ng, X, mk);  // X = gram^{-1} A_kS^T  (ng x mk)
+    for (int e = threadIdx.x; e < mk * mk; e += blockDim.x) {
+      const int r = e / mk, c = e - r * mk;
+      double t = 0.0;
+      for (int q = 0; q < ng; ++q) t = __fma_rn(AKS[r * ng + q], X[q * mk + c], t);
+      Lk[e] = __dsub_rn(Lk[e], t);
     }
     __syncthreads();
   }
+  const int ps = cta_chol(Lk, mk, nullptr);
+  if (ps >= 0) {
+    *piv = ps;
+    return 2;
+  }
+  return 0;
 }
 
-// build_row (fsai.cpp:18-43) for the explicit strict lower pattern of row k,
-// followed by G row k = L^{-1} [F_kS, I] written into G's value array.
+__device__ inline void report(FsaiErr* err, int row, int what, int piv, int cand) {
+  if (threadIdx.x == 0 && atomicCAS(&err->row, -1, row) == -1) {
+    err->pivot = piv;
+    err->what = what;
+    err->cand = cand;
+  }
+}
+
+// build_row for the explicit strict pattern of every row, then write row k of
+// G = L^{-1} [F_kS, I] (write_f = 0) or of F = [F_kS, I] itself (write_f = 1,
+// intermediate factors of a nested chain, fsai.cpp:243-253).
 struct RowArgs {
   MatView A;
   const int64_t* pat_ptr;  // strict pattern CSR
   const int32_t* pat_col;
-  double* gvals;           // G values, row k's blocks at gvoff[g_row_ptr[k] + q]
+  double* gvals;           // output values, row k's blocks at gvoff[g_row_ptr[k] + q]
   const int64_t* g_row_ptr;
   const int64_t* gvoff;
   int n;
   int mmax;
   int gmax;  // max strict pattern size in scalars
+  int write_f;
 };
 
 __global__ void __launch_bounds__(kFsaiThreads) fsai_row_kernel(RowArgs s, FsaiErr* err) {
   extern __shared__ double sm[];
   const int mm = s.mmax * s.mmax;
   double* gram = sm;                             // gmax^2
-  double* X = gram + (size_t)s.gmax * s.gmax;    // gmax x mmax (A_kS^T, then solution)
+  double* X = gram + (size_t)s.gmax * s.gmax;    // gmax x mmax
   double* AKS = X + (size_t)s.gmax * s.mmax;     // mmax x gmax
-  double* S = AKS + (size_t)s.gmax * s.mmax;     // mmax^2
-  double* Y = S + mm;                            // mmax x max(gmax, mmax)
+  double* Lk = AKS + (size_t)s.gmax * s.mmax;    // mmax^2
+  double* Y = Lk + mm;                           // mmax x (gmax + mmax)
   const MatView& A = s.A;
   for (int k = blockIdx.x; k < s.n; k += gridDim.x) {
     const int mk = A.rsz[k];
     const int64_t p0 = s.pat_ptr[k], p1 = s.pat_ptr[k + 1];
     const int ns = (int)(p1 - p0);
-    // scalar offsets of the strict pattern blocks
-    int ng = 0;
-    for (int64_t q = p0; q < p1; ++q) ng += A.rsz[s.pat_col[q]];
-    // S_kk = A_kk
-    cta_load_block(S, A.vals + A.voff[A.diag[k]], mk * mk);
-    if (ns > 0) {
-      // gram = A[S, S]
-      for (int e = threadIdx.x; e < ng * ng; e += blockDim.x) gram[e] = 0.0;
-      __syncthreads();
-      int ro = 0;
-      for (int64_t qa = p0; qa < p1; ++qa) {
-        const int ia = s.pat_col[qa], ma = A.rsz[ia];
-        int co = 0;
-        for (int64_t qb = p0; qb < p1; ++qb) {
-          const int ib = s.pat_col[qb], mb = A.rsz[ib];
-          const int64_t lo = A.row_ptr[ia], hi = A.row_ptr[ia + 1];
-          const int pos = find_col(A.col, lo, hi, ib);
-          if (pos < hi && A.col[pos] == ib) {
-            const double* blk = A.vals + A.voff[pos];
-            for (int e = threadIdx.x; e < ma * mb; e += blockDim.x) {
-              const int r = e / mb, c = e - r * mb;
-              gram[(ro + r) * ng + co + c] = blk[e];
-            }
-          }
-          co += mb;
-        }
-        ro += ma;
-      }
-      // A_kS (mk x ng) and X = A_kS^T
-      int co = 0;
-      for (int64_t q = p0; q < p1; ++q) {
-        const int j = s.pat_col[q], mj = A.rsz[j];
-        const int64_t lo = A.row_ptr[k], hi = A.row_ptr[k + 1];
-        const int pos = find_col(A.col, lo, hi, j);
-        const bool present = pos < hi && A.col[pos] == j;
-        const double* blk = present ? A.vals + A.voff[pos] : nullptr;
-        for (int e = threadIdx.x; e < mk * mj; e += blockDim.x) {
-          const int r = e / mj, c = e - r * mj;
-          const double v = present ? blk[e] : 0.0;
-          AKS[r * ng + co + c] = v;
-          X[(co + c) * mk + r] = v;
-        }
-        co += mj;
-      }
-      __syncthreads();
-      const int pg = cta_chol(gram, ng, nullptr);
-      if (pg >= 0) {
-        if (threadIdx.x == 0) atomicCAS(&err->row, -1, k) == -1 ? (err->pivot = pg, err->what = 1) : 0;
-        return;
-      }
-      cta_solve(gram, ng, X, mk);  // X = gram^{-1} A_kS^T  (ng x mk)
-      // S_kk -= A_kS X
-      for (int e = threadIdx.x; e < mk * mk; e += blockDim.x) {
-        const int r = e / mk, c = e - r * mk;
-        double t = 0.0;
-        for (int q = 0; q < ng; ++q) t = __fma_rn(AKS[r * ng + q], X[q * mk + c], t);
-        S[e] = __dsub_rn(S[e], t);
-      }
-      __syncthreads();
-    }
-    const int ps = cta_chol(S, mk, nullptr);
-    if (ps >= 0) {
-      if (threadIdx.x == 0) atomicCAS(&err->row, -1, k) == -1 ? (err->pivot = ps, err->what = 2) : 0;
+    int ng = 0, piv = -1;
+    const int st = row_factor(A, k, s.pat_col + p0, ns, gram, X, AKS, Lk, &ng, &piv);
+    if (st != 0) {
+      report(err, k, st, piv, -1);
       return;
     }
-    // Y = [F_kS | I] (mk x (ng + mk)), F_kS = -X^T; then Y <- L^{-1} Y
+    // Y = [F_kS | I] (mk x (ng + mk)), F_kS = -X^T; G: Y <- L^{-1} Y
     const int wy = ng + mk;
     for (int e = threadIdx.x; e < mk * wy; e += blockDim.x) {
       const int r = e / wy, c = e - r * wy;
       Y[e] = c < ng ? -X[c * mk + r] : (c - ng == r ? 1.0 : 0.0);
     }
     __syncthreads();
-    cta_solve_l(S, mk, Y, wy);
-    // scatter into G row k (blocks ascending: strict pattern, then diagonal)
+    if (!s.write_f) cta_solve_l(Lk, mk, Y, wy);
+    // scatter into row k (blocks ascending: strict pattern, then diagonal)
     const int64_t g0 = s.g_row_ptr[k];
     int co = 0;
     for (int q = 0; q <= ns; ++q) {
@@ -336,6 +280,208 @@ __global__ void __launch_bounds__(kFsaiThreads) fsai_row_kernel(RowArgs s, FsaiE
         dst[e] = Y[r * wy + co + c];
       }
       co += mj;
+    }
+    __syncthreads();
+  }
+}
+
+// adaptive_build (fsai.cpp:132-198) with P0 = diagonal for any t_max: per row,
+// t_max rounds of {rebuild row if stale; score every lower candidate c of
+// H row k = F_k A with delta_ratio (fsai.cpp:106-130); admit argmin rho if
+// rho < tau, else retire}.  Writes each row's final strict pattern.
+constexpr int kMaxT = 15;
+struct AdaptArgs {
+  MatView A;
+  int n, t_max, mmax;
+  double tau;
+  int32_t* pat;  // n x t_max, ascending
+  int* cnt;
+};
+
+__global__ void __launch_bounds__(kFsaiThreads) fsai_adaptive_kernel(AdaptArgs s, FsaiErr* err) {
+  extern __shared__ double sm[];
+  const int mm = s.mmax * s.mmax, gm = s.t_max * s.mmax;
+  double* gram = sm;                   // gm^2
+  double* X = gram + (size_t)gm * gm;  // gm x mm
+  double* AKS = X + (size_t)gm * s.mmax;
+  double* Lk = AKS + (size_t)gm * s.mmax;
+  double* H = Lk + mm;
+  double* W = H + mm;
+  double* U = W + mm;
+  double* T = U + mm;
+  double* ACS = T + mm;                   // mm x gm
+  double* Y = ACS + (size_t)gm * s.mmax;  // gm x mm
+  __shared__ int32_t S[kMaxT + 1];
+  __shared__ int ns_s, stale_s, best_s, cand_s, skip_s, ng_s;
+  __shared__ int64_t jpos[kMaxT + 1];
+  __shared__ double thr_s, best_rho_s, ldw_s, ldu_s;
+  const MatView& A = s.A;
+  for (int k = blockIdx.x; k < s.n; k += gridDim.x) {
+    const int mk = A.rsz[k];
+    if (threadIdx.x == 0) {
+      ns_s = 0;
+      stale_s = 1;
+    }
+    __syncthreads();
+    bool active = true;
+    for (int t = 1; t <= s.t_max && active; ++t) {
+      if (stale_s) {
+        int ng = 0, piv = -1;
+        const int st = row_factor(A, k, S, ns_s, gram, X, AKS, Lk, &ng, &piv);
+        if (st != 0) {
+          report(err, k, st, piv, -1);
+          return;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          stale_s = 0;
+          ng_s = ng;
+        }
+        __syncthreads();
+      }
+      const int ns = ns_s, ng = ng_s;
+      // H_kc = sum over j in S u {k} (ascending) of F_kj A_jc   (fsai.cpp:46-51)
+      auto h_block = [&](int c, double* out) {
+        const int mc = A.rsz[c];
+        if (threadIdx.x <= ns) {
+          const int j = threadIdx.x < ns ? S[threadIdx.x] : k;
+          const int64_t lo = A.row_ptr[j], hi = A.row_ptr[j + 1];
+          const int pos = find_col(A.col, lo, hi, c);
+          jpos[threadIdx.x] = (pos < hi && A.col[pos] == c) ? pos : -1;
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < mk * mc; e += blockDim.x) {
+          const int r = e / mc, cc = e - r * mc;
+          double acc = 0.0;
+          int off = 0;
+          for (int q = 0; q <= ns; ++q) {
+            const int j = q < ns ? S[q] : k;
+            const int mj = A.rsz[j];
+            if (jpos[q] >= 0) {
+              const double* a = A.vals + A.voff[jpos[q]];
+              double tt = 0.0;
+              for (int z = 0; z < mj; ++z) {
+                const double f = q < ns ? -X[(off + z) * mk + r] : (z == r ? 1.0 : 0.0);
+                tt = __fma_rn(f, a[z * mc + cc], tt);
+              }
+              acc = __dadd_rn(acc, tt);
+            }
+            off += mj;
+          }
+          out[e] = acc;
+        }
+        __syncthreads();
+      };
+      h_block(k, H);
+      if (threadIdx.x == 0) {
+        thr_s = 1e-12 * frob_serial(H, mk * mk);
+        best_s = -1;
+        best_rho_s = 0.0;
+        cand_s = -1;
+      }
+      __syncthreads();
+      for (;;) {
+        // next candidate: smallest column > cand of rows S u {k}, below k, not in S
+        if (threadIdx.x == 0) {
+          int nxt = k;
+          for (int q = 0; q <= ns; ++q) {
+            const int j = q < ns ? S[q] : k;
+            const int64_t lo = A.row_ptr[j], hi = A.row_ptr[j + 1];
+            int64_t p = find_col(A.col, lo, hi, cand_s + 1);
+            while (p < hi && A.col[p] < nxt) {
+              bool in_s = false;
+              for (int z = 0; z < ns; ++z) in_s |= (S[z] == A.col[p]);
+              if (!in_s) {
+                nxt = A.col[p];
+                break;
+              }
+              ++p;
+            }
+          }
+          cand_s = nxt < k ? nxt : -2;
+        }
+        __syncthreads();
+        const int c = cand_s;
+        if (c < 0) break;
+        const int mc = A.rsz[c];
+        h_block(c, H);
+        if (threadIdx.x == 0) skip_s = frob_serial(H, mk * mc) <= thr_s;
+        __syncthreads();
+        if (skip_s) continue;
+        // W = A_cc - A_cS gram^{-1} A_cS^T
+        const double* acc_blk = A.vals + A.voff[A.diag[c]];
+        cta_load_block(W, acc_blk, mc * mc);
+        if (ns > 0) {
+          int co = 0;
+          for (int q = 0; q < ns; ++q) {
+            const int j = S[q], mj = A.rsz[j];
+            const int64_t lo = A.row_ptr[c], hi = A.row_ptr[c + 1];
+            const int pos = find_col(A.col, lo, hi, j);
+            const bool present = pos < hi && A.col[pos] == j;
+            const double* blk = present ? A.vals + A.voff[pos] : nullptr;
+            for (int e = threadIdx.x; e < mc * mj; e += blockDim.x) {
+              const int r = e / mj, cc = e - r * mj;
+              const double v = present ? blk[e] : 0.0;
+              ACS[r * ng + co + cc] = v;
+              Y[(co + cc) * mc + r] = v;
+            }
+            co += mj;
+          }
+          __syncthreads();
+          cta_solve(gram, ng, Y, mc);
+          for (int e = threadIdx.x; e < mc * mc; e += blockDim.x) {
+            const int r = e / mc, q = e - r * mc;
+            double tt = 0.0;
+            for (int z = 0; z < ng; ++z) tt = __fma_rn(ACS[r * ng + z], Y[z * mc + q], tt);
+            W[e] = __dsub_rn(W[e], tt);
+          }
+          __syncthreads();
+        }
+        for (int e = threadIdx.x; e < mc * mc; e += blockDim.x) U[e] = W[e];
+        __syncthreads();
+        const int pw = cta_chol(W, mc, &ldw_s);
+        if (pw >= 0) {
+          report(err, k, 3, pw, c);
+          return;
+        }
+        // U = W - H_kc^T S_k^{-1} H_kc
+        for (int e = threadIdx.x; e < mk * mc; e += blockDim.x) T[e] = H[e];
+        __syncthreads();
+        cta_solve(Lk, mk, T, mc);
+        for (int e = threadIdx.x; e < mc * mc; e += blockDim.x) {
+          const int r = e / mc, q = e - r * mc;
+          double tt = 0.0;
+          for (int z = 0; z < mk; ++z) tt = __fma_rn(H[z * mc + r], T[z * mc + q], tt);
+          U[e] = __dsub_rn(U[e], tt);
+        }
+        __syncthreads();
+        const int pu = cta_chol(U, mc, &ldu_s);
+        if (threadIdx.x == 0) {
+          const double rho = pu >= 0 ? 0.0 : fmin(exp(__dsub_rn(ldu_s, ldw_s)), 1.0);
+          if (best_s < 0 || rho < best_rho_s) {  // ties keep the smallest column
+            best_s = c;
+            best_rho_s = rho;
+          }
+        }
+        __syncthreads();
+      }
+      if (best_s < 0 || !(best_rho_s < s.tau)) {
+        active = false;
+      } else if (threadIdx.x == 0) {
+        int q = ns_s;
+        while (q > 0 && S[q - 1] > best_s) {
+          S[q] = S[q - 1];
+          --q;
+        }
+        S[q] = best_s;
+        ++ns_s;
+        stale_s = 1;
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      s.cnt[k] = ns_s;
+      for (int q = 0; q < ns_s; ++q) s.pat[(int64_t)k * s.t_max + q] = S[q];
     }
     __syncthreads();
   }
@@ -415,13 +561,12 @@ int max_size(const std::vector<int>& s) {
   return m;
 }
 
-// build G for an explicit strict pattern; returns G (device) and G^T
-std::unique_ptr<Fsai> build_from_pattern(const Bsr& a, const Aux& aux,
-                                         const std::vector<int64_t>& pat_ptr,
-                                         const std::vector<int32_t>& pat_col) {
+// F (write_f) or G = L^{-1} F for an explicit strict pattern (row k: pattern
+// ascending, then k)
+std::unique_ptr<Bsr> factor_from_pattern(const Bsr& a, const Aux& aux, const std::vector<int64_t>& pat_ptr,
+                                         const std::vector<int32_t>& pat_col, bool write_f) {
   Ctx* ctx = a.ctx;
   const int n = a.nbr;
-  // G structure: row k = strict pattern (ascending) + k
   std::vector<int64_t> grp(n + 1, 0);
   std::vector<int32_t> gcol;
   gcol.reserve(pat_col.size() + n);
@@ -449,19 +594,58 @@ std::unique_ptr<Fsai> build_from_pattern(const Bsr& a, const Aux& aux,
   DBuf<kern::FsaiErr> derr(1);
   kern::FsaiErr e0{-1, -1, 0, -1};
   BMG_CUDA(cudaMemcpy(derr.p, &e0, sizeof(e0), cudaMemcpyHostToDevice));
-  kern::RowArgs ra{view(a, aux), dpp.p, dpc.p, G->vals.p, G->row_ptr.p, dgv.p, n, mmax, gmax};
+  kern::RowArgs ra{view(a, aux), dpp.p, dpc.p, G->vals.p, G->row_ptr.p, dgv.p, n, mmax, gmax, write_f ? 1 : 0};
   BMG_CUDA(cudaFuncSetAttribute(kern::fsai_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = std::max(1, std::min(n, ctx->sms * 16));
   kern::fsai_row_kernel<<<grid, kern::kFsaiThreads, smem, ctx->stream>>>(ra, derr.p);
   ctx->count();
   BMG_CUDA(cudaGetLastError());
   check_err(ctx, derr.p);
+  return G;
+}
+
+// adaptive_build pattern selection on the device (any t_max, P0 = diagonal)
+void adaptive_pattern(const Bsr& a, const Aux& aux, int t_max, double tau, std::vector<int64_t>& pp,
+                      std::vector<int32_t>& pc) {
+  Ctx* ctx = a.ctx;
+  const int n = a.nbr;
+  if (t_max > kern::kMaxT) fail(BMG_EINVAL, "adaptive_build: t_max above the device limit (15)");
+  const int mmax = max_size(a.rsz);
+  const size_t gm = (size_t)t_max * mmax, mm = (size_t)mmax * mmax;
+  const size_t smem = sizeof(double) * (gm * gm + 4 * gm * mmax + 5 * mm);
+  if (smem > 200 * 1024) fail(BMG_EINVAL, "adaptive_build: t_max x block size too large for the device build");
+  DBuf<int32_t> pat(std::max<size_t>((size_t)n * t_max, 1));
+  DBuf<int> cnt(std::max(n, 1));
+  DBuf<kern::FsaiErr> derr(1);
+  kern::FsaiErr e0{-1, -1, 0, -1};
+  BMG_CUDA(cudaMemcpy(derr.p, &e0, sizeof(e0), cudaMemcpyHostToDevice));
+  BMG_CUDA(cudaFuncSetAttribute(kern::fsai_adaptive_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern::AdaptArgs args{view(a, aux), n, t_max, mmax, tau, pat.p, cnt.p};
+  const int grid = std::max(1, std::min(n, ctx->sms * 16));
+  kern::fsai_adaptive_kernel<<<grid, kern::kFsaiThreads, smem, ctx->stream>>>(args, derr.p);
+  ctx->count();
+  BMG_CUDA(cudaGetLastError());
+  check_err(ctx, derr.p);
+  std::vector<int32_t> hp((size_t)n * t_max);
+  std::vector<int> hc(n);
+  if (n) {
+    BMG_CUDA(cudaMemcpy(hp.data(), pat.p, hp.size() * 4, cudaMemcpyDeviceToHost));
+    BMG_CUDA(cudaMemcpy(hc.data(), cnt.p, n * 4, cudaMemcpyDeviceToHost));
+  }
+  pp.assign(n + 1, 0);
+  pc.clear();
+  for (int k = 0; k < n; ++k) {
+    for (int q = 0; q < hc[k]; ++q) pc.push_back(hp[(size_t)k * t_max + q]);
+    pp[k + 1] = (int64_t)pc.size();
+  }
+}
+
+std::unique_ptr<Fsai> wrap(Ctx* ctx, int dim, std::vector<std::unique_ptr<Bsr>> fwd) {
   auto m = std::make_unique<Fsai>();
   m->ctx = ctx;
-  m->dim = a.dim_r;
-  auto GT = bsr_transpose(*G);
-  m->fwd.push_back(std::move(G));
-  m->bwd.push_back(std::move(GT));
+  m->dim = dim;
+  for (auto& f : fwd) m->bwd.push_back(bsr_transpose(*f));
+  m->fwd = std::move(fwd);
   return m;
 }
 
@@ -472,51 +656,42 @@ std::unique_ptr<Fsai> fsai_build(const Bsr& a, int kind, int t_max, double tau, 
   if (!a.sym) fail(BMG_EINVAL, "fsai: matrix must be symmetric");
   Ctx* ctx = a.ctx;
   const int n = a.nbr;
-  Aux aux = make_aux(a, true);
   std::vector<int64_t> pp(n + 1, 0);
   std::vector<int32_t> pc;
-  if (kind == BMG_FSAI_STATIC_LOWER) {
-    for (int k = 0; k < n; ++k) {
-      for (int64_t p = a.h_row_ptr[k]; p < a.h_row_ptr[k + 1]; ++p)
-        if (a.h_col[p] < k) pc.push_back(a.h_col[p]);
-      pp[k + 1] = (int64_t)pc.size();
-    }
-  } else if (kind == BMG_FSAI_DIAGONAL) {
-    // pattern stays diagonal
-  } else if (kind == BMG_FSAI_ADAPTIVE) {
-    if (t_max < 1) fail(BMG_EINVAL, "adaptive_build: t_max must be >= 1");
-    if (!(tau > 0.0 && tau <= 1.0)) fail(BMG_EINVAL, "adaptive_build: tau must be in (0, 1]");
-    if (nest < 0) fail(BMG_EINVAL, "nested_build: n_levels must be >= 0");
-    if (t_max != 1 || nest != 0)
-      fail(BMG_EINVAL, "device FSAI build supports t_max = 1, nest = 0 (the BASELINE configs)");
-    const int mmax = max_size(a.rsz);
-    DBuf<int> best(std::max(n, 1));
-    DBuf<double> rho(std::max(n, 1));
-    DBuf<kern::FsaiErr> derr(1);
-    kern::FsaiErr e0{-1, -1, 0, -1};
-    BMG_CUDA(cudaMemcpy(derr.p, &e0, sizeof(e0), cudaMemcpyHostToDevice));
-    const size_t smem = 5 * sizeof(double) * mmax * mmax;
-    BMG_CUDA(cudaFuncSetAttribute(kern::fsai_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int grid = std::max(1, std::min(n, ctx->sms * 16));
-    kern::fsai_select_kernel<<<grid, kern::kFsaiThreads, smem, ctx->stream>>>(view(a, aux), n, mmax, best.p,
-                                                                              rho.p, derr.p);
-    ctx->count();
-    BMG_CUDA(cudaGetLastError());
-    check_err(ctx, derr.p);
-    std::vector<int> hb(n);
-    std::vector<double> hr(n);
-    if (n) {
-      BMG_CUDA(cudaMemcpy(hb.data(), best.p, n * 4, cudaMemcpyDeviceToHost));
-      BMG_CUDA(cudaMemcpy(hr.data(), rho.p, n * 8, cudaMemcpyDeviceToHost));
-    }
-    for (int k = 0; k < n; ++k) {
-      if (hb[k] >= 0 && hr[k] < tau) pc.push_back(hb[k]);
-      pp[k + 1] = (int64_t)pc.size();
-    }
-  } else {
-    fail(BMG_EINVAL, "bmg_fsai_build: unknown kind");
+  std::vector<std::unique_ptr<Bsr>> fwd;
+  if (kind == BMG_FSAI_STATIC_LOWER || kind == BMG_FSAI_DIAGONAL) {
+    Aux aux = make_aux(a, true);
+    if (kind == BMG_FSAI_STATIC_LOWER)
+      for (int k = 0; k < n; ++k) {
+        for (int64_t p = a.h_row_ptr[k]; p < a.h_row_ptr[k + 1]; ++p)
+          if (a.h_col[p] < k) pc.push_back(a.h_col[p]);
+        pp[k + 1] = (int64_t)pc.size();
+      }
+    fwd.push_back(factor_from_pattern(a, aux, pp, pc, false));
+    return wrap(ctx, a.dim_r, std::move(fwd));
   }
-  return build_from_pattern(a, aux, pp, pc);
+  if (kind != BMG_FSAI_ADAPTIVE) fail(BMG_EINVAL, "bmg_fsai_build: unknown kind");
+  if (t_max < 1) fail(BMG_EINVAL, "adaptive_build: t_max must be >= 1");
+  if (!(tau > 0.0 && tau <= 1.0)) fail(BMG_EINVAL, "adaptive_build: tau must be in (0, 1]");
+  if (nest < 0) fail(BMG_EINVAL, "nested_build: n_levels must be >= 0");
+  // nested_build (fsai.cpp:243-253): A_0 = A, A_{k+1} = F_k A_k F_k^T; the chain
+  // applies F_0 .. F_{n-1} and G_n = L-hat^{-1} F_n
+  const Bsr* ak = &a;
+  std::unique_ptr<Bsr> ak_own;
+  for (int level = 0; level <= nest; ++level) {
+    Aux aux = make_aux(*ak, true);
+    adaptive_pattern(*ak, aux, t_max, tau, pp, pc);
+    if (level < nest) {
+      auto F = factor_from_pattern(*ak, aux, pp, pc, true);
+      auto next = triple_product(*F, *ak);
+      fwd.push_back(std::move(F));
+      ak_own = std::move(next);
+      ak = ak_own.get();
+    } else {
+      fwd.push_back(factor_from_pattern(*ak, aux, pp, pc, false));
+    }
+  }
+  return wrap(ctx, a.dim_r, std::move(fwd));
 }
 
 std::unique_ptr<Fsai> fsai_from_factors(Ctx* ctx, const Bsr& F, const double* shat) {

@@ -21,7 +21,7 @@ namespace kern {
 __global__ void pair_gemm_kernel(const double* __restrict__ A, const double* __restrict__ B,
                                  const int64_t* __restrict__ pair_ptr,
                                  const int2* __restrict__ pairs, double* __restrict__ out,
-                                 int64_t nout, int m, int bs_a, int bs_b, int bs_o, int transpose_a) {
+                                 int64_t nout, int m, int bs_a, int bs_b, int bs_o, int mode) {
   const int r = threadIdx.x / m, c = threadIdx.x - (threadIdx.x / m) * m;
   if (r >= m) return;
   for (int64_t o = blockIdx.x; o < nout; o += gridDim.x) {
@@ -31,9 +31,11 @@ __global__ void pair_gemm_kernel(const double* __restrict__ A, const double* __r
       const double* a = A + (int64_t)pr.x * bs_a;
       const double* b = B + (int64_t)pr.y * bs_b;
       double t = 0.0;
-      if (transpose_a)
+      if (mode == 1)  // a^T b  (kernels.cpp:82)
         for (int k = 0; k < m; ++k) t = __fma_rn(a[k * m + r], b[k * m + c], t);
-      else
+      else if (mode == 2)  // a b^T  (kernels.cpp:108)
+        for (int k = 0; k < m; ++k) t = __fma_rn(a[r * m + k], b[c * m + k], t);
+      else  // a b  (kernels.cpp:71)
         for (int k = 0; k < m; ++k) t = __fma_rn(a[r * m + k], b[k * m + c], t);
       acc = __dadd_rn(acc, t);
     }
@@ -144,7 +146,7 @@ Product symbolic(int nrows, const LeftRow& left, const std::vector<int64_t>& yrp
 }
 
 void pair_gemm(Ctx* ctx, const double* A, int bs_a, const double* B, int bs_b, const Product& pr, double* out,
-               int bs_o, int m, bool ta) {
+               int bs_o, int m, int mode) {
   const int64_t nout = (int64_t)pr.col.size();
   if (nout == 0) return;
   DBuf<int64_t> pp(pr.pair_ptr.size());
@@ -155,7 +157,7 @@ void pair_gemm(Ctx* ctx, const double* A, int bs_a, const double* B, int bs_b, c
   const int threads = ((m * m + 31) / 32) * 32;
   const int grid = (int)std::min<int64_t>(nout, (int64_t)ctx->sms * 32);
   kern::pair_gemm_kernel<<<grid, threads, 0, ctx->stream>>>(A, B, pp.p, pairs.p, out, nout, m, bs_a, bs_b, bs_o,
-                                                            ta ? 1 : 0);
+                                                            mode);
   ctx->count();
   BMG_CUDA(cudaGetLastError());
   BMG_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -198,9 +200,9 @@ std::unique_ptr<Bsr> galerkin(const Bsr& a, const Bsr& p) {
   // numeric
   const int bs = a.bs;
   DBuf<double> apv(std::max<size_t>(ap.col.size() * bs, 2));
-  pair_gemm(ctx, a.vals.p, bs, p.vals.p, p.bs, ap, apv.p, bs, m, false);
+  pair_gemm(ctx, a.vals.p, bs, p.vals.p, p.bs, ap, apv.p, bs, m, 0);
   DBuf<double> cv(std::max<size_t>(c.col.size() * bs, 2));
-  pair_gemm(ctx, p.vals.p, p.bs, apv.p, bs, c, cv.p, bs, m, true);
+  pair_gemm(ctx, p.vals.p, p.bs, apv.p, bs, c, cv.p, bs, m, 1);
   apv.release();
   // structural symmetry + transpose positions
   const int nc = p.nbc;
@@ -226,6 +228,180 @@ std::unique_ptr<Bsr> galerkin(const Bsr& a, const Bsr& p) {
     BMG_CUDA(cudaGetLastError());
   }
   BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+  return out;
+}
+
+// ============================================================================ triple product
+// triple_product (kernels.cpp:88-119): H = F A, then for j <= i
+// blk_ij = sum_k H_ik F_jk^T (ascending k), diagonal blocks symmetrised
+// 0.5 (blk + blk^T), blocks with zero squared norm dropped, stored with both
+// halves.  Symbolic phase on the host, numeric on the device.
+namespace kern {
+__global__ void sym_diag_sqnorm_kernel(double* __restrict__ L, const int64_t* __restrict__ diag_of,
+                                       int64_t nblk, int m, int bs, int* __restrict__ nonzero) {
+  for (int64_t o = blockIdx.x; o < nblk; o += gridDim.x) {
+    double* b = L + o * bs;
+    if (diag_of[o]) {
+      __shared__ double tmp[441];
+      for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+        const int r = e / m, c = e - r * m;
+        tmp[e] = __dmul_rn(0.5, __dadd_rn(b[r * m + c], b[c * m + r]));
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < m * m; e += blockDim.x) b[e] = tmp[e];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      double sq = 0.0;
+      for (int e = 0; e < m * m; ++e) sq = __dadd_rn(sq, __dmul_rn(b[e], b[e]));
+      nonzero[o] = sq != 0.0;
+    }
+    __syncthreads();
+  }
+}
+__global__ void gather_blocks_kernel(const double* __restrict__ src, const int64_t* __restrict__ from,
+                                     const int* __restrict__ trans, double* __restrict__ dst, int64_t nblk, int m,
+                                     int bs) {
+  for (int64_t o = blockIdx.x; o < nblk; o += gridDim.x) {
+    const double* s = src + from[o] * bs;
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+      const int r = e / m, c = e - r * m;
+      dst[o * bs + e] = trans[o] ? s[c * m + r] : s[e];
+    }
+  }
+}
+}  // namespace kern
+
+std::unique_ptr<Bsr> triple_product(const Bsr& f, const Bsr& a) {
+  if (!(f.rsz == f.csz && a.rsz == a.csz && f.rsz == a.rsz))
+    fail(BMG_EINVAL, "triple_product: layouts must be square and compatible");
+  if (!a.sym) fail(BMG_EINVAL, "triple_product: A must be symmetric");
+  if (!(a.uniform && f.uniform)) fail(BMG_EINVAL, "device triple_product: uniform block sizes required");
+  Ctx* ctx = a.ctx;
+  const int m = a.mr, bs = a.bs, n = a.nbr;
+  // H = F A
+  Product h = symbolic(
+      n,
+      [&](int i, auto&& emit) {
+        for (int64_t q = f.h_row_ptr[i]; q < f.h_row_ptr[i + 1]; ++q) emit(f.h_col[q], q);
+      },
+      a.h_row_ptr, a.h_col);
+  DBuf<double> hv(std::max<size_t>(h.col.size() * bs, 2));
+  pair_gemm(ctx, f.vals.p, f.bs, a.vals.p, bs, h, hv.p, bs, m, 0);
+  // F column index: column k -> rows j (ascending) holding F_jk
+  std::vector<int64_t> fc_ptr(n + 1, 0);
+  for (int64_t q = 0; q < f.nnzb; ++q) fc_ptr[f.h_col[q] + 1]++;
+  for (int j = 0; j < n; ++j) fc_ptr[j + 1] += fc_ptr[j];
+  std::vector<int32_t> fc_row(f.nnzb);
+  {
+    std::vector<int64_t> fillp(fc_ptr.begin(), fc_ptr.end() - 1);
+    for (int i = 0; i < n; ++i)
+      for (int64_t q = f.h_row_ptr[i]; q < f.h_row_ptr[i + 1]; ++q) fc_row[fillp[f.h_col[q]]++] = i;
+  }
+  // lower candidates (i, j <= i) with the ordered (H_ik, F_jk) pairs
+  Product lo;
+  lo.row_ptr.assign(n + 1, 0);
+  std::vector<std::vector<int32_t>> rc(n);
+  std::vector<std::vector<int64_t>> rpp(n);
+  std::vector<std::vector<int2>> rpr(n);
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int i = 0; i < n; ++i) {
+    std::vector<int32_t> cand;
+    for (int64_t q = h.row_ptr[i]; q < h.row_ptr[i + 1]; ++q) {
+      const int k = h.col[q];
+      for (int64_t t = fc_ptr[k]; t < fc_ptr[k + 1]; ++t)
+        if (fc_row[t] <= i) cand.push_back(fc_row[t]);
+    }
+    std::sort(cand.begin(), cand.end());
+    cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+    for (int j : cand) {
+      int64_t hp = h.row_ptr[i], fp = f.h_row_ptr[j];
+      const int64_t he = h.row_ptr[i + 1], fe = f.h_row_ptr[j + 1];
+      const size_t before = rpr[i].size();
+      while (hp < he && fp < fe) {
+        if (h.col[hp] < f.h_col[fp]) {
+          ++hp;
+        } else if (f.h_col[fp] < h.col[hp]) {
+          ++fp;
+        } else {
+          rpr[i].push_back(make_int2((int)hp, (int)fp));
+          ++hp;
+          ++fp;
+        }
+      }
+      if (rpr[i].size() > before) {
+        rc[i].push_back(j);
+        rpp[i].push_back((int64_t)before);
+      }
+    }
+  }
+  std::vector<int64_t> pbase(n + 1, 0);
+  for (int i = 0; i < n; ++i) {
+    lo.row_ptr[i + 1] = lo.row_ptr[i] + (int64_t)rc[i].size();
+    pbase[i + 1] = pbase[i] + (int64_t)rpr[i].size();
+  }
+  const int64_t nl = lo.row_ptr[n];
+  lo.col.resize(nl);
+  lo.pair_ptr.resize(nl + 1);
+  lo.pairs.resize(pbase[n]);
+  std::vector<int64_t> is_diag(nl);
+  for (int i = 0; i < n; ++i) {
+    for (size_t t = 0; t < rc[i].size(); ++t) {
+      lo.col[lo.row_ptr[i] + t] = rc[i][t];
+      lo.pair_ptr[lo.row_ptr[i] + t] = pbase[i] + rpp[i][t];
+      is_diag[lo.row_ptr[i] + t] = rc[i][t] == i;
+    }
+    std::copy(rpr[i].begin(), rpr[i].end(), lo.pairs.begin() + pbase[i]);
+  }
+  lo.pair_ptr[nl] = pbase[n];
+  DBuf<double> lv(std::max<size_t>((size_t)nl * bs, 2));
+  pair_gemm(ctx, hv.p, bs, f.vals.p, f.bs, lo, lv.p, bs, m, 2);
+  hv.release();
+  DBuf<int64_t> ddiag(std::max<int64_t>(nl, 1));
+  DBuf<int> dnz(std::max<int64_t>(nl, 1));
+  if (nl) {
+    BMG_CUDA(cudaMemcpy(ddiag.p, is_diag.data(), nl * 8, cudaMemcpyHostToDevice));
+    kern::sym_diag_sqnorm_kernel<<<(int)std::min<int64_t>(nl, ctx->sms * 32), 128, 0, ctx->stream>>>(
+        lv.p, ddiag.p, nl, m, bs, dnz.p);
+    ctx->count();
+    BMG_CUDA(cudaGetLastError());
+  }
+  std::vector<int> nz(nl);
+  if (nl) BMG_CUDA(cudaMemcpy(nz.data(), dnz.p, nl * 4, cudaMemcpyDeviceToHost));
+  // insert_symmetric of the kept lower blocks: row i gets (i, j) and row j gets (j, i)^T
+  std::vector<std::vector<std::tuple<int32_t, int64_t, int>>> rows(n);
+  for (int i = 0; i < n; ++i)
+    for (int64_t q = lo.row_ptr[i]; q < lo.row_ptr[i + 1]; ++q) {
+      if (!nz[q]) continue;
+      const int j = lo.col[q];
+      rows[i].emplace_back(j, q, 0);
+      if (j != i) rows[j].emplace_back(i, q, 1);
+    }
+  std::vector<int64_t> rp(n + 1, 0);
+  std::vector<int32_t> col;
+  std::vector<int64_t> from;
+  std::vector<int> trans;
+  for (int i = 0; i < n; ++i) {
+    std::sort(rows[i].begin(), rows[i].end());
+    for (auto& [j, q, t] : rows[i]) {
+      col.push_back(j);
+      from.push_back(q);
+      trans.push_back(t);
+    }
+    rp[i + 1] = (int64_t)col.size();
+  }
+  auto out = make_bsr_structure(ctx, n, a.rsz.data(), n, a.rsz.data(), std::move(rp), col, true);
+  if (!from.empty()) {
+    DBuf<int64_t> dfrom(from.size());
+    DBuf<int> dtrans(trans.size());
+    BMG_CUDA(cudaMemcpy(dfrom.p, from.data(), from.size() * 8, cudaMemcpyHostToDevice));
+    BMG_CUDA(cudaMemcpy(dtrans.p, trans.data(), trans.size() * 4, cudaMemcpyHostToDevice));
+    kern::gather_blocks_kernel<<<(int)std::min<size_t>(from.size(), (size_t)ctx->sms * 32), 128, 0, ctx->stream>>>(
+        lv.p, dfrom.p, dtrans.p, out->vals.p, (int64_t)from.size(), m, bs);
+    ctx->count();
+    BMG_CUDA(cudaGetLastError());
+    BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
   return out;
 }
 
@@ -446,6 +622,19 @@ int bmg_fsai_apply_transformed(const bmg_fsai* mh, const bmg_bsr* a, const bmg_v
     DBuf<double> t1(std::max(m->dim, 1)), t2(std::max(m->dim, 1));
     apply_transformed(*m, *B(a), V(x)->d.p, V(y)->d.p, t1.p, t2.p);
     BMG_CUDA(cudaStreamSynchronize(m->ctx->stream));
+  });
+}
+int bmg_triple_product(const bmg_bsr* f, const bmg_bsr* a, bmg_bsr** out) {
+  return guard([&] {
+    B(a)->ctx->activate();
+    *out = reinterpret_cast<bmg_bsr*>(triple_product(*B(f), *B(a)).release());
+  });
+}
+int bmg_fsai_chain_len(const bmg_fsai* m) { return (int)M(m)->fwd.size(); }
+int bmg_fsai_factor(const bmg_fsai* m, int k, const bmg_bsr** f) {
+  return guard([&] {
+    if (k < 0 || k >= (int)M(m)->fwd.size()) fail(BMG_ERANGE, "fsai: factor index out of range");
+    *f = reinterpret_cast<const bmg_bsr*>(M(m)->fwd[(size_t)k].get());
   });
 }
 int bmg_fsai_G(const bmg_fsai* m, const bmg_bsr** g) {

@@ -109,6 +109,9 @@ _SIGS = {
     "bmg_fsai_apply": (_I, [_P, _P, _P]),
     "bmg_fsai_apply_transformed": (_I, [_P, _P, _P, _P]),
     "bmg_fsai_G": (_I, [_P, _PP]),
+    "bmg_fsai_chain_len": (_I, [_P]),
+    "bmg_fsai_factor": (_I, [_P, _I, _PP]),
+    "bmg_triple_product": (_I, [_P, _P, _PP]),
     "bmg_cheb4_apply": (_I, [_P, _P, _P, _P, _D, _I]),
     "bmg_lanczos_lambda_max": (_I, [_P, _P, _I, _D, _U64, _PD]),
     "bmg_hier_setup": (_I, [_P, _I, _PP, C.POINTER(SetupParams), _PP]),

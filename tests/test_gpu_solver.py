@@ -244,3 +244,67 @@ def test_partitioned_vcycle_bitwise_equal_to_single(ctx, world, agg):
     hist1, it1, _ = h1.solve(3, 3, bv, x1, 1e-8, 6)
     hist2, it2, _ = h2.solve(3, 3, bv, x2, 1e-8, 6)
     assert it1 == it2 and np.array_equal(hist1, hist2)
+
+
+@pytest.mark.parametrize("t_max", [2, 3])
+def test_adaptive_fsai_general_tmax_bitwise(ctx, rng, t_max):
+    # adaptive_build with t_max > 1 (fsai.cpp:132-198): same pattern, bitwise G
+    host = pr.stencil_matrix(2, 12, 2, 10)
+    M = Fsai.build(BlockSparseMatrix(ctx, host), FSAI_ADAPTIVE, t_max=t_max)
+    of = O.Fsai(O.Mat(host), O.Fsai.NESTED, t_max=t_max)
+    _assert_same_bsr(M.G.download(host.row_sizes, host.col_sizes), of.G().export())
+    for rep in range(3):
+        sizes = random_layout(rng, 9, 3)
+        h2 = random_spd(rng, sizes, 0.7)
+        M2 = Fsai.build(BlockSparseMatrix(ctx, h2), FSAI_ADAPTIVE, t_max=t_max)
+        of2 = O.Fsai(O.Mat(h2), O.Fsai.NESTED, t_max=t_max)
+        _assert_same_bsr(M2.G.download(sizes, sizes), of2.G().export())
+
+
+def test_triple_product_bitwise(ctx, rng):
+    # kernels.cpp:88-119 on the device (F from a static FSAI of a stencil)
+    host = pr.stencil_matrix(2, 10, 2, 10)
+    of = O.Fsai(O.Mat(host), O.Fsai.STATIC)
+    F = of.factor(0).export()
+    want = O.triple_product(O.Mat(F), O.Mat(host)).export(symmetric=True)
+    from paper_2509_06744_b200 import triple_product
+
+    got = triple_product(BlockSparseMatrix(ctx, F), BlockSparseMatrix(ctx, host)).download(
+        host.row_sizes, host.col_sizes)
+    _assert_same_bsr(got, want)
+
+
+@pytest.mark.parametrize("t_max,nest", [(1, 1), (2, 1), (1, 2)])
+def test_nested_fsai_chain_matches_oracle(ctx, rng, t_max, nest):
+    # nested_build (fsai.cpp:243-253): F_0 .. F_{n-1} bitwise, G_n = L^-1 F_n bitwise,
+    # M r (chain apply, fsai.cpp:200-217) and beta within rounding
+    host = pr.stencil_matrix(2, 12, 2, 10)
+    A = BlockSparseMatrix(ctx, host)
+    M = Fsai.build(A, FSAI_ADAPTIVE, t_max=t_max, nest=nest)
+    om = O.Mat(host)
+    of = O.Fsai(om, O.Fsai.NESTED, t_max=t_max, nest=nest)
+    assert M.chain_len == of.chain_len() == nest + 1
+    for k in range(nest):
+        _assert_same_bsr(M.factor(k).download(host.row_sizes, host.col_sizes), of.factor(k).export())
+    _assert_same_bsr(M.G.download(host.row_sizes, host.col_sizes), of.G().export())
+    r = rng.standard_normal(host.dim_r)
+    z = Vector(ctx, host.dim_r)
+    M.apply(Vector(ctx, r), z)
+    want = of.apply(r)
+    assert np.linalg.norm(z.download() - want) <= 1e-12 * np.linalg.norm(want)
+    beta = lanczos_lambda_max(A, M, 100, 1.01, 42)
+    assert abs(beta - O.lanczos_lambda_max(om, of, 100, 1.01, 42)) <= 1e-10 * beta
+
+
+def test_nested_hierarchy_history_matches_oracle(ctx):
+    # C3's smoother (nest = 1) inside the V-cycle, small 2-D triharmonic-like problem
+    cfg = pr.CONFIGS["C3"].scaled(16, 2)
+    cfg.m = 10
+    A, T, b = pr.make_problem(cfg)
+    oh = O.Hierarchy(O.Mat(A), [O.Mat(p) for p in T], t_max=1, nest=1, coarse_dim_cap=1 << 30, probe=False)
+    dh = Hierarchy.setup(BlockSparseMatrix(ctx, A), [BlockSparseMatrix(ctx, p) for p in T],
+                         default_params(t_max=1, nest=1, coarse_dim_cap=1 << 30))
+    hist_o, it_o, st_o, _ = oh.solve(4, 4, b, np.zeros_like(b), 1e-8, 15)
+    hist_g, it_g, st_g = dh.solve(4, 4, Vector(ctx, b), Vector(ctx, b.size), 1e-8, 15)
+    assert it_o == it_g
+    assert np.all(np.abs(hist_g / hist_g[0] - hist_o / hist_o[0]) <= 1e-10)
