@@ -190,16 +190,20 @@ static int ring_stages() {
   return v;
 }
 
-// chunk size: about one phase-A item per consumer thread, capped by bytes so two
-// CTAs (4 stages each) fit per SM; BMG_CHUNK_KB overrides the byte cap
+// chunk size: about one phase-A item per consumer thread, capped in bytes so
+// several CTAs fit per SM.  Caps measured on B200 (tools/kernel_sweep.py, residual
+// pass on each config family's fine operator): 24 KB for m = 10 and 20, 32 KB for
+// m = 15 and 21.  BMG_CHUNK_KB overrides the cap for every m.
 static int chunk_blocks(int mr, int bs) {
-  static int cap = [] {
+  static int env_cap = [] {
     const char* e = std::getenv("BMG_CHUNK_KB");
-    int kb = e ? std::atoi(e) : 24;
+    if (!e) return 0;
+    int kb = std::atoi(e);
     if (kb < 2) kb = 2;
     if (kb > 48) kb = 48;
     return kb * 1024;
   }();
+  const int cap = env_cap ? env_cap : ((mr == 15 || mr == 21) ? 32 : 24) * 1024;
   const int by_items = std::max(1, kern::kConsumers / mr);
   const int by_bytes = std::max(1, cap / (bs * 8));
   return std::min(by_items, by_bytes);
