@@ -48,27 +48,71 @@ __global__ void symmetrize_dense_kernel(double* a, int64_t N) {
   }
 }
 
-// x = A0^{-1} b (dense, row-major): warp per row, double2 loads
-__global__ void __launch_bounds__(256) gemv_kernel(const double* __restrict__ a, const double* __restrict__ b,
-                                                   double* __restrict__ x, int64_t N) {
-  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (row >= N) return;
-  const double* ar = a + row * N;
-  double s = 0.0;
-  if ((N & 1) == 0) {
-    const double2* a2 = reinterpret_cast<const double2*>(ar);
-    const double2* b2 = reinterpret_cast<const double2*>(b);
-    for (int64_t q = lane; q < N / 2; q += 32) {
-      const double2 av = __ldg(a2 + q), bv = __ldg(b2 + q);
-      s = __fma_rn(av.x, bv.x, s);
-      s = __fma_rn(av.y, bv.y, s);
-    }
-  } else {
-    for (int64_t q = lane; q < N; q += 32) s = __fma_rn(__ldg(ar + q), __ldg(b + q), s);
+// Coarse solve x = A_0^{-1} b with the symmetric inverse stored as packed lower
+// 64 x 64 tiles (half the bytes of a dense GEMV).  Each tile (I, J), J <= I,
+// contributes tile * x_J to rows of I and (J < I) tile^T * x_I to rows of J;
+// partials are summed per row in ascending tile order (deterministic).
+constexpr int kTile = 64;
+
+__device__ __forceinline__ void tile_of(int64_t t, int* I, int* J) {
+  int i = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+  while ((int64_t)(i + 1) * (i + 2) / 2 <= t) ++i;
+  while ((int64_t)i * (i + 1) / 2 > t) --i;
+  *I = i;
+  *J = (int)(t - (int64_t)i * (i + 1) / 2);
+}
+
+__global__ void pack_lower_tiles_kernel(const double* __restrict__ full, int64_t N, double* __restrict__ tiles) {
+  int I, J;
+  tile_of(blockIdx.x, &I, &J);
+  double* dst = tiles + (int64_t)blockIdx.x * kTile * kTile;
+  for (int e = threadIdx.x; e < kTile * kTile; e += blockDim.x) {
+    const int r = e / kTile, c = e - r * kTile;
+    const int64_t gr = (int64_t)I * kTile + r, gc = (int64_t)J * kTile + c;
+    dst[e] = (gr < N && gc < N) ? full[gr * N + gc] : 0.0;
   }
-  for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o));
-  if (lane == 0) x[row] = s;
+}
+
+__global__ void __launch_bounds__(256) symv_tiles_kernel(const double* __restrict__ tiles,
+                                                         const double* __restrict__ x, int64_t N, int nt,
+                                                         double* __restrict__ part) {
+  __shared__ double tl[kTile][kTile + 1];
+  __shared__ double xi[kTile], xj[kTile];
+  int I, J;
+  tile_of(blockIdx.x, &I, &J);
+  const double2* src = reinterpret_cast<const double2*>(tiles + (int64_t)blockIdx.x * kTile * kTile);
+  for (int e = threadIdx.x; e < kTile * kTile / 2; e += blockDim.x) {
+    const double2 v = __ldg(src + e);
+    const int r = (2 * e) / kTile, c = (2 * e) - r * kTile;
+    tl[r][c] = v.x;
+    tl[r][c + 1] = v.y;
+  }
+  if (threadIdx.x < kTile) {
+    const int64_t gi = (int64_t)I * kTile + threadIdx.x, gj = (int64_t)J * kTile + threadIdx.x;
+    xi[threadIdx.x] = gi < N ? x[gi] : 0.0;
+    xj[threadIdx.x] = gj < N ? x[gj] : 0.0;
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t < kTile) {  // row part: tile * x_J
+    double s = 0.0;
+    for (int c = 0; c < kTile; ++c) s = __fma_rn(tl[t][c], xj[c], s);
+    part[((int64_t)I * nt + J) * kTile + t] = s;
+  } else if (t < 2 * kTile && J < I) {  // column part: tile^T * x_I
+    const int c = t - kTile;
+    double s = 0.0;
+    for (int r = 0; r < kTile; ++r) s = __fma_rn(tl[r][c], xi[r], s);
+    part[((int64_t)J * nt + I) * kTile + c] = s;
+  }
+}
+
+__global__ void symv_reduce_kernel(const double* __restrict__ part, int nt, int64_t N, double* __restrict__ y) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const int I = (int)(i / kTile), r = (int)(i - (int64_t)I * kTile);
+  double s = 0.0;
+  for (int J = 0; J < nt; ++J) s = __dadd_rn(s, part[((int64_t)I * nt + J) * kTile + r]);
+  y[i] = s;
 }
 
 // Partition-invariant squared norm: one fixed-shape tree per segment of
@@ -122,7 +166,8 @@ struct PLevel {  // one (virtual) rank's share of one level
 struct Part {
   int rank = 0;
   std::vector<PLevel> lv;
-  DBuf<double> ainv;  // dense A_0^{-1} (rank owning level 0)
+  DBuf<double> ainv;  // A_0^{-1} as packed lower 64x64 tiles (rank owning level 0)
+  DBuf<double> cpart; // per-(tile row, tile) partial sums of the coarse solve
 };
 
 struct LevelStats {  // global byte model inputs (bmg_hier_cycle_bytes)
@@ -278,10 +323,14 @@ static void coarse_solve(Hier& h) {
     PLevel& L = p.lv[0];
     if (!L.active()) continue;
     const int64_t N = h.n0;
-    kern::gemv_kernel<<<(int)((N * 32 + 255) / 256), 256, 0, h.ctx->stream>>>(p.ainv.p, vec(h, p, 0, VB) + L.off(),
-                                                                              vec(h, p, 0, VX) + L.off(), N);
-    h.ctx->count();
-    BMG_LAUNCHED(h.ctx->stream, "gemv_kernel");
+    const int nt = (int)((N + kern::kTile - 1) / kern::kTile);
+    const int64_t ntiles = (int64_t)nt * (nt + 1) / 2;
+    kern::symv_tiles_kernel<<<(unsigned)ntiles, 256, 0, h.ctx->stream>>>(p.ainv.p, vec(h, p, 0, VB) + L.off(), N, nt,
+                                                                        p.cpart.p);
+    kern::symv_reduce_kernel<<<(unsigned)((N + 255) / 256), 256, 0, h.ctx->stream>>>(p.cpart.p, nt, N,
+                                                                                      vec(h, p, 0, VX) + L.off());
+    h.ctx->count(2);
+    BMG_LAUNCHED(h.ctx->stream, "symv_kernels");
   }
 }
 
@@ -433,7 +482,17 @@ static void coarse_factor(Hier& h, Part& p) {
   kern::symmetrize_dense_kernel<<<grid1d(N * N), 256, 0, ctx->stream>>>(p.ainv.p, N);
   ctx->count();
   BMG_CUDA(cudaGetLastError());
+  // keep only the lower 64x64 tiles (packed); the dense copy is released
+  const int nt = (int)((N + kern::kTile - 1) / kern::kTile);
+  const int64_t ntiles = (int64_t)nt * (nt + 1) / 2;
+  DBuf<double> tiles((size_t)ntiles * kern::kTile * kern::kTile);
+  kern::pack_lower_tiles_kernel<<<(unsigned)ntiles, 256, 0, ctx->stream>>>(p.ainv.p, N, tiles.p);
+  ctx->count();
+  BMG_CUDA(cudaGetLastError());
   BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+  p.ainv = std::move(tiles);
+  p.cpart.alloc((size_t)nt * nt * kern::kTile);
+  BMG_CUDA(cudaMemsetAsync(p.cpart.p, 0, p.cpart.bytes(), ctx->stream));
 }
 
 static void alloc_vectors(Hier& h, PLevel& L, bool top) {
@@ -598,7 +657,10 @@ static void partition(Hier& h, int world, int rank, const int32_t* granule, int 
       }
       alloc_vectors(h, d, false);
     }
-    if (r == 0) p.ainv = std::move(G.ainv);
+    if (r == 0) {
+      p.ainv = std::move(G.ainv);
+      p.cpart = std::move(G.cpart);
+    }
     parts.push_back(std::move(p));
   }
   BMG_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -792,7 +854,7 @@ int bmg_hier_info(const bmg_hier* hh, int* nlevels, int64_t* device_bytes) {
     if (device_bytes) {
       int64_t b = 0;
       for (const Part& p : h->parts) {
-        b += (int64_t)p.ainv.bytes();
+        b += (int64_t)(p.ainv.bytes() + p.cpart.bytes());
         for (const auto& L : p.lv) {
           if (L.A_own) b += L.A_own->device_bytes();
           if (L.R_own) b += L.R_own->device_bytes();
@@ -848,7 +910,10 @@ int bmg_hier_cycle_bytes(const bmg_hier* hh, int kpre, int kpost, int64_t* bytes
       lvl += s.p_pass + 8 * nc + 16 * n;              // prolongation x += P e
       tot += lvl;
     }
-    tot += h->n0 * h->n0 * 8 + 16 * h->n0;  // dense coarse solve
+    {  // coarse solve: packed lower tiles of A_0^{-1}, x, b, tile partials
+      const int64_t nt = (h->n0 + 63) / 64;
+      tot += nt * (nt + 1) / 2 * 64 * 64 * 8 + 16 * h->n0 + 2 * nt * nt * 64 * 8;
+    }
     *bytes = tot;
   });
 }
