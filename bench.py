@@ -164,6 +164,42 @@ def run_reference(args, cfg):
 
 
 # ------------------------------------------------------------------ GPU arm
+def measure_c1(ctx, stream, steps):
+    """BASELINE configs[0] (C1): one fourth-kind smoother application, k = 3, static
+    block-FSAI lower(P(A)) on the 64^2 m = 10 operator.  Working set ~0.09 GB, so
+    the number is L2-resident by construction (labelled so)."""
+    import torch
+
+    from paper_2509_06744_b200 import (FSAI_STATIC_LOWER, BlockSparseMatrix, Fsai, Vector, cheb_fourth_apply,
+                                       lanczos_lambda_max)
+    from paper_2509_06744_b200 import problems as pr
+
+    c1 = pr.CONFIGS["C1"]
+    A = pr.stencil_matrix(c1.dim, c1.n, c1.power, c1.m, c1.seed, c1.reg)
+    dA = BlockSparseMatrix(ctx, A)
+    M = Fsai.build(dA, FSAI_STATIC_LOWER)
+    beta = lanczos_lambda_max(dA, M, 100, 1.01, 42)
+    b = Vector(ctx, pr.normal_vector(A.dim_r, c1.seed, 0))
+    x = Vector(ctx, pr.normal_vector(A.dim_r, c1.seed, 3))
+    for _ in range(5):
+        cheb_fourth_apply(dA, M, b, x, beta, c1.k)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = max(steps, 50)
+    e0.record(stream)
+    for _ in range(reps):
+        cheb_fourth_apply(dA, M, b, x, beta, c1.k)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    n = A.dim_r
+    g, gt = M.G, M.G.transpose()
+    per = c1.k * (dA.info()["pass_bytes"] + 24 * n + g.info()["pass_bytes"] + gt.info()["pass_bytes"] + 56 * n)
+    return {"workload": "C1: 64^2 patches, m=10, static block-FSAI lower(P(A)), one cheb4 application k=3",
+            "value": 1e3 / ms, "unit": "smoother applications/s", "ms": ms, "bytes_per_application": per,
+            "gbs": per / ms / 1e6, "l2": "L2-resident (0.09 GB working set < 126 MB L2)"}
+
+
 def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
@@ -300,6 +336,13 @@ def run_ours(args, cfg):
         e2e_ms = float(t.item())
     e2e_rate = (1 if scaling == "strong" else ws) * args.steps / (e2e_ms / 1e3)
 
+    extra = None
+    if rank == 0 and ws == 1:
+        try:
+            extra = {"C1": measure_c1(ctx, stream, args.steps)}
+        except Exception as e:  # secondary line; never fail the headline run
+            extra = {"C1": {"error": f"{type(e).__name__}: {e}"}}
+
     # ---- CPU baseline (rank 0, N = 1 only): bounded oracle sample
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -342,6 +385,8 @@ def run_ours(args, cfg):
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
+        if extra is not None:
+            line["extra_configs"] = extra
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()

@@ -65,6 +65,7 @@ struct Ctx {
   void* nccl = nullptr;  // ncclComm_t of a multi-GPU context (bmg_ctx_create_nccl)
   int rank = 0, world = 1;
   DBuf<double> red;          // reduction partials
+  DBuf<double> work;         // scratch of the standalone smoother
   double* h_red = nullptr;   // pinned result slot(s)
   void activate() const { BMG_CUDA(cudaSetDevice(device)); }
   void count(int n = 1) { launches += n; }

@@ -641,7 +641,8 @@ int bmg_fsai_G(const bmg_fsai* m, const bmg_bsr** g) {
   return guard([&] { *g = reinterpret_cast<const bmg_bsr*>(&M(m)->G()); });
 }
 
-// cheb_fourth_apply (chebyshev.hpp:48-69) on the device
+// cheb_fourth_apply (chebyshev.hpp:48-69) on the device; asynchronous on the
+// context stream, work vectors cached in the context
 int bmg_cheb4_apply(const bmg_bsr* ah, const bmg_fsai* mh, const bmg_vec* b, bmg_vec* x, double beta, int k) {
   return guard([&] {
     if (!(beta > 0.0)) fail(BMG_EINVAL, "cheb_fourth_apply: beta must be positive");
@@ -649,10 +650,14 @@ int bmg_cheb4_apply(const bmg_bsr* ah, const bmg_fsai* mh, const bmg_vec* b, bmg
     const Bsr* a = B(ah);
     need_len(V(b), a->dim_r, "cheb_fourth_apply");
     need_len(V(x), a->dim_r, "cheb_fourth_apply");
+    Ctx* ctx = a->ctx;
     const int64_t n = std::max<int64_t>(a->dim_r, 1);
-    DBuf<double> r(n), w(n), t(n), p(n);
-    smooth_single(*a, *M(mh), beta, k, V(b)->d.p, V(x)->d.p, r.p, w.p, t.p, p.p);
-    BMG_CUDA(cudaStreamSynchronize(a->ctx->stream));
+    if (ctx->work.n < (size_t)(4 * n)) {
+      BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+      ctx->work.alloc(4 * n);
+    }
+    double* w0 = ctx->work.p;
+    smooth_single(*a, *M(mh), beta, k, V(b)->d.p, V(x)->d.p, w0, w0 + n, w0 + 2 * n, w0 + 3 * n);
   });
 }
 
