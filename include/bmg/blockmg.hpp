@@ -47,6 +47,8 @@ inline void check(int status) {
   }
 }
 
+enum class SmootherKind { Richardson = 0, ChebFirst = 1, ChebFourth = 2 };  // chebyshev.hpp:10
+
 // Partition of {0..N-1} into blocks of sizes m_i >= 1 (block_layout.hpp:8-28).
 class BlockLayout {
  public:
@@ -195,6 +197,17 @@ inline void cheb_fourth_apply(const DeviceMatrix& a, const NestedFsai& m, const 
   check(bmg_cheb4_apply(a.get(), m.get(), b.get(), x.get(), beta, k));
 }
 
+struct SmootherSpec {  // chebyshev.hpp:12-18
+  SmootherKind kind = SmootherKind::ChebFourth;
+  int degree = 1;
+  double alpha = 0.0, beta = 1.0, omega = 1.0;
+};
+// x <- apply_smoother(spec, degree, A, M, b, x) (chebyshev.hpp:117-129), in place
+inline void apply_smoother(const SmootherSpec& s, int degree, const DeviceMatrix& a, const NestedFsai& m,
+                           const DeviceVector& b, DeviceVector& x) {
+  check(bmg_smoother_apply(a.get(), m.get(), (int)s.kind, s.alpha, s.beta, s.omega, degree, b.get(), x.get()));
+}
+
 inline double lanczos_lambda_max(const DeviceMatrix& a, const NestedFsai& m, int iters = 100,
                                  double safety = 1.01, uint64_t seed = 42) {
   double beta = 0.0;
@@ -209,7 +222,10 @@ struct CycleSpec {  // multilevel.hpp:13-19
   static CycleSpec v2k0(int k) { return {2 * k, 0}; }
 };
 
-struct SetupParams {  // multilevel.hpp:35-47 (fourth-kind smoothing)
+struct SetupParams {  // multilevel.hpp:35-47
+  SmootherKind kind = SmootherKind::ChebFourth;
+  double richardson_omega = 1.0;
+  double first_kind_fraction = 1.0 / 30.0;
   int t_max = 4;
   double tau = 1.0;
   int nest = 0;
@@ -258,6 +274,9 @@ inline Hierarchy setup(const DeviceMatrix& a_finest, const std::vector<const Dev
   c.lanczos_safety = p.lanczos_safety;
   c.seed = p.seed;
   c.coarse_dim_cap = p.coarse_dim_cap;
+  c.smoother_kind = (int)p.kind;
+  c.richardson_omega = p.richardson_omega;
+  c.first_kind_fraction = p.first_kind_fraction;
   std::vector<const bmg_bsr*> t;
   for (auto* m : transfers) t.push_back(m->get());
   bmg_hier* h = nullptr;

@@ -78,8 +78,7 @@ typedef struct bmg_vec bmg_vec;
 typedef struct bmg_fsai bmg_fsai;
 typedef struct bmg_hier bmg_hier;
 
-/* SetupParams (multilevel.hpp:35-47); only the fourth-kind smoother is on the
- * device path (SmootherKind::ChebFourth, the reference default). */
+/* SetupParams (multilevel.hpp:35-47) */
 typedef struct bmg_setup_params {
   int t_max;          /* 4 in the reference; 1 for the BASELINE configs */
   double tau;         /* 1.0 */
@@ -89,6 +88,9 @@ typedef struct bmg_setup_params {
   double lanczos_safety; /* 1.01 */
   uint64_t seed;      /* 42 */
   int coarse_dim_cap; /* 5000 */
+  int smoother_kind;  /* 0 Richardson, 1 first kind, 2 fourth kind (default) */
+  double richardson_omega;    /* 1.0 */
+  double first_kind_fraction; /* 1/30: first kind covers [fraction * beta, beta] */
 } bmg_setup_params;
 
 const char* bmg_last_error(void);
@@ -155,6 +157,10 @@ int bmg_fsai_factor(const bmg_fsai* m, int k, const bmg_bsr** f);
 /* ---- smoother / spectral bound ------------------------------------------ */
 int bmg_cheb4_apply(const bmg_bsr* a, const bmg_fsai* m, const bmg_vec* b, bmg_vec* x,
                     double beta, int k);
+/* apply_smoother (chebyshev.hpp:117-129): kind 0 Richardson (omega), 1 first kind
+ * on [alpha, beta], 2 fourth kind (beta); x updated in place */
+int bmg_smoother_apply(const bmg_bsr* a, const bmg_fsai* m, int kind, double alpha, double beta,
+                       double omega, int k, const bmg_vec* b, bmg_vec* x);
 int bmg_lanczos_lambda_max(const bmg_bsr* a, const bmg_fsai* m, int iters, double safety,
                            uint64_t seed, double* beta);
 
@@ -170,6 +176,8 @@ int bmg_hier_create(bmg_ctx* ctx, int nlevels, const bmg_bsr* const* A, const bm
 int bmg_hier_destroy(bmg_hier* h);
 int bmg_hier_info(const bmg_hier* h, int* nlevels, int64_t* device_bytes);
 int bmg_hier_beta(const bmg_hier* h, int level, double* beta);
+/* the level's SmootherSpec (Level::smoother, multilevel.hpp:25) */
+int bmg_hier_set_smoother(bmg_hier* h, int level, int kind, double alpha, double beta, double omega);
 int bmg_hier_level(const bmg_hier* h, int level, const bmg_bsr** a, const bmg_bsr** p,
                    const bmg_fsai** m);
 /* algorithmic HBM bytes of one V(k_pre,k_post) cycle on the finest level */

@@ -990,7 +990,9 @@ static Mat galerkin(const Mat& a, const Mat& p) {
 struct Level {
   Mat A, P;
   Nested fsai;
-  double beta = 1.0;
+  double beta = 1.0;  // SmootherSpec (chebyshev.hpp:12-18)
+  int kind = 2;
+  double alpha = 0.0, omega = 1.0;
 };
 
 struct Hier {
@@ -1058,7 +1060,7 @@ static double lanczos_lambda_max(const Mat& a, const Nested& f, int iters, doubl
 // setup: multilevel.cpp:36-75
 static Hier setup(const Mat& a_finest, std::vector<Mat> transfers, int t_max, double tau, int nest,
                   int fsai_kind, int lanczos_iters, double safety, uint64_t seed, int cap,
-                  bool probe) {
+                  bool probe, int kind, double omega, double fraction) {
   Hier h;
   const int depth = (int)transfers.size();
   h.levels.resize(depth + 1);
@@ -1082,6 +1084,9 @@ static Hier setup(const Mat& a_finest, std::vector<Mat> transfers, int t_max, do
     Level& lv = h.levels[l];
     lv.fsai = fsai_kind == 0 ? static_fsai(lv.A) : nested_build(lv.A, t_max, tau, nest);
     lv.beta = lanczos_lambda_max(lv.A, lv.fsai, lanczos_iters, safety, seed);
+    lv.kind = kind;  // multilevel.cpp:62-65
+    lv.alpha = fraction * lv.beta;
+    lv.omega = omega;
   }
   const int n0 = h.levels.front().A.rl.dim;
   if (n0 > cap) throw std::invalid_argument("setup: coarsest level exceeds the dense-solve cap");
@@ -1104,7 +1109,7 @@ static void v_cycle(const Hier& h, int k_pre, int k_post, int level, const doubl
   const int n = lv.A.rl.dim;
   auto a_op = [&](const double* in, double* out) { spmv(lv.A, in, out); };
   auto m_op = [&](const double* in, double* out) { nested_apply(lv.fsai, in, out); };
-  if (k_pre > 0) apply_smoother(2, 0.0, lv.beta, 1.0, k_pre, a_op, m_op, b, x, n);
+  if (k_pre > 0) apply_smoother(lv.kind, lv.alpha, lv.beta, lv.omega, k_pre, a_op, m_op, b, x, n);
   std::vector<double> r(n);
   spmv(lv.A, x, r.data());
   for (int i = 0; i < n; ++i) r[i] = b[i] - r[i];
@@ -1115,7 +1120,7 @@ static void v_cycle(const Hier& h, int k_pre, int k_post, int level, const doubl
   std::vector<double> pe(n);
   spmv(lv.P, ec.data(), pe.data());
   for (int i = 0; i < n; ++i) x[i] += pe[i];
-  if (k_post > 0) apply_smoother(2, 0.0, lv.beta, 1.0, k_post, a_op, m_op, b, x, n);
+  if (k_post > 0) apply_smoother(lv.kind, lv.alpha, lv.beta, lv.omega, k_post, a_op, m_op, b, x, n);
 }
 
 }  // namespace orc
@@ -1401,13 +1406,15 @@ double orc_fourth_kind_mu(int n) { return fourth_kind_mu(n); }
 
 int orc_setup(const orc_mat* a_finest, int ntransfers, const orc_mat* const* transfers, int t_max,
               double tau, int nest, int fsai_kind, int lanczos_iters, double lanczos_safety,
-              uint64_t seed, int coarse_dim_cap, int smallest_ritz_probe, orc_hier** out) {
+              uint64_t seed, int coarse_dim_cap, int smallest_ritz_probe, int smoother_kind,
+              double richardson_omega, double first_kind_fraction, orc_hier** out) {
   return guard([&] {
     std::vector<Mat> tr;
     for (int i = 0; i < ntransfers; ++i) tr.push_back(transfers[i]->m);
     *out = new orc_hier{setup(a_finest->m, std::move(tr), t_max, tau, nest, fsai_kind,
                               lanczos_iters, lanczos_safety, seed, coarse_dim_cap,
-                              smallest_ritz_probe != 0)};
+                              smallest_ritz_probe != 0, smoother_kind, richardson_omega,
+                              first_kind_fraction)};
   });
 }
 void orc_hier_destroy(orc_hier* h) { delete h; }

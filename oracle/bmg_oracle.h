@@ -111,6 +111,7 @@ double orc_fourth_kind_mu(int n);
 int orc_setup(const orc_mat* a_finest, int ntransfers, const orc_mat* const* transfers,
               int t_max, double tau, int nest, int fsai_kind, int lanczos_iters,
               double lanczos_safety, uint64_t seed, int coarse_dim_cap, int smallest_ritz_probe,
+              int smoother_kind, double richardson_omega, double first_kind_fraction,
               orc_hier** out);
 void orc_hier_destroy(orc_hier* h);
 int orc_hier_levels(const orc_hier* h);

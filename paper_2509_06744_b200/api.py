@@ -299,6 +299,12 @@ def cheb_fourth_apply(a: BlockSparseMatrix, m: Fsai, b: Vector, x: Vector, beta:
     check(lib().bmg_cheb4_apply(a.h, m.h, b.h, x.h, beta, k))
 
 
+def apply_smoother(a: BlockSparseMatrix, m: Fsai, kind: int, b: Vector, x: Vector, k: int, alpha=0.0, beta=1.0,
+                   omega=1.0):
+    """x <- apply_smoother(spec, k, A, M, b, x) (chebyshev.hpp:117-129), in place."""
+    check(lib().bmg_smoother_apply(a.h, m.h, kind, alpha, beta, omega, k, b.h, x.h))
+
+
 def lanczos_lambda_max(a: BlockSparseMatrix, m: Fsai, iters=100, safety=1.01, seed=42) -> float:
     out = C.c_double()
     check(lib().bmg_lanczos_lambda_max(a.h, m.h, iters, safety, seed, C.byref(out)))
@@ -356,6 +362,9 @@ class Hierarchy:
         out = C.c_double()
         check(lib().bmg_hier_beta(self.h, level, C.byref(out)))
         return out.value
+
+    def set_smoother(self, level: int, kind: int, alpha=0.0, beta=1.0, omega=1.0):
+        check(lib().bmg_hier_set_smoother(self.h, level, kind, alpha, beta, omega))
 
     def level(self, l: int):
         a, p, m = C.c_void_p(), C.c_void_p(), C.c_void_p()

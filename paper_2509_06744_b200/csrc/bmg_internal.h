@@ -147,6 +147,18 @@ void prolong_add(const Bsr& a, const double* e, double* x);
 // x = (xzero ? 0 : x) + dmu p
 void gt_cheb(const Bsr& gt, const double* w, double* p, double* x, double mu2, double dmu,
              bool first, bool xzero);
+// SmootherSpec (chebyshev.hpp:10-18): 0 Richardson, 1 first kind, 2 fourth kind
+struct SmootherSpec {
+  int kind = 2;
+  double alpha = 0.0, beta = 1.0, omega = 1.0;
+};
+// per step of a smoother application: p = first ? z : coef*p + z; x += c*p
+// (cheb_fourth_apply, cheb_first_apply, richardson_apply: chebyshev.hpp:48-115)
+struct StepScalars {
+  bool first;
+  double coef, c;
+};
+std::vector<StepScalars> smoother_schedule(const SmootherSpec& s, int k);
 double dot(Ctx* ctx, const double* a, const double* b, int64_t n);
 void fill(Ctx* ctx, double* p, int64_t n, double v);
 void copy(Ctx* ctx, double* dst, const double* src, int64_t n);

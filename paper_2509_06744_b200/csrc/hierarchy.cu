@@ -155,7 +155,7 @@ struct PLevel {  // one (virtual) rank's share of one level
   const Fsai* M = nullptr;
   std::unique_ptr<Bsr> A_own, R_own, P_own;
   std::unique_ptr<Fsai> M_own;
-  double beta = 1.0;
+  SmootherSpec spec;  // Level::smoother (multilevel.hpp:25)
   DBuf<double> v[VNUM];
   int64_t off() const { return (int64_t)(lo - wlo) * m; }
   int64_t n_own() const { return (int64_t)(hi - lo) * m; }
@@ -187,6 +187,7 @@ struct Hier {
   bool emulated = false;  // all virtual ranks live in this process
   std::vector<Part> parts;
   std::vector<int> nbr, msz;                  // per level
+  std::vector<size_t> nfactors;               // per level: FSAI chain length
   std::vector<std::vector<int32_t>> bounds;   // per level: world + 1
   std::vector<std::vector<int32_t>> wlo, whi; // per level, per rank
   int granule_top = 1;                        // block rows per norm segment (top level)
@@ -265,12 +266,26 @@ static void exchange(Hier& h, int l, Which w) {
 }
 
 // ============================================================================ V-cycle
-// one fourth-kind smoothing application on level l, all parts (chebyshev.hpp:48-69)
+// one smoother application (apply_smoother, chebyshev.hpp:117-129) on level l, all parts
 static void smooth(Hier& h, int l, int k, bool xzero) {
   if (k < 1) return;
-  for (int s = 1; s <= k; ++s) {
+  const SmootherSpec* spec = nullptr;
+  const Fsai* M0 = nullptr;
+  for (Part& p : h.parts)
+    if (p.lv[l].active()) {
+      spec = &p.lv[l].spec;
+      M0 = p.lv[l].M;
+    }
+  if (!spec) {  // this rank owns no rows of the level: it only serves halos
+    spec = &h.parts[0].lv[l].spec;
+  }
+  const auto steps = smoother_schedule(*spec, k);
+  const size_t nf = M0 ? M0->fwd.size() : h.nfactors[l], nb = nf;
+  for (size_t s = 0; s < steps.size(); ++s) {
+    const StepScalars& st = steps[s];
     Which src;
-    if (s == 1 && xzero) {
+    const bool zero_x = (s == 0 && xzero);
+    if (zero_x) {
       src = VB;  // A * 0 = 0: r = b exactly
     } else {
       exchange(h, l, VX);
@@ -284,10 +299,6 @@ static void smooth(Hier& h, int l, int k, bool xzero) {
     // forward chain w = F_n ... F_0 r (nest = 0: w = G r), then all but the last transpose
     Which cur = src;
     Which nxt = VW;
-    const Fsai* M0 = nullptr;
-    for (Part& p : h.parts)
-      if (p.lv[l].active()) M0 = p.lv[l].M;
-    const size_t nf = M0 ? M0->fwd.size() : 1, nb = M0 ? M0->bwd.size() : 1;
     for (size_t q = 0; q < nf + nb - 1; ++q) {
       exchange(h, l, cur);
       for (Part& p : h.parts) {
@@ -303,17 +314,8 @@ static void smooth(Hier& h, int l, int k, bool xzero) {
     for (Part& p : h.parts) {
       PLevel& L = p.lv[l];
       if (!L.active()) continue;
-      const double d = 4.0 / L.beta;
-      double* P = vec(h, p, l, VP) + L.off();
-      double* X = vec(h, p, l, VX) + L.off();
-      if (s == 1) {
-        const double dmu = d * ((2.0 * 0 + 1.0) / (2.0 * 0 + 3.0));
-        gt_cheb(*L.M->bwd[0], vec(h, p, l, cur), P, X, 0.0, dmu, true, xzero);
-      } else {
-        const double mu_prev = (2.0 * (s - 2) + 1.0) / (2.0 * (s - 2) + 3.0);
-        const double mu = (2.0 * (s - 1) + 1.0) / (2.0 * (s - 1) + 3.0);
-        gt_cheb(*L.M->bwd[0], vec(h, p, l, cur), P, X, mu_prev * mu_prev, d * mu, false, false);
-      }
+      gt_cheb(*L.M->bwd[0], vec(h, p, l, cur), vec(h, p, l, VP) + L.off(), vec(h, p, l, VX) + L.off(), st.coef,
+              st.c, st.first, zero_x);
     }
   }
 }
@@ -546,6 +548,8 @@ static void finish_whole(Hier& h, int cap) {
     h.whi[l][0] = h.nbr[l];
   }
   h.granule_top = 1;
+  h.nfactors.assign(L, 1);
+  for (int l = 1; l < L; ++l) h.nfactors[l] = p.lv[l].M->fwd.size();
   coarse_factor(h, p);
   record_stats(h);
 }
@@ -637,7 +641,7 @@ static void partition(Hier& h, int world, int rank, const int32_t* granule, int 
       d.wlo = WL[l][r];
       d.whi = WH[l][r];
       d.m = h.msz[l];
-      d.beta = s.beta;
+      d.spec = s.spec;
       const int nwin = d.whi - d.wlo;
       d.A_own = slice_rows(*s.A, d.lo, d.hi, d.wlo, nwin);
       d.A = d.A_own.get();
@@ -781,7 +785,11 @@ int bmg_hier_setup(const bmg_bsr* a_finest, int ntransfers, const bmg_bsr* const
       PLevel& L = p.lv[l];
       L.M_own = fsai_build(*L.A, prm.fsai_kind, prm.t_max, prm.tau, prm.nest);
       L.M = L.M_own.get();
-      L.beta = lanczos_lambda_max(*L.A, *L.M, prm.lanczos_iters, prm.lanczos_safety, prm.seed);
+      const double beta = lanczos_lambda_max(*L.A, *L.M, prm.lanczos_iters, prm.lanczos_safety, prm.seed);
+      L.spec.kind = prm.smoother_kind;  // multilevel.cpp:62-65
+      L.spec.beta = beta;
+      L.spec.alpha = prm.first_kind_fraction * beta;
+      L.spec.omega = prm.richardson_omega;
     }
     finish_whole(*h, prm.coarse_dim_cap);
     *out = reinterpret_cast<bmg_hier*>(h.release());
@@ -809,8 +817,10 @@ int bmg_hier_create(bmg_ctx* ctx, int nlevels, const bmg_bsr* const* A, const bm
         L.R_own = bsr_transpose(*L.P);
         L.R = L.R_own.get();
         L.M = M_(Mh[l]);
-        L.beta = beta[l];
-        if (!(L.beta > 0.0)) fail(BMG_EINVAL, "cheb_fourth_apply: beta must be positive");
+        L.spec.kind = 2;
+        L.spec.beta = beta[l];
+        L.spec.alpha = beta[l] / 30.0;
+        if (!(L.spec.beta > 0.0)) fail(BMG_EINVAL, "cheb_fourth_apply: beta must be positive");
       }
     }
     finish_whole(*h, coarse_dim_cap);
@@ -875,7 +885,22 @@ int bmg_hier_beta(const bmg_hier* hh, int level, double* beta) {
   return guard([&] {
     const Hier* h = H_(hh);
     if (level < 1 || level > h->finest()) fail(BMG_ERANGE, "hierarchy: level out of range");
-    *beta = h->parts[0].lv[level].beta;
+    *beta = h->parts[0].lv[level].spec.beta;
+  });
+}
+
+int bmg_hier_set_smoother(bmg_hier* hh, int level, int kind, double alpha, double beta, double omega) {
+  return guard([&] {
+    Hier* h = H_(hh);
+    if (level < 1 || level > h->finest()) fail(BMG_ERANGE, "hierarchy: level out of range");
+    SmootherSpec s;
+    s.kind = kind;
+    s.alpha = alpha;
+    s.beta = beta;
+    s.omega = omega;
+    smoother_schedule(s, 1);  // validates the spec
+    for (Part& p : h->parts) p.lv[level].spec = s;
+    h->drop_graphs();
   });
 }
 

@@ -518,13 +518,52 @@ double lanczos_lambda_max(const Bsr& a, const Fsai& m, int iters, double safety,
   return safety * ev.back();
 }
 
-// ============================================================================ standalone smoother
-// cheb_fourth_apply (chebyshev.hpp:48-69) on one device: r = b - A x; M r as the
+// ============================================================================ smoothers
+// Scalar sequences of the three smoothers, evaluated with the reference's own
+// expressions (chebyshev.hpp:42, 51-52, 78-99, 106-113).
+std::vector<StepScalars> smoother_schedule(const SmootherSpec& s, int k) {
+  std::vector<StepScalars> out;
+  if (s.kind == 2) {
+    if (!(s.beta > 0.0)) fail(BMG_EINVAL, "cheb_fourth_apply: beta must be positive");
+    if (k < 1) fail(BMG_EINVAL, "cheb_fourth_apply: degree must be >= 1");
+    const double d = 4.0 / s.beta;
+    double mu = (2.0 * 0 + 1.0) / (2.0 * 0 + 3.0);
+    out.push_back({true, 0.0, d * mu});
+    for (int i = 2; i <= k; ++i) {
+      const double mu2 = mu * mu;
+      mu = (2.0 * (i - 1) + 1.0) / (2.0 * (i - 1) + 3.0);
+      out.push_back({false, mu2, d * mu});
+    }
+  } else if (s.kind == 1) {
+    if (!(s.alpha > 0.0) || !(s.alpha < s.beta))
+      fail(BMG_EINVAL, "cheb_first_apply: interval must satisfy 0 < alpha < beta");
+    if (k < 1) fail(BMG_EINVAL, "cheb_first_apply: degree must be >= 1");
+    const double c = 0.5 * (s.alpha + s.beta);
+    const double d = 0.5 * (s.beta - s.alpha);
+    double omega = 1.0 / c;
+    double psi = 0.5 * (d * omega) * (d * omega);
+    out.push_back({true, 0.0, omega});
+    for (int i = 2; i <= k; ++i) {
+      const double coef = psi;
+      omega = 1.0 / (c - psi / omega);
+      psi = 0.25 * (d * omega) * (d * omega);
+      out.push_back({false, coef, omega});
+    }
+  } else if (s.kind == 0) {
+    if (k < 1) fail(BMG_EINVAL, "richardson_apply: step count must be >= 1");
+    for (int i = 0; i < k; ++i) out.push_back({true, 0.0, s.omega});
+  } else {
+    fail(BMG_EINVAL, "apply_smoother: unknown kind");
+  }
+  return out;
+}
+
+// apply_smoother (chebyshev.hpp:117-129) on one device: r = b - A x; M r as the
 // forward passes then the transposes, the last transpose fused with the update.
-static void smooth_single(const Bsr& A, const Fsai& M, double beta, int k, const double* b, double* x, double* r,
-                          double* w, double* t, double* p) {
-  const double d = 4.0 / beta;
-  for (int s = 1; s <= k; ++s) {
+static void smooth_single(const Bsr& A, const Fsai& M, const SmootherSpec& spec, int k, const double* b,
+                          double* x, double* r, double* w, double* t, double* p) {
+  const auto steps = smoother_schedule(spec, k);
+  for (const StepScalars& st : steps) {
     residual(A, b, x, r);
     const double* cur = r;
     double* bufs[2] = {w, t};
@@ -539,13 +578,7 @@ static void smooth_single(const Bsr& A, const Fsai& M, double beta, int k, const
       cur = bufs[sel];
       sel ^= 1;
     }
-    if (s == 1) {
-      gt_cheb(*M.bwd[0], cur, p, x, 0.0, d * ((2.0 * 0 + 1.0) / (2.0 * 0 + 3.0)), true, false);
-    } else {
-      const double mu_prev = (2.0 * (s - 2) + 1.0) / (2.0 * (s - 2) + 3.0);
-      const double mu = (2.0 * (s - 1) + 1.0) / (2.0 * (s - 1) + 3.0);
-      gt_cheb(*M.bwd[0], cur, p, x, mu_prev * mu_prev, d * mu, false, false);
-    }
+    gt_cheb(*M.bwd[0], cur, p, x, st.coef, st.c, st.first, false);
   }
 }
 
@@ -567,6 +600,9 @@ void need_len(const Vec* v, int64_t n, const char* what) {
 extern "C" {
 
 void bmg_setup_params_default(bmg_setup_params* p) {
+  p->smoother_kind = 2;
+  p->richardson_omega = 1.0;
+  p->first_kind_fraction = 1.0 / 30.0;
   p->t_max = 4;
   p->tau = 1.0;
   p->nest = 0;
@@ -641,23 +677,42 @@ int bmg_fsai_G(const bmg_fsai* m, const bmg_bsr** g) {
   return guard([&] { *g = reinterpret_cast<const bmg_bsr*>(&M(m)->G()); });
 }
 
-// cheb_fourth_apply (chebyshev.hpp:48-69) on the device; asynchronous on the
-// context stream, work vectors cached in the context
+// apply_smoother / cheb_fourth_apply (chebyshev.hpp:48-129) on the device;
+// asynchronous on the context stream, work vectors cached in the context
+static void smoother_abi(const bmg_bsr* ah, const bmg_fsai* mh, const SmootherSpec& spec, const bmg_vec* b,
+                         bmg_vec* x, int k) {
+  smoother_schedule(spec, k);  // validation before any launch
+  const Bsr* a = B(ah);
+  need_len(V(b), a->dim_r, "apply_smoother");
+  need_len(V(x), a->dim_r, "apply_smoother");
+  Ctx* ctx = a->ctx;
+  const int64_t n = std::max<int64_t>(a->dim_r, 1);
+  if (ctx->work.n < (size_t)(4 * n)) {
+    BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->work.alloc(4 * n);
+  }
+  double* w0 = ctx->work.p;
+  smooth_single(*a, *M(mh), spec, k, V(b)->d.p, V(x)->d.p, w0, w0 + n, w0 + 2 * n, w0 + 3 * n);
+}
+
 int bmg_cheb4_apply(const bmg_bsr* ah, const bmg_fsai* mh, const bmg_vec* b, bmg_vec* x, double beta, int k) {
   return guard([&] {
-    if (!(beta > 0.0)) fail(BMG_EINVAL, "cheb_fourth_apply: beta must be positive");
-    if (k < 1) fail(BMG_EINVAL, "cheb_fourth_apply: degree must be >= 1");
-    const Bsr* a = B(ah);
-    need_len(V(b), a->dim_r, "cheb_fourth_apply");
-    need_len(V(x), a->dim_r, "cheb_fourth_apply");
-    Ctx* ctx = a->ctx;
-    const int64_t n = std::max<int64_t>(a->dim_r, 1);
-    if (ctx->work.n < (size_t)(4 * n)) {
-      BMG_CUDA(cudaStreamSynchronize(ctx->stream));
-      ctx->work.alloc(4 * n);
-    }
-    double* w0 = ctx->work.p;
-    smooth_single(*a, *M(mh), beta, k, V(b)->d.p, V(x)->d.p, w0, w0 + n, w0 + 2 * n, w0 + 3 * n);
+    SmootherSpec s;
+    s.kind = 2;
+    s.beta = beta;
+    smoother_abi(ah, mh, s, b, x, k);
+  });
+}
+
+int bmg_smoother_apply(const bmg_bsr* ah, const bmg_fsai* mh, int kind, double alpha, double beta, double omega,
+                       int k, const bmg_vec* b, bmg_vec* x) {
+  return guard([&] {
+    SmootherSpec s;
+    s.kind = kind;
+    s.alpha = alpha;
+    s.beta = beta;
+    s.omega = omega;
+    smoother_abi(ah, mh, s, b, x, k);
   });
 }
 

@@ -21,6 +21,7 @@ HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "bmg_cuda.h")
 BMG_OK, BMG_EINVAL, BMG_ERANGE, BMG_ENOTSPD, BMG_ERUNTIME, BMG_ECUDA, BMG_ENCCL = 0, -1, -2, -3, -4, -5, -6
 BMG_SYMMETRIC = 1
 FSAI_STATIC_LOWER, FSAI_DIAGONAL, FSAI_ADAPTIVE = 0, 1, 3
+RICHARDSON, CHEB_FIRST, CHEB_FOURTH = 0, 1, 2  # SmootherKind (chebyshev.hpp:10)
 
 
 class BmgError(RuntimeError):
@@ -63,6 +64,9 @@ class SetupParams(C.Structure):
         ("lanczos_safety", C.c_double),
         ("seed", C.c_uint64),
         ("coarse_dim_cap", C.c_int),
+        ("smoother_kind", C.c_int),
+        ("richardson_omega", C.c_double),
+        ("first_kind_fraction", C.c_double),
     ]
 
 
@@ -114,6 +118,8 @@ _SIGS = {
     "bmg_triple_product": (_I, [_P, _P, _PP]),
     "bmg_cheb4_apply": (_I, [_P, _P, _P, _P, _D, _I]),
     "bmg_lanczos_lambda_max": (_I, [_P, _P, _I, _D, _U64, _PD]),
+    "bmg_smoother_apply": (_I, [_P, _P, _I, _D, _D, _D, _I, _P, _P]),
+    "bmg_hier_set_smoother": (_I, [_P, _I, _I, _D, _D, _D]),
     "bmg_hier_setup": (_I, [_P, _I, _PP, C.POINTER(SetupParams), _PP]),
     "bmg_hier_create": (_I, [_P, _I, _PP, _PP, _PP, _PD, _I, _PP]),
     "bmg_hier_destroy": (_I, [_P]),

@@ -308,3 +308,42 @@ def test_nested_hierarchy_history_matches_oracle(ctx):
     hist_g, it_g, st_g = dh.solve(4, 4, Vector(ctx, b), Vector(ctx, b.size), 1e-8, 15)
     assert it_o == it_g
     assert np.all(np.abs(hist_g / hist_g[0] - hist_o / hist_o[0]) <= 1e-10)
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2])
+def test_apply_smoother_kinds_match_oracle(ctx, kind):
+    # apply_smoother (chebyshev.hpp:117-129): Richardson, first kind on [beta/30, beta], fourth kind
+    from paper_2509_06744_b200 import apply_smoother
+
+    host = pr.stencil_matrix(2, 16, 2, 10)
+    A = BlockSparseMatrix(ctx, host)
+    om = O.Mat(host)
+    of = O.Fsai(om, O.Fsai.STATIC)
+    M = Fsai.build(A, FSAI_STATIC_LOWER)
+    beta = O.lanczos_lambda_max(om, of, 100, 1.01, 42)
+    alpha, omega = beta / 30.0, 1.0 / beta
+    b = pr.normal_vector(host.dim_r, 0, 0)
+    x0 = pr.normal_vector(host.dim_r, 0, 3)
+    for k in (1, 3, 4):
+        xv = Vector(ctx, x0)
+        apply_smoother(A, M, kind, Vector(ctx, b), xv, k, alpha=alpha, beta=beta, omega=omega)
+        want = O.smoother_apply(om, of, kind, b, x0, k, alpha=alpha, beta=beta, omega=omega)
+        assert np.linalg.norm(xv.download() - want) <= 1e-12 * np.linalg.norm(want)
+
+
+@pytest.mark.parametrize("kind,kpre,kpost", [(1, 2, 2), (0, 3, 3), (2, 6, 0)])
+def test_vcycle_smoother_kinds_and_v2k0(ctx, kind, kpre, kpost):
+    # SetupParams::kind / first_kind_fraction / richardson_omega (multilevel.hpp:39-42,
+    # multilevel.cpp:62-65) and CycleSpec::v2k0 (multilevel.hpp:18)
+    cfg = pr.CONFIGS["C2"].scaled(16, 3)
+    A, T, b = pr.make_problem(cfg)
+    omega = 0.3
+    oh = O.Hierarchy(O.Mat(A), [O.Mat(p) for p in T], t_max=1, coarse_dim_cap=1 << 30, probe=False,
+                     smoother_kind=kind, richardson_omega=omega)
+    dh = Hierarchy.setup(BlockSparseMatrix(ctx, A), [BlockSparseMatrix(ctx, p) for p in T],
+                         default_params(t_max=1, coarse_dim_cap=1 << 30, smoother_kind=kind,
+                                        richardson_omega=omega))
+    hist_o, it_o, _, _ = oh.solve(kpre, kpost, b, np.zeros_like(b), 1e-8, 8)
+    hist_g, it_g, _ = dh.solve(kpre, kpost, Vector(ctx, b), Vector(ctx, b.size), 1e-8, 8)
+    assert it_o == it_g
+    assert np.all(np.abs(hist_g / hist_g[0] - hist_o / hist_o[0]) <= 1e-10)
