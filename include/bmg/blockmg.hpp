@@ -34,6 +34,10 @@ struct NotPositiveDefinite : std::runtime_error {
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+struct IoError : std::runtime_error {  // matrix_io.hpp:10-13
+  int line;
+  IoError(int l, const std::string& msg) : std::runtime_error(msg), line(l) {}
+};
 
 inline void check(int status) {
   if (status == BMG_OK) return;
@@ -43,6 +47,7 @@ inline void check(int status) {
     case BMG_ERANGE: throw std::out_of_range(msg);
     case BMG_ENOTSPD: throw NotPositiveDefinite(bmg_last_pivot(), msg);
     case BMG_ECUDA: throw CudaError(msg);
+    case BMG_EIO: throw IoError(bmg_last_pivot(), msg);
     default: throw std::runtime_error(msg);
   }
 }

@@ -26,6 +26,8 @@
  *   setup (multilevel.hpp:59-60, multilevel.cpp:36-75) bmg_hier_setup
  *   v_cycle (multilevel.hpp:65, multilevel.cpp:77-103) bmg_vcycle / bmg_vcycle_host
  *   measure_rates loop (experiments.cpp:15-67)        bmg_solve (residual history)
+ *   read_matrix / write_matrix / read_vector /
+ *     write_vector (matrix_io.hpp:22-27)              bmg_io_*
  *
  * Conventions
  *   - Every entry returns BMG_OK (0) or a negative status; the message of the
@@ -58,6 +60,7 @@ enum {
   BMG_ERUNTIME = -4, /* std::runtime_error (e.g. multilevel.cpp:72-73) */
   BMG_ECUDA = -5,    /* CUDA runtime / cuSOLVER failure or no device */
   BMG_ENCCL = -6,    /* NCCL failure (multi-GPU contexts) */
+  BMG_EIO = -7,      /* bmg::IoError{line} (matrix_io.hpp:10-13); pivot slot = line */
 };
 
 /* bmg_bsr_create flags */
@@ -211,6 +214,14 @@ int bmg_partition_rows(int nbr, const int64_t* row_ptr, int world, int granule, 
                        int32_t* bounds);
 int bmg_row_window(const int64_t* row_ptr, const int32_t* col, int lo, int hi, int clo, int chi,
                    int32_t* ext_lo, int32_t* ext_hi);
+
+/* ---- reference exchange format (matrix_io.hpp:15-27) --------------------
+ * "%%block-matrix n n nnz" + 1-based scalar triplets, sidecar <path>.blocks
+ * with one block size per line; vectors one value per line (17 digits). */
+int bmg_io_read_matrix(bmg_ctx* ctx, const char* path, bmg_bsr** out, int* symmetric);
+int bmg_io_write_matrix(const bmg_bsr* a, const char* path);
+int bmg_io_read_vector(bmg_ctx* ctx, const char* path, bmg_vec** out);
+int bmg_io_write_vector(const bmg_vec* v, const char* path);
 
 /* ---- profiling helpers (bench.py) --------------------------------------- */
 /* time `reps` back-to-back launches of the residual pass r = b - A x on the

@@ -420,6 +420,30 @@ class Hierarchy:
             pass
 
 
+def read_matrix(ctx: Context, path: str):
+    """read_matrix (matrix_io.hpp:23) straight into a device matrix; returns (A, symmetric)."""
+    h = C.c_void_p()
+    sym = C.c_int()
+    check(lib().bmg_io_read_matrix(ctx.h, path.encode(), C.byref(h), C.byref(sym)))
+    return BlockSparseMatrix(ctx, _handle=h), bool(sym.value)
+
+
+def write_matrix(a: BlockSparseMatrix, path: str):
+    check(lib().bmg_io_write_matrix(a.h, path.encode()))
+
+
+def read_vector(ctx: Context, path: str) -> Vector:
+    h = C.c_void_p()
+    check(lib().bmg_io_read_vector(ctx.h, path.encode(), C.byref(h)))
+    v = Vector.__new__(Vector)
+    v.ctx, v.h, v.n = ctx, h, int(lib().bmg_vec_size(h))
+    return v
+
+
+def write_vector(v: Vector, path: str):
+    check(lib().bmg_io_write_vector(v.h, path.encode()))
+
+
 def partition_rows(row_ptr, world: int, granule: int = 1, agglomerate: bool = False) -> np.ndarray:
     rp = np.ascontiguousarray(row_ptr, np.int64)
     out = np.zeros(world + 1, np.int32)

@@ -18,7 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libbmgcuda.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "bmg_cuda.h")
 
-BMG_OK, BMG_EINVAL, BMG_ERANGE, BMG_ENOTSPD, BMG_ERUNTIME, BMG_ECUDA, BMG_ENCCL = 0, -1, -2, -3, -4, -5, -6
+BMG_OK, BMG_EINVAL, BMG_ERANGE, BMG_ENOTSPD, BMG_ERUNTIME, BMG_ECUDA, BMG_ENCCL, BMG_EIO = 0, -1, -2, -3, -4, -5, -6, -7
 BMG_SYMMETRIC = 1
 FSAI_STATIC_LOWER, FSAI_DIAGONAL, FSAI_ADAPTIVE = 0, 1, 3
 RICHARDSON, CHEB_FIRST, CHEB_FOURTH = 0, 1, 2  # SmootherKind (chebyshev.hpp:10)
@@ -50,6 +50,16 @@ class CudaError(BmgError):
 
 class NcclError(BmgError):
     status = BMG_ENCCL
+
+
+class IoError(BmgError):
+    """IoError{line} (matrix_io.hpp:10-13)."""
+
+    status = BMG_EIO
+
+    def __init__(self, msg, line):
+        super().__init__(msg)
+        self.line = line
 
 
 class SetupParams(C.Structure):
@@ -139,6 +149,10 @@ _SIGS = {
     "bmg_partition_rows": (_I, [_I, _PI64, _I, _I, _I, _PI32]),
     "bmg_row_window": (_I, [_PI64, _PI32, _I, _I, _I, _I, _PI32, _PI32]),
     "bmg_tridiag_eigs": (_I, [_I, _PD, _PD, _PD]),
+    "bmg_io_read_matrix": (_I, [_P, C.c_char_p, _PP, C.POINTER(_I)]),
+    "bmg_io_write_matrix": (_I, [_P, C.c_char_p]),
+    "bmg_io_read_vector": (_I, [_P, C.c_char_p, _PP]),
+    "bmg_io_write_vector": (_I, [_P, C.c_char_p]),
     "bmg_gen_stencil": (_I, [_I, _I, _I, _I, _U64, _D, _PI64, _PI64, _PI32, _PD]),
     "bmg_gen_prolongation": (_I, [_I, _I, _I, _U64, _I, _PI64, _PI64, _PI32, _PD]),
     "bmg_gen_normal": (_I, [_U64, _U64, _I64, _PD]),
@@ -185,6 +199,8 @@ def check(status: int) -> None:
         raise CudaError(msg)
     if status == BMG_ENCCL:
         raise NcclError(msg)
+    if status == BMG_EIO:
+        raise IoError(msg, lib().bmg_last_pivot())
     raise BmgError(msg)
 
 
