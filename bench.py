@@ -200,6 +200,43 @@ def measure_c1(ctx, stream, steps):
             "gbs": per / ms / 1e6, "l2": "L2-resident (0.09 GB working set < 126 MB L2)"}
 
 
+def measure_hierarchy(ctx, stream, cfg, steps):
+    """Extra line: V(k,k) cycles/s of another config's full device hierarchy."""
+    import torch
+
+    from paper_2509_06744_b200 import BlockSparseMatrix, Hierarchy, Vector, default_params
+    from paper_2509_06744_b200 import problems as pr
+
+    t0 = time.perf_counter()
+    A, T, b = pr.make_problem(cfg)
+    dA = BlockSparseMatrix(ctx, A)
+    dT = [BlockSparseMatrix(ctx, p) for p in T]
+    del A, T
+    H = Hierarchy.setup(dA, dT, default_params(t_max=1, coarse_dim_cap=1 << 30, nest=cfg.nest))
+    ctx.sync()
+    setup_s = time.perf_counter() - t0
+    bv, xv = Vector(ctx, b), Vector(ctx, b.size)
+    for _ in range(3):
+        H.v_cycle(cfg.k, cfg.k, bv, xv)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        H.v_cycle(cfg.k, cfg.k, bv, xv)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    cb = H.cycle_bytes(cfg.k, cfg.k)
+    peak, _ = hbm_peak()
+    out = {"workload": f"{cfg.name}: {cfg.n}^{cfg.dim} patches, m={cfg.m}, {cfg.levels} levels, V({cfg.k},{cfg.k})",
+           "value": 1e3 / ms, "unit": "V-cycles/s", "ms_per_step": ms, "cycle_bytes": cb,
+           "effective_gbs": cb / ms / 1e6, "frac_of_roofline": cb / ms / 1e6 / peak,
+           "device_gb": H.device_bytes / 1e9, "setup_s": round(setup_s, 1)}
+    del H, dA, dT, bv, xv
+    ctx.sync()
+    return out
+
+
 def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
@@ -338,10 +375,23 @@ def run_ours(args, cfg):
 
     extra = None
     if rank == 0 and ws == 1:
+        extra = {}
         try:
-            extra = {"C1": measure_c1(ctx, stream, args.steps)}
-        except Exception as e:  # secondary line; never fail the headline run
-            extra = {"C1": {"error": f"{type(e).__name__}: {e}"}}
+            extra["C1"] = measure_c1(ctx, stream, args.steps)
+        except Exception as e:  # secondary lines never fail the headline run
+            extra["C1"] = {"error": f"{type(e).__name__}: {e}"}
+        if not args.no_c4:
+            # largest single-GPU config (C4, ~110 GB): free the headline hierarchy first
+            del H, dA, dT, bv, xv, rv
+            ctx.sync()
+            try:
+                free = torch.cuda.mem_get_info()[0]
+                if free < 125e9:
+                    extra["C4"] = {"skipped": f"needs ~115 GB free, {free / 1e9:.0f} GB available"}
+                else:
+                    extra["C4"] = measure_hierarchy(ctx, stream, pr.CONFIGS["C4"], min(args.steps, 10))
+            except Exception as e:
+                extra["C4"] = {"error": f"{type(e).__name__}: {e}"}
 
     # ---- CPU baseline (rank 0, N = 1 only): bounded oracle sample
     cpu = None
@@ -401,6 +451,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of row strips")
+    ap.add_argument("--no-c4", action="store_true", help="skip the extra C4 (largest single-GPU config) line")
     args = ap.parse_args()
     from paper_2509_06744_b200 import problems as pr
 

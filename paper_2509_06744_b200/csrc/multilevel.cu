@@ -165,65 +165,235 @@ void pair_gemm(Ctx* ctx, const double* A, int bs_a, const double* B, int bs_b, c
 
 }  // namespace
 
+// Chunked formulation (memory ~ C plus one A P chunk, so C4's 3-D levels fit
+// one GPU): for fine-row chunks in ascending order, AP_chunk = A[chunk, :] P
+// (per (i, J): ascending k over A row i) is formed on the device, then every
+// coarse block accumulates its chunk contributions in place,
+// C_IJ += sum over i in chunk (ascending) of P_iI^T AP_iJ.  Reloading the stored
+// partial is exact, so the result is bitwise the unchunked order of
+// kernels.cpp:66-86.  Structures (AP rows, C rows, transpose positions) are
+// integer work on the host; every flop is on the device.
+namespace kern {
+
+__device__ __forceinline__ int64_t find_in(const int32_t* __restrict__ col, int64_t lo, int64_t hi, int j) {
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (col[mid] < j)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// AP rows [f0, f1): CTA per (fine row, output block); thread per block entry
+__global__ void ap_chunk_kernel(const double* __restrict__ Av, const int64_t* __restrict__ Arp,
+                                const int32_t* __restrict__ Acol, int bs_a, const double* __restrict__ Pv,
+                                const int64_t* __restrict__ Prp, const int32_t* __restrict__ Pcol, int bs_p,
+                                const int64_t* __restrict__ APrp, const int32_t* __restrict__ APcol, int f0, int f1,
+                                int64_t apbase, double* __restrict__ APv, int bs_o, int m) {
+  const int r = threadIdx.x / m, c = threadIdx.x - (threadIdx.x / m) * m;
+  const bool act = r < m;
+  const int64_t q0 = APrp[f0], q1 = APrp[f1];
+  for (int64_t q = q0 + blockIdx.x; q < q1; q += gridDim.x) {
+    // fine row of output block q (binary search over APrp[f0..f1])
+    int lo = f0, hi = f1 - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (APrp[mid] <= q)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    const int i = lo;
+    const int J = APcol[q];
+    double acc = 0.0;
+    for (int64_t pa = Arp[i]; pa < Arp[i + 1]; ++pa) {
+      const int k = Acol[pa];
+      const int64_t pp = find_in(Pcol, Prp[k], Prp[k + 1], J);
+      if (pp >= Prp[k + 1] || Pcol[pp] != J) continue;
+      if (act) {
+        const double* a = Av + pa * bs_a;
+        const double* b = Pv + pp * bs_p;
+        double t = 0.0;
+        for (int z = 0; z < m; ++z) t = __fma_rn(a[r * m + z], b[z * m + c], t);
+        acc = __dadd_rn(acc, t);
+      }
+    }
+    if (act) APv[(q - apbase) * bs_o + r * m + c] = acc;
+  }
+}
+
+// C_IJ += sum over fine rows i in [f0, f1) of P_iI^T AP_iJ (ascending i), coarse rows [I0, I1)
+__global__ void c_accum_kernel(const double* __restrict__ Pv, int bs_p, const int64_t* __restrict__ PTrp,
+                               const int32_t* __restrict__ PTrow, const int64_t* __restrict__ PTblk,
+                               const int64_t* __restrict__ APrp, const int32_t* __restrict__ APcol,
+                               const double* __restrict__ APv, int64_t apbase, int bs_ap,
+                               const int64_t* __restrict__ Crp, const int32_t* __restrict__ Ccol, int I0, int I1,
+                               int f0, int f1, double* __restrict__ Cv, int bs_c, int m) {
+  const int r = threadIdx.x / m, c = threadIdx.x - (threadIdx.x / m) * m;
+  const bool act = r < m;
+  const int64_t o0 = Crp[I0], o1 = Crp[I1];
+  for (int64_t o = o0 + blockIdx.x; o < o1; o += gridDim.x) {
+    int lo = I0, hi = I1 - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (Crp[mid] <= o)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    const int I = lo;
+    const int J = Ccol[o];
+    double acc = act ? Cv[o * bs_c + r * m + c] : 0.0;
+    bool any = false;
+    // fine rows of coarse column I inside the chunk (ascending)
+    int64_t t0 = PTrp[I], t1 = PTrp[I + 1];
+    while (t0 < t1 && PTrow[t0] < f0) ++t0;
+    for (int64_t t = t0; t < t1 && PTrow[t] < f1; ++t) {
+      const int i = PTrow[t];
+      const int64_t q = find_in(APcol, APrp[i], APrp[i + 1], J);
+      if (q >= APrp[i + 1] || APcol[q] != J) continue;
+      any = true;
+      if (act) {
+        const double* p = Pv + PTblk[t] * bs_p;
+        const double* ap = APv + (q - apbase) * bs_ap;
+        double s = 0.0;
+        for (int z = 0; z < m; ++z) s = __fma_rn(p[z * m + r], ap[z * m + c], s);
+        acc = __dadd_rn(acc, s);
+      }
+    }
+    if (any && act) Cv[o * bs_c + r * m + c] = acc;
+  }
+}
+
+}  // namespace kern
+
 std::unique_ptr<Bsr> galerkin(const Bsr& a, const Bsr& p) {
   if (!(a.rsz == a.csz) || !(a.rsz == p.rsz)) fail(BMG_EINVAL, "galerkin_coarsen: layouts do not match");
   if (!(a.uniform && p.uniform && a.mr == p.mc))
     fail(BMG_EINVAL, "device galerkin_coarsen: uniform square block sizes required");
   Ctx* ctx = a.ctx;
-  const int m = a.mr;
-  // AP = A * P: row i pairs (A_ik, P_kJ), ascending k per output block
-  Product ap = symbolic(
-      a.nbr,
-      [&](int i, auto&& emit) {
-        for (int64_t q = a.h_row_ptr[i]; q < a.h_row_ptr[i + 1]; ++q) emit(a.h_col[q], q);
-      },
-      p.h_row_ptr, p.h_col);
-  // P^T column index: coarse row I -> (fine row i, P block) ascending i
-  std::vector<int64_t> pt_ptr(p.nbc + 1, 0);
-  for (int64_t q = 0; q < p.nnzb; ++q) pt_ptr[p.h_col[q] + 1]++;
-  for (int j = 0; j < p.nbc; ++j) pt_ptr[j + 1] += pt_ptr[j];
-  std::vector<int64_t> pt_blk(p.nnzb), fillp(pt_ptr.begin(), pt_ptr.end() - 1);
-  std::vector<int32_t> pt_row(p.nnzb);
-  for (int i = 0; i < p.nbr; ++i)
-    for (int64_t q = p.h_row_ptr[i]; q < p.h_row_ptr[i + 1]; ++q) {
-      const int64_t t = fillp[p.h_col[q]]++;
-      pt_row[t] = i;
-      pt_blk[t] = q;
+  const int m = a.mr, bs = a.bs, nf = a.nbr, nc = p.nbc;
+  // ---- symbolic (host): AP rows, P^T index, C rows, transpose positions
+  std::vector<int64_t> aprp(nf + 1, 0);
+  std::vector<std::vector<int32_t>> aprow(nf);
+#pragma omp parallel for schedule(dynamic, 256)
+  for (int i = 0; i < nf; ++i) {
+    auto& v = aprow[i];
+    for (int64_t q = a.h_row_ptr[i]; q < a.h_row_ptr[i + 1]; ++q) {
+      const int k = a.h_col[q];
+      v.insert(v.end(), p.h_col.begin() + p.h_row_ptr[k], p.h_col.begin() + p.h_row_ptr[k + 1]);
     }
-  // C = P^T AP: coarse row I pairs (P_iI, AP_iJ), ascending i per output block
-  Product c = symbolic(
-      p.nbc,
-      [&](int I, auto&& emit) {
-        for (int64_t t = pt_ptr[I]; t < pt_ptr[I + 1]; ++t) emit(pt_row[t], pt_blk[t]);
-      },
-      ap.row_ptr, ap.col);
-  // numeric
-  const int bs = a.bs;
-  DBuf<double> apv(std::max<size_t>(ap.col.size() * bs, 2));
-  pair_gemm(ctx, a.vals.p, bs, p.vals.p, p.bs, ap, apv.p, bs, m, 0);
-  DBuf<double> cv(std::max<size_t>(c.col.size() * bs, 2));
-  pair_gemm(ctx, p.vals.p, p.bs, apv.p, bs, c, cv.p, bs, m, 1);
-  apv.release();
-  // structural symmetry + transpose positions
-  const int nc = p.nbc;
-  std::vector<int64_t> tpos(c.col.size(), -1);
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+  }
+  for (int i = 0; i < nf; ++i) aprp[i + 1] = aprp[i] + (int64_t)aprow[i].size();
+  std::vector<int32_t> apcol(aprp[nf]);
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < nf; ++i) std::copy(aprow[i].begin(), aprow[i].end(), apcol.begin() + aprp[i]);
+  std::vector<int64_t> ptrp(nc + 1, 0);
+  for (int64_t q = 0; q < p.nnzb; ++q) ptrp[p.h_col[q] + 1]++;
+  for (int j = 0; j < nc; ++j) ptrp[j + 1] += ptrp[j];
+  std::vector<int32_t> ptrow(p.nnzb);
+  std::vector<int64_t> ptblk(p.nnzb);
+  {
+    std::vector<int64_t> fillp(ptrp.begin(), ptrp.end() - 1);
+    for (int i = 0; i < nf; ++i)
+      for (int64_t q = p.h_row_ptr[i]; q < p.h_row_ptr[i + 1]; ++q) {
+        const int64_t t = fillp[p.h_col[q]]++;
+        ptrow[t] = i;
+        ptblk[t] = q;
+      }
+  }
+  std::vector<std::vector<int32_t>> crow(nc);
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int I = 0; I < nc; ++I) {
+    auto& v = crow[I];
+    for (int64_t t = ptrp[I]; t < ptrp[I + 1]; ++t) v.insert(v.end(), aprow[ptrow[t]].begin(), aprow[ptrow[t]].end());
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+  }
+  aprow.clear();
+  aprow.shrink_to_fit();
+  std::vector<int64_t> crp(nc + 1, 0);
+  for (int I = 0; I < nc; ++I) crp[I + 1] = crp[I] + (int64_t)crow[I].size();
+  std::vector<int32_t> ccol(crp[nc]);
+  for (int I = 0; I < nc; ++I) std::copy(crow[I].begin(), crow[I].end(), ccol.begin() + crp[I]);
+  crow.clear();
+  std::vector<int64_t> tpos(ccol.size(), -1);
+#pragma omp parallel for schedule(dynamic, 64)
   for (int I = 0; I < nc; ++I)
-    for (int64_t q = c.row_ptr[I]; q < c.row_ptr[I + 1]; ++q) {
-      const int J = c.col[q];
-      const auto b = c.col.begin() + c.row_ptr[J], e = c.col.begin() + c.row_ptr[J + 1];
+    for (int64_t q = crp[I]; q < crp[I + 1]; ++q) {
+      const int J = ccol[q];
+      const auto b = ccol.begin() + crp[J], e = ccol.begin() + crp[J + 1];
       auto it = std::lower_bound(b, e, I);
-      if (it == e || *it != I) fail(BMG_ERUNTIME, "galerkin_coarsen: P^T A P is not structurally symmetric");
-      tpos[q] = it - c.col.begin();
+      tpos[q] = (it == e || *it != I) ? -2 : (it - ccol.begin());
     }
+  for (int64_t v : tpos)
+    if (v == -2) fail(BMG_ERUNTIME, "galerkin_coarsen: P^T A P is not structurally symmetric");
+  // ---- device buffers
+  auto up64 = [&](const std::vector<int64_t>& h, DBuf<int64_t>& d) {
+    d.alloc(std::max<size_t>(h.size(), 1));
+    if (!h.empty()) BMG_CUDA(cudaMemcpy(d.p, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
+  };
+  auto up32 = [&](const std::vector<int32_t>& h, DBuf<int32_t>& d) {
+    d.alloc(std::max<size_t>(h.size(), 1));
+    if (!h.empty()) BMG_CUDA(cudaMemcpy(d.p, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+  };
+  DBuf<int64_t> d_aprp, d_ptrp, d_ptblk, d_crp, d_tpos;
+  DBuf<int32_t> d_apcol, d_ptrow, d_ccol;
+  up64(aprp, d_aprp);
+  up32(apcol, d_apcol);
+  up64(ptrp, d_ptrp);
+  up32(ptrow, d_ptrow);
+  up64(ptblk, d_ptblk);
+  up64(crp, d_crp);
+  up32(ccol, d_ccol);
+  const int64_t nblk = (int64_t)ccol.size();
+  DBuf<double> cv(std::max<int64_t>(nblk * bs, 2));
+  BMG_CUDA(cudaMemset(cv.p, 0, cv.bytes()));
+  // ---- chunks of fine rows, AP chunk within a memory budget
+  const int64_t budget_blocks = std::max<int64_t>(1, ((int64_t)4 << 30) / ((int64_t)bs * 8));
+  const int threads = ((m * m + 31) / 32) * 32;
+  DBuf<double> apv;
+  int f0 = 0;
+  while (f0 < nf) {
+    int f1 = f0 + 1;
+    while (f1 < nf && aprp[f1 + 1] - aprp[f0] <= budget_blocks) ++f1;
+    const int64_t napb = aprp[f1] - aprp[f0];
+    if (apv.n < (size_t)(napb * bs)) apv.alloc(std::max<int64_t>(napb * bs, 2));
+    // coarse rows touched by this chunk
+    int I0 = nc, I1 = 0;
+    for (int64_t q = p.h_row_ptr[f0]; q < p.h_row_ptr[f1]; ++q) {
+      I0 = std::min(I0, p.h_col[q]);
+      I1 = std::max(I1, p.h_col[q] + 1);
+    }
+    if (napb > 0) {
+      kern::ap_chunk_kernel<<<(int)std::min<int64_t>(napb, (int64_t)ctx->sms * 64), threads, 0, ctx->stream>>>(
+          a.vals.p, a.row_ptr.p, a.col.p, bs, p.vals.p, p.row_ptr.p, p.col.p, p.bs, d_aprp.p, d_apcol.p, f0, f1,
+          aprp[f0], apv.p, bs, m);
+      ctx->count();
+      BMG_CUDA(cudaGetLastError());
+    }
+    if (I1 > I0 && crp[I1] > crp[I0]) {
+      kern::c_accum_kernel<<<(int)std::min<int64_t>(crp[I1] - crp[I0], (int64_t)ctx->sms * 64), threads, 0,
+                             ctx->stream>>>(p.vals.p, p.bs, d_ptrp.p, d_ptrow.p, d_ptblk.p, d_aprp.p, d_apcol.p,
+                                            apv.p, aprp[f0], bs, d_crp.p, d_ccol.p, I0, I1, f0, f1, cv.p, bs, m);
+      ctx->count();
+      BMG_CUDA(cudaGetLastError());
+    }
+    BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+    f0 = f1;
+  }
+  apv.release();
+  // ---- A_c = (C + C^T)/2 blockwise (multilevel.cpp:16-26)
   std::vector<int> csz(nc, m);
-  auto out = make_bsr_structure(ctx, nc, csz.data(), nc, csz.data(), c.row_ptr, c.col, true);
-  DBuf<int64_t> dt(std::max<size_t>(tpos.size(), 1));
-  if (!tpos.empty()) BMG_CUDA(cudaMemcpy(dt.p, tpos.data(), tpos.size() * 8, cudaMemcpyHostToDevice));
-  const int64_t nblk = (int64_t)c.col.size();
+  auto out = make_bsr_structure(ctx, nc, csz.data(), nc, csz.data(), crp, ccol, true);
+  up64(tpos, d_tpos);
   if (nblk) {
-    const int threads = ((m * m + 31) / 32) * 32;
     kern::symmetrize_kernel<<<(int)std::min<int64_t>(nblk, (int64_t)ctx->sms * 32), threads, 0, ctx->stream>>>(
-        cv.p, dt.p, out->vals.p, nblk, m, bs);
+        cv.p, d_tpos.p, out->vals.p, nblk, m, bs);
     ctx->count();
     BMG_CUDA(cudaGetLastError());
   }
