@@ -267,19 +267,41 @@ def run_ours(args, cfg):
                             fsai_kind=0 if cfg.fsai == "static" else 3)
     H = Hierarchy.setup(dA, dT, params)
     granule = [(cfg.n >> (cfg.levels - 1 - l)) ** (cfg.dim - 1) for l in range(cfg.levels)]
-    agglomerate = min(2, cfg.levels)
+    agglomerate = 1  # the dense coarsest level on rank 0; every other level stays split
     cycle_bytes = H.cycle_bytes(cfg.k, cfg.k)
     n = A.dim_r
     lo_row, hi_row = 0, A.nbr
     scaling = "weak" if (ws > 1 and args.replicas) else "strong"
     if ws > 1 and not args.replicas:
         try:
+            # reference result of two unpartitioned cycles (every rank has the whole hierarchy)
+            H.partition(1, granule)
+            x_ref = Vector(ctx, n)
+            b_all = Vector(ctx, b)
+            for _ in range(2):
+                H.v_cycle(cfg.k, cfg.k, b_all, x_ref)
+            x_ref_h = x_ref.download()
+            del x_ref, b_all
+            H = Hierarchy.setup(dA, dT, params)
             H.partition(ws, granule, agglomerate=agglomerate, rank=rank)
             lo_row, hi_row, _, _ = H.part_info(cfg.levels - 1, rank)
-            mode = f"row strips x{ws} (NCCL halos, coarsest {agglomerate} levels on rank 0)"
+            # the partitioned cycle must reproduce it bitwise on every rank's strip
+            m_ = cfg.m
+            bp = Vector(ctx, np.ascontiguousarray(b[lo_row * m_:hi_row * m_]))
+            xp = Vector(ctx, (hi_row - lo_row) * m_)
+            for _ in range(2):
+                H.v_cycle(cfg.k, cfg.k, bp, xp)
+            ok = bool(np.array_equal(xp.download(), x_ref_h[lo_row * m_:hi_row * m_]))
+            flags = torch.tensor([1 if ok else 0], device="cuda")
+            dist.all_reduce(flags, op=dist.ReduceOp.MIN)
+            if flags.item() != 1:
+                raise RuntimeError("partitioned V-cycle differs from the 1-GPU cycle")
+            del bp, xp
+            mode = f"row strips x{ws} (NCCL halos, coarsest {agglomerate} level(s) on rank 0; verified bitwise)"
             scaling = "strong"
         except Exception as e:  # keep the run alive: independent replicas instead
             H = Hierarchy.setup(dA, dT, params)
+            lo_row, hi_row = 0, A.nbr
             mode = f"replicas x{ws} (partitioned path failed: {type(e).__name__}: {e})"
             scaling = "weak"
     elif ws > 1:

@@ -15,6 +15,8 @@ from paper_2509_06744_b200 import problems as pr  # noqa
 
 mode = sys.argv[1] if len(sys.argv) > 1 else "cycle"
 cfg = pr.CONFIGS[sys.argv[2] if len(sys.argv) > 2 else "C2"]
+if len(sys.argv) > 3:
+    cfg = cfg.scaled(int(sys.argv[3]))
 ctx = Context(0)
 ctx.set_stream(torch.cuda.current_stream().cuda_stream)
 A, T, b = pr.make_problem(cfg)
@@ -27,7 +29,7 @@ for _ in range(3):
 torch.cuda.synchronize()
 if mode == "cycle":
     torch.cuda.profiler.start()
-    for _ in range(2):
+    for _ in range(1 if cfg.dim == 3 else 2):
         H.v_cycle(cfg.k, cfg.k, bv, xv)
     torch.cuda.synchronize()
     torch.cuda.profiler.stop()
