@@ -145,6 +145,26 @@ static void nccl_check(ncclResult_t r, const char* what) {
 // ============================================================================ data model
 enum Which { VB = 0, VX, VR, VW, VP, VT, VNUM };
 
+// A local matrix cut into row slices (local rows [row0, row0 + nbr)): the
+// interior slice reads only the rank's own columns and runs while the halo
+// exchange is in flight; boundary slices run after it lands.
+struct Slice {
+  int row0 = 0;
+  const Bsr* m = nullptr;
+  std::unique_ptr<Bsr> own;
+  bool interior = true;
+};
+struct SplitMat {
+  std::vector<Slice> s;  // interior slice first
+  void whole(const Bsr* a) {
+    s.clear();
+    if (!a) return;
+    Slice x;
+    x.m = a;
+    s.push_back(std::move(x));
+  }
+};
+
 struct PLevel {  // one (virtual) rank's share of one level
   int lo = 0, hi = 0;    // own block rows
   int wlo = 0, whi = 0;  // vector window (block rows)
@@ -155,6 +175,8 @@ struct PLevel {  // one (virtual) rank's share of one level
   const Fsai* M = nullptr;
   std::unique_ptr<Bsr> A_own, R_own, P_own;
   std::unique_ptr<Fsai> M_own;
+  SplitMat sA, sR, sP;                 // the matrices as launched
+  std::vector<SplitMat> sF, sB;        // FSAI chain factors and their transposes
   SmootherSpec spec;  // Level::smoother (multilevel.hpp:25)
   DBuf<double> v[VNUM];
   int64_t off() const { return (int64_t)(lo - wlo) * m; }
@@ -200,10 +222,15 @@ struct Hier {
   };
   std::map<GraphKey, Captured> graphs;
   DBuf<double> io_b, io_x, seg;
+  cudaStream_t comm = nullptr;  // halo exchanges overlap interior slices
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   const double* user_b = nullptr;
   double* user_x = nullptr;
   ~Hier() {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (comm) cudaStreamDestroy(comm);
   }
   int finest() const { return (int)nbr.size() - 1; }
   bool whole() const { return world == 1; }
@@ -265,6 +292,47 @@ static void exchange(Hier& h, int l, Which w) {
   nccl_check(ncclGroupEnd(), "ncclGroupEnd");
 }
 
+// One streaming pass over a split matrix whose input is vector `in` of level
+// `in_level`: the exchange of its halo runs on the comm stream while the
+// interior slices compute; boundary slices wait for the exchange.  `get`
+// returns the SplitMat of a part (nullptr: nothing to do), `launch` runs one
+// slice (row offset in scalars = slice.row0 * m of the output level).
+template <class Get, class Launch>
+static void run_pass(Hier& h, int in_level, Which in, int out_level, Get get, Launch launch) {
+  Ctx* ctx = h.ctx;
+  if (h.world == 1) {
+    for (Part& p : h.parts) {
+      PLevel& L = p.lv[out_level];
+      const SplitMat* sm = get(p);
+      if (!L.active() || !sm) continue;
+      for (const Slice& sl : sm->s) launch(p, L, sl);
+    }
+    return;
+  }
+  BMG_CUDA(cudaEventRecord(h.ev_fork, ctx->stream));
+  BMG_CUDA(cudaStreamWaitEvent(h.comm, h.ev_fork, 0));
+  cudaStream_t main = ctx->stream;
+  ctx->stream = h.comm;
+  try {
+    exchange(h, in_level, in);
+  } catch (...) {
+    ctx->stream = main;
+    throw;
+  }
+  ctx->stream = main;
+  BMG_CUDA(cudaEventRecord(h.ev_join, h.comm));
+  for (int phase = 0; phase < 2; ++phase) {
+    if (phase == 1) BMG_CUDA(cudaStreamWaitEvent(ctx->stream, h.ev_join, 0));
+    for (Part& p : h.parts) {
+      PLevel& L = p.lv[out_level];
+      const SplitMat* sm = get(p);
+      if (!L.active() || !sm) continue;
+      for (const Slice& sl : sm->s)
+        if (sl.interior == (phase == 0)) launch(p, L, sl);
+    }
+  }
+}
+
 // ============================================================================ V-cycle
 // one smoother application (apply_smoother, chebyshev.hpp:117-129) on level l, all parts
 static void smooth(Hier& h, int l, int k, bool xzero) {
@@ -288,35 +356,36 @@ static void smooth(Hier& h, int l, int k, bool xzero) {
     if (zero_x) {
       src = VB;  // A * 0 = 0: r = b exactly
     } else {
-      exchange(h, l, VX);
-      for (Part& p : h.parts) {
-        PLevel& L = p.lv[l];
-        if (!L.active()) continue;
-        residual(*L.A, vec(h, p, l, VB) + L.off(), vec(h, p, l, VX), vec(h, p, l, VR) + L.off());
-      }
+      run_pass(h, l, VX, l, [&](Part& p) { return &p.lv[l].sA; },
+               [&](Part& p, PLevel& L, const Slice& sl) {
+                 const int64_t o = L.off() + (int64_t)sl.row0 * L.m;
+                 residual(*sl.m, vec(h, p, l, VB) + o, vec(h, p, l, VX), vec(h, p, l, VR) + o);
+               });
       src = VR;
     }
     // forward chain w = F_n ... F_0 r (nest = 0: w = G r), then all but the last transpose
     Which cur = src;
     Which nxt = VW;
     for (size_t q = 0; q < nf + nb - 1; ++q) {
-      exchange(h, l, cur);
-      for (Part& p : h.parts) {
-        PLevel& L = p.lv[l];
-        if (!L.active()) continue;
-        const Bsr& f = q < nf ? *L.M->fwd[q] : *L.M->bwd[nb - 1 - (q - nf)];
-        spmv(f, vec(h, p, l, cur), vec(h, p, l, nxt) + L.off());
-      }
+      const Which in = cur, out = nxt;
+      run_pass(h, l, in, l,
+               [&](Part& p) -> const SplitMat* {
+                 PLevel& L = p.lv[l];
+                 if (L.sF.empty()) return nullptr;
+                 return q < nf ? &L.sF[q] : &L.sB[nb - 1 - (q - nf)];
+               },
+               [&](Part& p, PLevel& L, const Slice& sl) {
+                 spmv(*sl.m, vec(h, p, l, in), vec(h, p, l, out) + L.off() + (int64_t)sl.row0 * L.m);
+               });
       cur = nxt;
       nxt = (nxt == VW) ? VT : VW;
     }
-    exchange(h, l, cur);
-    for (Part& p : h.parts) {
-      PLevel& L = p.lv[l];
-      if (!L.active()) continue;
-      gt_cheb(*L.M->bwd[0], vec(h, p, l, cur), vec(h, p, l, VP) + L.off(), vec(h, p, l, VX) + L.off(), st.coef,
-              st.c, st.first, zero_x);
-    }
+    run_pass(h, l, cur, l, [&](Part& p) -> const SplitMat* { return p.lv[l].sB.empty() ? nullptr : &p.lv[l].sB[0]; },
+             [&](Part& p, PLevel& L, const Slice& sl) {
+               const int64_t o = L.off() + (int64_t)sl.row0 * L.m;
+               gt_cheb(*sl.m, vec(h, p, l, cur), vec(h, p, l, VP) + o, vec(h, p, l, VX) + o, st.coef, st.c, st.first,
+                       zero_x);
+             });
   }
 }
 
@@ -350,28 +419,25 @@ static void enqueue_vcycle(Hier& h, int kpre, int kpost) {
       r = VB;
     }
     if (r == VR) {
-      exchange(h, l, VX);
-      for (Part& p : h.parts) {
-        PLevel& L = p.lv[l];
-        if (!L.active()) continue;
-        residual(*L.A, vec(h, p, l, VB) + L.off(), vec(h, p, l, VX), vec(h, p, l, VR) + L.off());
-      }
+      run_pass(h, l, VX, l, [&](Part& p) { return &p.lv[l].sA; },
+               [&](Part& p, PLevel& L, const Slice& sl) {
+                 const int64_t o = L.off() + (int64_t)sl.row0 * L.m;
+                 residual(*sl.m, vec(h, p, l, VB) + o, vec(h, p, l, VX), vec(h, p, l, VR) + o);
+               });
     }
-    exchange(h, l, r);
-    for (Part& p : h.parts) {  // rc = P^T r  (multilevel.cpp:95)
-      PLevel& C = p.lv[l - 1];
-      if (!C.active()) continue;
-      spmv(*p.lv[l].R, vec(h, p, l, r), vec(h, p, l - 1, VB) + C.off());
-    }
+    // rc = P^T r  (multilevel.cpp:95): R rows are own rows of level l - 1
+    run_pass(h, l, r, l - 1, [&](Part& p) { return &p.lv[l].sR; },
+             [&](Part& p, PLevel& C, const Slice& sl) {
+               spmv(*sl.m, vec(h, p, l, r), vec(h, p, l - 1, VB) + C.off() + (int64_t)sl.row0 * C.m);
+             });
   }
   coarse_solve(h);
   for (int l = 1; l <= top; ++l) {
-    exchange(h, l - 1, VX);
-    for (Part& p : h.parts) {  // x += P ec  (multilevel.cpp:98-100)
-      PLevel& L = p.lv[l];
-      if (!L.active()) continue;
-      prolong_add(*L.P, vec(h, p, l - 1, VX), vec(h, p, l, VX) + L.off());
-    }
+    // x += P ec  (multilevel.cpp:98-100)
+    run_pass(h, l - 1, VX, l, [&](Part& p) { return &p.lv[l].sP; },
+             [&](Part& p, PLevel& L, const Slice& sl) {
+               prolong_add(*sl.m, vec(h, p, l - 1, VX), vec(h, p, l, VX) + L.off() + (int64_t)sl.row0 * L.m);
+             });
     smooth(h, l, kpost, false);
   }
 }
@@ -550,6 +616,20 @@ static void finish_whole(Hier& h, int cap) {
   h.granule_top = 1;
   h.nfactors.assign(L, 1);
   for (int l = 1; l < L; ++l) h.nfactors[l] = p.lv[l].M->fwd.size();
+  for (int l = 0; l < L; ++l) {
+    PLevel& lv = p.lv[l];
+    lv.sA.whole(lv.A);
+    if (l >= 1) {
+      lv.sR.whole(lv.R);
+      lv.sP.whole(lv.P);
+      lv.sF.clear();
+      lv.sF.resize(lv.M->fwd.size());
+      lv.sB.clear();
+      lv.sB.resize(lv.M->bwd.size());
+      for (size_t q = 0; q < lv.M->fwd.size(); ++q) lv.sF[q].whole(lv.M->fwd[q].get());
+      for (size_t q = 0; q < lv.M->bwd.size(); ++q) lv.sB[q].whole(lv.M->bwd[q].get());
+    }
+  }
   coarse_factor(h, p);
   record_stats(h);
 }
@@ -573,6 +653,46 @@ static std::unique_ptr<Bsr> slice_rows(const Bsr& g, int lo, int hi, int col_lo,
     BMG_CUDA(cudaMemcpyAsync(out->vals.p, g.vals.p + v0, (v1 - v0) * sizeof(double), cudaMemcpyDeviceToDevice,
                              g.ctx->stream));
   return out;
+}
+
+// Rows [lo, hi) of global g (columns shifted into the window [wlo, wlo + nwin)),
+// cut into the longest run of rows reading only own columns [own_lo, own_hi)
+// (interior) and the boundary rows before / after it.
+static SplitMat split_rows(const Bsr& g, int lo, int hi, int wlo, int nwin, int own_lo, int own_hi) {
+  SplitMat sm;
+  if (hi <= lo) return sm;
+  auto interior = [&](int i) {
+    const int64_t p0 = g.h_row_ptr[i], p1 = g.h_row_ptr[i + 1];
+    return p1 == p0 || (g.h_col[p0] >= own_lo && g.h_col[p1 - 1] < own_hi);
+  };
+  int ia = hi, ib = hi, best = 0;
+  for (int i = lo; i < hi;) {
+    if (!interior(i)) {
+      ++i;
+      continue;
+    }
+    int j = i;
+    while (j < hi && interior(j)) ++j;
+    if (j - i > best) {
+      best = j - i;
+      ia = i;
+      ib = j;
+    }
+    i = j;
+  }
+  auto add = [&](int a, int b, bool in) {
+    if (b <= a) return;
+    Slice x;
+    x.row0 = a - lo;
+    x.own = slice_rows(g, a, b, wlo, nwin);
+    x.m = x.own.get();
+    x.interior = in;
+    sm.s.push_back(std::move(x));
+  };
+  add(ia, ib, true);
+  add(lo, std::min(ia, hi), false);
+  add(ib, hi, false);
+  return sm;
 }
 
 // Split the (identically built) whole hierarchy into row strips.  rank < 0:
@@ -643,21 +763,16 @@ static void partition(Hier& h, int world, int rank, const int32_t* granule, int 
       d.m = h.msz[l];
       d.spec = s.spec;
       const int nwin = d.whi - d.wlo;
-      d.A_own = slice_rows(*s.A, d.lo, d.hi, d.wlo, nwin);
-      d.A = d.A_own.get();
+      d.sA = split_rows(*s.A, d.lo, d.hi, d.wlo, nwin, d.lo, d.hi);
+      d.A = d.sA.s.empty() ? nullptr : d.sA.s[0].m;
       if (l >= 1) {
-        if (d.hi > d.lo) {
-          d.M_own = std::make_unique<Fsai>();
-          d.M_own->ctx = ctx;
-          d.M_own->dim = (int)d.n_own();
-          for (auto& f : s.M->fwd) d.M_own->fwd.push_back(slice_rows(*f, d.lo, d.hi, d.wlo, nwin));
-          for (auto& f : s.M->bwd) d.M_own->bwd.push_back(slice_rows(*f, d.lo, d.hi, d.wlo, nwin));
-          d.M = d.M_own.get();
-        }
-        d.P_own = slice_rows(*s.P, d.lo, d.hi, WL[l - 1][r], WH[l - 1][r] - WL[l - 1][r]);
-        d.P = d.P_own.get();
-        d.R_own = slice_rows(*s.R, B[l - 1][r], B[l - 1][r + 1], d.wlo, nwin);
-        d.R = d.R_own.get();
+        d.M = nullptr;  // chain length comes from h.nfactors
+        for (auto& f : s.M->fwd) d.sF.push_back(split_rows(*f, d.lo, d.hi, d.wlo, nwin, d.lo, d.hi));
+        for (auto& f : s.M->bwd) d.sB.push_back(split_rows(*f, d.lo, d.hi, d.wlo, nwin, d.lo, d.hi));
+        d.sP = split_rows(*s.P, d.lo, d.hi, WL[l - 1][r], WH[l - 1][r] - WL[l - 1][r], B[l - 1][r], B[l - 1][r + 1]);
+        d.sR = split_rows(*s.R, B[l - 1][r], B[l - 1][r + 1], d.wlo, nwin, d.lo, d.hi);
+        d.P = d.sP.s.empty() ? nullptr : d.sP.s[0].m;
+        d.R = d.sR.s.empty() ? nullptr : d.sR.s[0].m;
       }
       alloc_vectors(h, d, false);
     }
@@ -676,6 +791,11 @@ static void partition(Hier& h, int world, int rank, const int32_t* granule, int 
   h.wlo = WL;
   h.whi = WH;
   h.granule_top = granule ? std::max(1, granule[L - 1]) : 1;
+  if (!h.comm) {
+    BMG_CUDA(cudaStreamCreateWithFlags(&h.comm, cudaStreamNonBlocking));
+    BMG_CUDA(cudaEventCreateWithFlags(&h.ev_fork, cudaEventDisableTiming));
+    BMG_CUDA(cudaEventCreateWithFlags(&h.ev_join, cudaEventDisableTiming));
+  }
 }
 
 // partition-invariant ||r||_2 of the finest level (segments = granules)
@@ -720,12 +840,11 @@ static void finest_residual(Hier& h, const double* b, double* x, double* rtmp) {
   h.user_b = b;
   h.user_x = x;
   stage_in(h, b, x);
-  exchange(h, top, VX);
-  for (Part& p : h.parts) {
-    PLevel& L = p.lv[top];
-    if (!L.active()) continue;
-    residual(*L.A, L.v[VB].p + L.off(), L.v[VX].p, L.v[VR].p + L.off());
-  }
+  run_pass(h, top, VX, top, [&](Part& p) { return &p.lv[top].sA; },
+           [&](Part& p, PLevel& L, const Slice& sl) {
+             const int64_t o = L.off() + (int64_t)sl.row0 * L.m;
+             residual(*sl.m, L.v[VB].p + o, L.v[VX].p, L.v[VR].p + o);
+           });
 }
 
 }  // namespace bmg
@@ -874,6 +993,15 @@ int bmg_hier_info(const bmg_hier* hh, int* nlevels, int64_t* device_bytes) {
             for (auto& f : L.M_own->bwd) b += f->device_bytes();
           }
           for (int w = 0; w < VNUM; ++w) b += (int64_t)L.v[w].bytes();
+          auto sb = [&](const SplitMat& sm) {
+            for (const Slice& sl : sm.s)
+              if (sl.own) b += sl.own->device_bytes();
+          };
+          sb(L.sA);
+          sb(L.sR);
+          sb(L.sP);
+          for (auto& f : L.sF) sb(f);
+          for (auto& f : L.sB) sb(f);
         }
       }
       *device_bytes = b;
