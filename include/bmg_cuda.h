@@ -209,6 +209,28 @@ int bmg_hier_partition(bmg_hier* h, int world, int rank, const int32_t* granule,
 /* own rows [lo, hi) and vector window [wlo, whi) of `rank` on `level` */
 int bmg_hier_part_info(const bmg_hier* h, int level, int rank, int32_t* lo, int32_t* hi, int32_t* wlo,
                        int32_t* whi);
+/* ---- distributed setup (multilevel.cpp:36-75 on row strips) ------------
+ * For systems that do not fit one GPU (BASELINE C3, C5): no rank ever holds a
+ * whole partitioned level.  Levels >= agglomerate are split into equal
+ * granule-aligned strips; each rank passes the plan's EXTENDED strip (own rows
+ * +- halo granules, global column indices) of the finest A and of P_l for
+ * l > agglomerate, and the whole P_l for l <= agglomerate.  radius[l] bounds
+ * the granule distance A_l couples (checked); P must be a 2:1 granule
+ * coarsening (checked).  The result is bitwise the hierarchy bmg_hier_setup +
+ * bmg_hier_partition would build on one device (same beta, same cycles).
+ * bmg_dist_plan: bounds[l*(world+1)+r], ext_lo/ext_hi[l*world+r], halo[l]
+ * (granules); any output may be NULL.  No device needed. */
+int bmg_dist_plan(int nlevels, const int32_t* nbr, const int32_t* granule, const int32_t* radius, int world,
+                  int agglomerate, const bmg_setup_params* params, int32_t* bounds, int32_t* ext_lo,
+                  int32_t* ext_hi, int32_t* halo);
+/* this rank's share; world/rank from the NCCL context (plain context: world 1) */
+int bmg_hier_setup_dist(bmg_ctx* ctx, int nlevels, const int32_t* granule, const int32_t* radius, int agglomerate,
+                        const bmg_bsr* a_ext, const bmg_bsr* const* transfers, const bmg_setup_params* params,
+                        bmg_hier** out);
+/* every rank in this process: a_ext[r], transfers[r*(nlevels-1) + l-1] */
+int bmg_hier_setup_dist_emulated(bmg_ctx* ctx, int world, int nlevels, const int32_t* granule,
+                                 const int32_t* radius, int agglomerate, const bmg_bsr* const* a_ext,
+                                 const bmg_bsr* const* transfers, const bmg_setup_params* params, bmg_hier** out);
 /* host planning (no device needed): balanced contiguous row ranges; column hull */
 int bmg_partition_rows(int nbr, const int64_t* row_ptr, int world, int granule, int agglomerate,
                        int32_t* bounds);
@@ -234,13 +256,15 @@ int bmg_tridiag_eigs(int n, const double* d, const double* e, double* out);
 
 /* ---- synthetic BASELINE problems (host generator) -------- */
 /* S_p = L_D^p block stencil on an n^dim patch grid (dim 2 or 3), blocks
- * A_ij = S_ij C (+ reg D_i on the diagonal).  Two calls: arrays NULL to query
- * nnzb, then filled. */
-int bmg_gen_stencil(int dim, int n, int power, int m, uint64_t seed, double reg, int64_t* nnzb,
-                    int64_t* row_ptr, int32_t* col_idx, double* vals);
-/* prolongation from an (n/2)^dim coarse grid to the n^dim fine grid */
-int bmg_gen_prolongation(int dim, int n_fine, int m, uint64_t seed, int level, int64_t* nnzb,
-                         int64_t* row_ptr, int32_t* col_idx, double* vals);
+ * A_ij = S_ij C (+ reg D_i on the diagonal); block rows [row_lo, row_hi)
+ * (row_hi < 0: all) with global column indices.  Two calls: arrays NULL to
+ * query nnzb, then filled. */
+int bmg_gen_stencil(int dim, int n, int power, int m, uint64_t seed, double reg, int64_t row_lo,
+                    int64_t row_hi, int64_t* nnzb, int64_t* row_ptr, int32_t* col_idx, double* vals);
+/* prolongation from an (n/2)^dim coarse grid to the n^dim fine grid, rows as above */
+int bmg_gen_prolongation(int dim, int n_fine, int m, uint64_t seed, int level, int64_t row_lo,
+                         int64_t row_hi, int64_t* nnzb, int64_t* row_ptr, int32_t* col_idx,
+                         double* vals);
 /* N(0,1) vector (Box-Muller on the counter RNG), stream `tag` */
 int bmg_gen_normal(uint64_t seed, uint64_t tag, int64_t n, double* out);
 

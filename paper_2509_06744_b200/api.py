@@ -346,6 +346,36 @@ class Hierarchy:
         check(lib().bmg_hier_create(ctx.h, L, aa, pp, mm, dptr(bb), coarse_dim_cap, C.byref(h)))
         return cls(ctx, h, keep=[*A, *P, *M])
 
+    @classmethod
+    def setup_dist(cls, ctx, a_ext: BlockSparseMatrix, transfers, granule, radius, agglomerate: int = 1,
+                   params: N.SetupParams | None = None) -> "Hierarchy":
+        """This rank's share of the distributed setup (bmg_hier_setup_dist):
+        a_ext / transfers are the plan's extended strips (problems.dist_inputs)."""
+        arr = (C.c_void_p * max(len(transfers), 1))(*[t.h.value for t in transfers])
+        g = np.ascontiguousarray(granule, np.int32)
+        r = np.ascontiguousarray(radius, np.int32)
+        h = C.c_void_p()
+        check(lib().bmg_hier_setup_dist(ctx.h, len(transfers) + 1, i32ptr(g), i32ptr(r), agglomerate, a_ext.h, arr,
+                                        C.byref(params) if params is not None else None, C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def setup_dist_emulated(cls, ctx, a_ext, transfers, granule, radius, agglomerate: int = 1,
+                            params: N.SetupParams | None = None) -> "Hierarchy":
+        """Every rank of the distributed setup in this process: a_ext[r] and
+        transfers[r] (a list per rank)."""
+        world = len(a_ext)
+        L = len(transfers[0]) + 1
+        aa = (C.c_void_p * world)(*[a.h.value for a in a_ext])
+        flat = [t.h.value for ts in transfers for t in ts]
+        tt = (C.c_void_p * max(len(flat), 1))(*flat)
+        g = np.ascontiguousarray(granule, np.int32)
+        r = np.ascontiguousarray(radius, np.int32)
+        h = C.c_void_p()
+        check(lib().bmg_hier_setup_dist_emulated(ctx.h, world, L, i32ptr(g), i32ptr(r), agglomerate, aa, tt,
+                                                 C.byref(params) if params is not None else None, C.byref(h)))
+        return cls(ctx, h)
+
     @property
     def levels(self) -> int:
         n = C.c_int()
@@ -418,6 +448,22 @@ class Hierarchy:
             self.close()
         except Exception:
             pass
+
+
+def dist_plan(nbr, granule, radius, world: int, agglomerate: int = 1, params: N.SetupParams | None = None):
+    """bmg_dist_plan: (bounds [L, world+1], ext_lo [L, world], ext_hi [L, world], halo [L])."""
+    L = len(nbr)
+    n = np.ascontiguousarray(nbr, np.int32)
+    g = np.ascontiguousarray(granule, np.int32)
+    r = np.ascontiguousarray(radius, np.int32)
+    b = np.zeros((L, world + 1), np.int32)
+    lo = np.zeros((L, world), np.int32)
+    hi = np.zeros((L, world), np.int32)
+    ha = np.zeros(L, np.int32)
+    check(lib().bmg_dist_plan(L, i32ptr(n), i32ptr(g), i32ptr(r), world, agglomerate,
+                              C.byref(params) if params is not None else None, i32ptr(b), i32ptr(lo), i32ptr(hi),
+                              i32ptr(ha)))
+    return b, lo, hi, ha
 
 
 def read_matrix(ctx: Context, path: str):

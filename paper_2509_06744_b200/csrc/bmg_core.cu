@@ -749,13 +749,15 @@ int bmg_time_residual(const bmg_bsr* ah, const bmg_vec* bh, const bmg_vec* xh, b
   });
 }
 
-int bmg_gen_stencil(int dim, int n, int power, int m, uint64_t seed, double reg, int64_t* nnzb,
-                    int64_t* row_ptr, int32_t* col_idx, double* vals) {
-  return guard([&] { *nnzb = gen_stencil(dim, n, power, m, seed, reg, row_ptr, col_idx, vals); });
+int bmg_gen_stencil(int dim, int n, int power, int m, uint64_t seed, double reg, int64_t row_lo, int64_t row_hi,
+                    int64_t* nnzb, int64_t* row_ptr, int32_t* col_idx, double* vals) {
+  return guard([&] { *nnzb = gen_stencil(dim, n, power, m, seed, reg, row_lo, row_hi, row_ptr, col_idx, vals); });
 }
-int bmg_gen_prolongation(int dim, int n_fine, int m, uint64_t seed, int level, int64_t* nnzb,
-                         int64_t* row_ptr, int32_t* col_idx, double* vals) {
-  return guard([&] { *nnzb = gen_prolongation(dim, n_fine, m, seed, level, row_ptr, col_idx, vals); });
+int bmg_gen_prolongation(int dim, int n_fine, int m, uint64_t seed, int level, int64_t row_lo, int64_t row_hi,
+                         int64_t* nnzb, int64_t* row_ptr, int32_t* col_idx, double* vals) {
+  return guard([&] {
+    *nnzb = gen_prolongation(dim, n_fine, m, seed, level, row_lo, row_hi, row_ptr, col_idx, vals);
+  });
 }
 int bmg_gen_normal(uint64_t seed, uint64_t tag, int64_t n, double* out) {
   return guard([&] { gen_normal(seed, tag, n, out); });

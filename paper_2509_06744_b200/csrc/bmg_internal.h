@@ -180,10 +180,10 @@ void row_window(const int64_t* row_ptr, const int32_t* col, int lo, int hi, int 
 std::vector<double> tridiag_eigenvalues(std::vector<double> d, std::vector<double> e);
 
 // generator (generator.cpp)
-int64_t gen_stencil(int dim, int n, int power, int m, uint64_t seed, double reg, int64_t* row_ptr,
-                    int32_t* col_idx, double* vals);
-int64_t gen_prolongation(int dim, int n_fine, int m, uint64_t seed, int level, int64_t* row_ptr,
-                         int32_t* col_idx, double* vals);
+int64_t gen_stencil(int dim, int n, int power, int m, uint64_t seed, double reg, int64_t row_lo,
+                    int64_t row_hi, int64_t* row_ptr, int32_t* col_idx, double* vals);
+int64_t gen_prolongation(int dim, int n_fine, int m, uint64_t seed, int level, int64_t row_lo, int64_t row_hi,
+                         int64_t* row_ptr, int32_t* col_idx, double* vals);
 void gen_normal(uint64_t seed, uint64_t tag, int64_t n, double* out);
 
 }  // namespace bmg

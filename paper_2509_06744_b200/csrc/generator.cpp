@@ -128,23 +128,26 @@ static std::vector<double> make_c(int m, uint64_t seed) {
 
 }  // namespace gen
 
-int64_t gen_stencil(int dim, int n, int power, int m, uint64_t seed, double reg, int64_t* row_ptr,
-                    int32_t* col_idx, double* vals) {
+int64_t gen_stencil(int dim, int n, int power, int m, uint64_t seed, double reg, int64_t row_lo,
+                    int64_t row_hi, int64_t* row_ptr, int32_t* col_idx, double* vals) {
   using namespace gen;
   if (dim != 2 && dim != 3) throw std::invalid_argument("gen_stencil: dim must be 2 or 3");
   if (n < 1 || power < 1 || m < 1) throw std::invalid_argument("gen_stencil: bad sizes");
   Grid g{dim, n};
-  const int64_t nodes = g.count();
-  if (nodes >= (int64_t)1 << 31) throw std::invalid_argument("gen_stencil: grid too large");
+  const int64_t total = g.count();
+  if (total >= (int64_t)1 << 31) throw std::invalid_argument("gen_stencil: grid too large");
+  if (row_hi < 0) row_hi = total;
+  if (row_lo < 0 || row_lo > row_hi || row_hi > total) throw std::invalid_argument("gen_stencil: bad row range");
+  const int64_t nodes = row_hi - row_lo;  // rows [row_lo, row_hi), global column indices
   // pass 1: counts
   std::vector<int64_t> cnt(nodes + 1, 0);
 #pragma omp parallel
   {
     std::vector<int64_t> c, v;
 #pragma omp for schedule(static)
-    for (int64_t i = 0; i < nodes; ++i) {
-      stencil_row(g, power, i, c, v);
-      cnt[i + 1] = (int64_t)c.size();
+    for (int64_t li = 0; li < nodes; ++li) {
+      stencil_row(g, power, row_lo + li, c, v);
+      cnt[li + 1] = (int64_t)c.size();
     }
   }
   for (int64_t i = 0; i < nodes; ++i) cnt[i + 1] += cnt[i];
@@ -159,9 +162,10 @@ int64_t gen_stencil(int dim, int n, int power, int m, uint64_t seed, double reg,
     std::vector<int64_t> c, v;
     std::vector<double> R(mm);
 #pragma omp for schedule(static)
-    for (int64_t i = 0; i < nodes; ++i) {
+    for (int64_t li = 0; li < nodes; ++li) {
+      const int64_t i = row_lo + li;
       stencil_row(g, power, i, c, v);
-      int64_t p = cnt[i];
+      int64_t p = cnt[li];
       for (size_t q = 0; q < c.size(); ++q, ++p) {
         col_idx[p] = (int32_t)c[q];
         double* blk = vals + (size_t)p * mm;
@@ -189,13 +193,16 @@ int64_t gen_stencil(int dim, int n, int power, int m, uint64_t seed, double reg,
 // P rows: fine patch -> parent (coords >> 1) and the parent's 8 (2-D) / 26 (3-D)
 // neighbours clipped to the coarse grid; entries N(0,1)/9; each fine block row
 // scaled to Frobenius norm sqrt(m) (BASELINE.md §4 decision 2).
-int64_t gen_prolongation(int dim, int n_fine, int m, uint64_t seed, int level, int64_t* row_ptr,
-                         int32_t* col_idx, double* vals) {
+int64_t gen_prolongation(int dim, int n_fine, int m, uint64_t seed, int level, int64_t row_lo, int64_t row_hi,
+                         int64_t* row_ptr, int32_t* col_idx, double* vals) {
   using namespace gen;
   if (dim != 2 && dim != 3) throw std::invalid_argument("gen_prolongation: dim must be 2 or 3");
   if (n_fine < 2 || (n_fine & 1)) throw std::invalid_argument("gen_prolongation: n_fine must be even");
   const int nf = n_fine, nc = n_fine / 2;
-  const int64_t nodes = dim == 2 ? (int64_t)nf * nf : (int64_t)nf * nf * nf;
+  const int64_t total = dim == 2 ? (int64_t)nf * nf : (int64_t)nf * nf * nf;
+  if (row_hi < 0) row_hi = total;
+  if (row_lo < 0 || row_lo > row_hi || row_hi > total) throw std::invalid_argument("gen_prolongation: bad row range");
+  const int64_t nodes = row_hi - row_lo;
   const int zr = dim == 3 ? 1 : 0;
   auto row_cols = [&](int64_t i, std::vector<int32_t>& cols) {
     cols.clear();
@@ -215,9 +222,9 @@ int64_t gen_prolongation(int dim, int n_fine, int m, uint64_t seed, int level, i
   {
     std::vector<int32_t> c;
 #pragma omp for schedule(static)
-    for (int64_t i = 0; i < nodes; ++i) {
-      row_cols(i, c);
-      cnt[i + 1] = (int64_t)c.size();
+    for (int64_t li = 0; li < nodes; ++li) {
+      row_cols(row_lo + li, c);
+      cnt[li + 1] = (int64_t)c.size();
     }
   }
   for (int64_t i = 0; i < nodes; ++i) cnt[i + 1] += cnt[i];
@@ -231,9 +238,10 @@ int64_t gen_prolongation(int dim, int n_fine, int m, uint64_t seed, int level, i
   {
     std::vector<int32_t> c;
 #pragma omp for schedule(static)
-    for (int64_t i = 0; i < nodes; ++i) {
+    for (int64_t li = 0; li < nodes; ++li) {
+      const int64_t i = row_lo + li;
       row_cols(i, c);
-      const int64_t p0 = cnt[i];
+      const int64_t p0 = cnt[li];
       double ss = 0.0;
       for (size_t q = 0; q < c.size(); ++q) {
         col_idx[p0 + q] = c[q];

@@ -65,6 +65,17 @@ __global__ void rng_symmetric_kernel(double* v, int64_t n, uint64_t seed) {
     v[i] = __dsub_rn(__dmul_rn(2.0, u), 1.0);
   }
 }
+// partial[s] = sum over segment s (seg scalars, fma chain ascending) of a*b
+__global__ void seg_dot_kernel(const double* __restrict__ a, const double* __restrict__ b, int64_t n, int seg,
+                               double* __restrict__ partial) {
+  const int64_t nseg = (n + seg - 1) / seg;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg; s += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i0 = s * seg, i1 = min(n, i0 + seg);
+    double t = 0.0;
+    for (int64_t i = i0; i < i1; ++i) t = __fma_rn(a[i], b[i], t);
+    partial[s] = t;
+  }
+}
 __global__ void scale_div_kernel(double* v, int64_t n, double d) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     v[i] = __ddiv_rn(v[i], d);
@@ -653,15 +664,37 @@ static void apply_transformed(const Fsai& m, const Bsr& a, const double* x, doub
   }
 }
 
+// Partition-invariant dot used by Lanczos: one fma chain per block row (seg =
+// m for uniform layouts, 1 otherwise), the row partials summed in global row
+// order on the host -- the distributed setup sums the same partials.
+double seg_dot(Ctx* ctx, const double* a, const double* b, int64_t n, int seg, DBuf<double>& part,
+               std::vector<double>& host) {
+  const int64_t nseg = (n + seg - 1) / seg;
+  if (part.n < (size_t)nseg) part.alloc(std::max<int64_t>(nseg, 1));
+  kern::seg_dot_kernel<<<grid1d(nseg), 256, 0, ctx->stream>>>(a, b, n, seg, part.p);
+  ctx->count();
+  BMG_CUDA(cudaGetLastError());
+  host.resize(nseg);
+  BMG_CUDA(cudaMemcpyAsync(host.data(), part.p, nseg * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+  double s = 0.0;
+  for (int64_t i = 0; i < nseg; ++i) s += host[i];
+  return s;
+}
+
 double lanczos_lambda_max(const Bsr& a, const Fsai& m, int iters, double safety, uint64_t seed) {
   Ctx* ctx = a.ctx;
   const int64_t n = a.dim_r;
   if (n < 1) fail(BMG_EINVAL, "lanczos: operator dimension must be >= 1");
   iters = (int)std::min<int64_t>(iters, n);
+  const int seg = a.uniform ? a.mr : 1;
+  DBuf<double> part;
+  std::vector<double> hpart;
+  auto dot = [&](const double* x, const double* y) { return seg_dot(ctx, x, y, n, seg, part, hpart); };
   DBuf<double> v(n), vp(n), w(n), t1(n), t2(n);
   kern::rng_symmetric_kernel<<<grid1d(n), 256, 0, ctx->stream>>>(v.p, n, seed);
   ctx->count();
-  const double nv = std::sqrt(dot(ctx, v.p, v.p, n));
+  const double nv = std::sqrt(dot(v.p, v.p));
   kern::scale_div_kernel<<<grid1d(n), 256, 0, ctx->stream>>>(v.p, n, nv);
   ctx->count();
   fill(ctx, vp.p, n, 0.0);
@@ -669,11 +702,11 @@ double lanczos_lambda_max(const Bsr& a, const Fsai& m, int iters, double safety,
   double beta = 0.0;
   for (int j = 0; j < iters; ++j) {
     apply_transformed(m, a, v.p, w.p, t1.p, t2.p);
-    const double alpha = dot(ctx, v.p, w.p, n);
+    const double alpha = dot(v.p, w.p);
     diag.push_back(alpha);
     kern::lanczos_update_kernel<<<grid1d(n), 256, 0, ctx->stream>>>(w.p, v.p, vp.p, n, alpha, beta);
     ctx->count();
-    beta = std::sqrt(dot(ctx, w.p, w.p, n));
+    beta = std::sqrt(dot(w.p, w.p));
     if (j + 1 == iters) break;
     if (beta <= 1e-14 * std::fabs(alpha) || beta == 0.0) break;
     off.push_back(beta);

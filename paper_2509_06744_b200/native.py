@@ -145,6 +145,9 @@ _SIGS = {
     "bmg_nccl_unique_id": (_I, [C.c_char_p]),
     "bmg_ctx_create_nccl": (_I, [_I, _I, _I, C.c_char_p, _PP]),
     "bmg_hier_partition": (_I, [_P, _I, _I, _PI32, _I]),
+    "bmg_dist_plan": (_I, [_I, _PI32, _PI32, _PI32, _I, _I, C.POINTER(SetupParams), _PI32, _PI32, _PI32, _PI32]),
+    "bmg_hier_setup_dist": (_I, [_P, _I, _PI32, _PI32, _I, _P, _PP, C.POINTER(SetupParams), _PP]),
+    "bmg_hier_setup_dist_emulated": (_I, [_P, _I, _I, _PI32, _PI32, _I, _PP, _PP, C.POINTER(SetupParams), _PP]),
     "bmg_hier_part_info": (_I, [_P, _I, _I, _PI32, _PI32, _PI32, _PI32]),
     "bmg_partition_rows": (_I, [_I, _PI64, _I, _I, _I, _PI32]),
     "bmg_row_window": (_I, [_PI64, _PI32, _I, _I, _I, _I, _PI32, _PI32]),
@@ -153,8 +156,8 @@ _SIGS = {
     "bmg_io_write_matrix": (_I, [_P, C.c_char_p]),
     "bmg_io_read_vector": (_I, [_P, C.c_char_p, _PP]),
     "bmg_io_write_vector": (_I, [_P, C.c_char_p]),
-    "bmg_gen_stencil": (_I, [_I, _I, _I, _I, _U64, _D, _PI64, _PI64, _PI32, _PD]),
-    "bmg_gen_prolongation": (_I, [_I, _I, _I, _U64, _I, _PI64, _PI64, _PI32, _PD]),
+    "bmg_gen_stencil": (_I, [_I, _I, _I, _I, _U64, _D, _I64, _I64, _PI64, _PI64, _PI32, _PD]),
+    "bmg_gen_prolongation": (_I, [_I, _I, _I, _U64, _I, _I64, _I64, _PI64, _PI64, _PI32, _PD]),
     "bmg_gen_normal": (_I, [_U64, _U64, _I64, _PD]),
 }
 

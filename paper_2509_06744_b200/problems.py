@@ -51,30 +51,36 @@ CONFIGS = {
 }
 
 
-def stencil_matrix(dim: int, n: int, power: int, m: int, seed: int = 0, reg: float = 0.01) -> HostBsr:
-    """A = S_p (x) C + reg blockdiag(D_i) on an n^dim patch grid."""
+def stencil_matrix(dim: int, n: int, power: int, m: int, seed: int = 0, reg: float = 0.01,
+                   rows: tuple | None = None) -> HostBsr:
+    """A = S_p (x) C + reg blockdiag(D_i) on an n^dim patch grid; `rows` = (lo, hi)
+    restricts to those block rows (global column indices, not symmetric then)."""
+    lo, hi = rows if rows is not None else (0, -1)
     nnzb = C.c_int64()
-    check(lib().bmg_gen_stencil(dim, n, power, m, seed, reg, C.byref(nnzb), None, None, None))
+    check(lib().bmg_gen_stencil(dim, n, power, m, seed, reg, lo, hi, C.byref(nnzb), None, None, None))
     nodes = n ** dim
-    rp = np.zeros(nodes + 1, np.int64)
+    nr = (hi if hi >= 0 else nodes) - lo
+    rp = np.zeros(nr + 1, np.int64)
     ci = np.zeros(nnzb.value, np.int32)
     vals = np.zeros(nnzb.value * m * m)
-    check(lib().bmg_gen_stencil(dim, n, power, m, seed, reg, C.byref(nnzb), i64ptr(rp), i32ptr(ci), dptr(vals)))
-    sizes = np.full(nodes, m, np.int32)
-    return HostBsr(sizes, sizes, rp, ci, vals, symmetric=True)
+    check(lib().bmg_gen_stencil(dim, n, power, m, seed, reg, lo, hi, C.byref(nnzb), i64ptr(rp), i32ptr(ci),
+                                dptr(vals)))
+    return HostBsr(np.full(nr, m, np.int32), np.full(nodes, m, np.int32), rp, ci, vals, symmetric=rows is None)
 
 
-def prolongation(dim: int, n_fine: int, m: int, seed: int = 0, level: int = 1) -> HostBsr:
+def prolongation(dim: int, n_fine: int, m: int, seed: int = 0, level: int = 1, rows: tuple | None = None) -> HostBsr:
+    lo, hi = rows if rows is not None else (0, -1)
     nnzb = C.c_int64()
-    check(lib().bmg_gen_prolongation(dim, n_fine, m, seed, level, C.byref(nnzb), None, None, None))
+    check(lib().bmg_gen_prolongation(dim, n_fine, m, seed, level, lo, hi, C.byref(nnzb), None, None, None))
     nf = n_fine ** dim
     nc = (n_fine // 2) ** dim
-    rp = np.zeros(nf + 1, np.int64)
+    nr = (hi if hi >= 0 else nf) - lo
+    rp = np.zeros(nr + 1, np.int64)
     ci = np.zeros(nnzb.value, np.int32)
     vals = np.zeros(nnzb.value * m * m)
-    check(lib().bmg_gen_prolongation(dim, n_fine, m, seed, level, C.byref(nnzb), i64ptr(rp), i32ptr(ci),
+    check(lib().bmg_gen_prolongation(dim, n_fine, m, seed, level, lo, hi, C.byref(nnzb), i64ptr(rp), i32ptr(ci),
                                      dptr(vals)))
-    return HostBsr(np.full(nf, m, np.int32), np.full(nc, m, np.int32), rp, ci, vals, symmetric=False)
+    return HostBsr(np.full(nr, m, np.int32), np.full(nc, m, np.int32), rp, ci, vals, symmetric=False)
 
 
 def normal_vector(n: int, seed: int = 0, tag: int = 0) -> np.ndarray:
@@ -92,3 +98,40 @@ def make_problem(cfg: Config):
         transfers.append(prolongation(cfg.dim, n_l, cfg.m, cfg.seed, l))
     b = normal_vector(A.dim_r, cfg.seed, 0)
     return A, transfers, b
+
+
+# ---------------------------------------------------------------------------
+# distributed setup inputs (bmg_hier_setup_dist): the plan's extended strips
+def level_grid(cfg: Config):
+    """Per level (coarsest first): block rows, granule (one grid row in 2-D, one
+    plane in 3-D) and coupling radius in granules (S_p: p; Galerkin with the 2:1
+    prolongation's support: floor((R + 5) / 2))."""
+    L = cfg.levels
+    ns = [cfg.n >> (L - 1 - l) for l in range(L)]
+    nbr = [n ** cfg.dim for n in ns]
+    gran = [n ** (cfg.dim - 1) for n in ns]
+    rad = [0] * L
+    rad[L - 1] = cfg.power
+    for l in range(L - 1, 0, -1):
+        rad[l - 1] = (rad[l] + 5) // 2
+    return ns, nbr, gran, rad
+
+
+def dist_inputs(cfg: Config, world: int, rank: int, agglomerate: int = 1, params=None):
+    """(A_ext, transfers, b_own, plan) for one rank: rows [ext_lo, ext_hi) of the
+    finest A and of P_l (l > agglomerate), whole P_l below; b's own rows."""
+    from .api import dist_plan
+    ns, nbr, gran, rad = level_grid(cfg)
+    L = cfg.levels
+    bounds, elo, ehi, halo = dist_plan(nbr, gran, rad, world, agglomerate, params)
+    top = L - 1
+    A = stencil_matrix(cfg.dim, cfg.n, cfg.power, cfg.m, cfg.seed, cfg.reg,
+                       rows=(int(elo[top, rank]), int(ehi[top, rank])))
+    agg = max(1, min(agglomerate, L - 1))
+    transfers = []
+    for l in range(1, L):
+        rows = (int(elo[l, rank]), int(ehi[l, rank])) if l > agg else None
+        transfers.append(prolongation(cfg.dim, ns[l], cfg.m, cfg.seed, l, rows=rows))
+    b = normal_vector(nbr[top] * cfg.m, cfg.seed, 0)
+    lo, hi = int(bounds[top, rank]), int(bounds[top, rank + 1])
+    return A, transfers, b[lo * cfg.m:hi * cfg.m], (bounds, elo, ehi, halo, gran, rad)

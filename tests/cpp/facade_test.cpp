@@ -9,26 +9,26 @@
 
 static bmg::HostBsr stencil(int n, int m) {
   int64_t nnzb = 0;
-  bmg::check(bmg_gen_stencil(2, n, 2, m, 0, 0.01, &nnzb, nullptr, nullptr, nullptr));
+  bmg::check(bmg_gen_stencil(2, n, 2, m, 0, 0.01, 0, -1, &nnzb, nullptr, nullptr, nullptr));
   bmg::HostBsr h;
   h.rows = h.cols = bmg::BlockLayout::uniform(n * n, m);
   h.row_ptr.resize((size_t)n * n + 1);
   h.col_idx.resize((size_t)nnzb);
   h.vals.resize((size_t)nnzb * m * m);
-  bmg::check(bmg_gen_stencil(2, n, 2, m, 0, 0.01, &nnzb, h.row_ptr.data(), h.col_idx.data(), h.vals.data()));
+  bmg::check(bmg_gen_stencil(2, n, 2, m, 0, 0.01, 0, -1, &nnzb, h.row_ptr.data(), h.col_idx.data(), h.vals.data()));
   h.symmetric = true;
   return h;
 }
 static bmg::HostBsr prolong(int nf, int m, int level) {
   int64_t nnzb = 0;
-  bmg::check(bmg_gen_prolongation(2, nf, m, 0, level, &nnzb, nullptr, nullptr, nullptr));
+  bmg::check(bmg_gen_prolongation(2, nf, m, 0, level, 0, -1, &nnzb, nullptr, nullptr, nullptr));
   bmg::HostBsr h;
   h.rows = bmg::BlockLayout::uniform(nf * nf, m);
   h.cols = bmg::BlockLayout::uniform(nf * nf / 4, m);
   h.row_ptr.resize((size_t)nf * nf + 1);
   h.col_idx.resize((size_t)nnzb);
   h.vals.resize((size_t)nnzb * m * m);
-  bmg::check(bmg_gen_prolongation(2, nf, m, 0, level, &nnzb, h.row_ptr.data(), h.col_idx.data(), h.vals.data()));
+  bmg::check(bmg_gen_prolongation(2, nf, m, 0, level, 0, -1, &nnzb, h.row_ptr.data(), h.col_idx.data(), h.vals.data()));
   return h;
 }
 
