@@ -205,6 +205,13 @@ int bmg_solve(bmg_hier* h, int k_pre, int k_post, const bmg_vec* b, bmg_vec* x, 
  * bitwise equal to the unpartitioned cycle. */
 int bmg_nccl_unique_id(unsigned char* id128);
 int bmg_ctx_create_nccl(int device, int rank, int world, const unsigned char* id128, bmg_ctx** out);
+/* Loopback transport: `world` ranks as host threads of ONE process, each with
+ * its own context on the same device; sends and receives are matched in-process
+ * (host-side waits only).  Runs the exact NCCL code path where one GPU exists. */
+typedef struct bmg_loopback bmg_loopback;
+int bmg_loopback_create(int world, bmg_loopback** out);
+int bmg_loopback_destroy(bmg_loopback* g);
+int bmg_ctx_create_loopback(int device, bmg_loopback* g, int rank, bmg_ctx** out);
 int bmg_hier_partition(bmg_hier* h, int world, int rank, const int32_t* granule, int agglomerate);
 /* own rows [lo, hi) and vector window [wlo, whi) of `rank` on `level` */
 int bmg_hier_part_info(const bmg_hier* h, int level, int rank, int32_t* lo, int32_t* hi, int32_t* wlo,

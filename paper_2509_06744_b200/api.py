@@ -71,18 +71,45 @@ class HostBsr:
         return out
 
 
+class LoopbackGroup:
+    """bmg_loopback: `world` ranks as threads of this process on one device."""
+
+    def __init__(self, world: int):
+        self.h = C.c_void_p()
+        self.world = world
+        check(lib().bmg_loopback_create(world, C.byref(self.h)))
+
+    def close(self):
+        if self.h:
+            check(lib().bmg_loopback_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Context:
-    def __init__(self, device: int = 0, nccl: tuple | None = None):
-        """nccl = (rank, world, unique_id_bytes) for a multi-GPU context."""
+    def __init__(self, device: int = 0, nccl: tuple | None = None, loopback: tuple | None = None):
+        """nccl = (rank, world, unique_id_bytes) for a multi-GPU context;
+        loopback = (LoopbackGroup, rank) for a rank thread of a loopback group."""
         h = C.c_void_p()
-        if nccl is None:
-            check(lib().bmg_ctx_create(device, C.byref(h)))
-        else:
+        if nccl is not None:
             rank, world, uid = nccl
             check(lib().bmg_ctx_create_nccl(device, rank, world, bytes(uid), C.byref(h)))
+        elif loopback is not None:
+            group, rank = loopback
+            world = group.world
+            check(lib().bmg_ctx_create_loopback(device, group.h, rank, C.byref(h)))
+            self._group = group
+        else:
+            rank, world = 0, 1
+            check(lib().bmg_ctx_create(device, C.byref(h)))
         self.h = h
         self.device = device
-        self.rank, self.world = (nccl[0], nccl[1]) if nccl else (0, 1)
+        self.rank, self.world = rank, world
 
     @staticmethod
     def nccl_unique_id() -> bytes:

@@ -1,7 +1,6 @@
 // bmg_core.cu -- context, device BSR storage + streaming plans, vectors, the
 // streaming-kernel launchers, reductions and the corresponding C ABI.
 #include <cuda_runtime.h>
-#include <nccl.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -39,7 +38,7 @@ thread_local int g_last_pivot = -1;
 
 // ============================================================================ context
 Ctx::~Ctx() {
-  if (nccl) ncclCommDestroy(static_cast<ncclComm_t>(nccl));
+  comm.reset();
   if (solver) cusolverDnDestroy(solver);
   if (h_red) cudaFreeHost(h_red);
   if (own) cudaStreamDestroy(own);
@@ -212,7 +211,8 @@ static int chunk_blocks(int mr, int bs) {
 template <int MR, int MC>
 static int stream_occupancy(size_t smem) {
   auto kfn = kern::bsr_stream_kernel<MR, MC, kern::EpiStore>;
-  BMG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // the launch cap stays at the maximum (launch_stream_t); the query uses `smem`
+  BMG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   int occ = 0;
   BMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kern::kThreads, smem));
   return std::max(occ, 1);
@@ -470,12 +470,12 @@ static void launch_stream_t(const Bsr& a, const double* x, Epi epi) {
   s.rmax = a.plan.rmax;
   s.stages = a.plan.stages;
   // one attribute per template instantiation (covers the largest plan)
-  static bool attr_set = false;
-  if (!attr_set) {
+  static const bool attr_set = [] {  // thread-safe one-time init (contexts may live on several threads)
     BMG_CUDA(cudaFuncSetAttribute(kern::bsr_stream_kernel<MR, MC, Epi>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr_set = true;
-  }
+    return true;
+  }();
+  (void)attr_set;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.plan.nctas);
   cfg.blockDim = dim3(kern::kThreads);

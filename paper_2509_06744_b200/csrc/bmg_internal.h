@@ -55,6 +55,28 @@ struct DBuf {
 };
 
 // ---- context ------------------------------------------------------------------
+// ---- rank-to-rank transport ---------------------------------------------------
+// NCCL over NVLink for real multi-GPU runs (bmg_ctx_create_nccl); a loopback
+// transport (bmg_ctx_create_loopback: one host thread per rank, all on one GPU,
+// send/recv matched in-process) runs the exact same exchange code where only one
+// GPU exists.  Semantics follow NCCL: group_start / group_end bracket sends and
+// receives; sends and receives between a pair match in posting order.
+enum class DType { F64, I32, I64 };
+enum class ROp { Sum, Max };
+struct Comm {
+  virtual ~Comm() = default;
+  virtual void group_start() = 0;
+  virtual void group_end() = 0;
+  virtual void send(const void* p, size_t count, DType t, int peer, cudaStream_t s) = 0;
+  virtual void recv(void* p, size_t count, DType t, int peer, cudaStream_t s) = 0;
+  virtual void allreduce(const void* sb, void* rb, size_t count, DType t, ROp op, cudaStream_t s) = 0;
+  virtual bool capturable() const = 0;  // may run inside CUDA graph capture
+};
+struct LoopGroup;
+std::unique_ptr<Comm> make_nccl_comm(int rank, int world, const unsigned char* id128);
+std::unique_ptr<Comm> make_loopback_comm(LoopGroup* g, int rank);
+void nccl_unique_id(unsigned char* id128);
+
 struct Ctx {
   int device = 0;
   int sms = 148;
@@ -62,7 +84,7 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   int64_t launches = 0;
   cusolverDnHandle_t solver = nullptr;
-  void* nccl = nullptr;  // ncclComm_t of a multi-GPU context (bmg_ctx_create_nccl)
+  std::unique_ptr<Comm> comm;  // multi-rank context: NCCL or loopback transport
   int rank = 0, world = 1;
   DBuf<double> red;          // reduction partials
   DBuf<double> work;         // scratch of the standalone smoother

@@ -13,7 +13,6 @@
 // partition, so partitioned cycles are bitwise equal to the 1-GPU cycle.
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
-#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -138,9 +137,6 @@ __global__ void __launch_bounds__(256) segment_sq_kernel(const double* __restric
 
 static int grid1d(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)); }
 
-static void nccl_check(ncclResult_t r, const char* what) {
-  if (r != ncclSuccess) fail(BMG_ENCCL, std::string(what) + ": " + ncclGetErrorString(r));
-}
 
 // ============================================================================ data model
 enum Which { VB = 0, VX, VR, VW, VP, VT, VNUM };
@@ -272,24 +268,20 @@ static void exchange(Hier& h, int l, Which w) {
   Part& me = h.parts[0];
   const int r = me.rank;
   double* base = vec(h, me, l, w);
-  ncclComm_t comm = static_cast<ncclComm_t>(ctx->nccl);
-  nccl_check(ncclGroupStart(), "ncclGroupStart");
+  Comm& comm = *ctx->comm;
+  comm.group_start();
   for (int s = 0; s < h.world; ++s) {
     if (s == r) continue;
     // send my own rows inside s's window
     const int a0 = std::max(B[r], h.wlo[l][s]), a1 = std::min(B[r + 1], h.whi[l][s]);
     if (a1 > a0)
-      nccl_check(ncclSend(base + (int64_t)(a0 - h.wlo[l][r]) * m, (size_t)(a1 - a0) * m, ncclDouble, s, comm,
-                          ctx->stream),
-                 "ncclSend");
+      comm.send(base + (int64_t)(a0 - h.wlo[l][r]) * m, (size_t)(a1 - a0) * m, DType::F64, s, ctx->stream);
     // receive s's own rows inside my window
     const int b0 = std::max(B[s], h.wlo[l][r]), b1 = std::min(B[s + 1], h.whi[l][r]);
     if (b1 > b0)
-      nccl_check(ncclRecv(base + (int64_t)(b0 - h.wlo[l][r]) * m, (size_t)(b1 - b0) * m, ncclDouble, s, comm,
-                          ctx->stream),
-                 "ncclRecv");
+      comm.recv(base + (int64_t)(b0 - h.wlo[l][r]) * m, (size_t)(b1 - b0) * m, DType::F64, s, ctx->stream);
   }
-  nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+  comm.group_end();
 }
 
 // One streaming pass over a split matrix whose input is vector `in` of level
@@ -477,7 +469,7 @@ static void run_vcycle(Hier& h, int kpre, int kpost, const double* bf, double* x
     stage_out(h, xf);
     return;
   }
-  if (!h.use_graph) {
+  if (!h.use_graph || (ctx->comm && !ctx->comm->capturable())) {
     stage_in(h, bf, xf);
     enqueue_vcycle(h, kpre, kpost);
     stage_out(h, xf);
@@ -711,7 +703,7 @@ static void partition(Hier& h, int world, int rank, const int32_t* granule, int 
     h.granule_top = granule ? std::max(1, granule[h.finest()]) : 1;
     return;
   }
-  if (rank >= 0 && (!h.ctx->nccl || h.ctx->world != world || h.ctx->rank != rank))
+  if (rank >= 0 && (!h.ctx->comm || h.ctx->world != world || h.ctx->rank != rank))
     fail(BMG_EINVAL, "partition: context is not an NCCL context of this rank/world");
   Ctx* ctx = h.ctx;
   BMG_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -824,9 +816,7 @@ static double finest_norm(Hier& h, const double* r_whole) {
   }
   if (!h.whole() && !h.emulated) {
     // one rank owns each segment; the others contribute exact zeros
-    nccl_check(ncclAllReduce(h.seg.p, h.seg.p, nseg, ncclDouble, ncclSum, static_cast<ncclComm_t>(ctx->nccl),
-                             ctx->stream),
-               "ncclAllReduce");
+    ctx->comm->allreduce(h.seg.p, h.seg.p, nseg, DType::F64, ROp::Sum, ctx->stream);
   }
   std::vector<double> hs(nseg);
   BMG_CUDA(cudaMemcpyAsync(hs.data(), h.seg.p, nseg * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1074,10 +1064,10 @@ static std::vector<std::unique_ptr<Bsr>> fetch_rows_emulated(Ctx* ctx, const std
 }
 
 // NCCL: the same exchange, this rank's piece only (row counts, then cols + values)
-static std::unique_ptr<Bsr> fetch_rows_nccl(Ctx* ctx, const Bsr* mine, const std::vector<int32_t>& B,
+static std::unique_ptr<Bsr> fetch_rows_comm(Ctx* ctx, const Bsr* mine, const std::vector<int32_t>& B,
                                             const std::vector<int32_t>& want_lo, const std::vector<int32_t>& want_hi,
                                             int ncols, int m, bool sym) {
-  ncclComm_t comm = static_cast<ncclComm_t>(ctx->nccl);
+  Comm& comm = *ctx->comm;
   const int world = ctx->world, me = ctx->rank;
   const int bs = (m * m + 1) & ~1;
   const int nown = B[me + 1] - B[me];
@@ -1097,7 +1087,7 @@ static std::unique_ptr<Bsr> fetch_rows_nccl(Ctx* ctx, const Bsr* mine, const std
     a = std::max(B[s], want_lo[me]);
     b = std::min(B[s + 1], want_hi[me]);
   };
-  nccl_check(ncclGroupStart(), "ncclGroupStart");
+  comm.group_start();
   for (int s = 0; s < world; ++s) {
     int a, b;
     recv_range(s, a, b);
@@ -1106,12 +1096,12 @@ static std::unique_ptr<Bsr> fetch_rows_nccl(Ctx* ctx, const Bsr* mine, const std
         BMG_CUDA(cudaMemcpyAsync(rcnt.p + (a - wlo), mycnt.p + (a - B[me]), (size_t)(b - a) * 8,
                                  cudaMemcpyDeviceToDevice, ctx->stream));
       else
-        nccl_check(ncclRecv(rcnt.p + (a - wlo), b - a, ncclInt64, s, comm, ctx->stream), "ncclRecv");
+        comm.recv(rcnt.p + (a - wlo), b - a, DType::I64, s, ctx->stream);
     }
     send_range(s, a, b);
-    if (b > a && s != me) nccl_check(ncclSend(mycnt.p + (a - B[me]), b - a, ncclInt64, s, comm, ctx->stream), "ncclSend");
+    if (b > a && s != me) comm.send(mycnt.p + (a - B[me]), b - a, DType::I64, s, ctx->stream);
   }
-  nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+  comm.group_end();
   std::vector<int64_t> c(nwant), rp(nwant + 1, 0);
   if (nwant) BMG_CUDA(cudaMemcpyAsync(c.data(), rcnt.p, (size_t)nwant * 8, cudaMemcpyDeviceToHost, ctx->stream));
   BMG_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -1119,7 +1109,7 @@ static std::unique_ptr<Bsr> fetch_rows_nccl(Ctx* ctx, const Bsr* mine, const std
   const int64_t tot = rp[nwant];
   DBuf<int32_t> dcol(std::max<int64_t>(tot, 1));
   DBuf<double> dval(std::max<int64_t>(tot * bs, 1));
-  nccl_check(ncclGroupStart(), "ncclGroupStart");
+  comm.group_start();
   for (int s = 0; s < world; ++s) {
     int a, b;
     recv_range(s, a, b);
@@ -1133,8 +1123,8 @@ static std::unique_ptr<Bsr> fetch_rows_nccl(Ctx* ctx, const Bsr* mine, const std
           BMG_CUDA(cudaMemcpyAsync(dval.p + q0 * bs, mine->vals.p + p0 * bs, (size_t)(q1 - q0) * bs * 8,
                                    cudaMemcpyDeviceToDevice, ctx->stream));
         } else {
-          nccl_check(ncclRecv(dcol.p + q0, q1 - q0, ncclInt32, s, comm, ctx->stream), "ncclRecv");
-          nccl_check(ncclRecv(dval.p + q0 * bs, (q1 - q0) * bs, ncclDouble, s, comm, ctx->stream), "ncclRecv");
+          comm.recv(dcol.p + q0, q1 - q0, DType::I32, s, ctx->stream);
+          comm.recv(dval.p + q0 * bs, (q1 - q0) * bs, DType::F64, s, ctx->stream);
         }
       }
     }
@@ -1142,12 +1132,12 @@ static std::unique_ptr<Bsr> fetch_rows_nccl(Ctx* ctx, const Bsr* mine, const std
     if (b > a && s != me) {
       const int64_t p0 = mine->h_row_ptr[a - B[me]], p1 = mine->h_row_ptr[b - B[me]];
       if (p1 > p0) {
-        nccl_check(ncclSend(mine->col.p + p0, p1 - p0, ncclInt32, s, comm, ctx->stream), "ncclSend");
-        nccl_check(ncclSend(mine->vals.p + p0 * bs, (p1 - p0) * bs, ncclDouble, s, comm, ctx->stream), "ncclSend");
+        comm.send(mine->col.p + p0, p1 - p0, DType::I32, s, ctx->stream);
+        comm.send(mine->vals.p + p0 * bs, (p1 - p0) * bs, DType::F64, s, ctx->stream);
       }
     }
   }
-  nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+  comm.group_end();
   BMG_CUDA(cudaStreamSynchronize(ctx->stream));
   if (nwant == 0) return nullptr;
   std::vector<int32_t> col(tot);
@@ -1227,7 +1217,7 @@ static std::vector<std::vector<Kept>> dist_build(Ctx* ctx, const DistPlan& P, bo
       for (int r = 0; r < world; ++r) own[r] = K[r][l - 1].A.get();
       aext = fetch_rows_emulated(ctx, own, P.B[l - 1], P.elo[l - 1], P.ehi[l - 1], P.nbr[l - 1], m, false);
     } else if (world > 1) {
-      aext[0] = fetch_rows_nccl(ctx, K[0][l - 1].A.get(), P.B[l - 1], P.elo[l - 1], P.ehi[l - 1], P.nbr[l - 1], m,
+      aext[0] = fetch_rows_comm(ctx, K[0][l - 1].A.get(), P.B[l - 1], P.elo[l - 1], P.ehi[l - 1], P.nbr[l - 1], m,
                                 false);
     } else {
       aext[0] = slice_rows(*K[0][l - 1].A, 0, P.nbr[l - 1], 0, P.nbr[l - 1]);
@@ -1249,9 +1239,7 @@ static void dist_dot_partials(Hier& h, int l, Which a, Which b, DBuf<double>& pa
     ctx->count();
   }
   if (!h.emulated && h.world > 1)
-    nccl_check(ncclAllReduce(part.p, part.p, n, ncclDouble, ncclSum, static_cast<ncclComm_t>(ctx->nccl),
-                             ctx->stream),
-               "ncclAllReduce");
+    ctx->comm->allreduce(part.p, part.p, n, DType::F64, ROp::Sum, ctx->stream);
 }
 static double dist_dot(Hier& h, int l, Which a, Which b, DBuf<double>& part, std::vector<double>& hp) {
   dist_dot_partials(h, l, a, b, part);
@@ -1358,7 +1346,7 @@ static std::unique_ptr<Hier> dist_setup(Ctx* ctx, const DistPlan& P, int rank, s
       for (int r = 0; r < world; ++r) own[r] = K[r][agg].A.get();
       a_agg = std::move(fetch_rows_emulated(ctx, own, P.B[agg], wl, wh, P.nbr[agg], m, true)[0]);
     } else {
-      a_agg = fetch_rows_nccl(ctx, K[0][agg].A.get(), P.B[agg], wl, wh, P.nbr[agg], m, true);
+      a_agg = fetch_rows_comm(ctx, K[0][agg].A.get(), P.B[agg], wl, wh, P.nbr[agg], m, true);
     }
   }
   const int root = 0;  // index into K of the part holding rank 0 (emulation: rank 0; NCCL: this rank if 0)
@@ -1443,9 +1431,7 @@ static std::unique_ptr<Hier> dist_setup(Ctx* ctx, const DistPlan& P, int rank, s
     }
     DBuf<int32_t> d(buf.size());
     BMG_CUDA(cudaMemcpy(d.p, buf.data(), buf.size() * 4, cudaMemcpyHostToDevice));
-    nccl_check(ncclAllReduce(d.p, d.p, buf.size(), ncclInt32, ncclSum, static_cast<ncclComm_t>(ctx->nccl),
-                             ctx->stream),
-               "ncclAllReduce");
+    ctx->comm->allreduce(d.p, d.p, buf.size(), DType::I32, ROp::Sum, ctx->stream);
     BMG_CUDA(cudaMemcpyAsync(buf.data(), d.p, buf.size() * 4, cudaMemcpyDeviceToHost, ctx->stream));
     BMG_CUDA(cudaStreamSynchronize(ctx->stream));
     for (int l = 0; l < L; ++l)
@@ -1524,8 +1510,7 @@ static std::unique_ptr<Hier> dist_setup(Ctx* ctx, const DistPlan& P, int rank, s
     for (int l = 0; l < L; ++l) nf[l] = (int32_t)h->nfactors[l];
     DBuf<int32_t> d(L);
     BMG_CUDA(cudaMemcpy(d.p, nf.data(), L * 4, cudaMemcpyHostToDevice));
-    nccl_check(ncclAllReduce(d.p, d.p, L, ncclInt32, ncclMax, static_cast<ncclComm_t>(ctx->nccl), ctx->stream),
-               "ncclAllReduce");
+    ctx->comm->allreduce(d.p, d.p, L, DType::I32, ROp::Max, ctx->stream);
     BMG_CUDA(cudaMemcpyAsync(nf.data(), d.p, L * 4, cudaMemcpyDeviceToHost, ctx->stream));
     BMG_CUDA(cudaStreamSynchronize(ctx->stream));
     for (int l = 0; l < L; ++l) h->nfactors[l] = nf[l];
@@ -1558,8 +1543,7 @@ static std::unique_ptr<Hier> dist_setup(Ctx* ctx, const DistPlan& P, int rank, s
     int64_t n0 = h->n0;
     DBuf<int64_t> d(1);
     BMG_CUDA(cudaMemcpy(d.p, &n0, 8, cudaMemcpyHostToDevice));
-    nccl_check(ncclAllReduce(d.p, d.p, 1, ncclInt64, ncclMax, static_cast<ncclComm_t>(ctx->nccl), ctx->stream),
-               "ncclAllReduce");
+    ctx->comm->allreduce(d.p, d.p, 1, DType::I64, ROp::Max, ctx->stream);
     BMG_CUDA(cudaMemcpyAsync(&n0, d.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
     BMG_CUDA(cudaStreamSynchronize(ctx->stream));
     h->n0 = n0;
@@ -1586,9 +1570,7 @@ static std::unique_ptr<Hier> dist_setup(Ctx* ctx, const DistPlan& P, int rank, s
     if (!h->emulated && world > 1) {
       DBuf<int64_t> d(st.size());
       BMG_CUDA(cudaMemcpy(d.p, st.data(), st.size() * 8, cudaMemcpyHostToDevice));
-      nccl_check(ncclAllReduce(d.p, d.p, st.size(), ncclInt64, ncclSum, static_cast<ncclComm_t>(ctx->nccl),
-                               ctx->stream),
-                 "ncclAllReduce");
+      ctx->comm->allreduce(d.p, d.p, st.size(), DType::I64, ROp::Sum, ctx->stream);
       BMG_CUDA(cudaMemcpyAsync(st.data(), d.p, st.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
       BMG_CUDA(cudaStreamSynchronize(ctx->stream));
     }
@@ -1752,7 +1734,7 @@ int bmg_hier_setup_dist(bmg_ctx* ch, int nlevels, const int32_t* granule, const 
     else
       bmg_setup_params_default(&prm);
     if (!radius) fail(BMG_EINVAL, "dist setup: radius is required");
-    const int world = ctx->nccl ? ctx->world : 1, rank = ctx->nccl ? ctx->rank : 0;
+    const int world = ctx->comm ? ctx->world : 1, rank = ctx->comm ? ctx->rank : 0;
     std::vector<int32_t> nbr;
     dist_inputs(nlevels, a_ext, transfers, nbr);
     const DistPlan P = dist_plan(nlevels, nbr.data(), granule, radius, world, agglomerate, prm);
@@ -1988,11 +1970,7 @@ int bmg_ctx_create_nccl(int device, int rank, int world, const unsigned char* id
     if (st != BMG_OK) fail(st, bmg_last_error());
     Ctx* ctx = reinterpret_cast<Ctx*>(c);
     std::unique_ptr<Ctx> own(ctx);
-    ncclUniqueId id;
-    std::memcpy(&id, id128, sizeof(id));
-    ncclComm_t comm;
-    nccl_check(ncclCommInitRank(&comm, world, id, rank), "ncclCommInitRank");
-    ctx->nccl = comm;
+    ctx->comm = make_nccl_comm(rank, world, id128);
     ctx->rank = rank;
     ctx->world = world;
     *out = reinterpret_cast<bmg_ctx*>(own.release());
@@ -2000,12 +1978,7 @@ int bmg_ctx_create_nccl(int device, int rank, int world, const unsigned char* id
 }
 
 int bmg_nccl_unique_id(unsigned char* id128) {
-  return guard([&] {
-    ncclUniqueId id;
-    nccl_check(ncclGetUniqueId(&id), "ncclGetUniqueId");
-    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
-    std::memcpy(id128, &id, sizeof(id));
-  });
+  return guard([&] { nccl_unique_id(id128); });
 }
 
 }  // extern "C"

@@ -144,6 +144,9 @@ _SIGS = {
     "bmg_time_residual": (_I, [_P, _P, _P, _P, _I, _PD]),
     "bmg_nccl_unique_id": (_I, [C.c_char_p]),
     "bmg_ctx_create_nccl": (_I, [_I, _I, _I, C.c_char_p, _PP]),
+    "bmg_loopback_create": (_I, [_I, _PP]),
+    "bmg_loopback_destroy": (_I, [_P]),
+    "bmg_ctx_create_loopback": (_I, [_I, _P, _I, _PP]),
     "bmg_hier_partition": (_I, [_P, _I, _I, _PI32, _I]),
     "bmg_dist_plan": (_I, [_I, _PI32, _PI32, _PI32, _I, _I, C.POINTER(SetupParams), _PI32, _PI32, _PI32, _PI32]),
     "bmg_hier_setup_dist": (_I, [_P, _I, _PI32, _PI32, _I, _P, _PP, C.POINTER(SetupParams), _PP]),
