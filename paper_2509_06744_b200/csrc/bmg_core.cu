@@ -365,6 +365,28 @@ static void validate_structure(int nbr, int nbc, const int64_t* row_ptr, const i
   }
 }
 
+BlkView blk_view(const Bsr& a) {
+  BlkView v;
+  v.bs = a.bs;
+  v.mr = a.mr;
+  v.mc = a.mc;
+  if (!a.uniform) {
+    v.voff = a.voff.p;
+    v.rsz = a.d_rsz.p;
+    v.csz = a.d_csz.p;
+    v.roff = a.d_roff.p;
+    v.coff = a.d_coff.p;
+  }
+  return v;
+}
+
+int max_block(const Bsr& a) {
+  int m = 1;
+  for (int x : a.rsz) m = std::max(m, x);
+  for (int x : a.csz) m = std::max(m, x);
+  return m;
+}
+
 std::unique_ptr<Bsr> make_bsr_structure(Ctx* ctx, int nbr, const int* rsz, int nbc, const int* csz,
                                         std::vector<int64_t> row_ptr, std::vector<int32_t> col,
                                         bool sym) {

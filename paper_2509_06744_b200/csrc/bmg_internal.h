@@ -135,6 +135,28 @@ struct Bsr {
   int64_t device_bytes() const;
 };
 
+// Device view of a block layout for the setup kernels: uniform layouts address
+// block q at q * bs with m_r x m_c blocks; variable layouts through per-block
+// value offsets and per-row / per-column sizes and scalar offsets.
+struct BlkView {
+  const int64_t* voff = nullptr;  // nullptr: q * bs
+  int bs = 0;
+  const int* rsz = nullptr;  // nullptr: mr
+  const int* csz = nullptr;  // nullptr: mc
+  const int* roff = nullptr;
+  const int* coff = nullptr;
+  int mr = 0, mc = 0;
+#ifdef __CUDACC__
+  __device__ __forceinline__ int64_t off(int64_t q) const { return voff ? voff[q] : q * bs; }
+  __device__ __forceinline__ int r(int i) const { return rsz ? rsz[i] : mr; }
+  __device__ __forceinline__ int c(int j) const { return csz ? csz[j] : mc; }
+  __device__ __forceinline__ int64_t ro(int i) const { return roff ? (int64_t)roff[i] : (int64_t)i * mr; }
+  __device__ __forceinline__ int64_t co(int j) const { return coff ? (int64_t)coff[j] : (int64_t)j * mc; }
+#endif
+};
+BlkView blk_view(const struct Bsr& a);
+int max_block(const struct Bsr& a);
+
 struct Vec {
   Ctx* ctx = nullptr;
   int64_t n = 0;

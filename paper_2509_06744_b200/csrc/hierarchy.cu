@@ -26,17 +26,21 @@
 namespace bmg {
 namespace kern {
 
-__global__ void bsr_to_dense_kernel(const double* __restrict__ vals, const int64_t* __restrict__ row_ptr,
-                                    const int32_t* __restrict__ col, int nbr, int m, int bs,
-                                    double* __restrict__ dense, int64_t N) {
-  for (int i = blockIdx.x; i < nbr; i += gridDim.x)
+__global__ void bsr_to_dense_kernel(const double* __restrict__ vals, BlkView V, const int64_t* __restrict__ row_ptr,
+                                    const int32_t* __restrict__ col, int nbr, double* __restrict__ dense, int64_t N) {
+  for (int i = blockIdx.x; i < nbr; i += gridDim.x) {
+    const int rows = V.r(i);
+    const int64_t ro = V.ro(i);
     for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
       const int j = col[p];
-      for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-        const int r = e / m, c = e - r * m;
-        dense[((int64_t)i * m + r) * N + (int64_t)j * m + c] = vals[p * bs + e];
+      const int cols = V.c(j);
+      const int64_t co = V.co(j), off = V.off(p);
+      for (int e = threadIdx.x; e < rows * cols; e += blockDim.x) {
+        const int r = e / cols, c = e - r * cols;
+        dense[(ro + r) * N + co + c] = vals[off + e];
       }
     }
+  }
 }
 
 __global__ void symmetrize_dense_kernel(double* a, int64_t N) {
@@ -175,9 +179,10 @@ struct PLevel {  // one (virtual) rank's share of one level
   std::vector<SplitMat> sF, sB;        // FSAI chain factors and their transposes
   SmootherSpec spec;  // Level::smoother (multilevel.hpp:25)
   DBuf<double> v[VNUM];
-  int64_t off() const { return (int64_t)(lo - wlo) * m; }
-  int64_t n_own() const { return (int64_t)(hi - lo) * m; }
-  int64_t n_win() const { return (int64_t)(whi - wlo) * m; }
+  int64_t dim = 0;        // scalar length (variable layouts: m = 0, whole levels only)
+  int64_t off() const { return m ? (int64_t)(lo - wlo) * m : 0; }
+  int64_t n_own() const { return m ? (int64_t)(hi - lo) * m : dim; }
+  int64_t n_win() const { return m ? (int64_t)(whi - wlo) * m : dim; }
   bool active() const { return hi > lo; }
 };
 
@@ -511,13 +516,13 @@ static void run_vcycle(Hier& h, int kpre, int kpost, const double* bf, double* x
 static void coarse_factor(Hier& h, Part& p) {
   Ctx* ctx = h.ctx;
   const Bsr& a0 = *p.lv[0].A;
-  if (!(a0.uniform && a0.mr == a0.mc)) fail(BMG_EINVAL, "coarse solve: uniform block sizes required");
+  if (!(a0.rsz == a0.csz)) fail(BMG_EINVAL, "coarse solve: square block layout required");
   const int64_t N = a0.dim_r;
   h.n0 = N;
   p.ainv.alloc(std::max<int64_t>(N * N, 1));
   BMG_CUDA(cudaMemsetAsync(p.ainv.p, 0, p.ainv.bytes(), ctx->stream));
   kern::bsr_to_dense_kernel<<<std::max(1, std::min(a0.nbr, ctx->sms * 8)), 128, 0, ctx->stream>>>(
-      a0.vals.p, a0.row_ptr.p, a0.col.p, a0.nbr, a0.mr, a0.bs, p.ainv.p, N);
+      a0.vals.p, blk_view(a0), a0.row_ptr.p, a0.col.p, a0.nbr, p.ainv.p, N);
   ctx->count();
   BMG_CUDA(cudaGetLastError());
   cusolverDnHandle_t s = ctx->cusolver();
@@ -588,12 +593,13 @@ static void finish_whole(Hier& h, int cap) {
   h.msz.assign(L, 0);
   for (int l = 0; l < L; ++l) {
     PLevel& lv = p.lv[l];
-    if (!(lv.A->uniform && lv.A->mr == lv.A->mc)) fail(BMG_EINVAL, "hierarchy: uniform square blocks required");
+    if (!(lv.A->rsz == lv.A->csz)) fail(BMG_EINVAL, "hierarchy: square block layouts required");
     h.nbr[l] = lv.A->nbr;
-    h.msz[l] = lv.A->mr;
+    h.msz[l] = lv.A->uniform ? lv.A->mr : 0;  // 0: variable block sizes
     lv.lo = lv.wlo = 0;
     lv.hi = lv.whi = lv.A->nbr;
-    lv.m = lv.A->mr;
+    lv.m = h.msz[l];
+    lv.dim = lv.A->dim_r;
   }
   const int64_t n0 = p.lv[0].A->dim_r;
   if (n0 > cap) fail(BMG_EINVAL, "setup: coarsest level exceeds the dense-solve cap");
@@ -698,6 +704,8 @@ static SplitMat split_rows(const Bsr& g, int lo, int hi, int wlo, int nwin, int 
 static void partition(Hier& h, int world, int rank, const int32_t* granule, int agglomerate) {
   if (!h.whole()) fail(BMG_EINVAL, "partition: hierarchy is already partitioned");
   if (world < 1) fail(BMG_EINVAL, "partition: world must be >= 1");
+  for (int m : h.msz)
+    if (m == 0) fail(BMG_EINVAL, "partition: variable block layouts are not supported (uniform levels only)");
   if (world == 1) {  // nothing to split; record the norm segmentation so 1-rank
                      // and N-rank residual norms are summed identically
     h.granule_top = granule ? std::max(1, granule[h.finest()]) : 1;
@@ -801,16 +809,19 @@ static double finest_norm(Hier& h, const double* r_whole) {
   const int top = h.finest();
   const int m = h.msz[top];
   const int gran = h.granule_top;
-  const int nseg = (h.nbr[top] + gran - 1) / gran;
-  if (h.seg.n < (size_t)nseg) h.seg.alloc(nseg);
+  // variable layouts (whole levels only): fixed 256-scalar segments
+  const int64_t dimv = m ? 0 : h.parts[0].lv[top].dim;
+  const int nseg = m ? (h.nbr[top] + gran - 1) / gran : (int)((dimv + 255) / 256);
+  if (h.seg.n < (size_t)nseg) h.seg.alloc(std::max(nseg, 1));
   BMG_CUDA(cudaMemsetAsync(h.seg.p, 0, nseg * sizeof(double), ctx->stream));
   for (Part& p : h.parts) {
     PLevel& L = p.lv[top];
     if (!L.active()) continue;
     const double* r = h.whole() ? r_whole : L.v[VR].p + L.off();
-    const int s0 = L.lo / gran;
-    const int ns = (L.hi - L.lo + gran - 1) / gran;
-    kern::segment_sq_kernel<<<ns, 256, 0, ctx->stream>>>(r, L.n_own(), (int64_t)gran * m, h.seg.p + s0);
+    const int s0 = m ? L.lo / gran : 0;
+    const int ns = m ? (L.hi - L.lo + gran - 1) / gran : nseg;
+    if (ns == 0) continue;
+    kern::segment_sq_kernel<<<ns, 256, 0, ctx->stream>>>(r, L.n_own(), m ? (int64_t)gran * m : 256, h.seg.p + s0);
     ctx->count();
     BMG_CUDA(cudaGetLastError());
   }
@@ -1605,7 +1616,8 @@ void need_len(const Vec* v, int64_t n, const char* what) {
 // length of the finest-level vectors the caller passes
 int64_t finest_len(const Hier& h) {
   const int top = h.finest();
-  if (h.whole() || h.emulated) return (int64_t)h.nbr[top] * h.msz[top];
+  if (h.whole()) return h.parts[0].lv[top].n_own();
+  if (h.emulated) return (int64_t)h.nbr[top] * h.msz[top];
   return h.parts[0].lv[top].n_own();
 }
 }  // namespace

@@ -18,40 +18,62 @@ namespace kern {
 // out = pairs-accumulated block products (Galerkin numeric phase):
 // out[o] = sum over pairs (in order) of a_blk * b_blk   (kernels.cpp:71)
 //                                   or a_blk^T * b_blk  (kernels.cpp:82)
-__global__ void pair_gemm_kernel(const double* __restrict__ A, const double* __restrict__ B,
-                                 const int64_t* __restrict__ pair_ptr,
-                                 const int2* __restrict__ pairs, double* __restrict__ out,
-                                 int64_t nout, int m, int bs_a, int bs_b, int bs_o, int mode) {
-  const int r = threadIdx.x / m, c = threadIdx.x - (threadIdx.x / m) * m;
-  if (r >= m) return;
-  for (int64_t o = blockIdx.x; o < nout; o += gridDim.x) {
+// Output block o (rows i = orow[o], cols j = ocol[o]) = sum over its ordered
+// pairs of a_x (op) b_y; all blocks on one square layout with sizes `sz`
+// (nullptr: uniform m).  Inner size: the column of operand-A block x (acol[x]).
+struct PairArgs {
+  const double* A;
+  const int64_t* Aoff;  // nullptr: x * bs
+  const int32_t* acol;
+  const double* B;
+  const int64_t* Boff;
+  const int64_t* pair_ptr;
+  const int2* pairs;
+  double* out;
+  const int64_t* Ooff;
+  const int32_t* orow;
+  const int32_t* ocol;
+  const int* sz;
+  int64_t nout;
+  int m, bs, M, mode;
+};
+__global__ void pair_gemm_kernel(PairArgs g) {
+  const int r = threadIdx.x / g.M, c = threadIdx.x - (threadIdx.x / g.M) * g.M;
+  for (int64_t o = blockIdx.x; o < g.nout; o += gridDim.x) {
+    const int rows = g.sz ? g.sz[g.orow[o]] : g.m, cols = g.sz ? g.sz[g.ocol[o]] : g.m;
+    if (r >= rows || c >= cols) continue;
     double acc = 0.0;
-    for (int64_t q = pair_ptr[o]; q < pair_ptr[o + 1]; ++q) {
-      const int2 pr = pairs[q];
-      const double* a = A + (int64_t)pr.x * bs_a;
-      const double* b = B + (int64_t)pr.y * bs_b;
+    for (int64_t q = g.pair_ptr[o]; q < g.pair_ptr[o + 1]; ++q) {
+      const int2 pr = g.pairs[q];
+      const int K = g.sz ? g.sz[g.acol[pr.x]] : g.m;
+      const double* a = g.A + (g.Aoff ? g.Aoff[pr.x] : (int64_t)pr.x * g.bs);
+      const double* b = g.B + (g.Boff ? g.Boff[pr.y] : (int64_t)pr.y * g.bs);
       double t = 0.0;
-      if (mode == 1)  // a^T b  (kernels.cpp:82)
-        for (int k = 0; k < m; ++k) t = __fma_rn(a[k * m + r], b[k * m + c], t);
-      else if (mode == 2)  // a b^T  (kernels.cpp:108)
-        for (int k = 0; k < m; ++k) t = __fma_rn(a[r * m + k], b[c * m + k], t);
+      if (g.mode == 1)  // a^T b  (kernels.cpp:82)
+        for (int k = 0; k < K; ++k) t = __fma_rn(a[k * rows + r], b[k * cols + c], t);
+      else if (g.mode == 2)  // a b^T  (kernels.cpp:108)
+        for (int k = 0; k < K; ++k) t = __fma_rn(a[r * K + k], b[c * K + k], t);
       else  // a b  (kernels.cpp:71)
-        for (int k = 0; k < m; ++k) t = __fma_rn(a[r * m + k], b[k * m + c], t);
+        for (int k = 0; k < K; ++k) t = __fma_rn(a[r * K + k], b[k * cols + c], t);
       acc = __dadd_rn(acc, t);
     }
-    out[o * bs_o + r * m + c] = acc;
+    g.out[(g.Ooff ? g.Ooff[o] : o * g.bs) + r * cols + c] = acc;
   }
 }
 
-// out(I,J)[r][c] = 0.5 * (C_IJ[r][c] + C_JI[c][r])   (multilevel.cpp:16-26)
+// out(I,J)[r][c] = 0.5 * (C_IJ[r][c] + C_JI[c][r])   (multilevel.cpp:16-26);
+// C and out share the layout `L` (block rows `brow`, columns `bcol`)
 __global__ void symmetrize_kernel(const double* __restrict__ C, const int64_t* __restrict__ tpos,
-                                  double* __restrict__ out, int64_t nblk, int m, int bs) {
-  const int r = threadIdx.x / m, c = threadIdx.x - (threadIdx.x / m) * m;
-  if (r >= m) return;
+                                  double* __restrict__ out, int64_t nblk, BlkView L, const int32_t* __restrict__ brow,
+                                  const int32_t* __restrict__ bcol, int M) {
+  const int r = threadIdx.x / M, c = threadIdx.x - (threadIdx.x / M) * M;
   for (int64_t o = blockIdx.x; o < nblk; o += gridDim.x) {
+    const int rows = L.rsz ? L.r(brow[o]) : L.mr, cols = L.csz ? L.c(bcol[o]) : L.mc;
+    if (r >= rows || c >= cols) continue;
     const int64_t t = tpos[o];
-    const double v = C[o * bs + r * m + c];
-    out[o * bs + r * m + c] = t >= 0 ? __dmul_rn(0.5, __dadd_rn(v, C[t * bs + c * m + r])) : __dmul_rn(v, 0.5);
+    const double v = C[L.off(o) + r * cols + c];
+    out[L.off(o) + r * cols + c] =
+        t >= 0 ? __dmul_rn(0.5, __dadd_rn(v, C[L.off(t) + c * rows + r])) : __dmul_rn(v, 0.5);
   }
 }
 
@@ -156,22 +178,72 @@ Product symbolic(int nrows, const LeftRow& left, const std::vector<int64_t>& yrp
   return out;
 }
 
-void pair_gemm(Ctx* ctx, const double* A, int bs_a, const double* B, int bs_b, const Product& pr, double* out,
-               int bs_o, int m, int mode) {
+// operands / output of one pair product on a square layout
+struct PairSide {
+  const double* vals;
+  const int64_t* off;  // device offsets or nullptr (uniform)
+};
+void pair_gemm(Ctx* ctx, PairSide A, const int32_t* acol, PairSide B, const Product& pr, PairSide out,
+               const Bsr& layout, int mode) {
   const int64_t nout = (int64_t)pr.col.size();
   if (nout == 0) return;
+  const bool uni = layout.uniform;
   DBuf<int64_t> pp(pr.pair_ptr.size());
   DBuf<int2> pairs(std::max<size_t>(pr.pairs.size(), 1));
   BMG_CUDA(cudaMemcpy(pp.p, pr.pair_ptr.data(), pr.pair_ptr.size() * 8, cudaMemcpyHostToDevice));
   if (!pr.pairs.empty())
     BMG_CUDA(cudaMemcpy(pairs.p, pr.pairs.data(), pr.pairs.size() * sizeof(int2), cudaMemcpyHostToDevice));
-  const int threads = ((m * m + 31) / 32) * 32;
+  DBuf<int32_t> orow, ocol;
+  DBuf<int> sz;
+  if (!uni) {
+    std::vector<int32_t> rr(nout);
+    for (size_t i = 0; i + 1 < pr.row_ptr.size(); ++i)
+      for (int64_t q = pr.row_ptr[i]; q < pr.row_ptr[i + 1]; ++q) rr[q] = (int32_t)i;
+    orow.alloc(nout);
+    ocol.alloc(nout);
+    sz.alloc(layout.rsz.size());
+    BMG_CUDA(cudaMemcpy(orow.p, rr.data(), nout * 4, cudaMemcpyHostToDevice));
+    BMG_CUDA(cudaMemcpy(ocol.p, pr.col.data(), nout * 4, cudaMemcpyHostToDevice));
+    BMG_CUDA(cudaMemcpy(sz.p, layout.rsz.data(), layout.rsz.size() * 4, cudaMemcpyHostToDevice));
+  }
+  const int M = max_block(layout);
+  kern::PairArgs g;
+  g.A = A.vals;
+  g.Aoff = uni ? nullptr : A.off;
+  g.acol = acol;
+  g.B = B.vals;
+  g.Boff = uni ? nullptr : B.off;
+  g.pair_ptr = pp.p;
+  g.pairs = pairs.p;
+  g.out = const_cast<double*>(out.vals);
+  g.Ooff = uni ? nullptr : out.off;
+  g.orow = orow.p;
+  g.ocol = ocol.p;
+  g.sz = uni ? nullptr : sz.p;
+  g.nout = nout;
+  g.m = layout.mr;
+  g.bs = layout.bs;
+  g.M = M;
+  g.mode = mode;
+  const int threads = ((M * M + 31) / 32) * 32;
   const int grid = (int)std::min<int64_t>(nout, (int64_t)ctx->sms * 32);
-  kern::pair_gemm_kernel<<<grid, threads, 0, ctx->stream>>>(A, B, pp.p, pairs.p, out, nout, m, bs_a, bs_b, bs_o,
-                                                            mode);
+  kern::pair_gemm_kernel<<<grid, threads, 0, ctx->stream>>>(g);
   ctx->count();
   BMG_CUDA(cudaGetLastError());
   BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+// unpadded offsets of a product's blocks on a square layout
+std::vector<int64_t> product_offsets(const Product& pr, const std::vector<int>& sz) {
+  std::vector<int64_t> off(pr.col.size() + 1, 0);
+  int64_t v = 0;
+  for (size_t i = 0; i + 1 < pr.row_ptr.size(); ++i)
+    for (int64_t q = pr.row_ptr[i]; q < pr.row_ptr[i + 1]; ++q) {
+      off[q] = v;
+      v += (int64_t)sz[i] * sz[pr.col[q]];
+    }
+  off[pr.col.size()] = v;
+  return off;
 }
 
 }  // namespace
@@ -197,14 +269,15 @@ __device__ __forceinline__ int64_t find_in(const int32_t* __restrict__ col, int6
   return lo;
 }
 
-// AP rows [f0, f1): CTA per (fine row, output block); thread per block entry
-__global__ void ap_chunk_kernel(const double* __restrict__ Av, const int64_t* __restrict__ Arp,
-                                const int32_t* __restrict__ Acol, int bs_a, const double* __restrict__ Pv,
-                                const int64_t* __restrict__ Prp, const int32_t* __restrict__ Pcol, int bs_p,
+// AP rows [f0, f1): CTA per (fine row, output block); thread per block entry.
+// AP block q (fine row i, coarse column J) is m_i x mc_J at APv + APo(q - apbase).
+__global__ void ap_chunk_kernel(const double* __restrict__ Av, BlkView A, const int64_t* __restrict__ Arp,
+                                const int32_t* __restrict__ Acol, const double* __restrict__ Pv, BlkView P,
+                                const int64_t* __restrict__ Prp, const int32_t* __restrict__ Pcol,
                                 const int64_t* __restrict__ APrp, const int32_t* __restrict__ APcol, int f0, int f1,
-                                int64_t apbase, double* __restrict__ APv, int bs_o, int m) {
-  const int r = threadIdx.x / m, c = threadIdx.x - (threadIdx.x / m) * m;
-  const bool act = r < m;
+                                int64_t apbase, const int64_t* __restrict__ APoff, int bs_o, double* __restrict__ APv,
+                                int M) {
+  const int r = threadIdx.x / M, c = threadIdx.x - (threadIdx.x / M) * M;
   const int64_t q0 = APrp[f0], q1 = APrp[f1];
   for (int64_t q = q0 + blockIdx.x; q < q1; q += gridDim.x) {
     // fine row of output block q (binary search over APrp[f0..f1])
@@ -218,32 +291,34 @@ __global__ void ap_chunk_kernel(const double* __restrict__ Av, const int64_t* __
     }
     const int i = lo;
     const int J = APcol[q];
+    const int rows = A.r(i), cols = P.c(J);
+    const bool act = r < rows && c < cols;
     double acc = 0.0;
     for (int64_t pa = Arp[i]; pa < Arp[i + 1]; ++pa) {
       const int k = Acol[pa];
       const int64_t pp = find_in(Pcol, Prp[k], Prp[k + 1], J);
       if (pp >= Prp[k + 1] || Pcol[pp] != J) continue;
       if (act) {
-        const double* a = Av + pa * bs_a;
-        const double* b = Pv + pp * bs_p;
+        const int mk = A.c(k);
+        const double* a = Av + A.off(pa);
+        const double* b = Pv + P.off(pp);
         double t = 0.0;
-        for (int z = 0; z < m; ++z) t = __fma_rn(a[r * m + z], b[z * m + c], t);
+        for (int z = 0; z < mk; ++z) t = __fma_rn(a[r * mk + z], b[z * cols + c], t);
         acc = __dadd_rn(acc, t);
       }
     }
-    if (act) APv[(q - apbase) * bs_o + r * m + c] = acc;
+    if (act) APv[(APoff ? APoff[q] - APoff[apbase] : (q - apbase) * bs_o) + r * cols + c] = acc;
   }
 }
 
 // C_IJ += sum over fine rows i in [f0, f1) of P_iI^T AP_iJ (ascending i), coarse rows [I0, I1)
-__global__ void c_accum_kernel(const double* __restrict__ Pv, int bs_p, const int64_t* __restrict__ PTrp,
+__global__ void c_accum_kernel(const double* __restrict__ Pv, BlkView P, const int64_t* __restrict__ PTrp,
                                const int32_t* __restrict__ PTrow, const int64_t* __restrict__ PTblk,
                                const int64_t* __restrict__ APrp, const int32_t* __restrict__ APcol,
-                               const double* __restrict__ APv, int64_t apbase, int bs_ap,
-                               const int64_t* __restrict__ Crp, const int32_t* __restrict__ Ccol, int I0, int I1,
-                               int f0, int f1, double* __restrict__ Cv, int bs_c, int m) {
-  const int r = threadIdx.x / m, c = threadIdx.x - (threadIdx.x / m) * m;
-  const bool act = r < m;
+                               const double* __restrict__ APv, int64_t apbase, const int64_t* __restrict__ APoff,
+                               int bs_ap, const int64_t* __restrict__ Crp, const int32_t* __restrict__ Ccol, int I0,
+                               int I1, int f0, int f1, double* __restrict__ Cv, BlkView Cl, int M) {
+  const int r = threadIdx.x / M, c = threadIdx.x - (threadIdx.x / M) * M;
   const int64_t o0 = Crp[I0], o1 = Crp[I1];
   for (int64_t o = o0 + blockIdx.x; o < o1; o += gridDim.x) {
     int lo = I0, hi = I1 - 1;
@@ -256,7 +331,10 @@ __global__ void c_accum_kernel(const double* __restrict__ Pv, int bs_p, const in
     }
     const int I = lo;
     const int J = Ccol[o];
-    double acc = act ? Cv[o * bs_c + r * m + c] : 0.0;
+    const int rows = P.c(I), cols = P.c(J);
+    const bool act = r < rows && c < cols;
+    double* cb = Cv + Cl.off(o);
+    double acc = act ? cb[r * cols + c] : 0.0;
     bool any = false;
     // fine rows of coarse column I inside the chunk (ascending)
     int64_t t0 = PTrp[I], t1 = PTrp[I + 1];
@@ -267,14 +345,15 @@ __global__ void c_accum_kernel(const double* __restrict__ Pv, int bs_p, const in
       if (q >= APrp[i + 1] || APcol[q] != J) continue;
       any = true;
       if (act) {
-        const double* p = Pv + PTblk[t] * bs_p;
-        const double* ap = APv + (q - apbase) * bs_ap;
+        const int mi = P.r(i);
+        const double* p = Pv + P.off(PTblk[t]);
+        const double* ap = APv + (APoff ? APoff[q] - APoff[apbase] : (q - apbase) * bs_ap);
         double s = 0.0;
-        for (int z = 0; z < m; ++z) s = __fma_rn(p[z * m + r], ap[z * m + c], s);
+        for (int z = 0; z < mi; ++z) s = __fma_rn(p[z * rows + r], ap[z * cols + c], s);
         acc = __dadd_rn(acc, s);
       }
     }
-    if (any && act) Cv[o * bs_c + r * m + c] = acc;
+    if (any && act) cb[r * cols + c] = acc;
   }
 }
 
@@ -282,10 +361,11 @@ __global__ void c_accum_kernel(const double* __restrict__ Pv, int bs_p, const in
 
 std::unique_ptr<Bsr> galerkin(const Bsr& a, const Bsr& p) {
   if (!(a.rsz == a.csz) || !(a.rsz == p.rsz)) fail(BMG_EINVAL, "galerkin_coarsen: layouts do not match");
-  if (!(a.uniform && p.uniform && a.mr == p.mc))
-    fail(BMG_EINVAL, "device galerkin_coarsen: uniform square block sizes required");
   Ctx* ctx = a.ctx;
-  const int m = a.mr, bs = a.bs, nf = a.nbr, nc = p.nbc;
+  const bool uni = a.uniform && p.uniform && a.mr == p.mc;  // C keeps P's column layout
+  const int nf = a.nbr, nc = p.nbc;
+  const int M = std::max(max_block(a), max_block(p));
+  if (M > 32) fail(BMG_EINVAL, "device galerkin_coarsen: block sizes above 32 are not supported");
   // ---- symbolic (host): AP rows, P^T index, C rows, transpose positions
   std::vector<int64_t> aprp(nf + 1, 0);
   std::vector<std::vector<int32_t>> aprow(nf);
@@ -362,18 +442,38 @@ std::unique_ptr<Bsr> galerkin(const Bsr& a, const Bsr& p) {
   up64(crp, d_crp);
   up32(ccol, d_ccol);
   const int64_t nblk = (int64_t)ccol.size();
-  DBuf<double> cv(std::max<int64_t>(nblk * bs, 2));
+  // A_c's structure (P's column layout) first: C accumulates in the same layout
+  auto out = make_bsr_structure(ctx, nc, p.csz.data(), nc, p.csz.data(), crp, ccol, true);
+  const BlkView Av = blk_view(a), Pv = blk_view(p), Cv = blk_view(*out);
+  DBuf<double> cv(std::max<int64_t>(out->h_voff[nblk], 2));
   BMG_CUDA(cudaMemset(cv.p, 0, cv.bytes()));
-  // ---- chunks of fine rows, AP chunk within a memory budget
-  const int64_t budget_blocks = std::max<int64_t>(1, ((int64_t)4 << 30) / ((int64_t)bs * 8));
-  const int threads = ((m * m + 31) / 32) * 32;
+  // A P block offsets (m_i x mc_J; uniform: padded stride bs)
+  const int bs = uni ? a.bs : 0;
+  std::vector<int64_t> apoff;
+  if (!uni) {
+    apoff.resize(aprp[nf] + 1);
+    int64_t v = 0;
+    for (int i = 0; i < nf; ++i)
+      for (int64_t q = aprp[i]; q < aprp[i + 1]; ++q) {
+        apoff[q] = v;
+        v += (int64_t)a.rsz[i] * p.csz[apcol[q]];
+      }
+    apoff[aprp[nf]] = v;
+  }
+  auto ap_doubles = [&](int64_t q0, int64_t q1) { return uni ? (q1 - q0) * bs : apoff[q1] - apoff[q0]; };
+  DBuf<int64_t> d_apoff;
+  up64(apoff, d_apoff);
+  // ---- chunks of fine rows, AP chunk within a memory budget (4 GB)
+  const int64_t budget = (int64_t)1 << 29;  // doubles
+  const int threads = ((M * M + 31) / 32) * 32;
   DBuf<double> apv;
   int f0 = 0;
   while (f0 < nf) {
     int f1 = f0 + 1;
-    while (f1 < nf && aprp[f1 + 1] - aprp[f0] <= budget_blocks) ++f1;
+    while (f1 < nf && ap_doubles(aprp[f0], aprp[f1 + 1]) <= budget) ++f1;
     const int64_t napb = aprp[f1] - aprp[f0];
-    if (apv.n < (size_t)(napb * bs)) apv.alloc(std::max<int64_t>(napb * bs, 2));
+    const int64_t napd = ap_doubles(aprp[f0], aprp[f1]);
+    if (apv.n < (size_t)napd) apv.alloc(std::max<int64_t>(napd, 2));
     // coarse rows touched by this chunk
     int I0 = nc, I1 = 0;
     for (int64_t q = p.h_row_ptr[f0]; q < p.h_row_ptr[f1]; ++q) {
@@ -382,15 +482,16 @@ std::unique_ptr<Bsr> galerkin(const Bsr& a, const Bsr& p) {
     }
     if (napb > 0) {
       kern::ap_chunk_kernel<<<(int)std::min<int64_t>(napb, (int64_t)ctx->sms * 64), threads, 0, ctx->stream>>>(
-          a.vals.p, a.row_ptr.p, a.col.p, bs, p.vals.p, p.row_ptr.p, p.col.p, p.bs, d_aprp.p, d_apcol.p, f0, f1,
-          aprp[f0], apv.p, bs, m);
+          a.vals.p, Av, a.row_ptr.p, a.col.p, p.vals.p, Pv, p.row_ptr.p, p.col.p, d_aprp.p, d_apcol.p, f0, f1,
+          aprp[f0], uni ? nullptr : d_apoff.p, bs, apv.p, M);
       ctx->count();
       BMG_CUDA(cudaGetLastError());
     }
     if (I1 > I0 && crp[I1] > crp[I0]) {
       kern::c_accum_kernel<<<(int)std::min<int64_t>(crp[I1] - crp[I0], (int64_t)ctx->sms * 64), threads, 0,
-                             ctx->stream>>>(p.vals.p, p.bs, d_ptrp.p, d_ptrow.p, d_ptblk.p, d_aprp.p, d_apcol.p,
-                                            apv.p, aprp[f0], bs, d_crp.p, d_ccol.p, I0, I1, f0, f1, cv.p, bs, m);
+                             ctx->stream>>>(p.vals.p, Pv, d_ptrp.p, d_ptrow.p, d_ptblk.p, d_aprp.p, d_apcol.p,
+                                            apv.p, aprp[f0], uni ? nullptr : d_apoff.p, bs, d_crp.p, d_ccol.p, I0,
+                                            I1, f0, f1, cv.p, Cv, M);
       ctx->count();
       BMG_CUDA(cudaGetLastError());
     }
@@ -399,12 +500,17 @@ std::unique_ptr<Bsr> galerkin(const Bsr& a, const Bsr& p) {
   }
   apv.release();
   // ---- A_c = (C + C^T)/2 blockwise (multilevel.cpp:16-26)
-  std::vector<int> csz(nc, m);
-  auto out = make_bsr_structure(ctx, nc, csz.data(), nc, csz.data(), crp, ccol, true);
   up64(tpos, d_tpos);
+  DBuf<int32_t> d_crow;
+  if (!uni) {
+    std::vector<int32_t> crow_of(nblk);
+    for (int I = 0; I < nc; ++I)
+      for (int64_t q = crp[I]; q < crp[I + 1]; ++q) crow_of[q] = I;
+    up32(crow_of, d_crow);
+  }
   if (nblk) {
     kern::symmetrize_kernel<<<(int)std::min<int64_t>(nblk, (int64_t)ctx->sms * 32), threads, 0, ctx->stream>>>(
-        cv.p, d_tpos.p, out->vals.p, nblk, m, bs);
+        cv.p, d_tpos.p, out->vals.p, nblk, Cv, uni ? nullptr : d_crow.p, d_ccol.p, M);
     ctx->count();
     BMG_CUDA(cudaGetLastError());
   }
@@ -418,36 +524,44 @@ std::unique_ptr<Bsr> galerkin(const Bsr& a, const Bsr& p) {
 // 0.5 (blk + blk^T), blocks with zero squared norm dropped, stored with both
 // halves.  Symbolic phase on the host, numeric on the device.
 namespace kern {
-__global__ void sym_diag_sqnorm_kernel(double* __restrict__ L, const int64_t* __restrict__ diag_of,
-                                       int64_t nblk, int m, int bs, int* __restrict__ nonzero) {
+// lower block o (row i, column j): symmetrise diagonal blocks, flag nonzero ones
+__global__ void sym_diag_sqnorm_kernel(double* __restrict__ L, const int64_t* __restrict__ Loff,
+                                       const int64_t* __restrict__ diag_of, const int32_t* __restrict__ orow,
+                                       const int32_t* __restrict__ ocol, const int* __restrict__ sz, int64_t nblk,
+                                       int m, int bs, int* __restrict__ nonzero) {
   for (int64_t o = blockIdx.x; o < nblk; o += gridDim.x) {
-    double* b = L + o * bs;
+    double* b = L + (Loff ? Loff[o] : o * bs);
+    const int rows = sz ? sz[orow[o]] : m, cols = sz ? sz[ocol[o]] : m;
     if (diag_of[o]) {
-      __shared__ double tmp[441];
-      for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-        const int r = e / m, c = e - r * m;
-        tmp[e] = __dmul_rn(0.5, __dadd_rn(b[r * m + c], b[c * m + r]));
+      __shared__ double tmp[64 * 64];
+      for (int e = threadIdx.x; e < rows * rows; e += blockDim.x) {
+        const int r = e / rows, c = e - r * rows;
+        tmp[e] = __dmul_rn(0.5, __dadd_rn(b[r * rows + c], b[c * rows + r]));
       }
       __syncthreads();
-      for (int e = threadIdx.x; e < m * m; e += blockDim.x) b[e] = tmp[e];
+      for (int e = threadIdx.x; e < rows * rows; e += blockDim.x) b[e] = tmp[e];
       __syncthreads();
     }
     if (threadIdx.x == 0) {
       double sq = 0.0;
-      for (int e = 0; e < m * m; ++e) sq = __dadd_rn(sq, __dmul_rn(b[e], b[e]));
+      for (int e = 0; e < rows * cols; ++e) sq = __dadd_rn(sq, __dmul_rn(b[e], b[e]));
       nonzero[o] = sq != 0.0;
     }
     __syncthreads();
   }
 }
-__global__ void gather_blocks_kernel(const double* __restrict__ src, const int64_t* __restrict__ from,
-                                     const int* __restrict__ trans, double* __restrict__ dst, int64_t nblk, int m,
-                                     int bs) {
+// out block o (row i, col j) = lower block from[o] (or its transpose)
+__global__ void gather_blocks_kernel(const double* __restrict__ src, const int64_t* __restrict__ Soff,
+                                     const int64_t* __restrict__ from, const int* __restrict__ trans,
+                                     double* __restrict__ dst, BlkView D, const int32_t* __restrict__ orow,
+                                     const int32_t* __restrict__ ocol, int64_t nblk, int m, int bs) {
   for (int64_t o = blockIdx.x; o < nblk; o += gridDim.x) {
-    const double* s = src + from[o] * bs;
-    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-      const int r = e / m, c = e - r * m;
-      dst[o * bs + e] = trans[o] ? s[c * m + r] : s[e];
+    const double* s = src + (Soff ? Soff[from[o]] : from[o] * bs);
+    const int rows = D.rsz ? D.r(orow[o]) : m, cols = D.csz ? D.c(ocol[o]) : m;
+    double* d = dst + D.off(o);
+    for (int e = threadIdx.x; e < rows * cols; e += blockDim.x) {
+      const int r = e / cols, c = e - r * cols;
+      d[e] = trans[o] ? s[c * rows + r] : s[e];
     }
   }
 }
@@ -457,9 +571,10 @@ std::unique_ptr<Bsr> triple_product(const Bsr& f, const Bsr& a) {
   if (!(f.rsz == f.csz && a.rsz == a.csz && f.rsz == a.rsz))
     fail(BMG_EINVAL, "triple_product: layouts must be square and compatible");
   if (!a.sym) fail(BMG_EINVAL, "triple_product: A must be symmetric");
-  if (!(a.uniform && f.uniform)) fail(BMG_EINVAL, "device triple_product: uniform block sizes required");
   Ctx* ctx = a.ctx;
+  const bool uni = a.uniform && f.uniform;
   const int m = a.mr, bs = a.bs, n = a.nbr;
+  if (max_block(a) > 32) fail(BMG_EINVAL, "device triple_product: block sizes above 32 are not supported");
   // H = F A
   Product h = symbolic(
       n,
@@ -467,8 +582,18 @@ std::unique_ptr<Bsr> triple_product(const Bsr& f, const Bsr& a) {
         for (int64_t q = f.h_row_ptr[i]; q < f.h_row_ptr[i + 1]; ++q) emit(f.h_col[q], q);
       },
       a.h_row_ptr, a.h_col);
-  DBuf<double> hv(std::max<size_t>(h.col.size() * bs, 2));
-  pair_gemm(ctx, f.vals.p, f.bs, a.vals.p, bs, h, hv.p, bs, m, 0);
+  auto up64v = [&](const std::vector<int64_t>& v, DBuf<int64_t>& d) {
+    d.alloc(std::max<size_t>(v.size(), 1));
+    if (!v.empty()) BMG_CUDA(cudaMemcpy(d.p, v.data(), v.size() * 8, cudaMemcpyHostToDevice));
+  };
+  std::vector<int64_t> hoff;
+  DBuf<int64_t> d_hoff;
+  if (!uni) {
+    hoff = product_offsets(h, a.rsz);
+    up64v(hoff, d_hoff);
+  }
+  DBuf<double> hv(std::max<int64_t>(uni ? (int64_t)h.col.size() * bs : hoff.back(), 2));
+  pair_gemm(ctx, {f.vals.p, f.voff.p}, f.col.p, {a.vals.p, a.voff.p}, h, {hv.p, d_hoff.p}, a, 0);
   // F column index: column k -> rows j (ascending) holding F_jk
   std::vector<int64_t> fc_ptr(n + 1, 0);
   for (int64_t q = 0; q < f.nnzb; ++q) fc_ptr[f.h_col[q] + 1]++;
@@ -535,15 +660,36 @@ std::unique_ptr<Bsr> triple_product(const Bsr& f, const Bsr& a) {
     std::copy(rpr[i].begin(), rpr[i].end(), lo.pairs.begin() + pbase[i]);
   }
   lo.pair_ptr[nl] = pbase[n];
-  DBuf<double> lv(std::max<size_t>((size_t)nl * bs, 2));
-  pair_gemm(ctx, hv.p, bs, f.vals.p, f.bs, lo, lv.p, bs, m, 2);
+  std::vector<int64_t> loff;
+  DBuf<int64_t> d_loff;
+  DBuf<int32_t> d_hcol, d_lrow, d_lcol;
+  DBuf<int> d_sz;
+  if (!uni) {
+    loff = product_offsets(lo, a.rsz);
+    up64v(loff, d_loff);
+    d_hcol.alloc(std::max<size_t>(h.col.size(), 1));
+    if (!h.col.empty()) BMG_CUDA(cudaMemcpy(d_hcol.p, h.col.data(), h.col.size() * 4, cudaMemcpyHostToDevice));
+    std::vector<int32_t> lrow(nl);
+    for (int i = 0; i < n; ++i)
+      for (int64_t q = lo.row_ptr[i]; q < lo.row_ptr[i + 1]; ++q) lrow[q] = i;
+    d_lrow.alloc(std::max<int64_t>(nl, 1));
+    d_lcol.alloc(std::max<int64_t>(nl, 1));
+    d_sz.alloc(n);
+    if (nl) {
+      BMG_CUDA(cudaMemcpy(d_lrow.p, lrow.data(), nl * 4, cudaMemcpyHostToDevice));
+      BMG_CUDA(cudaMemcpy(d_lcol.p, lo.col.data(), nl * 4, cudaMemcpyHostToDevice));
+    }
+    BMG_CUDA(cudaMemcpy(d_sz.p, a.rsz.data(), n * 4, cudaMemcpyHostToDevice));
+  }
+  DBuf<double> lv(std::max<int64_t>(uni ? (int64_t)nl * bs : loff.back(), 2));
+  pair_gemm(ctx, {hv.p, d_hoff.p}, d_hcol.p, {f.vals.p, f.voff.p}, lo, {lv.p, d_loff.p}, a, 2);
   hv.release();
   DBuf<int64_t> ddiag(std::max<int64_t>(nl, 1));
   DBuf<int> dnz(std::max<int64_t>(nl, 1));
   if (nl) {
     BMG_CUDA(cudaMemcpy(ddiag.p, is_diag.data(), nl * 8, cudaMemcpyHostToDevice));
     kern::sym_diag_sqnorm_kernel<<<(int)std::min<int64_t>(nl, ctx->sms * 32), 128, 0, ctx->stream>>>(
-        lv.p, ddiag.p, nl, m, bs, dnz.p);
+        lv.p, uni ? nullptr : d_loff.p, ddiag.p, d_lrow.p, d_lcol.p, uni ? nullptr : d_sz.p, nl, m, bs, dnz.p);
     ctx->count();
     BMG_CUDA(cudaGetLastError());
   }
@@ -571,14 +717,20 @@ std::unique_ptr<Bsr> triple_product(const Bsr& f, const Bsr& a) {
     }
     rp[i + 1] = (int64_t)col.size();
   }
+  std::vector<int32_t> orow_h(col.size());
+  for (int i = 0; i < n; ++i)
+    for (int64_t q = rp[i]; q < rp[i + 1]; ++q) orow_h[q] = i;
   auto out = make_bsr_structure(ctx, n, a.rsz.data(), n, a.rsz.data(), std::move(rp), col, true);
   if (!from.empty()) {
     DBuf<int64_t> dfrom(from.size());
     DBuf<int> dtrans(trans.size());
+    DBuf<int32_t> dorow(orow_h.size());
     BMG_CUDA(cudaMemcpy(dfrom.p, from.data(), from.size() * 8, cudaMemcpyHostToDevice));
     BMG_CUDA(cudaMemcpy(dtrans.p, trans.data(), trans.size() * 4, cudaMemcpyHostToDevice));
+    BMG_CUDA(cudaMemcpy(dorow.p, orow_h.data(), orow_h.size() * 4, cudaMemcpyHostToDevice));
     kern::gather_blocks_kernel<<<(int)std::min<size_t>(from.size(), (size_t)ctx->sms * 32), 128, 0, ctx->stream>>>(
-        lv.p, dfrom.p, dtrans.p, out->vals.p, (int64_t)from.size(), m, bs);
+        lv.p, uni ? nullptr : d_loff.p, dfrom.p, dtrans.p, out->vals.p, blk_view(*out), dorow.p, out->col.p,
+        (int64_t)from.size(), m, bs);
     ctx->count();
     BMG_CUDA(cudaGetLastError());
     BMG_CUDA(cudaStreamSynchronize(ctx->stream));

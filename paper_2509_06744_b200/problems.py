@@ -135,3 +135,44 @@ def dist_inputs(cfg: Config, world: int, rank: int, agglomerate: int = 1, params
     b = normal_vector(nbr[top] * cfg.m, cfg.seed, 0)
     lo, hi = int(bounds[top, rank]), int(bounds[top, rank + 1])
     return A, transfers, b[lo * cfg.m:hi * cfg.m], (bounds, elo, ehi, halo, gran, rad)
+
+
+# ---------------------------------------------------------------------------
+# variable block layouts (the paper's PUM systems mix block sizes: boundary
+# patches carry fewer functions, e.g. 6 vs 10).  Each block of the uniform
+# operator is truncated to [:m_i, :m_j], i.e. A is the principal submatrix of the
+# uniform S_p (x) C + reg D that keeps the first m_i functions of every patch, so
+# it stays symmetric positive definite.
+def boundary_sizes(dim: int, n: int, m_int: int, m_bnd: int) -> np.ndarray:
+    idx = np.arange(n ** dim)
+    on_bnd = np.zeros(idx.size, bool)
+    for d in range(dim):
+        c = (idx // n ** d) % n
+        on_bnd |= (c == 0) | (c == n - 1)
+    return np.where(on_bnd, m_bnd, m_int).astype(np.int32)
+
+
+def truncate_blocks(h: HostBsr, row_sizes, col_sizes, symmetric=None) -> HostBsr:
+    rs = np.asarray(row_sizes, np.int32)
+    cs = np.asarray(col_sizes, np.int32)
+    mr, mc = int(h.row_sizes[0]), int(h.col_sizes[0])
+    vals = []
+    for i in range(len(rs)):
+        for p in range(h.row_ptr[i], h.row_ptr[i + 1]):
+            j = h.col_idx[p]
+            blk = h.vals[p * mr * mc:(p + 1) * mr * mc].reshape(mr, mc)
+            vals.append(blk[:rs[i], :cs[j]].ravel())
+    v = np.concatenate(vals) if vals else np.zeros(0)
+    return HostBsr(rs, cs, h.row_ptr.copy(), h.col_idx.copy(), v,
+                   h.symmetric if symmetric is None else symmetric)
+
+
+def make_variable_problem(cfg: Config, m_bnd: int):
+    """make_problem with boundary patches truncated to m_bnd functions on every level."""
+    A, T, _ = make_problem(cfg)
+    L = cfg.levels
+    sizes = [boundary_sizes(cfg.dim, cfg.n >> (L - 1 - l), cfg.m, m_bnd) for l in range(L)]
+    Av = truncate_blocks(A, sizes[-1], sizes[-1])
+    Tv = [truncate_blocks(T[l - 1], sizes[l], sizes[l - 1], symmetric=False) for l in range(1, L)]
+    b = normal_vector(int(sizes[-1].sum()), cfg.seed, 0)
+    return Av, Tv, b
