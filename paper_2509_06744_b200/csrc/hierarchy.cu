@@ -15,6 +15,9 @@
 #include <cusolverDn.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -511,6 +514,26 @@ static void run_vcycle(Hier& h, int kpre, int kpost, const double* bf, double* x
   BMG_CUDA(cudaGraphLaunch(it->second.exec, ctx->stream));
   ctx->launches += it->second.kernels;
 }
+
+// BMG_SETUP_TIMING=1: per-phase wall time of the setup on stderr (device synced)
+struct SetupClock {
+  Ctx* ctx;
+  bool on;
+  std::chrono::steady_clock::time_point t;
+  explicit SetupClock(Ctx* c) : ctx(c) {
+    const char* e = std::getenv("BMG_SETUP_TIMING");
+    on = e && e[0] == '1';
+    t = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what, int level) {
+    if (!on) return;
+    cudaStreamSynchronize(ctx->stream);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[bmg setup] level %d %-24s %8.3f s\n", level, what,
+                 std::chrono::duration<double>(now - t).count());
+    t = now;
+  }
+};
 
 // ============================================================================ construction
 static void coarse_factor(Hier& h, Part& p) {
@@ -1644,25 +1667,31 @@ int bmg_hier_setup(const bmg_bsr* a_finest, int ntransfers, const bmg_bsr* const
     const int depth = ntransfers;
     p.lv.resize(depth + 1);
     p.lv[depth].A = af;
+    SetupClock clk(ctx);
     for (int l = depth; l >= 1; --l) {
       PLevel& L = p.lv[l];
       L.P = B_(transfers[l - 1]);
       L.R_own = bsr_transpose(*L.P);
       L.R = L.R_own.get();
+      clk.mark("transpose P", l);
       p.lv[l - 1].A_own = galerkin(*L.A, *L.P);
       p.lv[l - 1].A = p.lv[l - 1].A_own.get();
+      clk.mark("galerkin", l);
     }
     for (int l = 1; l <= depth; ++l) {
       PLevel& L = p.lv[l];
       L.M_own = fsai_build(*L.A, prm.fsai_kind, prm.t_max, prm.tau, prm.nest);
       L.M = L.M_own.get();
+      clk.mark("fsai", l);
       const double beta = lanczos_lambda_max(*L.A, *L.M, prm.lanczos_iters, prm.lanczos_safety, prm.seed);
+      clk.mark("lanczos", l);
       L.spec.kind = prm.smoother_kind;  // multilevel.cpp:62-65
       L.spec.beta = beta;
       L.spec.alpha = prm.first_kind_fraction * beta;
       L.spec.omega = prm.richardson_omega;
     }
     finish_whole(*h, prm.coarse_dim_cap);
+    clk.mark("coarse factor + vectors", 0);
     *out = reinterpret_cast<bmg_hier*>(h.release());
   });
 }

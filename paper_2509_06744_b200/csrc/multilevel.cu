@@ -4,10 +4,14 @@
 #include <cusolverDn.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <map>
 #include <tuple>
+#include <type_traits>
 
 #include "bmg_abi.h"
 #include "bmg_internal.h"
@@ -269,19 +273,44 @@ __device__ __forceinline__ int64_t find_in(const int32_t* __restrict__ col, int6
   return lo;
 }
 
-// AP rows [f0, f1): CTA per (fine row, output block); thread per block entry.
+// Warp per output block; lane (g, c) = (lane / cols, lane % cols) owns column c
+// of rows r = g, g + G, ... (G = 32 / cols groups), accumulating in registers.
+// Per output entry the arithmetic is the reference order: t = fma chain over the
+// inner index from 0, then acc += t per term in ascending term order.
+template <int MAXR>
+struct LaneTile {
+  int G, g, c, nr;
+  bool act;
+  __device__ __forceinline__ LaneTile(int rows, int cols) {
+    const int lane = threadIdx.x & 31;
+    G = max(1, 32 / cols);
+    g = lane / cols;
+    c = lane - g * cols;
+    act = g < G;
+    nr = act ? (rows - g + G - 1) / G : 0;
+  }
+  __device__ __forceinline__ int row(int j) const { return g + G * j; }
+};
+
+// AP rows [f0, f1): AP_iJ = sum over k in A row i (ascending) of A_ik P_kJ.
 // AP block q (fine row i, coarse column J) is m_i x mc_J at APv + APo(q - apbase).
-__global__ void ap_chunk_kernel(const double* __restrict__ Av, BlkView A, const int64_t* __restrict__ Arp,
-                                const int32_t* __restrict__ Acol, const double* __restrict__ Pv, BlkView P,
-                                const int64_t* __restrict__ Prp, const int32_t* __restrict__ Pcol,
-                                const int64_t* __restrict__ APrp, const int32_t* __restrict__ APcol, int f0, int f1,
-                                int64_t apbase, const int64_t* __restrict__ APoff, int bs_o, double* __restrict__ APv,
-                                int M) {
-  const int r = threadIdx.x / M, c = threadIdx.x - (threadIdx.x / M) * M;
+template <int MAXR>
+__global__ void __launch_bounds__(128) ap_chunk_kernel(const double* __restrict__ Av, BlkView A,
+                                                       const int64_t* __restrict__ Arp,
+                                                       const int32_t* __restrict__ Acol, const double* __restrict__ Pv,
+                                                       BlkView P, const int64_t* __restrict__ Prp,
+                                                       const int32_t* __restrict__ Pcol,
+                                                       const int64_t* __restrict__ APrp,
+                                                       const int32_t* __restrict__ APcol, int f0, int f1,
+                                                       int64_t apbase, const int64_t* __restrict__ APoff, int bs_o,
+                                                       double* __restrict__ APv) {
+  __shared__ double tiles[4][32 * 32];  // one block tile per warp (128 threads)
+  double* tile = tiles[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
   const int64_t q0 = APrp[f0], q1 = APrp[f1];
-  for (int64_t q = q0 + blockIdx.x; q < q1; q += gridDim.x) {
-    // fine row of output block q (binary search over APrp[f0..f1])
-    int lo = f0, hi = f1 - 1;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t q = q0 + (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < q1; q += warps) {
+    int lo = f0, hi = f1 - 1;  // fine row of block q
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
       if (APrp[mid] <= q)
@@ -292,35 +321,80 @@ __global__ void ap_chunk_kernel(const double* __restrict__ Av, BlkView A, const 
     const int i = lo;
     const int J = APcol[q];
     const int rows = A.r(i), cols = P.c(J);
-    const bool act = r < rows && c < cols;
-    double acc = 0.0;
-    for (int64_t pa = Arp[i]; pa < Arp[i + 1]; ++pa) {
+    const LaneTile<MAXR> L(rows, cols);
+    double acc[MAXR];
+#pragma unroll
+    for (int j = 0; j < MAXR; ++j) acc[j] = 0.0;
+    const int64_t a0 = Arp[i], a1 = Arp[i + 1];
+    for (int64_t base = a0; base < a1; base += 32) {
+      const int64_t pl = base + lane;
+      int64_t ppl = -1;
+      if (pl < a1) {
+        const int kl = Acol[pl];
+        const int64_t pp = find_in(Pcol, Prp[kl], Prp[kl + 1], J);
+        if (pp < Prp[kl + 1] && Pcol[pp] == J) ppl = pp;
+      }
+      unsigned mask = __ballot_sync(0xffffffffu, ppl >= 0);
+      while (mask) {
+      const int src = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const int64_t pa = base + src;
+      const int64_t pp = __shfl_sync(0xffffffffu, ppl, src);
       const int k = Acol[pa];
-      const int64_t pp = find_in(Pcol, Prp[k], Prp[k + 1], J);
-      if (pp >= Prp[k + 1] || Pcol[pp] != J) continue;
-      if (act) {
-        const int mk = A.c(k);
-        const double* a = Av + A.off(pa);
-        const double* b = Pv + P.off(pp);
-        double t = 0.0;
-        for (int z = 0; z < mk; ++z) t = __fma_rn(a[r * mk + z], b[z * cols + c], t);
-        acc = __dadd_rn(acc, t);
+      const int mk = A.c(k);
+      const double* a = Av + A.off(pa);
+      const double* b = Pv + P.off(pp);
+      // one coalesced burst: A_ik into this warp's shared tile, P_kJ's column c into registers
+      __syncwarp();
+      for (int e = lane; e < rows * mk; e += 32) tile[e] = a[e];
+      __syncwarp();
+      double t[MAXR];
+#pragma unroll
+      for (int j = 0; j < MAXR; ++j) t[j] = 0.0;
+      for (int z0 = 0; z0 < mk; z0 += 8) {
+        double bc[8];
+#pragma unroll
+        for (int zz = 0; zz < 8; ++zz)
+          if (z0 + zz < mk) bc[zz] = b[(z0 + zz) * cols + L.c];
+#pragma unroll
+        for (int zz = 0; zz < 8; ++zz) {
+          if (z0 + zz < mk) {
+#pragma unroll
+            for (int j = 0; j < MAXR; ++j)
+              if (j < L.nr) t[j] = __fma_rn(tile[L.row(j) * mk + z0 + zz], bc[zz], t[j]);
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < MAXR; ++j) acc[j] = __dadd_rn(acc[j], t[j]);
       }
     }
-    if (act) APv[(APoff ? APoff[q] - APoff[apbase] : (q - apbase) * bs_o) + r * cols + c] = acc;
+    double* o = APv + (APoff ? APoff[q] - APoff[apbase] : (q - apbase) * bs_o);
+#pragma unroll
+    for (int j = 0; j < MAXR; ++j)
+      if (j < L.nr) o[L.row(j) * cols + L.c] = acc[j];
   }
 }
 
 // C_IJ += sum over fine rows i in [f0, f1) of P_iI^T AP_iJ (ascending i), coarse rows [I0, I1)
-__global__ void c_accum_kernel(const double* __restrict__ Pv, BlkView P, const int64_t* __restrict__ PTrp,
-                               const int32_t* __restrict__ PTrow, const int64_t* __restrict__ PTblk,
-                               const int64_t* __restrict__ APrp, const int32_t* __restrict__ APcol,
-                               const double* __restrict__ APv, int64_t apbase, const int64_t* __restrict__ APoff,
-                               int bs_ap, const int64_t* __restrict__ Crp, const int32_t* __restrict__ Ccol, int I0,
-                               int I1, int f0, int f1, double* __restrict__ Cv, BlkView Cl, int M) {
-  const int r = threadIdx.x / M, c = threadIdx.x - (threadIdx.x / M) * M;
+template <int MAXR>
+__global__ void __launch_bounds__(128) c_accum_kernel(const double* __restrict__ Pv, BlkView P,
+                                                      const int64_t* __restrict__ PTrp,
+                                                      const int32_t* __restrict__ PTrow,
+                                                      const int64_t* __restrict__ PTblk,
+                                                      const int64_t* __restrict__ APrp,
+                                                      const int32_t* __restrict__ APcol,
+                                                      const double* __restrict__ APv, int64_t apbase,
+                                                      const int64_t* __restrict__ APoff, int bs_ap,
+                                                      const int64_t* __restrict__ Crp,
+                                                      const int32_t* __restrict__ Ccol, int I0, int I1, int f0,
+                                                      int f1, double* __restrict__ Cv, BlkView Cl) {
+  __shared__ double tiles[4][32 * 32];
+  double* tile = tiles[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
   const int64_t o0 = Crp[I0], o1 = Crp[I1];
-  for (int64_t o = o0 + blockIdx.x; o < o1; o += gridDim.x) {
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t o = o0 + (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); o < o1; o += warps) {
     int lo = I0, hi = I1 - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
@@ -332,32 +406,104 @@ __global__ void c_accum_kernel(const double* __restrict__ Pv, BlkView P, const i
     const int I = lo;
     const int J = Ccol[o];
     const int rows = P.c(I), cols = P.c(J);
-    const bool act = r < rows && c < cols;
+    const LaneTile<MAXR> L(rows, cols);
     double* cb = Cv + Cl.off(o);
-    double acc = act ? cb[r * cols + c] : 0.0;
+    double acc[MAXR];
+#pragma unroll
+    for (int j = 0; j < MAXR; ++j) acc[j] = j < L.nr ? cb[L.row(j) * cols + L.c] : 0.0;
     bool any = false;
-    // fine rows of coarse column I inside the chunk (ascending)
-    int64_t t0 = PTrp[I], t1 = PTrp[I + 1];
-    while (t0 < t1 && PTrow[t0] < f0) ++t0;
-    for (int64_t t = t0; t < t1 && PTrow[t] < f1; ++t) {
+    // fine rows of coarse column I inside the chunk (ascending): 32 searches at a
+    // time (one per lane), then the matches in ascending order
+    const int64_t t0 = PTrp[I], t1 = PTrp[I + 1];
+    for (int64_t base = t0; base < t1; base += 32) {
+      const int64_t tl = base + lane;
+      int64_t ql = -1;
+      if (tl < t1) {
+        const int il = PTrow[tl];
+        if (il >= f0 && il < f1) {
+          const int64_t q = find_in(APcol, APrp[il], APrp[il + 1], J);
+          if (q < APrp[il + 1] && APcol[q] == J) ql = q;
+        }
+      }
+      unsigned mask = __ballot_sync(0xffffffffu, ql >= 0);
+      while (mask) {
+      const int src = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const int64_t t = base + src;
+      const int64_t q = __shfl_sync(0xffffffffu, ql, src);
       const int i = PTrow[t];
-      const int64_t q = find_in(APcol, APrp[i], APrp[i + 1], J);
-      if (q >= APrp[i + 1] || APcol[q] != J) continue;
       any = true;
-      if (act) {
-        const int mi = P.r(i);
-        const double* p = Pv + P.off(PTblk[t]);
-        const double* ap = APv + (APoff ? APoff[q] - APoff[apbase] : (q - apbase) * bs_ap);
-        double s = 0.0;
-        for (int z = 0; z < mi; ++z) s = __fma_rn(p[z * rows + r], ap[z * cols + c], s);
-        acc = __dadd_rn(acc, s);
+      const int mi = P.r(i);
+      const double* p = Pv + P.off(PTblk[t]);
+      const double* ap = APv + (APoff ? APoff[q] - APoff[apbase] : (q - apbase) * bs_ap);
+      __syncwarp();
+      for (int e = lane; e < mi * rows; e += 32) tile[e] = p[e];
+      __syncwarp();
+      double sm[MAXR];
+#pragma unroll
+      for (int j = 0; j < MAXR; ++j) sm[j] = 0.0;
+      for (int z0 = 0; z0 < mi; z0 += 8) {
+        double ac[8];
+#pragma unroll
+        for (int zz = 0; zz < 8; ++zz)
+          if (z0 + zz < mi) ac[zz] = ap[(z0 + zz) * cols + L.c];
+#pragma unroll
+        for (int zz = 0; zz < 8; ++zz) {
+          if (z0 + zz < mi) {
+#pragma unroll
+            for (int j = 0; j < MAXR; ++j)
+              if (j < L.nr) sm[j] = __fma_rn(tile[(z0 + zz) * rows + L.row(j)], ac[zz], sm[j]);
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < MAXR; ++j) acc[j] = __dadd_rn(acc[j], sm[j]);
       }
     }
-    if (any && act) cb[r * cols + c] = acc;
+    if (any) {
+#pragma unroll
+      for (int j = 0; j < MAXR; ++j)
+        if (j < L.nr) cb[L.row(j) * cols + L.c] = acc[j];
+    }
   }
 }
 
 }  // namespace kern
+
+// registers per lane for the lane-column tiles: ceil(M / (32 / M)) rounded up
+template <class F>
+static void tile_dispatch(int M, F&& f) {
+  const int G = std::max(1, 32 / M);
+  const int need = (M + G - 1) / G;
+  if (need <= 4) return f(std::integral_constant<int, 4>());
+  if (need <= 8) return f(std::integral_constant<int, 8>());
+  if (need <= 12) return f(std::integral_constant<int, 12>());
+  if (need <= 16) return f(std::integral_constant<int, 16>());
+  if (need <= 20) return f(std::integral_constant<int, 20>());
+  if (need <= 21) return f(std::integral_constant<int, 21>());
+  if (need <= 24) return f(std::integral_constant<int, 24>());
+  return f(std::integral_constant<int, 32>());
+}
+
+namespace {
+struct PhaseTimer {  // BMG_SETUP_TIMING=1
+  bool on;
+  Ctx* ctx;
+  std::chrono::steady_clock::time_point t;
+  explicit PhaseTimer(Ctx* c) : ctx(c) {
+    const char* e = std::getenv("BMG_SETUP_TIMING");
+    on = e && e[0] == '1';
+    t = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(ctx->stream);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[bmg setup]   %-30s %8.3f s\n", what, std::chrono::duration<double>(now - t).count());
+    t = now;
+  }
+};
+}  // namespace
 
 std::unique_ptr<Bsr> galerkin(const Bsr& a, const Bsr& p) {
   if (!(a.rsz == a.csz) || !(a.rsz == p.rsz)) fail(BMG_EINVAL, "galerkin_coarsen: layouts do not match");
@@ -366,6 +512,7 @@ std::unique_ptr<Bsr> galerkin(const Bsr& a, const Bsr& p) {
   const int nf = a.nbr, nc = p.nbc;
   const int M = std::max(max_block(a), max_block(p));
   if (M > 32) fail(BMG_EINVAL, "device galerkin_coarsen: block sizes above 32 are not supported");
+  PhaseTimer tm(ctx);
   // ---- symbolic (host): AP rows, P^T index, C rows, transpose positions
   std::vector<int64_t> aprp(nf + 1, 0);
   std::vector<std::vector<int32_t>> aprow(nf);
@@ -379,6 +526,7 @@ std::unique_ptr<Bsr> galerkin(const Bsr& a, const Bsr& p) {
     std::sort(v.begin(), v.end());
     v.erase(std::unique(v.begin(), v.end()), v.end());
   }
+  tm.mark("galerkin: AP rows (host)");
   for (int i = 0; i < nf; ++i) aprp[i + 1] = aprp[i] + (int64_t)aprow[i].size();
   std::vector<int32_t> apcol(aprp[nf]);
 #pragma omp parallel for schedule(static)
@@ -397,6 +545,7 @@ std::unique_ptr<Bsr> galerkin(const Bsr& a, const Bsr& p) {
         ptblk[t] = q;
       }
   }
+  tm.mark("galerkin: P^T index (host)");
   std::vector<std::vector<int32_t>> crow(nc);
 #pragma omp parallel for schedule(dynamic, 64)
   for (int I = 0; I < nc; ++I) {
@@ -412,6 +561,7 @@ std::unique_ptr<Bsr> galerkin(const Bsr& a, const Bsr& p) {
   std::vector<int32_t> ccol(crp[nc]);
   for (int I = 0; I < nc; ++I) std::copy(crow[I].begin(), crow[I].end(), ccol.begin() + crp[I]);
   crow.clear();
+  tm.mark("galerkin: C rows (host)");
   std::vector<int64_t> tpos(ccol.size(), -1);
 #pragma omp parallel for schedule(dynamic, 64)
   for (int I = 0; I < nc; ++I)
@@ -423,6 +573,7 @@ std::unique_ptr<Bsr> galerkin(const Bsr& a, const Bsr& p) {
     }
   for (int64_t v : tpos)
     if (v == -2) fail(BMG_ERUNTIME, "galerkin_coarsen: P^T A P is not structurally symmetric");
+  tm.mark("galerkin: transpose positions");
   // ---- device buffers
   auto up64 = [&](const std::vector<int64_t>& h, DBuf<int64_t>& d) {
     d.alloc(std::max<size_t>(h.size(), 1));
@@ -481,17 +632,22 @@ std::unique_ptr<Bsr> galerkin(const Bsr& a, const Bsr& p) {
       I1 = std::max(I1, p.h_col[q] + 1);
     }
     if (napb > 0) {
-      kern::ap_chunk_kernel<<<(int)std::min<int64_t>(napb, (int64_t)ctx->sms * 64), threads, 0, ctx->stream>>>(
-          a.vals.p, Av, a.row_ptr.p, a.col.p, p.vals.p, Pv, p.row_ptr.p, p.col.p, d_aprp.p, d_apcol.p, f0, f1,
-          aprp[f0], uni ? nullptr : d_apoff.p, bs, apv.p, M);
+      const unsigned grid = (unsigned)std::min<int64_t>((napb + 3) / 4, (int64_t)ctx->sms * 128);
+      tile_dispatch(M, [&](auto R) {
+        kern::ap_chunk_kernel<decltype(R)::value><<<grid, 128, 0, ctx->stream>>>(
+            a.vals.p, Av, a.row_ptr.p, a.col.p, p.vals.p, Pv, p.row_ptr.p, p.col.p, d_aprp.p, d_apcol.p, f0, f1,
+            aprp[f0], uni ? nullptr : d_apoff.p, bs, apv.p);
+      });
       ctx->count();
       BMG_CUDA(cudaGetLastError());
     }
     if (I1 > I0 && crp[I1] > crp[I0]) {
-      kern::c_accum_kernel<<<(int)std::min<int64_t>(crp[I1] - crp[I0], (int64_t)ctx->sms * 64), threads, 0,
-                             ctx->stream>>>(p.vals.p, Pv, d_ptrp.p, d_ptrow.p, d_ptblk.p, d_aprp.p, d_apcol.p,
-                                            apv.p, aprp[f0], uni ? nullptr : d_apoff.p, bs, d_crp.p, d_ccol.p, I0,
-                                            I1, f0, f1, cv.p, Cv, M);
+      const unsigned grid = (unsigned)std::min<int64_t>((crp[I1] - crp[I0] + 3) / 4, (int64_t)ctx->sms * 128);
+      tile_dispatch(M, [&](auto R) {
+        kern::c_accum_kernel<decltype(R)::value><<<grid, 128, 0, ctx->stream>>>(
+            p.vals.p, Pv, d_ptrp.p, d_ptrow.p, d_ptblk.p, d_aprp.p, d_apcol.p, apv.p, aprp[f0],
+            uni ? nullptr : d_apoff.p, bs, d_crp.p, d_ccol.p, I0, I1, f0, f1, cv.p, Cv);
+      });
       ctx->count();
       BMG_CUDA(cudaGetLastError());
     }
@@ -499,6 +655,7 @@ std::unique_ptr<Bsr> galerkin(const Bsr& a, const Bsr& p) {
     f0 = f1;
   }
   apv.release();
+  tm.mark("galerkin: numeric (device)");
   // ---- A_c = (C + C^T)/2 blockwise (multilevel.cpp:16-26)
   up64(tpos, d_tpos);
   DBuf<int32_t> d_crow;
