@@ -134,6 +134,9 @@ int64_t bmg_vec_size(const bmg_vec* v);
 
 /* ---- kernels (kernels.cpp) --------------------------------------------- */
 int bmg_spmv(const bmg_bsr* a, const bmg_vec* x, bmg_vec* y);
+/* Y = A X for nrhs (1, 2, 4, 8) right-hand sides interleaved per scalar row
+ * (x[j*nrhs + v]); each column bitwise equal to bmg_spmv */
+int bmg_spmv_batch(const bmg_bsr* a, int nrhs, const bmg_vec* x, bmg_vec* y);
 int bmg_spmv_t(const bmg_bsr* a, const bmg_vec* x, bmg_vec* y);
 int bmg_residual(const bmg_bsr* a, const bmg_vec* b, const bmg_vec* x, bmg_vec* r);
 int bmg_dot(const bmg_vec* a, const bmg_vec* b, double* out);
@@ -185,11 +188,19 @@ int bmg_hier_level(const bmg_hier* h, int level, const bmg_bsr** a, const bmg_bs
                    const bmg_fsai** m);
 /* algorithmic HBM bytes of one V(k_pre,k_post) cycle on the finest level */
 int bmg_hier_cycle_bytes(const bmg_hier* h, int k_pre, int k_post, int64_t* bytes);
+int bmg_hier_cycle_bytes_batch(const bmg_hier* h, int k_pre, int k_post, int nrhs, int64_t* bytes);
 /* 1 (default) = replay each cycle from a captured CUDA graph */
 int bmg_hier_use_graph(bmg_hier* h, int on);
 int bmg_vcycle(bmg_hier* h, int k_pre, int k_post, const bmg_vec* b, bmg_vec* x);
 /* end-to-end: host b, host x (in/out); H2D + cycle + D2H inside the call */
 int bmg_vcycle_host(bmg_hier* h, int k_pre, int k_post, const double* b, double* x);
+/* K right-hand sides in one cycle (K = 1, 2, 4, 8), interleaved per scalar row:
+ * b[i*K + v], x[i*K + v].  The reference allows concurrent v_cycle calls on
+ * distinct right-hand sides (SURVEY.md §8(b) Threading); batching them lets one
+ * stream of every matrix serve all K.  Each right-hand side is bitwise the
+ * single cycle.  Vectors hold n*K values (n = finest length for K = 1). */
+int bmg_vcycle_batch(bmg_hier* h, int k_pre, int k_post, int nrhs, const bmg_vec* b, bmg_vec* x);
+int bmg_vcycle_batch_host(bmg_hier* h, int k_pre, int k_post, int nrhs, const double* b, double* x);
 int bmg_solve(bmg_hier* h, int k_pre, int k_post, const bmg_vec* b, bmg_vec* x, double tol,
               int max_iter, double* hist, int* iters, int* status);
 

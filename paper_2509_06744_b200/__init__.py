@@ -5,7 +5,7 @@ is the Python mirror of the reference's hot-path interface over that ABI.
 """
 from .native import (CHEB_FIRST, CHEB_FOURTH, RICHARDSON, BmgError, IoError, CudaError, InvalidArgument, NotPositiveDefinite, OutOfRange,  # noqa: F401
                      FSAI_ADAPTIVE, FSAI_DIAGONAL, FSAI_STATIC_LOWER, SetupParams, lib)
-from .api import (apply_smoother, BlockSparseMatrix, Context, LoopbackGroup, Fsai, Hierarchy, HostBsr, Vector, cheb_fourth_apply,  # noqa: F401
+from .api import (apply_smoother, spmv_batch, BlockSparseMatrix, Context, LoopbackGroup, Fsai, Hierarchy, HostBsr, Vector, cheb_fourth_apply,  # noqa: F401
                   default_params, dot, galerkin_coarsen, lanczos_lambda_max, residual, spmv, spmv_transpose,
                   triple_product, read_matrix, write_matrix, read_vector, write_vector,
                   tridiag_eigs)

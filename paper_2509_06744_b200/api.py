@@ -241,6 +241,11 @@ def spmv(a: BlockSparseMatrix, x: Vector, y: Vector):
     check(lib().bmg_spmv(a.h, x.h, y.h))
 
 
+def spmv_batch(a: BlockSparseMatrix, nrhs: int, x: Vector, y: Vector):
+    """Y = A X, nrhs right-hand sides interleaved per scalar row (bmg_spmv_batch)."""
+    check(lib().bmg_spmv_batch(a.h, nrhs, x.h, y.h))
+
+
 def spmv_transpose(a: BlockSparseMatrix, x: Vector, y: Vector):
     check(lib().bmg_spmv_t(a.h, x.h, y.h))
 
@@ -431,9 +436,9 @@ class Hierarchy:
         M = Fsai(self.ctx, m, owned=False) if m.value else None
         return A, P, M
 
-    def cycle_bytes(self, k_pre, k_post) -> int:
+    def cycle_bytes(self, k_pre, k_post, nrhs: int = 1) -> int:
         out = C.c_int64()
-        check(lib().bmg_hier_cycle_bytes(self.h, k_pre, k_post, C.byref(out)))
+        check(lib().bmg_hier_cycle_bytes_batch(self.h, k_pre, k_post, nrhs, C.byref(out)))
         return out.value
 
     def partition(self, world: int, granule, agglomerate: int = 1, rank: int = -1):
@@ -451,6 +456,16 @@ class Hierarchy:
 
     def v_cycle(self, k_pre, k_post, b: Vector, x: Vector):
         check(lib().bmg_vcycle(self.h, k_pre, k_post, b.h, x.h))
+
+    def v_cycle_batch(self, k_pre, k_post, nrhs: int, b: Vector, x: Vector):
+        """K right-hand sides interleaved per scalar row (b[i*K + v]); bmg_vcycle_batch."""
+        check(lib().bmg_vcycle_batch(self.h, k_pre, k_post, nrhs, b.h, x.h))
+
+    def v_cycle_batch_host(self, k_pre, k_post, nrhs: int, b: np.ndarray, x: np.ndarray):
+        check(lib().bmg_vcycle_batch_host(self.h, k_pre, k_post, nrhs, dptr(b), dptr(x)))
+
+    def v_cycle_batch_host_ptr(self, k_pre, k_post, nrhs: int, b_ptr: int, x_ptr: int):
+        check(lib().bmg_vcycle_batch_host(self.h, k_pre, k_post, nrhs, C.cast(b_ptr, N._PD), C.cast(x_ptr, N._PD)))
 
     def v_cycle_host(self, k_pre, k_post, b: np.ndarray, x: np.ndarray):
         check(lib().bmg_vcycle_host(self.h, k_pre, k_post, dptr(b), dptr(x)))

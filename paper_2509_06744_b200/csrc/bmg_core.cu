@@ -208,30 +208,49 @@ static int chunk_blocks(int mr, int bs) {
   return std::min(by_items, by_bytes);
 }
 
-template <int MR, int MC>
-static int stream_occupancy(size_t smem) {
-  auto kfn = kern::bsr_stream_kernel<MR, MC, kern::EpiStore>;
-  // the launch cap stays at the maximum (launch_stream_t); the query uses `smem`
+// shared-memory attributes of one instantiation: the largest dynamic size; batched
+// (K > 1) kernels also ask for the max-shared carveout (their partials grow with
+// K); K = 1 keeps the default split, whose larger L1 serves the x gathers
+template <class F>
+static void stream_attrs(F kfn, int K) {
   BMG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  if (K > 1)
+    BMG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  (int)cudaSharedmemCarveoutMaxShared));
+}
+
+template <int MR, int MC, int K>
+static int stream_occupancy(size_t smem) {
+  auto kfn = kern::bsr_stream_kernel<MR, MC, K, kern::EpiStore>;
+  stream_attrs(kfn, K);
   int occ = 0;
   BMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kern::kThreads, smem));
   return std::max(occ, 1);
 }
 
-static int occupancy_for(int mr, int mc, size_t smem) {
+template <int MR, int MC>
+static int occupancy_k(size_t smem, int K) {
+  switch (K) {
+    case 2: return stream_occupancy<MR, MC, 2>(smem);
+    case 4: return stream_occupancy<MR, MC, 4>(smem);
+    case 8: return stream_occupancy<MR, MC, 8>(smem);
+  }
+  return stream_occupancy<MR, MC, 1>(smem);
+}
+
+static int occupancy_for(int mr, int mc, size_t smem, int K = 1) {
   switch (mr) {
-    case 10: return stream_occupancy<10, 10>(smem);
-    case 15: return stream_occupancy<15, 15>(smem);
-    case 20: return stream_occupancy<20, 20>(smem);
-    case 21: return stream_occupancy<21, 21>(smem);
+    case 10: return occupancy_k<10, 10>(smem, K);
+    case 15: return occupancy_k<15, 15>(smem, K);
+    case 20: return occupancy_k<20, 20>(smem, K);
+    case 21: return occupancy_k<21, 21>(smem, K);
   }
   return 1;
 }
 
 // Partition block rows into per-CTA ranges balanced by blocks; cut each
 // range's contiguous block span into chunks of cb_max blocks (bsr_stream.cuh).
-void build_plan(Bsr& a) {
-  Plan& P = a.plan;
+static void build_plan_into(const Bsr& a, Plan& P, int K) {
   P = Plan();
   if (!(a.uniform && stream_supported(a.mr, a.mc)) || a.nbr == 0) return;
   P.cb_max = chunk_blocks(a.mr, a.bs);
@@ -242,8 +261,8 @@ void build_plan(Bsr& a) {
   std::vector<int> cta;
   int rmax = 1;
   // first pass with a provisional rmax to size smem and query occupancy
-  const size_t smem0 = kern::SmemLayout(a.bs, P.cb_max, P.cb_max + 2, a.mr, P.stages).total;
-  const int occ = occupancy_for(a.mr, a.mc, smem0);
+  const size_t smem0 = kern::SmemLayout(a.bs, P.cb_max, P.cb_max + 2, a.mr, P.stages, K).total;
+  const int occ = occupancy_for(a.mr, a.mc, smem0, K);
   const int64_t gmax = (int64_t)a.ctx->sms * occ;
   const int64_t per = std::max<int64_t>(1, (a.nnzb + gmax - 1) / gmax);
   int row = 0;
@@ -279,13 +298,26 @@ void build_plan(Bsr& a) {
   P.rmax = rmax;
   P.nctas = (int)cta.size() - 1;
   P.nchunks = (int)chunks.size();
-  P.smem = kern::SmemLayout(a.bs, P.cb_max, P.rmax, a.mr, P.stages).total;
+  P.smem = kern::SmemLayout(a.bs, P.cb_max, P.rmax, a.mr, P.stages, K).total;
   if (P.smem > 227 * 1024) fail(BMG_EINVAL, "plan: chunk does not fit in shared memory");
-  occupancy_for(a.mr, a.mc, P.smem);  // sets the dynamic smem attribute
+  occupancy_for(a.mr, a.mc, P.smem, K);  // sets the shared-memory attributes
   P.chunks.alloc(chunks.size());
   P.cta_chunk.alloc(cta.size());
   BMG_CUDA(cudaMemcpy(P.chunks.p, chunks.data(), chunks.size() * sizeof(int4), cudaMemcpyHostToDevice));
   BMG_CUDA(cudaMemcpy(P.cta_chunk.p, cta.data(), cta.size() * sizeof(int), cudaMemcpyHostToDevice));
+}
+
+void build_plan(Bsr& a) { build_plan_into(a, a.plan, 1); }
+
+const Plan& plan_for(const Bsr& a, int nrhs) {
+  if (nrhs <= 1) return a.plan;
+  const int idx = nrhs == 2 ? 1 : nrhs == 4 ? 2 : 3;
+  if (!a.kplan[idx]) {
+    auto p = std::make_unique<Plan>();
+    build_plan_into(a, *p, nrhs);
+    a.kplan[idx] = std::move(p);
+  }
+  return *a.kplan[idx];
 }
 
 static void finish_layouts(Bsr& a, int nbr, const int* rsz, int nbc, const int* csz) {
@@ -478,52 +510,64 @@ static bool pdl_enabled() {
   return on;
 }
 
-template <int MR, int MC, class Epi>
+template <int MR, int MC, int K, class Epi>
 static void launch_stream_t(const Bsr& a, const double* x, Epi epi) {
+  const Plan& P = plan_for(a, K);
   kern::StreamArgs s;
   s.vals = a.vals.p;
   s.col = a.col.p;
   s.row_ptr = a.row_ptr.p;
-  s.chunks = a.plan.chunks.p;
-  s.cta_chunk = a.plan.cta_chunk.p;
+  s.chunks = P.chunks.p;
+  s.cta_chunk = P.cta_chunk.p;
   s.x = x;
   s.bs = a.bs;
-  s.cb_max = a.plan.cb_max;
-  s.rmax = a.plan.rmax;
-  s.stages = a.plan.stages;
+  s.cb_max = P.cb_max;
+  s.rmax = P.rmax;
+  s.stages = P.stages;
   // one attribute per template instantiation (covers the largest plan)
   static const bool attr_set = [] {  // thread-safe one-time init (contexts may live on several threads)
-    BMG_CUDA(cudaFuncSetAttribute(kern::bsr_stream_kernel<MR, MC, Epi>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    stream_attrs(kern::bsr_stream_kernel<MR, MC, K, Epi>, K);
     return true;
   }();
   (void)attr_set;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(a.plan.nctas);
+  cfg.gridDim = dim3(P.nctas);
   cfg.blockDim = dim3(kern::kThreads);
-  cfg.dynamicSmemBytes = a.plan.smem;
+  cfg.dynamicSmemBytes = P.smem;
   cfg.stream = a.ctx->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  BMG_CUDA(cudaLaunchKernelEx(&cfg, kern::bsr_stream_kernel<MR, MC, Epi>, s, epi));
+  BMG_CUDA(cudaLaunchKernelEx(&cfg, kern::bsr_stream_kernel<MR, MC, K, Epi>, s, epi));
   a.ctx->count();
   BMG_LAUNCHED(a.ctx->stream, "bsr_stream_kernel");
 }
 
+template <int MR, int MC, class Epi>
+static void launch_stream_k(const Bsr& a, const double* x, Epi epi, int nrhs) {
+  switch (nrhs) {
+    case 1: return launch_stream_t<MR, MC, 1>(a, x, epi);
+    case 2: return launch_stream_t<MR, MC, 2>(a, x, epi);
+    case 4: return launch_stream_t<MR, MC, 4>(a, x, epi);
+    case 8: return launch_stream_t<MR, MC, 8>(a, x, epi);
+  }
+  fail(BMG_EINVAL, "right-hand-side batch must be 1, 2, 4 or 8");
+}
+
 template <class Epi>
-static void launch(const Bsr& a, const double* x, Epi epi) {
+static void launch(const Bsr& a, const double* x, Epi epi, int nrhs) {
   if (a.nbr == 0) return;
   if (a.uniform && stream_supported(a.mr, a.mc)) {
     switch (a.mr) {
-      case 10: return launch_stream_t<10, 10>(a, x, epi);
-      case 15: return launch_stream_t<15, 15>(a, x, epi);
-      case 20: return launch_stream_t<20, 20>(a, x, epi);
-      case 21: return launch_stream_t<21, 21>(a, x, epi);
+      case 10: return launch_stream_k<10, 10>(a, x, epi, nrhs);
+      case 15: return launch_stream_k<15, 15>(a, x, epi, nrhs);
+      case 20: return launch_stream_k<20, 20>(a, x, epi, nrhs);
+      case 21: return launch_stream_k<21, 21>(a, x, epi, nrhs);
     }
   }
+  if (nrhs < 1 || nrhs > 8) fail(BMG_EINVAL, "right-hand-side batch must be 1..8");
   kern::VarArgs s;
   s.vals = a.vals.p;
   s.col = a.col.p;
@@ -535,20 +579,21 @@ static void launch(const Bsr& a, const double* x, Epi epi) {
   s.csz = a.d_csz.p;
   s.x = x;
   s.nbr = a.nbr;
+  s.nrhs = nrhs;
   const int blocks = (int)(((int64_t)a.nbr * 32 + 255) / 256);
   kern::bsr_var_kernel<Epi><<<blocks, 256, 0, a.ctx->stream>>>(s, epi);
   a.ctx->count();
   BMG_LAUNCHED(a.ctx->stream, "bsr_var_kernel");
 }
 
-void spmv(const Bsr& a, const double* x, double* y) { launch(a, x, kern::EpiStore{y}); }
-void residual(const Bsr& a, const double* b, const double* x, double* r) {
-  launch(a, x, kern::EpiResidual{b, r});
+void spmv(const Bsr& a, const double* x, double* y, int nrhs) { launch(a, x, kern::EpiStore{y}, nrhs); }
+void residual(const Bsr& a, const double* b, const double* x, double* r, int nrhs) {
+  launch(a, x, kern::EpiResidual{b, r}, nrhs);
 }
-void prolong_add(const Bsr& a, const double* e, double* x) { launch(a, e, kern::EpiAdd{x}); }
+void prolong_add(const Bsr& a, const double* e, double* x, int nrhs) { launch(a, e, kern::EpiAdd{x}, nrhs); }
 void gt_cheb(const Bsr& gt, const double* w, double* p, double* x, double mu2, double dmu,
-             bool first, bool xzero) {
-  launch(gt, w, kern::EpiCheb{p, x, mu2, dmu, first ? 1 : 0, xzero ? 1 : 0});
+             bool first, bool xzero, int nrhs) {
+  launch(gt, w, kern::EpiCheb{p, x, mu2, dmu, first ? 1 : 0, xzero ? 1 : 0}, nrhs);
 }
 
 }  // namespace bmg
@@ -712,6 +757,17 @@ int bmg_spmv(const bmg_bsr* ah, const bmg_vec* xh, bmg_vec* yh) {
     check_len(x, a->dim_c, "spmv");
     check_len(y, a->dim_r, "spmv");
     spmv(*a, x->d.p, y->d.p);
+  });
+}
+int bmg_spmv_batch(const bmg_bsr* ah, int nrhs, const bmg_vec* xh, bmg_vec* yh) {
+  return guard([&] {
+    const Bsr* a = reinterpret_cast<const Bsr*>(ah);
+    const Vec* x = reinterpret_cast<const Vec*>(xh);
+    Vec* y = reinterpret_cast<Vec*>(yh);
+    if (nrhs < 1) fail(BMG_EINVAL, "spmv: nrhs must be >= 1");
+    check_len(x, (int64_t)a->dim_c * nrhs, "spmv");
+    check_len(y, (int64_t)a->dim_r * nrhs, "spmv");
+    spmv(*a, x->d.p, y->d.p, nrhs);
   });
 }
 int bmg_spmv_t(const bmg_bsr* ah, const bmg_vec* xh, bmg_vec* yh) {

@@ -129,7 +129,8 @@ struct Bsr {
   DBuf<double> vals;
   DBuf<int64_t> voff;           // variable layouts only
   DBuf<int> d_roff, d_coff, d_rsz, d_csz;
-  Plan plan;
+  Plan plan;                              // single right-hand side
+  mutable std::unique_ptr<Plan> kplan[4];  // batched: index log2(nrhs), built on first use
   std::unique_ptr<Bsr> tcache;  // device transpose (spmv_t)
   int64_t pass_bytes() const;
   int64_t device_bytes() const;
@@ -182,15 +183,20 @@ std::unique_ptr<Bsr> make_bsr_structure(Ctx* ctx, int nbr, const int* rsz, int n
                                         bool sym);
 std::unique_ptr<Bsr> bsr_transpose(const Bsr& a);
 void build_plan(Bsr& a);
+// launch plan for nrhs right-hand sides (shared-memory size and CTA count depend
+// on it); call outside graph capture before the first batched launch
+const Plan& plan_for(const Bsr& a, int nrhs);
 
 // ---- device operations (all enqueue on ctx->stream) --------------------------
-void spmv(const Bsr& a, const double* x, double* y);
-void residual(const Bsr& a, const double* b, const double* x, double* r);
-void prolong_add(const Bsr& a, const double* e, double* x);
+// nrhs > 1: right-hand sides interleaved per scalar row (x[i * nrhs + v]); every
+// RHS is computed with the single-vector arithmetic order
+void spmv(const Bsr& a, const double* x, double* y, int nrhs = 1);
+void residual(const Bsr& a, const double* b, const double* x, double* r, int nrhs = 1);
+void prolong_add(const Bsr& a, const double* e, double* x, int nrhs = 1);
 // z = G^T w fused with the fourth-kind update: p = first ? z : mu2 p + z;
 // x = (xzero ? 0 : x) + dmu p
 void gt_cheb(const Bsr& gt, const double* w, double* p, double* x, double mu2, double dmu,
-             bool first, bool xzero);
+             bool first, bool xzero, int nrhs = 1);
 // SmootherSpec (chebyshev.hpp:10-18): 0 Richardson, 1 first kind, 2 fourth kind
 struct SmootherSpec {
   int kind = 2;

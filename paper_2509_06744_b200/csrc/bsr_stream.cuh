@@ -153,7 +153,7 @@ __host__ __device__ inline int stage_cols_of(int cb_max) { return (cb_max + 8 + 
 
 struct SmemLayout {
   uint32_t vals, cols, part, carry, bars, total;
-  __host__ __device__ SmemLayout(int bs, int cb_max, int rmax, int mr, int kStages) {
+  __host__ __device__ SmemLayout(int bs, int cb_max, int rmax, int mr, int kStages, int nrhs = 1) {
     uint32_t o = 0;
     auto al = [](uint32_t v, uint32_t a) { return (v + a - 1) / a * a; };
     (void)rmax;
@@ -162,20 +162,24 @@ struct SmemLayout {
     cols = o;
     o += al((uint32_t)kStages * stage_cols_of(cb_max) * 4, 128);
     part = o;  // double-buffered partial sums
-    o += al((uint32_t)2 * cb_max * mr * 8, 16);
+    o += al((uint32_t)2 * cb_max * mr * (nrhs > 1 ? nrhs + 1 : 1) * 8, 16);
     carry = o;  // double-buffered row carry
-    o += al((uint32_t)2 * mr * 8, 16);
+    o += al((uint32_t)2 * mr * nrhs * 8, 16);
     bars = o;
     o += 2 * kStages * 8;
     total = al(o, 128);
   }
 };
 
-template <int MR, int MC, class Epi>
+// K right-hand sides interleaved per scalar row (x[i * K + v]): one matrix stream
+// serves K vectors; each RHS keeps the single-vector arithmetic order.
+template <int MR, int MC, int K, class Epi>
 __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi epi) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int kStages = s.stages;
-  const SmemLayout L(s.bs, s.cb_max, s.rmax, MR, kStages);
+  const SmemLayout L(s.bs, s.cb_max, s.rmax, MR, kStages, K);
+  // partials of one (block, row) item for K > 1 sit at stride K + 1 (bank spread)
+  constexpr int KP = K > 1 ? K + 1 : 1;
   double* vals_s = reinterpret_cast<double*>(smem + L.vals);
   int* cols_s = reinterpret_cast<int*>(smem + L.cols);
   double* part_s = reinterpret_cast<double*>(smem + L.part);
@@ -235,30 +239,72 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
     const int nrows = (int)((unsigned)d.w & kRowMask);
     const bool cin = ((unsigned)d.w & kCarryIn) != 0;
     const bool cout = ((unsigned)d.w & kCarryOut) != 0;
-    double* part = part_s + pb * s.cb_max * MR;
+    double* part = part_s + pb * s.cb_max * MR * KP;
 
     // early loads for this thread's first phase-B item (row bounds + epilogue inputs)
-    const int ritems = nrows * MR;
+    const int ritems = nrows * MR * K;
     int64_t rlo0 = 0, rhi0 = 0;
     typename Epi::Pre pre0{};
     if (tid < ritems) {
-      const int rr = tid / MR;
+      const int rr = tid / (MR * K);
       rlo0 = __ldg(s.row_ptr + d.z + rr);
       rhi0 = __ldg(s.row_ptr + d.z + rr + 1);
-      pre0 = epi.load((int64_t)(d.z + rr) * MR + (tid - rr * MR));
+      pre0 = epi.load((int64_t)(d.z + rr) * MR * K + (tid - rr * MR * K));
     }
     mbar_wait(&full[st], (it / kStages) & 1);
 
     // phase A: partial dot products per (block, scalar row)
     const double* vs = vals_s + (size_t)st * stage_vals;
     const int* cs = cols_s + st * stage_cols + (d.x & 3);
-    const int items = d.y * MR;
+    if constexpr (K > 1) {
+      // items (block, rhs, row group), row group fastest: each thread gathers one
+      // RHS column of the block's x segment once and reuses it for the rows
+      // g, g + RG, ...; lanes of one RHS read consecutive rows of the staged block
+      constexpr int RG = MR / K > 0 ? MR / K : 1;
+      constexpr int RPG = (MR + RG - 1) / RG;
+      const int kitems = d.y * RG * K;
+      for (int item = tid; item < kitems; item += kConsumers) {
+        const int b = item / (RG * K);
+        const int rem = item - b * RG * K;
+        const int v = rem / RG, g = rem - (rem / RG) * RG;
+        const double* __restrict__ xj = s.x + (int64_t)cs[b] * MC * K + v;
+        double xv[MC];
+#pragma unroll
+        for (int q = 0; q < MC; ++q) xv[q] = __ldg(xj + q * K);
+        const double* ab = vs + b * s.bs;
+#pragma unroll
+        for (int rr = 0; rr < RPG; ++rr) {
+          const int r = g + RG * rr;
+          if (r < MR) {
+            const double* a = ab + r * MC;
+            double t = 0.0;
+            if constexpr (MC % 2 == 0) {
+#pragma unroll
+              for (int q = 0; q < MC / 2; ++q) {
+                const double2 a2 = reinterpret_cast<const double2*>(a)[q];
+                t = __fma_rn(a2.x, xv[2 * q], t);
+                t = __fma_rn(a2.y, xv[2 * q + 1], t);
+              }
+            } else {
+#pragma unroll
+              for (int q = 0; q < MC; ++q) t = __fma_rn(a[q], xv[q], t);
+            }
+            part[(b * MR + r) * KP + v] = t;
+          }
+        }
+      }
+    }
+    const int items = K > 1 ? 0 : d.y * MR;
     for (int item = tid; item < items; item += kConsumers) {
       const int b = item / MR;
       const int r = item - b * MR;
       const int j = cs[b];
-      const double* __restrict__ xj = s.x + (int64_t)j * MC;
+      const double* __restrict__ xj = s.x + (int64_t)j * MC * K;
       const double* a = vs + b * s.bs + r * MC;
+      if constexpr (K > 1) {
+        // unreachable: K > 1 uses the (block, row group, rhs) items below
+        continue;
+      }
       double xv[MC];
       if constexpr (MC % 2 == 0) {
 #pragma unroll
@@ -289,26 +335,27 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
     if (tid == 0) mbar_arrive(&empty[st]);
 
     // phase B: ordered row sums + fused epilogue
-    const double* carry_in = carry_s + (pb ^ 1) * MR;
-    double* carry_out = carry_s + pb * MR;
+    const double* carry_in = carry_s + (pb ^ 1) * MR * K;
+    double* carry_out = carry_s + pb * MR * K;
     for (int item = tid; item < ritems; item += kConsumers) {
-      const int rr = item / MR;
-      const int r = item - rr * MR;
+      const int rr = item / (MR * K);
+      const int rv = item - rr * MR * K;  // r * K + v
       int64_t rlo = rlo0, rhi = rhi0;
       typename Epi::Pre pre = pre0;
       if (item != tid) {
         rlo = __ldg(s.row_ptr + d.z + rr);
         rhi = __ldg(s.row_ptr + d.z + rr + 1);
-        pre = epi.load((int64_t)(d.z + rr) * MR + r);
+        pre = epi.load((int64_t)(d.z + rr) * MR * K + rv);
       }
       const int lo = (int)(max(rlo, (int64_t)d.x) - d.x);
       const int hi = (int)(min(rhi, (int64_t)(d.x + d.y)) - d.x);
-      double acc = (rr == 0 && cin) ? carry_in[r] : 0.0;
-      for (int b = lo; b < hi; ++b) acc = __dadd_rn(acc, part[b * MR + r]);
+      double acc = (rr == 0 && cin) ? carry_in[rv] : 0.0;
+      const int r = rv / K, v = rv - (rv / K) * K;
+      for (int b = lo; b < hi; ++b) acc = __dadd_rn(acc, part[(b * MR + r) * KP + v]);
       if (rr == nrows - 1 && cout)
-        carry_out[r] = acc;
+        carry_out[rv] = acc;
       else
-        epi.store((int64_t)(d.z + rr) * MR + r, acc, pre);
+        epi.store((int64_t)(d.z + rr) * MR * K + rv, acc, pre);
     }
   }
 }
@@ -327,6 +374,7 @@ struct VarArgs {
   const int* csz;
   const double* x;
   int nbr;
+  int nrhs;  // right-hand sides interleaved per scalar row
 };
 
 template <class Epi>
@@ -336,22 +384,24 @@ __global__ void __launch_bounds__(256) bsr_var_kernel(VarArgs s, Epi epi) {
   if (warp >= s.nbr) return;
   const int mi = s.rsz[warp];
   const int64_t b0 = s.row_ptr[warp], b1 = s.row_ptr[warp + 1];
-  for (int r0 = 0; r0 < mi; r0 += 32) {
-    const int r = r0 + lane;
+  const int K = s.nrhs;
+  for (int r0 = 0; r0 < mi * K; r0 += 32) {
+    const int rv = r0 + lane;  // r * K + v
+    const int r = rv / K, v = rv - (rv / K) * K;
     double acc = 0.0;
     for (int64_t b = b0; b < b1; ++b) {
       const int j = s.col[b];
       const int mj = s.csz[j];
-      const double* xj = s.x + s.coff[j];
+      const double* xj = s.x + (int64_t)s.coff[j] * K + v;
       const double* a = s.vals + s.voff[b];
       if (r < mi) {
         double t = 0.0;
-        for (int q = 0; q < mj; ++q) t = __fma_rn(a[(int64_t)r * mj + q], __ldg(xj + q), t);
+        for (int q = 0; q < mj; ++q) t = __fma_rn(a[(int64_t)r * mj + q], __ldg(xj + (int64_t)q * K), t);
         acc = __dadd_rn(acc, t);
       }
     }
     if (r < mi) {
-      const int64_t i = (int64_t)s.roff[warp] + r;
+      const int64_t i = ((int64_t)s.roff[warp] + r) * K + v;
       epi.store(i, acc, epi.load(i));
     }
   }

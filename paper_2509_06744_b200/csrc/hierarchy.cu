@@ -79,11 +79,12 @@ __global__ void pack_lower_tiles_kernel(const double* __restrict__ full, int64_t
   }
 }
 
+// K right-hand sides interleaved per scalar row; K = 1 is the plain symv
 __global__ void __launch_bounds__(256) symv_tiles_kernel(const double* __restrict__ tiles,
                                                          const double* __restrict__ x, int64_t N, int nt,
-                                                         double* __restrict__ part) {
+                                                         double* __restrict__ part, int K) {
   __shared__ double tl[kTile][kTile + 1];
-  __shared__ double xi[kTile], xj[kTile];
+  __shared__ double xi[8][kTile], xj[8][kTile];
   int I, J;
   tile_of(blockIdx.x, &I, &J);
   const double2* src = reinterpret_cast<const double2*>(tiles + (int64_t)blockIdx.x * kTile * kTile);
@@ -93,32 +94,39 @@ __global__ void __launch_bounds__(256) symv_tiles_kernel(const double* __restric
     tl[r][c] = v.x;
     tl[r][c + 1] = v.y;
   }
-  if (threadIdx.x < kTile) {
-    const int64_t gi = (int64_t)I * kTile + threadIdx.x, gj = (int64_t)J * kTile + threadIdx.x;
-    xi[threadIdx.x] = gi < N ? x[gi] : 0.0;
-    xj[threadIdx.x] = gj < N ? x[gj] : 0.0;
+  for (int e = threadIdx.x; e < kTile * K; e += blockDim.x) {
+    const int t = e / K, v = e - (e / K) * K;
+    const int64_t gi = (int64_t)I * kTile + t, gj = (int64_t)J * kTile + t;
+    xi[v][t] = gi < N ? x[gi * K + v] : 0.0;
+    xj[v][t] = gj < N ? x[gj * K + v] : 0.0;
   }
   __syncthreads();
-  const int t = threadIdx.x;
-  if (t < kTile) {  // row part: tile * x_J
-    double s = 0.0;
-    for (int c = 0; c < kTile; ++c) s = __fma_rn(tl[t][c], xj[c], s);
-    part[((int64_t)I * nt + J) * kTile + t] = s;
-  } else if (t < 2 * kTile && J < I) {  // column part: tile^T * x_I
-    const int c = t - kTile;
-    double s = 0.0;
-    for (int r = 0; r < kTile; ++r) s = __fma_rn(tl[r][c], xi[r], s);
-    part[((int64_t)J * nt + I) * kTile + c] = s;
+  for (int it = threadIdx.x; it < 2 * kTile * K; it += blockDim.x) {
+    const int half = it / (kTile * K);
+    const int rem = it - half * kTile * K;
+    const int t = rem / K, v = rem - (rem / K) * K;
+    if (half == 0) {  // row part: tile * x_J
+      double s = 0.0;
+      for (int c = 0; c < kTile; ++c) s = __fma_rn(tl[t][c], xj[v][c], s);
+      part[(((int64_t)I * nt + J) * kTile + t) * K + v] = s;
+    } else if (J < I) {  // column part: tile^T * x_I
+      double s = 0.0;
+      for (int r = 0; r < kTile; ++r) s = __fma_rn(tl[r][t], xi[v][r], s);
+      part[(((int64_t)J * nt + I) * kTile + t) * K + v] = s;
+    }
   }
 }
 
-__global__ void symv_reduce_kernel(const double* __restrict__ part, int nt, int64_t N, double* __restrict__ y) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= N) return;
+__global__ void symv_reduce_kernel(const double* __restrict__ part, int nt, int64_t N, double* __restrict__ y,
+                                   int K) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= N * K) return;
+  const int64_t i = e / K;
+  const int v = (int)(e - i * K);
   const int I = (int)(i / kTile), r = (int)(i - (int64_t)I * kTile);
   double s = 0.0;
-  for (int J = 0; J < nt; ++J) s = __dadd_rn(s, part[((int64_t)I * nt + J) * kTile + r]);
-  y[i] = s;
+  for (int J = 0; J < nt; ++J) s = __dadd_rn(s, part[(((int64_t)I * nt + J) * kTile + r) * K + v]);
+  y[e] = s;
 }
 
 // Partition-invariant squared norm: one fixed-shape tree per segment of
@@ -183,9 +191,11 @@ struct PLevel {  // one (virtual) rank's share of one level
   SmootherSpec spec;  // Level::smoother (multilevel.hpp:25)
   DBuf<double> v[VNUM];
   int64_t dim = 0;        // scalar length (variable layouts: m = 0, whole levels only)
-  int64_t off() const { return m ? (int64_t)(lo - wlo) * m : 0; }
-  int64_t n_own() const { return m ? (int64_t)(hi - lo) * m : dim; }
-  int64_t n_win() const { return m ? (int64_t)(whi - wlo) * m : dim; }
+  int k = 1;              // right-hand sides per scalar row (batched cycles)
+  int64_t off() const { return m ? (int64_t)(lo - wlo) * m * k : 0; }
+  int64_t n_own() const { return (m ? (int64_t)(hi - lo) * m : dim) * k; }
+  int64_t n_win() const { return (m ? (int64_t)(whi - wlo) * m : dim) * k; }
+  int64_t sc(int rows) const { return (int64_t)rows * m * k; }  // scalar offset of local rows
   bool active() const { return hi > lo; }
 };
 
@@ -201,10 +211,12 @@ struct LevelStats {  // global byte model inputs (bmg_hier_cycle_bytes)
 };
 
 struct GraphKey {
-  int kpre, kpost;
+  int kpre, kpost, nrhs;
   const double* b;
   double* x;
-  bool operator<(const GraphKey& o) const { return std::tie(kpre, kpost, b, x) < std::tie(o.kpre, o.kpost, o.b, o.x); }
+  bool operator<(const GraphKey& o) const {
+    return std::tie(kpre, kpost, nrhs, b, x) < std::tie(o.kpre, o.kpost, o.nrhs, o.b, o.x);
+  }
 };
 
 struct Hier {
@@ -212,6 +224,7 @@ struct Hier {
   int world = 1;          // ranks the rows are split over
   bool emulated = false;  // all virtual ranks live in this process
   std::vector<Part> parts;
+  int nrhs = 1;                               // right-hand sides of the current cycle batch
   std::vector<int> nbr, msz;                  // per level
   std::vector<size_t> nfactors;               // per level: FSAI chain length
   std::vector<std::vector<int32_t>> bounds;   // per level: world + 1
@@ -257,7 +270,7 @@ static double* vec(Hier& h, Part& p, int l, Which w) {
 static void exchange(Hier& h, int l, Which w) {
   if (h.world == 1) return;
   Ctx* ctx = h.ctx;
-  const int m = h.msz[l];
+  const int m = h.msz[l] * h.nrhs;  // scalars per block row
   const auto& B = h.bounds[l];
   if (h.emulated) {
     for (Part& dst : h.parts)
@@ -358,8 +371,8 @@ static void smooth(Hier& h, int l, int k, bool xzero) {
     } else {
       run_pass(h, l, VX, l, [&](Part& p) { return &p.lv[l].sA; },
                [&](Part& p, PLevel& L, const Slice& sl) {
-                 const int64_t o = L.off() + (int64_t)sl.row0 * L.m;
-                 residual(*sl.m, vec(h, p, l, VB) + o, vec(h, p, l, VX), vec(h, p, l, VR) + o);
+                 const int64_t o = L.off() + L.sc(sl.row0);
+                 residual(*sl.m, vec(h, p, l, VB) + o, vec(h, p, l, VX), vec(h, p, l, VR) + o, h.nrhs);
                });
       src = VR;
     }
@@ -375,16 +388,16 @@ static void smooth(Hier& h, int l, int k, bool xzero) {
                  return q < nf ? &L.sF[q] : &L.sB[nb - 1 - (q - nf)];
                },
                [&](Part& p, PLevel& L, const Slice& sl) {
-                 spmv(*sl.m, vec(h, p, l, in), vec(h, p, l, out) + L.off() + (int64_t)sl.row0 * L.m);
+                 spmv(*sl.m, vec(h, p, l, in), vec(h, p, l, out) + L.off() + L.sc(sl.row0), h.nrhs);
                });
       cur = nxt;
       nxt = (nxt == VW) ? VT : VW;
     }
     run_pass(h, l, cur, l, [&](Part& p) -> const SplitMat* { return p.lv[l].sB.empty() ? nullptr : &p.lv[l].sB[0]; },
              [&](Part& p, PLevel& L, const Slice& sl) {
-               const int64_t o = L.off() + (int64_t)sl.row0 * L.m;
+               const int64_t o = L.off() + L.sc(sl.row0);
                gt_cheb(*sl.m, vec(h, p, l, cur), vec(h, p, l, VP) + o, vec(h, p, l, VX) + o, st.coef, st.c, st.first,
-                       zero_x);
+                       zero_x, h.nrhs);
              });
   }
 }
@@ -396,10 +409,11 @@ static void coarse_solve(Hier& h) {
     const int64_t N = h.n0;
     const int nt = (int)((N + kern::kTile - 1) / kern::kTile);
     const int64_t ntiles = (int64_t)nt * (nt + 1) / 2;
+    const int K = h.nrhs;
     kern::symv_tiles_kernel<<<(unsigned)ntiles, 256, 0, h.ctx->stream>>>(p.ainv.p, vec(h, p, 0, VB) + L.off(), N, nt,
-                                                                        p.cpart.p);
-    kern::symv_reduce_kernel<<<(unsigned)((N + 255) / 256), 256, 0, h.ctx->stream>>>(p.cpart.p, nt, N,
-                                                                                      vec(h, p, 0, VX) + L.off());
+                                                                        p.cpart.p, K);
+    kern::symv_reduce_kernel<<<(unsigned)((N * K + 255) / 256), 256, 0, h.ctx->stream>>>(
+        p.cpart.p, nt, N, vec(h, p, 0, VX) + L.off(), K);
     h.ctx->count(2);
     BMG_LAUNCHED(h.ctx->stream, "symv_kernels");
   }
@@ -421,14 +435,14 @@ static void enqueue_vcycle(Hier& h, int kpre, int kpost) {
     if (r == VR) {
       run_pass(h, l, VX, l, [&](Part& p) { return &p.lv[l].sA; },
                [&](Part& p, PLevel& L, const Slice& sl) {
-                 const int64_t o = L.off() + (int64_t)sl.row0 * L.m;
-                 residual(*sl.m, vec(h, p, l, VB) + o, vec(h, p, l, VX), vec(h, p, l, VR) + o);
+                 const int64_t o = L.off() + L.sc(sl.row0);
+                 residual(*sl.m, vec(h, p, l, VB) + o, vec(h, p, l, VX), vec(h, p, l, VR) + o, h.nrhs);
                });
     }
     // rc = P^T r  (multilevel.cpp:95): R rows are own rows of level l - 1
     run_pass(h, l, r, l - 1, [&](Part& p) { return &p.lv[l].sR; },
              [&](Part& p, PLevel& C, const Slice& sl) {
-               spmv(*sl.m, vec(h, p, l, r), vec(h, p, l - 1, VB) + C.off() + (int64_t)sl.row0 * C.m);
+               spmv(*sl.m, vec(h, p, l, r), vec(h, p, l - 1, VB) + C.off() + C.sc(sl.row0), h.nrhs);
              });
   }
   coarse_solve(h);
@@ -436,7 +450,7 @@ static void enqueue_vcycle(Hier& h, int kpre, int kpost) {
     // x += P ec  (multilevel.cpp:98-100)
     run_pass(h, l - 1, VX, l, [&](Part& p) { return &p.lv[l].sP; },
              [&](Part& p, PLevel& L, const Slice& sl) {
-               prolong_add(*sl.m, vec(h, p, l - 1, VX), vec(h, p, l, VX) + L.off() + (int64_t)sl.row0 * L.m);
+               prolong_add(*sl.m, vec(h, p, l - 1, VX), vec(h, p, l, VX) + L.off() + L.sc(sl.row0), h.nrhs);
              });
     smooth(h, l, kpost, false);
   }
@@ -450,7 +464,7 @@ static void stage_in(Hier& h, const double* b, const double* x) {
   for (Part& p : h.parts) {
     PLevel& L = p.lv[top];
     if (!L.active()) continue;
-    const int64_t src = h.emulated ? (int64_t)L.lo * L.m : 0;
+    const int64_t src = h.emulated ? L.sc(L.lo) : 0;
     copy(h.ctx, L.v[VB].p + L.off(), b + src, L.n_own());
     copy(h.ctx, L.v[VX].p + L.off(), x + src, L.n_own());
   }
@@ -461,9 +475,43 @@ static void stage_out(Hier& h, double* x) {
   for (Part& p : h.parts) {
     PLevel& L = p.lv[top];
     if (!L.active()) continue;
-    const int64_t dst = h.emulated ? (int64_t)L.lo * L.m : 0;
+    const int64_t dst = h.emulated ? L.sc(L.lo) : 0;
     copy(h.ctx, x + dst, L.v[VX].p + L.off(), L.n_own());
   }
+}
+
+// batch size of the following cycles: every level's vectors hold K interleaved
+// right-hand sides (grown on demand; setup, Lanczos and solve run at K = 1)
+static void set_nrhs(Hier& h, int K) {
+  if (K != 1 && K != 2 && K != 4 && K != 8) fail(BMG_EINVAL, "v_cycle batch: nrhs must be 1, 2, 4 or 8");
+  if (K == h.nrhs) return;
+  BMG_CUDA(cudaStreamSynchronize(h.ctx->stream));
+  h.nrhs = K;
+  for (Part& p : h.parts) {
+    for (PLevel& L : p.lv) {
+      // launch plans for this batch size (built here, never inside graph capture)
+      auto plans = [&](const SplitMat& sm) {
+        for (const Slice& sl : sm.s) plan_for(*sl.m, K);
+      };
+      plans(L.sA);
+      plans(L.sR);
+      plans(L.sP);
+      for (auto& f : L.sF) plans(f);
+      for (auto& f : L.sB) plans(f);
+      L.k = K;
+      for (int w = 0; w < VNUM; ++w) {
+        if (!L.v[w].p || L.v[w].n >= (size_t)std::max<int64_t>(L.n_win(), 1)) continue;
+        L.v[w].alloc(L.n_win());
+        BMG_CUDA(cudaMemsetAsync(L.v[w].p, 0, L.v[w].bytes(), h.ctx->stream));
+      }
+    }
+    if (p.cpart.p) {
+      const int64_t nt = (h.n0 + kern::kTile - 1) / kern::kTile;
+      const size_t need = (size_t)(nt * nt * kern::kTile * K);
+      if (p.cpart.n < need) p.cpart.alloc(need);
+    }
+  }
+  BMG_CUDA(cudaStreamSynchronize(h.ctx->stream));
 }
 
 static void run_vcycle(Hier& h, int kpre, int kpost, const double* bf, double* xf) {
@@ -483,7 +531,7 @@ static void run_vcycle(Hier& h, int kpre, int kpost, const double* bf, double* x
     stage_out(h, xf);
     return;
   }
-  GraphKey key{kpre, kpost, bf, xf};
+  GraphKey key{kpre, kpost, h.nrhs, bf, xf};
   auto it = h.graphs.find(key);
   if (it == h.graphs.end()) {
     cudaStream_t user = ctx->stream;
@@ -871,7 +919,7 @@ static void finest_residual(Hier& h, const double* b, double* x, double* rtmp) {
   stage_in(h, b, x);
   run_pass(h, top, VX, top, [&](Part& p) { return &p.lv[top].sA; },
            [&](Part& p, PLevel& L, const Slice& sl) {
-             const int64_t o = L.off() + (int64_t)sl.row0 * L.m;
+             const int64_t o = L.off() + L.sc(sl.row0);
              residual(*sl.m, L.v[VB].p + o, L.v[VX].p, L.v[VR].p + o);
            });
 }
@@ -1319,7 +1367,7 @@ static double dist_lanczos(Hier& h, int l, int iters, double safety, uint64_t se
     auto step = [&](auto get, Which out) {
       const Which in = cur;
       run_pass(h, l, in, l, get, [&](Part& p, PLevel& L, const Slice& sl) {
-        spmv(*sl.m, vec(h, p, l, in), vec(h, p, l, out) + L.off() + (int64_t)sl.row0 * L.m);
+        spmv(*sl.m, vec(h, p, l, in), vec(h, p, l, out) + L.off() + L.sc(sl.row0), h.nrhs);
       });
       cur = out;
     };
@@ -1640,7 +1688,7 @@ void need_len(const Vec* v, int64_t n, const char* what) {
 int64_t finest_len(const Hier& h) {
   const int top = h.finest();
   if (h.whole()) return h.parts[0].lv[top].n_own();
-  if (h.emulated) return (int64_t)h.nbr[top] * h.msz[top];
+  if (h.emulated) return (int64_t)h.nbr[top] * h.msz[top] * h.nrhs;
   return h.parts[0].lv[top].n_own();
 }
 }  // namespace
@@ -1914,13 +1962,20 @@ int bmg_hier_level(const bmg_hier* hh, int level, const bmg_bsr** a, const bmg_b
 // algorithmic HBM bytes of one V(k_pre, k_post) cycle over all ranks (BASELINE.md
 // §3 byte model, with the exact A*0 skip on coarse levels)
 int bmg_hier_cycle_bytes(const bmg_hier* hh, int kpre, int kpost, int64_t* bytes) {
+  return bmg_hier_cycle_bytes_batch(hh, kpre, kpost, 1, bytes);
+}
+
+// algorithmic bytes of one (batched) cycle: every matrix streamed once, vector
+// traffic per right-hand side
+int bmg_hier_cycle_bytes_batch(const bmg_hier* hh, int kpre, int kpost, int nrhs, int64_t* bytes) {
   return guard([&] {
     const Hier* h = H_(hh);
+    const int64_t K = std::max(1, nrhs);
     int64_t tot = 0;
     const int top = h->finest();
     for (int l = 1; l <= top; ++l) {
       const LevelStats& s = h->stats[l];
-      const int64_t n = s.n, nc = h->stats[l - 1].n;
+      const int64_t n = s.n * K, nc = h->stats[l - 1].n * K;
       const int64_t apass = s.a_pass + 24 * n;  // x, b read; r write
       const int64_t gvec = 16 * n + 40 * n;     // G: r, w; G^T+cheb: w, p rw, x rw
       const int steps = kpre + kpost;
@@ -1933,7 +1988,7 @@ int bmg_hier_cycle_bytes(const bmg_hier* hh, int kpre, int kpost, int64_t* bytes
     }
     {  // coarse solve: packed lower tiles of A_0^{-1}, x, b, tile partials
       const int64_t nt = (h->n0 + 63) / 64;
-      tot += nt * (nt + 1) / 2 * 64 * 64 * 8 + 16 * h->n0 + 2 * nt * nt * 64 * 8;
+      tot += nt * (nt + 1) / 2 * 64 * 64 * 8 + (16 * h->n0 + 2 * nt * nt * 64 * 8) * K;
     }
     *bytes = tot;
   });
@@ -1944,8 +1999,14 @@ int bmg_hier_use_graph(bmg_hier* hh, int on) {
 }
 
 int bmg_vcycle(bmg_hier* hh, int kpre, int kpost, const bmg_vec* b, bmg_vec* x) {
+  return bmg_vcycle_batch(hh, kpre, kpost, 1, b, x);
+}
+
+int bmg_vcycle_batch(bmg_hier* hh, int kpre, int kpost, int nrhs, const bmg_vec* b, bmg_vec* x) {
   return guard([&] {
     Hier* h = H_(hh);
+    h->ctx->activate();
+    set_nrhs(*h, nrhs);
     const int64_t n = finest_len(*h);
     need_len(V_(b), n, "v_cycle");
     need_len(V_(x), n, "v_cycle");
@@ -1954,9 +2015,15 @@ int bmg_vcycle(bmg_hier* hh, int kpre, int kpost, const bmg_vec* b, bmg_vec* x) 
 }
 
 int bmg_vcycle_host(bmg_hier* hh, int kpre, int kpost, const double* b, double* x) {
+  return bmg_vcycle_batch_host(hh, kpre, kpost, 1, b, x);
+}
+
+int bmg_vcycle_batch_host(bmg_hier* hh, int kpre, int kpost, int nrhs, const double* b, double* x) {
   return guard([&] {
     Hier* h = H_(hh);
     Ctx* ctx = h->ctx;
+    ctx->activate();
+    set_nrhs(*h, nrhs);
     const int64_t n = finest_len(*h);
     if (h->io_b.n < (size_t)n) {
       h->io_b.alloc(std::max<int64_t>(n, 1));
@@ -1975,6 +2042,7 @@ int bmg_solve(bmg_hier* hh, int kpre, int kpost, const bmg_vec* bh, bmg_vec* xh,
               double* hist, int* iters, int* status) {
   return guard([&] {
     Hier* h = H_(hh);
+    set_nrhs(*h, 1);
     const int64_t n = finest_len(*h);
     need_len(V_(bh), n, "solve");
     need_len(V_(xh), n, "solve");

@@ -113,6 +113,7 @@ _SIGS = {
     "bmg_vec_device_ptr": (_P, [_P]),
     "bmg_vec_size": (_I64, [_P]),
     "bmg_spmv": (_I, [_P, _P, _P]),
+    "bmg_spmv_batch": (_I, [_P, _I, _P, _P]),
     "bmg_spmv_t": (_I, [_P, _P, _P]),
     "bmg_residual": (_I, [_P, _P, _P, _P]),
     "bmg_dot": (_I, [_P, _P, _PD]),
@@ -137,6 +138,9 @@ _SIGS = {
     "bmg_hier_beta": (_I, [_P, _I, _PD]),
     "bmg_hier_level": (_I, [_P, _I, _PP, _PP, _PP]),
     "bmg_hier_cycle_bytes": (_I, [_P, _I, _I, _PI64]),
+    "bmg_hier_cycle_bytes_batch": (_I, [_P, _I, _I, _I, _PI64]),
+    "bmg_vcycle_batch": (_I, [_P, _I, _I, _I, _P, _P]),
+    "bmg_vcycle_batch_host": (_I, [_P, _I, _I, _I, _PD, _PD]),
     "bmg_hier_use_graph": (_I, [_P, _I]),
     "bmg_vcycle": (_I, [_P, _I, _I, _P, _P]),
     "bmg_vcycle_host": (_I, [_P, _I, _I, _PD, _PD]),
