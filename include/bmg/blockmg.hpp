@@ -156,6 +156,9 @@ class DeviceVector {
 inline void spmv(const DeviceMatrix& a, const DeviceVector& x, DeviceVector& y) {
   check(bmg_spmv(a.get(), x.get(), y.get()));
 }
+inline void spmv_batch(const DeviceMatrix& a, int nrhs, const DeviceVector& x, DeviceVector& y) {
+  check(bmg_spmv_batch(a.get(), nrhs, x.get(), y.get()));
+}
 inline void spmv_transpose(const DeviceMatrix& a, const DeviceVector& x, DeviceVector& y) {
   check(bmg_spmv_t(a.get(), x.get(), y.get()));
 }
@@ -296,6 +299,17 @@ inline void v_cycle(const Hierarchy& h, const CycleSpec& spec, const DeviceVecto
 inline void v_cycle(const Hierarchy& h, const CycleSpec& spec, const std::vector<double>& b,
                     std::vector<double>& x) {
   check(bmg_vcycle_host(h.get(), spec.k_pre, spec.k_post, b.data(), x.data()));
+}
+
+// K right-hand sides per cycle (K = 1, 2, 4, 8), interleaved per scalar row
+// (b[i*K + v]); each RHS bitwise equal to v_cycle on it alone
+inline void v_cycle_batch(const Hierarchy& h, const CycleSpec& spec, int nrhs, const DeviceVector& b,
+                          DeviceVector& x) {
+  check(bmg_vcycle_batch(h.get(), spec.k_pre, spec.k_post, nrhs, b.get(), x.get()));
+}
+inline void v_cycle_batch(const Hierarchy& h, const CycleSpec& spec, int nrhs, const std::vector<double>& b,
+                          std::vector<double>& x) {
+  check(bmg_vcycle_batch_host(h.get(), spec.k_pre, spec.k_post, nrhs, b.data(), x.data()));
 }
 
 struct SolveReport {  // residual-history analogue of RateReport (experiments.hpp:17-27)
