@@ -282,8 +282,21 @@ def run_ours(args, cfg):
                 H.v_cycle(cfg.k, cfg.k, b_all, x_ref)
             x_ref_h = x_ref.download()
             del x_ref, b_all
-            H = Hierarchy.setup(dA, dT, params)
-            H.partition(ws, granule, agglomerate=agglomerate, rank=rank)
+            del H
+            try:
+                # the scalable route: every rank builds only its extended strips
+                # (bmg_hier_setup_dist); no rank holds a whole partitioned level
+                _, _, gran_l, rad_l = pr.level_grid(cfg)
+                A_ext, T_ext, _, _ = pr.dist_inputs(cfg, ws, rank, agglomerate, params)
+                H = Hierarchy.setup_dist(ctx, BlockSparseMatrix(ctx, A_ext),
+                                         [BlockSparseMatrix(ctx, p) for p in T_ext], gran_l, rad_l, agglomerate,
+                                         params)
+                del A_ext, T_ext
+                setup_kind = "distributed setup"
+            except Exception as e:  # every rank builds the whole hierarchy and keeps its strip
+                H = Hierarchy.setup(dA, dT, params)
+                H.partition(ws, granule, agglomerate=agglomerate, rank=rank)
+                setup_kind = f"replicated setup ({type(e).__name__} in the distributed one)"
             lo_row, hi_row, _, _ = H.part_info(cfg.levels - 1, rank)
             # the partitioned cycle must reproduce it bitwise on every rank's strip
             m_ = cfg.m
@@ -297,7 +310,8 @@ def run_ours(args, cfg):
             if flags.item() != 1:
                 raise RuntimeError("partitioned V-cycle differs from the 1-GPU cycle")
             del bp, xp
-            mode = f"row strips x{ws} (NCCL halos, coarsest {agglomerate} level(s) on rank 0; verified bitwise)"
+            mode = (f"row strips x{ws} ({setup_kind}, NCCL halos, coarsest {agglomerate} level(s) on rank 0; "
+                    f"verified bitwise against the 1-GPU cycle)")
             scaling = "strong"
         except Exception as e:  # keep the run alive: independent replicas instead
             H = Hierarchy.setup(dA, dT, params)

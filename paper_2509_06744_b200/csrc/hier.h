@@ -1,0 +1,227 @@
+// hier.h -- internal data model of the device multilevel hierarchy, shared by
+// hierarchy.cu (construction, partition, C ABI), vcycle.cu (halo exchange, the
+// V-cycle and the solve loop) and dist_setup.cu (distributed setup).
+//
+// Every level of every (virtual) rank keeps its vectors in one contiguous window
+// of global block rows [wlo, whi) that contains its own rows [lo, hi) plus the
+// halo its matrices read; local matrices index columns as `global - wlo`.  A halo
+// exchange therefore moves contiguous slices: rank s sends [max(lo_s, wlo_r),
+// min(hi_s, whi_r)) to rank r.  Per-row arithmetic does not depend on the
+// partition, so partitioned cycles are bitwise equal to the 1-GPU cycle.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <memory>
+#include <tuple>
+#include <vector>
+
+#include "bmg_internal.h"
+
+namespace bmg {
+namespace kern {
+
+// Coarse solve x = A_0^{-1} b with the symmetric inverse stored as packed lower
+// 64 x 64 tiles (half the bytes of a dense GEMV).  Each tile (I, J), J <= I,
+// contributes tile * x_J to rows of I and (J < I) tile^T * x_I to rows of J;
+// partials are summed per row in ascending tile order (deterministic).
+constexpr int kTile = 64;
+
+__device__ __forceinline__ void tile_of(int64_t t, int* I, int* J) {
+  int i = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+  while ((int64_t)(i + 1) * (i + 2) / 2 <= t) ++i;
+  while ((int64_t)i * (i + 1) / 2 > t) --i;
+  *I = i;
+  *J = (int)(t - (int64_t)i * (i + 1) / 2);
+}
+
+}  // namespace kern
+
+inline int grid1d(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)); }
+
+// ============================================================================ data model
+enum Which { VB = 0, VX, VR, VW, VP, VT, VNUM };
+
+// A local matrix cut into row slices (local rows [row0, row0 + nbr)): the
+// interior slice reads only the rank's own columns and runs while the halo
+// exchange is in flight; boundary slices run after it lands.
+struct Slice {
+  int row0 = 0;
+  const Bsr* m = nullptr;
+  std::unique_ptr<Bsr> own;
+  bool interior = true;
+};
+struct SplitMat {
+  std::vector<Slice> s;  // interior slice first
+  void whole(const Bsr* a) {
+    s.clear();
+    if (!a) return;
+    Slice x;
+    x.m = a;
+    s.push_back(std::move(x));
+  }
+};
+
+struct PLevel {  // one (virtual) rank's share of one level
+  int lo = 0, hi = 0;    // own block rows
+  int wlo = 0, whi = 0;  // vector window (block rows)
+  int m = 0;             // uniform block size on this level
+  const Bsr* A = nullptr;
+  const Bsr* R = nullptr;  // restriction to level l-1 (rows: own rows of l-1)
+  const Bsr* P = nullptr;  // prolongation from level l-1 (rows: own rows of l)
+  const Fsai* M = nullptr;
+  std::unique_ptr<Bsr> A_own, R_own, P_own;
+  std::unique_ptr<Fsai> M_own;
+  SplitMat sA, sR, sP;                 // the matrices as launched
+  std::vector<SplitMat> sF, sB;        // FSAI chain factors and their transposes
+  SmootherSpec spec;  // Level::smoother (multilevel.hpp:25)
+  DBuf<double> v[VNUM];
+  int64_t dim = 0;        // scalar length (variable layouts: m = 0, whole levels only)
+  int k = 1;              // right-hand sides per scalar row (batched cycles)
+  int64_t off() const { return m ? (int64_t)(lo - wlo) * m * k : 0; }
+  int64_t n_own() const { return (m ? (int64_t)(hi - lo) * m : dim) * k; }
+  int64_t n_win() const { return (m ? (int64_t)(whi - wlo) * m : dim) * k; }
+  int64_t sc(int rows) const { return (int64_t)rows * m * k; }  // scalar offset of local rows
+  bool active() const { return hi > lo; }
+};
+
+struct Part {
+  int rank = 0;
+  std::vector<PLevel> lv;
+  DBuf<double> ainv;  // A_0^{-1} as packed lower 64x64 tiles (rank owning level 0)
+  DBuf<double> cpart; // per-(tile row, tile) partial sums of the coarse solve
+};
+
+struct LevelStats {  // global byte model inputs (bmg_hier_cycle_bytes)
+  int64_t n = 0, a_pass = 0, m_pass = 0, r_pass = 0, p_pass = 0;
+};
+
+struct GraphKey {
+  int kpre, kpost, nrhs;
+  const double* b;
+  double* x;
+  bool operator<(const GraphKey& o) const {
+    return std::tie(kpre, kpost, nrhs, b, x) < std::tie(o.kpre, o.kpost, o.nrhs, o.b, o.x);
+  }
+};
+
+struct Hier {
+  Ctx* ctx = nullptr;
+  int world = 1;          // ranks the rows are split over
+  bool emulated = false;  // all virtual ranks live in this process
+  std::vector<Part> parts;
+  int nrhs = 1;                               // right-hand sides of the current cycle batch
+  std::vector<int> nbr, msz;                  // per level
+  std::vector<size_t> nfactors;               // per level: FSAI chain length
+  std::vector<std::vector<int32_t>> bounds;   // per level: world + 1
+  std::vector<std::vector<int32_t>> wlo, whi; // per level, per rank
+  int granule_top = 1;                        // block rows per norm segment (top level)
+  int64_t n0 = 0;
+  std::vector<LevelStats> stats;
+  bool use_graph = true;
+  struct Captured {
+    cudaGraphExec_t exec;
+    int64_t kernels;
+  };
+  std::map<GraphKey, Captured> graphs;
+  DBuf<double> io_b, io_x, seg;
+  cudaStream_t comm = nullptr;  // halo exchanges overlap interior slices
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  const double* user_b = nullptr;
+  double* user_x = nullptr;
+  ~Hier() {
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (comm) cudaStreamDestroy(comm);
+  }
+  int finest() const { return (int)nbr.size() - 1; }
+  bool whole() const { return world == 1; }
+  void drop_graphs() {
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
+    graphs.clear();
+  }
+};
+
+// vector of level l on part p; the unpartitioned top level uses the caller's b, x
+inline double* vec(Hier& h, Part& p, int l, Which w) {
+  if (h.whole() && l == h.finest()) {
+    if (w == VB) return const_cast<double*>(h.user_b);
+    if (w == VX) return h.user_x;
+  }
+  return p.lv[l].v[w].p;
+}
+
+// ---- shared operations (vcycle.cu, hierarchy.cu) --------------------------------
+void exchange(Hier& h, int l, Which w);
+void set_nrhs(Hier& h, int K);
+void run_vcycle(Hier& h, int kpre, int kpost, const double* bf, double* xf);
+double finest_norm(Hier& h, const double* r_whole);
+void finest_residual(Hier& h, const double* b, double* x, double* rtmp);
+void coarse_factor(Hier& h, Part& p);
+void alloc_vectors(Hier& h, PLevel& L, bool top);
+std::unique_ptr<Bsr> slice_rows(const Bsr& g, int lo, int hi, int col_lo, int ncols);
+SplitMat split_rows(const Bsr& g, int lo, int hi, int wlo, int nwin, int own_lo, int own_hi);
+
+// One streaming pass over a split matrix whose input is vector `in` of level
+// `in_level`: the exchange of its halo runs on the comm stream while the
+// interior slices compute; boundary slices wait for the exchange.  `get`
+// returns the SplitMat of a part (nullptr: nothing to do), `launch` runs one
+// slice (row offset in scalars = slice.row0 * m of the output level).
+template <class Get, class Launch>
+static void run_pass(Hier& h, int in_level, Which in, int out_level, Get get, Launch launch) {
+  Ctx* ctx = h.ctx;
+  if (h.world == 1) {
+    for (Part& p : h.parts) {
+      PLevel& L = p.lv[out_level];
+      const SplitMat* sm = get(p);
+      if (!L.active() || !sm) continue;
+      for (const Slice& sl : sm->s) launch(p, L, sl);
+    }
+    return;
+  }
+  BMG_CUDA(cudaEventRecord(h.ev_fork, ctx->stream));
+  BMG_CUDA(cudaStreamWaitEvent(h.comm, h.ev_fork, 0));
+  cudaStream_t main = ctx->stream;
+  ctx->stream = h.comm;
+  try {
+    exchange(h, in_level, in);
+  } catch (...) {
+    ctx->stream = main;
+    throw;
+  }
+  ctx->stream = main;
+  BMG_CUDA(cudaEventRecord(h.ev_join, h.comm));
+  for (int phase = 0; phase < 2; ++phase) {
+    if (phase == 1) BMG_CUDA(cudaStreamWaitEvent(ctx->stream, h.ev_join, 0));
+    for (Part& p : h.parts) {
+      PLevel& L = p.lv[out_level];
+      const SplitMat* sm = get(p);
+      if (!L.active() || !sm) continue;
+      for (const Slice& sl : sm->s)
+        if (sl.interior == (phase == 0)) launch(p, L, sl);
+    }
+  }
+}
+
+// ---- C ABI handle casts ----------------------------------------------------------
+inline const Bsr* B_(const bmg_bsr* a) { return reinterpret_cast<const Bsr*>(a); }
+inline const Vec* V_(const bmg_vec* v) { return reinterpret_cast<const Vec*>(v); }
+inline Vec* V_(bmg_vec* v) { return reinterpret_cast<Vec*>(v); }
+inline const Fsai* M_(const bmg_fsai* m) { return reinterpret_cast<const Fsai*>(m); }
+inline Hier* H_(bmg_hier* h) { return reinterpret_cast<Hier*>(h); }
+inline const Hier* H_(const bmg_hier* h) { return reinterpret_cast<const Hier*>(h); }
+inline void need_len(const Vec* v, int64_t n, const char* what) {
+  if (v->n != n) fail(BMG_EINVAL, std::string(what) + ": vector length does not match layout");
+}
+// length of the finest-level vectors the caller passes
+inline int64_t finest_len(const Hier& h) {
+  const int top = h.finest();
+  if (h.whole()) return h.parts[0].lv[top].n_own();
+  if (h.emulated) return (int64_t)h.nbr[top] * h.msz[top] * h.nrhs;
+  return h.parts[0].lv[top].n_own();
+}
+
+}  // namespace bmg

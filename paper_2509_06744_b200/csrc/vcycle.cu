@@ -1,0 +1,397 @@
+// vcycle.cu -- halo exchange, the device-resident V-cycle (multilevel.cpp:77-103;
+// captured as a CUDA graph), batched right-hand sides and the residual norm of the
+// measure_rates-style solve loop (experiments.cpp:15-67).
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <tuple>
+
+#include "bmg_abi.h"
+#include "hier.h"
+
+namespace bmg {
+namespace kern {
+// K right-hand sides interleaved per scalar row; K = 1 is the plain symv
+__global__ void __launch_bounds__(256) symv_tiles_kernel(const double* __restrict__ tiles,
+                                                         const double* __restrict__ x, int64_t N, int nt,
+                                                         double* __restrict__ part, int K) {
+  __shared__ double tl[kTile][kTile + 1];
+  __shared__ double xi[8][kTile], xj[8][kTile];
+  int I, J;
+  tile_of(blockIdx.x, &I, &J);
+  const double2* src = reinterpret_cast<const double2*>(tiles + (int64_t)blockIdx.x * kTile * kTile);
+  for (int e = threadIdx.x; e < kTile * kTile / 2; e += blockDim.x) {
+    const double2 v = __ldg(src + e);
+    const int r = (2 * e) / kTile, c = (2 * e) - r * kTile;
+    tl[r][c] = v.x;
+    tl[r][c + 1] = v.y;
+  }
+  for (int e = threadIdx.x; e < kTile * K; e += blockDim.x) {
+    const int t = e / K, v = e - (e / K) * K;
+    const int64_t gi = (int64_t)I * kTile + t, gj = (int64_t)J * kTile + t;
+    xi[v][t] = gi < N ? x[gi * K + v] : 0.0;
+    xj[v][t] = gj < N ? x[gj * K + v] : 0.0;
+  }
+  __syncthreads();
+  for (int it = threadIdx.x; it < 2 * kTile * K; it += blockDim.x) {
+    const int half = it / (kTile * K);
+    const int rem = it - half * kTile * K;
+    const int t = rem / K, v = rem - (rem / K) * K;
+    if (half == 0) {  // row part: tile * x_J
+      double s = 0.0;
+      for (int c = 0; c < kTile; ++c) s = __fma_rn(tl[t][c], xj[v][c], s);
+      part[(((int64_t)I * nt + J) * kTile + t) * K + v] = s;
+    } else if (J < I) {  // column part: tile^T * x_I
+      double s = 0.0;
+      for (int r = 0; r < kTile; ++r) s = __fma_rn(tl[r][t], xi[v][r], s);
+      part[(((int64_t)J * nt + I) * kTile + t) * K + v] = s;
+    }
+  }
+}
+
+__global__ void symv_reduce_kernel(const double* __restrict__ part, int nt, int64_t N, double* __restrict__ y,
+                                   int K) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= N * K) return;
+  const int64_t i = e / K;
+  const int v = (int)(e - i * K);
+  const int I = (int)(i / kTile), r = (int)(i - (int64_t)I * kTile);
+  double s = 0.0;
+  for (int J = 0; J < nt; ++J) s = __dadd_rn(s, part[(((int64_t)I * nt + J) * kTile + r) * K + v]);
+  y[e] = s;
+}
+
+// Partition-invariant squared norm: one fixed-shape tree per segment of
+// `seg_len` scalars (a segment = one granule of block rows, never split
+// across ranks); segment sums are then added in order on the host.
+__global__ void __launch_bounds__(256) segment_sq_kernel(const double* __restrict__ v, int64_t n, int64_t seg_len,
+                                                         double* __restrict__ out) {
+  __shared__ double sh[256];
+  const int64_t s0 = blockIdx.x * seg_len;
+  const int64_t s1 = min(n, s0 + seg_len);
+  double acc = 0.0;
+  for (int64_t i = s0 + threadIdx.x; i < s1; i += 256) acc = __fma_rn(v[i], v[i], acc);
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = sh[0];
+}
+}  // namespace kern
+
+// ============================================================================ halo exchange
+void exchange(Hier& h, int l, Which w) {
+  if (h.world == 1) return;
+  Ctx* ctx = h.ctx;
+  const int m = h.msz[l] * h.nrhs;  // scalars per block row
+  const auto& B = h.bounds[l];
+  if (h.emulated) {
+    for (Part& dst : h.parts)
+      for (Part& src : h.parts) {
+        if (&dst == &src) continue;
+        const int r = dst.rank, s = src.rank;
+        const int g0 = std::max(B[s], h.wlo[l][r]), g1 = std::min(B[s + 1], h.whi[l][r]);
+        if (g1 <= g0) continue;
+        double* d = vec(h, dst, l, w) + (int64_t)(g0 - h.wlo[l][r]) * m;
+        const double* sp = vec(h, src, l, w) + (int64_t)(g0 - h.wlo[l][s]) * m;
+        BMG_CUDA(cudaMemcpyAsync(d, sp, (size_t)(g1 - g0) * m * sizeof(double), cudaMemcpyDeviceToDevice,
+                                 ctx->stream));
+      }
+    return;
+  }
+  Part& me = h.parts[0];
+  const int r = me.rank;
+  double* base = vec(h, me, l, w);
+  Comm& comm = *ctx->comm;
+  comm.group_start();
+  for (int s = 0; s < h.world; ++s) {
+    if (s == r) continue;
+    // send my own rows inside s's window
+    const int a0 = std::max(B[r], h.wlo[l][s]), a1 = std::min(B[r + 1], h.whi[l][s]);
+    if (a1 > a0)
+      comm.send(base + (int64_t)(a0 - h.wlo[l][r]) * m, (size_t)(a1 - a0) * m, DType::F64, s, ctx->stream);
+    // receive s's own rows inside my window
+    const int b0 = std::max(B[s], h.wlo[l][r]), b1 = std::min(B[s + 1], h.whi[l][r]);
+    if (b1 > b0)
+      comm.recv(base + (int64_t)(b0 - h.wlo[l][r]) * m, (size_t)(b1 - b0) * m, DType::F64, s, ctx->stream);
+  }
+  comm.group_end();
+}
+
+// ============================================================================ V-cycle
+// one smoother application (apply_smoother, chebyshev.hpp:117-129) on level l, all parts
+static void smooth(Hier& h, int l, int k, bool xzero) {
+  if (k < 1) return;
+  const SmootherSpec* spec = nullptr;
+  const Fsai* M0 = nullptr;
+  for (Part& p : h.parts)
+    if (p.lv[l].active()) {
+      spec = &p.lv[l].spec;
+      M0 = p.lv[l].M;
+    }
+  if (!spec) {  // this rank owns no rows of the level: it only serves halos
+    spec = &h.parts[0].lv[l].spec;
+  }
+  const auto steps = smoother_schedule(*spec, k);
+  const size_t nf = M0 ? M0->fwd.size() : h.nfactors[l], nb = nf;
+  for (size_t s = 0; s < steps.size(); ++s) {
+    const StepScalars& st = steps[s];
+    Which src;
+    const bool zero_x = (s == 0 && xzero);
+    if (zero_x) {
+      src = VB;  // A * 0 = 0: r = b exactly
+    } else {
+      run_pass(h, l, VX, l, [&](Part& p) { return &p.lv[l].sA; },
+               [&](Part& p, PLevel& L, const Slice& sl) {
+                 const int64_t o = L.off() + L.sc(sl.row0);
+                 residual(*sl.m, vec(h, p, l, VB) + o, vec(h, p, l, VX), vec(h, p, l, VR) + o, h.nrhs);
+               });
+      src = VR;
+    }
+    // forward chain w = F_n ... F_0 r (nest = 0: w = G r), then all but the last transpose
+    Which cur = src;
+    Which nxt = VW;
+    for (size_t q = 0; q < nf + nb - 1; ++q) {
+      const Which in = cur, out = nxt;
+      run_pass(h, l, in, l,
+               [&](Part& p) -> const SplitMat* {
+                 PLevel& L = p.lv[l];
+                 if (L.sF.empty()) return nullptr;
+                 return q < nf ? &L.sF[q] : &L.sB[nb - 1 - (q - nf)];
+               },
+               [&](Part& p, PLevel& L, const Slice& sl) {
+                 spmv(*sl.m, vec(h, p, l, in), vec(h, p, l, out) + L.off() + L.sc(sl.row0), h.nrhs);
+               });
+      cur = nxt;
+      nxt = (nxt == VW) ? VT : VW;
+    }
+    run_pass(h, l, cur, l, [&](Part& p) -> const SplitMat* { return p.lv[l].sB.empty() ? nullptr : &p.lv[l].sB[0]; },
+             [&](Part& p, PLevel& L, const Slice& sl) {
+               const int64_t o = L.off() + L.sc(sl.row0);
+               gt_cheb(*sl.m, vec(h, p, l, cur), vec(h, p, l, VP) + o, vec(h, p, l, VX) + o, st.coef, st.c, st.first,
+                       zero_x, h.nrhs);
+             });
+  }
+}
+
+static void coarse_solve(Hier& h) {
+  for (Part& p : h.parts) {
+    PLevel& L = p.lv[0];
+    if (!L.active()) continue;
+    const int64_t N = h.n0;
+    const int nt = (int)((N + kern::kTile - 1) / kern::kTile);
+    const int64_t ntiles = (int64_t)nt * (nt + 1) / 2;
+    const int K = h.nrhs;
+    kern::symv_tiles_kernel<<<(unsigned)ntiles, 256, 0, h.ctx->stream>>>(p.ainv.p, vec(h, p, 0, VB) + L.off(), N, nt,
+                                                                        p.cpart.p, K);
+    kern::symv_reduce_kernel<<<(unsigned)((N * K + 255) / 256), 256, 0, h.ctx->stream>>>(
+        p.cpart.p, nt, N, vec(h, p, 0, VX) + L.off(), K);
+    h.ctx->count(2);
+    BMG_LAUNCHED(h.ctx->stream, "symv_kernels");
+  }
+}
+
+// v_cycle (multilevel.cpp:77-103), recursion unrolled: down, coarse solve, up
+static void enqueue_vcycle(Hier& h, int kpre, int kpost) {
+  const int top = h.finest();
+  for (int l = top; l >= 1; --l) {
+    const bool xzero = l < top;
+    Which r = VR;
+    if (kpre > 0) {
+      smooth(h, l, kpre, xzero);
+    } else if (xzero) {
+      for (Part& p : h.parts)
+        if (p.lv[l].active()) fill(h.ctx, vec(h, p, l, VX) + p.lv[l].off(), p.lv[l].n_own(), 0.0);
+      r = VB;
+    }
+    if (r == VR) {
+      run_pass(h, l, VX, l, [&](Part& p) { return &p.lv[l].sA; },
+               [&](Part& p, PLevel& L, const Slice& sl) {
+                 const int64_t o = L.off() + L.sc(sl.row0);
+                 residual(*sl.m, vec(h, p, l, VB) + o, vec(h, p, l, VX), vec(h, p, l, VR) + o, h.nrhs);
+               });
+    }
+    // rc = P^T r  (multilevel.cpp:95): R rows are own rows of level l - 1
+    run_pass(h, l, r, l - 1, [&](Part& p) { return &p.lv[l].sR; },
+             [&](Part& p, PLevel& C, const Slice& sl) {
+               spmv(*sl.m, vec(h, p, l, r), vec(h, p, l - 1, VB) + C.off() + C.sc(sl.row0), h.nrhs);
+             });
+  }
+  coarse_solve(h);
+  for (int l = 1; l <= top; ++l) {
+    // x += P ec  (multilevel.cpp:98-100)
+    run_pass(h, l - 1, VX, l, [&](Part& p) { return &p.lv[l].sP; },
+             [&](Part& p, PLevel& L, const Slice& sl) {
+               prolong_add(*sl.m, vec(h, p, l - 1, VX), vec(h, p, l, VX) + L.off() + L.sc(sl.row0), h.nrhs);
+             });
+    smooth(h, l, kpost, false);
+  }
+}
+
+// copy the caller's finest-level b, x into the partitioned buffers (and back);
+// emulated: global vectors; NCCL: this rank's own rows
+static void stage_in(Hier& h, const double* b, const double* x) {
+  if (h.whole()) return;
+  const int top = h.finest();
+  for (Part& p : h.parts) {
+    PLevel& L = p.lv[top];
+    if (!L.active()) continue;
+    const int64_t src = h.emulated ? L.sc(L.lo) : 0;
+    copy(h.ctx, L.v[VB].p + L.off(), b + src, L.n_own());
+    copy(h.ctx, L.v[VX].p + L.off(), x + src, L.n_own());
+  }
+}
+static void stage_out(Hier& h, double* x) {
+  if (h.whole()) return;
+  const int top = h.finest();
+  for (Part& p : h.parts) {
+    PLevel& L = p.lv[top];
+    if (!L.active()) continue;
+    const int64_t dst = h.emulated ? L.sc(L.lo) : 0;
+    copy(h.ctx, x + dst, L.v[VX].p + L.off(), L.n_own());
+  }
+}
+
+// batch size of the following cycles: every level's vectors hold K interleaved
+// right-hand sides (grown on demand; setup, Lanczos and solve run at K = 1)
+void set_nrhs(Hier& h, int K) {
+  if (K != 1 && K != 2 && K != 4 && K != 8) fail(BMG_EINVAL, "v_cycle batch: nrhs must be 1, 2, 4 or 8");
+  if (K == h.nrhs) return;
+  BMG_CUDA(cudaStreamSynchronize(h.ctx->stream));
+  h.nrhs = K;
+  for (Part& p : h.parts) {
+    for (PLevel& L : p.lv) {
+      // launch plans for this batch size (built here, never inside graph capture)
+      auto plans = [&](const SplitMat& sm) {
+        for (const Slice& sl : sm.s) plan_for(*sl.m, K);
+      };
+      plans(L.sA);
+      plans(L.sR);
+      plans(L.sP);
+      for (auto& f : L.sF) plans(f);
+      for (auto& f : L.sB) plans(f);
+      L.k = K;
+      for (int w = 0; w < VNUM; ++w) {
+        if (!L.v[w].p || L.v[w].n >= (size_t)std::max<int64_t>(L.n_win(), 1)) continue;
+        L.v[w].alloc(L.n_win());
+        BMG_CUDA(cudaMemsetAsync(L.v[w].p, 0, L.v[w].bytes(), h.ctx->stream));
+      }
+    }
+    if (p.cpart.p) {
+      const int64_t nt = (h.n0 + kern::kTile - 1) / kern::kTile;
+      const size_t need = (size_t)(nt * nt * kern::kTile * K);
+      if (p.cpart.n < need) p.cpart.alloc(need);
+    }
+  }
+  BMG_CUDA(cudaStreamSynchronize(h.ctx->stream));
+}
+
+void run_vcycle(Hier& h, int kpre, int kpost, const double* bf, double* xf) {
+  if (kpre + kpost < 1) fail(BMG_EINVAL, "v_cycle: cycle needs at least one smoothing step");
+  Ctx* ctx = h.ctx;
+  h.user_b = bf;
+  h.user_x = xf;
+  if (h.finest() == 0) {
+    stage_in(h, bf, xf);
+    coarse_solve(h);
+    stage_out(h, xf);
+    return;
+  }
+  if (!h.use_graph || (ctx->comm && !ctx->comm->capturable())) {
+    stage_in(h, bf, xf);
+    enqueue_vcycle(h, kpre, kpost);
+    stage_out(h, xf);
+    return;
+  }
+  GraphKey key{kpre, kpost, h.nrhs, bf, xf};
+  auto it = h.graphs.find(key);
+  if (it == h.graphs.end()) {
+    cudaStream_t user = ctx->stream;
+    ctx->stream = ctx->own;
+    const int64_t before = ctx->launches;
+    BMG_CUDA(cudaStreamBeginCapture(ctx->own, cudaStreamCaptureModeThreadLocal));
+    try {
+      stage_in(h, bf, xf);
+      enqueue_vcycle(h, kpre, kpost);
+      stage_out(h, xf);
+    } catch (...) {
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(ctx->own, &g);
+      if (g) cudaGraphDestroy(g);
+      ctx->stream = user;
+      ctx->launches = before;
+      throw;
+    }
+    cudaGraph_t g;
+    BMG_CUDA(cudaStreamEndCapture(ctx->own, &g));
+    ctx->stream = user;
+    cudaGraphExec_t ex;
+    BMG_CUDA(cudaGraphInstantiate(&ex, g, 0));
+    cudaGraphDestroy(g);
+    it = h.graphs.emplace(key, Hier::Captured{ex, ctx->launches - before}).first;
+    ctx->launches = before;
+  }
+  BMG_CUDA(cudaGraphLaunch(it->second.exec, ctx->stream));
+  ctx->launches += it->second.kernels;
+}
+
+// partition-invariant ||r||_2 of the finest level (segments = granules)
+double finest_norm(Hier& h, const double* r_whole) {
+  Ctx* ctx = h.ctx;
+  const int top = h.finest();
+  const int m = h.msz[top];
+  const int gran = h.granule_top;
+  // variable layouts (whole levels only): fixed 256-scalar segments
+  const int64_t dimv = m ? 0 : h.parts[0].lv[top].dim;
+  const int nseg = m ? (h.nbr[top] + gran - 1) / gran : (int)((dimv + 255) / 256);
+  if (h.seg.n < (size_t)nseg) h.seg.alloc(std::max(nseg, 1));
+  BMG_CUDA(cudaMemsetAsync(h.seg.p, 0, nseg * sizeof(double), ctx->stream));
+  for (Part& p : h.parts) {
+    PLevel& L = p.lv[top];
+    if (!L.active()) continue;
+    const double* r = h.whole() ? r_whole : L.v[VR].p + L.off();
+    const int s0 = m ? L.lo / gran : 0;
+    const int ns = m ? (L.hi - L.lo + gran - 1) / gran : nseg;
+    if (ns == 0) continue;
+    kern::segment_sq_kernel<<<ns, 256, 0, ctx->stream>>>(r, L.n_own(), m ? (int64_t)gran * m : 256, h.seg.p + s0);
+    ctx->count();
+    BMG_CUDA(cudaGetLastError());
+  }
+  if (!h.whole() && !h.emulated) {
+    // one rank owns each segment; the others contribute exact zeros
+    ctx->comm->allreduce(h.seg.p, h.seg.p, nseg, DType::F64, ROp::Sum, ctx->stream);
+  }
+  std::vector<double> hs(nseg);
+  BMG_CUDA(cudaMemcpyAsync(hs.data(), h.seg.p, nseg * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+  double s = 0.0;
+  for (double v : hs) s += v;
+  return std::sqrt(s);
+}
+
+void finest_residual(Hier& h, const double* b, double* x, double* rtmp) {
+  const int top = h.finest();
+  if (h.whole()) {
+    residual(*h.parts[0].lv[top].A, b, x, rtmp);
+    return;
+  }
+  h.user_b = b;
+  h.user_x = x;
+  stage_in(h, b, x);
+  run_pass(h, top, VX, top, [&](Part& p) { return &p.lv[top].sA; },
+           [&](Part& p, PLevel& L, const Slice& sl) {
+             const int64_t o = L.off() + L.sc(sl.row0);
+             residual(*sl.m, L.v[VB].p + o, L.v[VX].p, L.v[VR].p + o);
+           });
+}
+
+}  // namespace bmg
