@@ -118,3 +118,30 @@ def test_batched_partitioned_loopback(ctx):
     if errs:
         raise errs[0]
     assert np.array_equal(np.concatenate(out), want)
+
+
+@pytest.mark.parametrize("kpre,kpost", [(0, 4), (5, 0), (1, 2)])
+def test_batched_asymmetric_cycles(ctx, kpre, kpost):
+    cfg = pr.CONFIGS["C2"].scaled(32, 3)
+    h, A, T, b = _hier(ctx, cfg)
+    B, X = _rhs(b.size, 4, 9)
+    want = []
+    for v in range(4):
+        xv = Vector(ctx, X[:, v].copy())
+        h.v_cycle(kpre, kpost, Vector(ctx, B[:, v].copy()), xv)
+        want.append(xv.download())
+    bv, xv = Vector(ctx, B.ravel().copy()), Vector(ctx, X.ravel().copy())
+    h.v_cycle_batch(kpre, kpost, 4, bv, xv)
+    assert np.array_equal(xv.download().reshape(-1, 4), np.stack(want, axis=1))
+
+
+def test_batch_rejects_bad_sizes(ctx):
+    from paper_2509_06744_b200.native import InvalidArgument
+    cfg = pr.CONFIGS["C2"].scaled(16, 2)
+    h, A, T, b = _hier(ctx, cfg)
+    with pytest.raises(InvalidArgument):
+        h.v_cycle_batch(3, 3, 3, Vector(ctx, b.size * 3), Vector(ctx, b.size * 3))
+    with pytest.raises(InvalidArgument):
+        h.v_cycle_batch(3, 3, 4, Vector(ctx, b.size * 2), Vector(ctx, b.size * 2))
+    with pytest.raises(InvalidArgument):
+        h.v_cycle_batch(0, 0, 2, Vector(ctx, b.size * 2), Vector(ctx, b.size * 2))

@@ -331,7 +331,7 @@ def test_apply_smoother_kinds_match_oracle(ctx, kind):
         assert np.linalg.norm(xv.download() - want) <= 1e-12 * np.linalg.norm(want)
 
 
-@pytest.mark.parametrize("kind,kpre,kpost", [(1, 2, 2), (0, 3, 3), (2, 6, 0)])
+@pytest.mark.parametrize("kind,kpre,kpost", [(1, 2, 2), (0, 3, 3), (2, 6, 0), (2, 0, 4), (2, 1, 5)])
 def test_vcycle_smoother_kinds_and_v2k0(ctx, kind, kpre, kpost):
     # SetupParams::kind / first_kind_fraction / richardson_omega (multilevel.hpp:39-42,
     # multilevel.cpp:62-65) and CycleSpec::v2k0 (multilevel.hpp:18)
