@@ -268,6 +268,7 @@ void set_nrhs(Hier& h, int K) {
   if (K == h.nrhs) return;
   BMG_CUDA(cudaStreamSynchronize(h.ctx->stream));
   h.nrhs = K;
+  bool moved = false;  // captured graphs of every batch size point at the old buffers
   for (Part& p : h.parts) {
     for (PLevel& L : p.lv) {
       // launch plans for this batch size (built here, never inside graph capture)
@@ -282,6 +283,7 @@ void set_nrhs(Hier& h, int K) {
       L.k = K;
       for (int w = 0; w < VNUM; ++w) {
         if (!L.v[w].p || L.v[w].n >= (size_t)std::max<int64_t>(L.n_win(), 1)) continue;
+        moved = true;
         L.v[w].alloc(L.n_win());
         BMG_CUDA(cudaMemsetAsync(L.v[w].p, 0, L.v[w].bytes(), h.ctx->stream));
       }
@@ -289,9 +291,13 @@ void set_nrhs(Hier& h, int K) {
     if (p.cpart.p) {
       const int64_t nt = (h.n0 + kern::kTile - 1) / kern::kTile;
       const size_t need = (size_t)(nt * nt * kern::kTile * K);
-      if (p.cpart.n < need) p.cpart.alloc(need);
+      if (p.cpart.n < need) {
+        moved = true;
+        p.cpart.alloc(need);
+      }
     }
   }
+  if (moved) h.drop_graphs();
   BMG_CUDA(cudaStreamSynchronize(h.ctx->stream));
 }
 
