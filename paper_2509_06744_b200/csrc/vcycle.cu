@@ -60,11 +60,21 @@ __global__ void symv_reduce_kernel(const double* __restrict__ part, int nt, int6
                                    int K) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= N * K) return;
-  const int64_t i = e / K;
+  const int64_t i = K == 1 ? e : e / K;
   const int v = (int)(e - i * K);
   const int I = (int)(i / kTile), r = (int)(i - (int64_t)I * kTile);
+  const double* __restrict__ pp = part + (((int64_t)I * nt) * kTile + r) * K + v;
+  const int64_t stride = (int64_t)kTile * K;
   double s = 0.0;
-  for (int J = 0; J < nt; ++J) s = __dadd_rn(s, part[(((int64_t)I * nt + J) * kTile + r) * K + v]);
+  int J = 0;
+  for (; J + 16 <= nt; J += 16) {  // sixteen loads in flight, additions in tile order
+    double t[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) t[u] = __ldg(pp + (int64_t)(J + u) * stride);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) s = __dadd_rn(s, t[u]);
+  }
+  for (; J < nt; ++J) s = __dadd_rn(s, __ldg(pp + (int64_t)J * stride));
   y[e] = s;
 }
 
