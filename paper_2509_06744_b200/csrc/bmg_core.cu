@@ -209,14 +209,13 @@ static int chunk_blocks(int mr, int bs) {
 }
 
 // shared-memory attributes of one instantiation: the largest dynamic size; batched
-// (K > 1) kernels also ask for the max-shared carveout (their partials grow with
-// K); K = 1 keeps the default split, whose larger L1 serves the x gathers
+// (K > 1) kernels also ask for a larger shared-memory carveout (their partials grow
+// with K) but not the maximum: the x gathers live in L1; K = 1 keeps the default
 template <class F>
 static void stream_attrs(F kfn, int K) {
   BMG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-  if (K > 1)
-    BMG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                  (int)cudaSharedmemCarveoutMaxShared));
+  if (K > 1)  // ~196 KB of shared memory (3 CTAs of the batched plans), ~60 KB left to L1 for x
+    BMG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 86));
 }
 
 template <int MR, int MC, int K>
