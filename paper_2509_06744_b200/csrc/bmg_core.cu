@@ -193,7 +193,7 @@ static int ring_stages() {
 // several CTAs fit per SM.  Caps measured on B200 (tools/kernel_sweep.py, residual
 // pass on each config family's fine operator): 24 KB for m = 10 and 20, 32 KB for
 // m = 15 and 21.  BMG_CHUNK_KB overrides the cap for every m.
-static int chunk_blocks(int mr, int bs) {
+static int chunk_blocks(int mr, int bs, int K = 1) {
   static int env_cap = [] {
     const char* e = std::getenv("BMG_CHUNK_KB");
     if (!e) return 0;
@@ -202,7 +202,12 @@ static int chunk_blocks(int mr, int bs) {
     if (kb > 48) kb = 48;
     return kb * 1024;
   }();
-  const int cap = env_cap ? env_cap : ((mr == 15 || mr == 21) ? 32 : 24) * 1024;
+  // measured sweeps (profiles/r01_kernel_sweep.jsonl, r01_batched_spmv_sweep.jsonl):
+  // batched 3-D m = 20 wants more blocks per barrier, batched m = 10 fewer
+  int kb = (mr == 15 || mr == 21) ? 32 : 24;
+  if (K > 1 && mr == 20) kb = 48;
+  if (K == 8 && mr == 10) kb = 16;
+  const int cap = env_cap ? env_cap : kb * 1024;
   const int by_items = std::max(1, kern::kConsumers / mr);
   const int by_bytes = std::max(1, cap / (bs * 8));
   return std::min(by_items, by_bytes);
@@ -252,7 +257,7 @@ static int occupancy_for(int mr, int mc, size_t smem, int K = 1) {
 static void build_plan_into(const Bsr& a, Plan& P, int K) {
   P = Plan();
   if (!(a.uniform && stream_supported(a.mr, a.mc)) || a.nbr == 0) return;
-  P.cb_max = chunk_blocks(a.mr, a.bs);
+  P.cb_max = chunk_blocks(a.mr, a.bs, K);
   P.stages = ring_stages();
   const auto& rp = a.h_row_ptr;
   // chunk list per CTA range
