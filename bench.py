@@ -424,10 +424,10 @@ def run_ours(args, cfg):
             extra["C1"] = measure_c1(ctx, stream, args.steps)
         except Exception as e:  # secondary lines never fail the headline run
             extra["C1"] = {"error": f"{type(e).__name__}: {e}"}
-        try:  # the same hierarchy on 4 right-hand sides per cycle (bmg_vcycle_batch)
-            extra["C2x4"] = measure_batch(ctx, stream, H, b_own, k, 4, args.steps)
+        try:  # the same hierarchy on 8 right-hand sides per cycle (bmg_vcycle_batch)
+            extra["C2x8"] = measure_batch(ctx, stream, H, b_own, k, 8, args.steps)
         except Exception as e:
-            extra["C2x4"] = {"error": f"{type(e).__name__}: {e}"}
+            extra["C2x8"] = {"error": f"{type(e).__name__}: {e}"}
         if not args.no_c4:
             # largest single-GPU config (C4, ~110 GB): free the headline hierarchy first
             del H, dA, dT, bv, xv, rv
