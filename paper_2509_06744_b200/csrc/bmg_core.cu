@@ -40,8 +40,17 @@ thread_local int g_last_pivot = -1;
 Ctx::~Ctx() {
   comm.reset();
   if (solver) cusolverDnDestroy(solver);
+  if (blas) cublasDestroy(blas);
   if (h_red) cudaFreeHost(h_red);
   if (own) cudaStreamDestroy(own);
+}
+
+cublasHandle_t Ctx::cublas() {
+  if (!blas) {
+    if (cublasCreate(&blas) != CUBLAS_STATUS_SUCCESS) fail(BMG_ECUDA, "cublasCreate failed");
+  }
+  cublasSetStream(blas, stream);
+  return blas;
 }
 
 cusolverDnHandle_t Ctx::cusolver() {

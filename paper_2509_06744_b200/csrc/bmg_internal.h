@@ -1,6 +1,7 @@
 // bmg_internal.h -- host-side object model behind the C ABI (include/bmg_cuda.h).
 #pragma once
 #include <cuda_runtime.h>
+#include <cublas_v2.h>
 #include <cusolverDn.h>
 
 #include <cstdint>
@@ -92,6 +93,8 @@ struct Ctx {
   void activate() const { BMG_CUDA(cudaSetDevice(device)); }
   void count(int n = 1) { launches += n; }
   cusolverDnHandle_t cusolver();
+  cublasHandle_t blas = nullptr;
+  cublasHandle_t cublas();
   ~Ctx();
 };
 

@@ -90,7 +90,9 @@ struct PLevel {  // one (virtual) rank's share of one level
 struct Part {
   int rank = 0;
   std::vector<PLevel> lv;
-  DBuf<double> ainv;  // A_0^{-1} as packed lower 64x64 tiles (rank owning level 0)
+  DBuf<double> ainv;  // A_0^{-1} as packed lower 64x64 tiles (rank owning level 0), or
+                      // W = L^{-1} (A_0 = L L^T) when the coarse level is triangular
+  bool tri = false;   // coarse solve as x = W^T (W b): N0^2 >= 2^31 (no 64-bit potri)
   DBuf<double> cpart; // per-(tile row, tile) partial sums of the coarse solve
 };
 

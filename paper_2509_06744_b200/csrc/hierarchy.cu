@@ -45,14 +45,17 @@ __global__ void symmetrize_dense_kernel(double* a, int64_t N) {
   }
 }
 
-__global__ void pack_lower_tiles_kernel(const double* __restrict__ full, int64_t N, double* __restrict__ tiles) {
+// lower 64x64 tiles of a row-major N x N matrix; `strict` zeroes entries above the
+// diagonal (a triangular matrix whose upper half holds other data)
+__global__ void pack_lower_tiles_kernel(const double* __restrict__ full, int64_t N, double* __restrict__ tiles,
+                                        int strict) {
   int I, J;
   tile_of(blockIdx.x, &I, &J);
   double* dst = tiles + (int64_t)blockIdx.x * kTile * kTile;
   for (int e = threadIdx.x; e < kTile * kTile; e += blockDim.x) {
     const int r = e / kTile, c = e - r * kTile;
     const int64_t gr = (int64_t)I * kTile + r, gc = (int64_t)J * kTile + c;
-    dst[e] = (gr < N && gc < N) ? full[gr * N + gc] : 0.0;
+    dst[e] = (gr < N && gc < N && (!strict || gc <= gr)) ? full[gr * N + gc] : 0.0;
   }
 }
 
@@ -79,6 +82,55 @@ struct SetupClock {
 };
 
 // ============================================================================ construction
+// In-place inverse of the lower-triangular column-major n x n block at `a` (leading
+// dimension lda).  cuSOLVER's Xtrtri rejects n^2 >= 2^31, so larger blocks recurse on
+// their diagonal halves and finish the off-diagonal block with two in-place 64-bit
+// TRMMs: W21 = -W22 L21 W11.
+static void tri_inverse(Ctx* ctx, double* a, int64_t n, int64_t lda, DBuf<double>& scratch) {
+  constexpr int64_t kMax = ((int64_t)1 << 31) - 1;
+  if (n * n < kMax) {
+    const bool compact = lda != n;
+    double* w = a;
+    if (compact) {
+      if (scratch.n < (size_t)(n * n)) scratch.alloc(n * n);
+      w = scratch.p;
+      BMG_CUDA(cudaMemcpy2DAsync(w, n * 8, a, lda * 8, n * 8, n, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    cusolverDnHandle_t s = ctx->cusolver();
+    size_t dws = 0, hws = 0;
+    if (cusolverDnXtrtri_bufferSize(s, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, n, CUDA_R_64F, w, n, &dws,
+                                    &hws) != CUSOLVER_STATUS_SUCCESS)
+      fail(BMG_ECUDA, "cusolverDnXtrtri_bufferSize failed");
+    DBuf<unsigned char> dwork(std::max<size_t>(dws, 1));
+    std::vector<unsigned char> hwork(std::max<size_t>(hws, 1));
+    DBuf<int> info(1);
+    const auto st = cusolverDnXtrtri(s, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, n, CUDA_R_64F, w, n, dwork.p,
+                                     dws, hwork.data(), hws, info.p);
+    if (st != CUSOLVER_STATUS_SUCCESS)
+      fail(BMG_ECUDA, "cusolverDnXtrtri failed (status " + std::to_string((int)st) + ", n " + std::to_string(n) + ")");
+    int hinfo = 0;
+    BMG_CUDA(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (hinfo != 0) fail(BMG_ERUNTIME, "setup: coarse triangular inverse failed");
+    if (compact)
+      BMG_CUDA(cudaMemcpy2DAsync(a, lda * 8, w, n * 8, n * 8, n, cudaMemcpyDeviceToDevice, ctx->stream));
+    return;
+  }
+  const int64_t n1 = (n / 2 + 63) / 64 * 64, n2 = n - n1;
+  double* a22 = a + n1 + n1 * lda;
+  double* a21 = a + n1;
+  tri_inverse(ctx, a, n1, lda, scratch);
+  tri_inverse(ctx, a22, n2, lda, scratch);
+  cublasHandle_t b = ctx->cublas();
+  const double one = 1.0, minus = -1.0;
+  if (cublasDtrmm_v2_64(b, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, n2, n1, &one,
+                        a, lda, a21, lda, a21, lda) != CUBLAS_STATUS_SUCCESS)
+    fail(BMG_ECUDA, "cublasDtrmm (L21 W11) failed");
+  if (cublasDtrmm_v2_64(b, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, n2, n1, &minus,
+                        a22, lda, a21, lda, a21, lda) != CUBLAS_STATUS_SUCCESS)
+    fail(BMG_ECUDA, "cublasDtrmm (W22 L21 W11) failed");
+}
+
 void coarse_factor(Hier& h, Part& p) {
   Ctx* ctx = h.ctx;
   const Bsr& a0 = *p.lv[0].A;
@@ -92,24 +144,60 @@ void coarse_factor(Hier& h, Part& p) {
   ctx->count();
   BMG_CUDA(cudaGetLastError());
   cusolverDnHandle_t s = ctx->cusolver();
-  int lwork = 0, lwork2 = 0;
-  if (cusolverDnDpotrf_bufferSize(s, CUBLAS_FILL_MODE_LOWER, (int)N, p.ainv.p, (int)N, &lwork) != CUSOLVER_STATUS_SUCCESS)
-    fail(BMG_ECUDA, "cusolverDnDpotrf_bufferSize failed");
-  if (cusolverDnDpotri_bufferSize(s, CUBLAS_FILL_MODE_LOWER, (int)N, p.ainv.p, (int)N, &lwork2) != CUSOLVER_STATUS_SUCCESS)
-    fail(BMG_ECUDA, "cusolverDnDpotri_bufferSize failed");
-  DBuf<double> work(std::max(std::max(lwork, lwork2), 1));
+  // 32-bit potrf + potri while N^2 < 2^31; beyond that (C3, C5 coarsest levels) the
+  // 64-bit Xpotrf + Xtrtri give W = L^{-1} and the solve is x = W^T (W b)
+  static const bool force_tri = [] {
+    const char* e = std::getenv("BMG_COARSE_TRIANGULAR");
+    return e && e[0] == '1';
+  }();
+  p.tri = force_tri || N * N >= ((int64_t)1 << 31) - 1;
   DBuf<int> info(1);
-  if (cusolverDnDpotrf(s, CUBLAS_FILL_MODE_LOWER, (int)N, p.ainv.p, (int)N, work.p, lwork, info.p) != CUSOLVER_STATUS_SUCCESS)
-    fail(BMG_ECUDA, "cusolverDnDpotrf failed");
   int hinfo = 0;
-  BMG_CUDA(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-  BMG_CUDA(cudaStreamSynchronize(ctx->stream));
-  if (hinfo != 0) fail(BMG_ERUNTIME, "setup: coarsest operator is not positive definite");
-  if (cusolverDnDpotri(s, CUBLAS_FILL_MODE_LOWER, (int)N, p.ainv.p, (int)N, work.p, lwork2, info.p) != CUSOLVER_STATUS_SUCCESS)
-    fail(BMG_ECUDA, "cusolverDnDpotri failed");
-  BMG_CUDA(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-  BMG_CUDA(cudaStreamSynchronize(ctx->stream));
-  if (hinfo != 0) fail(BMG_ERUNTIME, "setup: coarse inverse failed");
+  auto check_info = [&](const char* what) {
+    BMG_CUDA(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (hinfo != 0) fail(BMG_ERUNTIME, what);
+  };
+  if (!p.tri) {
+    int lwork = 0, lwork2 = 0;
+    if (cusolverDnDpotrf_bufferSize(s, CUBLAS_FILL_MODE_LOWER, (int)N, p.ainv.p, (int)N, &lwork) !=
+        CUSOLVER_STATUS_SUCCESS)
+      fail(BMG_ECUDA, "cusolverDnDpotrf_bufferSize failed");
+    if (cusolverDnDpotri_bufferSize(s, CUBLAS_FILL_MODE_LOWER, (int)N, p.ainv.p, (int)N, &lwork2) !=
+        CUSOLVER_STATUS_SUCCESS)
+      fail(BMG_ECUDA, "cusolverDnDpotri_bufferSize failed");
+    DBuf<double> work(std::max(std::max(lwork, lwork2), 1));
+    if (cusolverDnDpotrf(s, CUBLAS_FILL_MODE_LOWER, (int)N, p.ainv.p, (int)N, work.p, lwork, info.p) !=
+        CUSOLVER_STATUS_SUCCESS)
+      fail(BMG_ECUDA, "cusolverDnDpotrf failed");
+    check_info("setup: coarsest operator is not positive definite");
+    if (cusolverDnDpotri(s, CUBLAS_FILL_MODE_LOWER, (int)N, p.ainv.p, (int)N, work.p, lwork2, info.p) !=
+        CUSOLVER_STATUS_SUCCESS)
+      fail(BMG_ECUDA, "cusolverDnDpotri failed");
+    check_info("setup: coarse inverse failed");
+  } else {
+    cusolverDnParams_t prm = nullptr;
+    if (cusolverDnCreateParams(&prm) != CUSOLVER_STATUS_SUCCESS) fail(BMG_ECUDA, "cusolverDnCreateParams failed");
+    size_t dws = 0, hws = 0;
+    if (cusolverDnXpotrf_bufferSize(s, prm, CUBLAS_FILL_MODE_LOWER, N, CUDA_R_64F, p.ainv.p, N, CUDA_R_64F, &dws,
+                                    &hws) != CUSOLVER_STATUS_SUCCESS) {
+      cusolverDnDestroyParams(prm);
+      fail(BMG_ECUDA, "cusolverDnXpotrf_bufferSize failed");
+    }
+    {
+      DBuf<unsigned char> dwork(std::max<size_t>(dws, 1));
+      std::vector<unsigned char> hwork(std::max<size_t>(hws, 1));
+      const auto st = cusolverDnXpotrf(s, prm, CUBLAS_FILL_MODE_LOWER, N, CUDA_R_64F, p.ainv.p, N, CUDA_R_64F,
+                                       dwork.p, dws, hwork.data(), hws, info.p);
+      cusolverDnDestroyParams(prm);
+      if (st != CUSOLVER_STATUS_SUCCESS) fail(BMG_ECUDA, "cusolverDnXpotrf failed");
+      check_info("setup: coarsest operator is not positive definite");
+    }
+    DBuf<double> scratch;
+    tri_inverse(ctx, p.ainv.p, N, N, scratch);
+    BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  // column-major lower = row-major upper: mirror it into the row-major lower half
   kern::symmetrize_dense_kernel<<<grid1d(N * N), 256, 0, ctx->stream>>>(p.ainv.p, N);
   ctx->count();
   BMG_CUDA(cudaGetLastError());
@@ -117,7 +205,7 @@ void coarse_factor(Hier& h, Part& p) {
   const int nt = (int)((N + kern::kTile - 1) / kern::kTile);
   const int64_t ntiles = (int64_t)nt * (nt + 1) / 2;
   DBuf<double> tiles((size_t)ntiles * kern::kTile * kern::kTile);
-  kern::pack_lower_tiles_kernel<<<(unsigned)ntiles, 256, 0, ctx->stream>>>(p.ainv.p, N, tiles.p);
+  kern::pack_lower_tiles_kernel<<<(unsigned)ntiles, 256, 0, ctx->stream>>>(p.ainv.p, N, tiles.p, p.tri ? 1 : 0);
   ctx->count();
   BMG_CUDA(cudaGetLastError());
   BMG_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -580,9 +668,13 @@ int bmg_hier_cycle_bytes_batch(const bmg_hier* hh, int kpre, int kpost, int nrhs
       lvl += s.p_pass + 8 * nc + 16 * n;              // prolongation x += P e
       tot += lvl;
     }
-    {  // coarse solve: packed lower tiles of A_0^{-1}, x, b, tile partials
+    {  // coarse solve: packed lower tiles of A_0^{-1} (or W = L^{-1}, read twice), x, b, partials
       const int64_t nt = (h->n0 + 63) / 64;
-      tot += nt * (nt + 1) / 2 * 64 * 64 * 8 + (16 * h->n0 + 2 * nt * nt * 64 * 8) * K;
+      bool tri = h->n0 * h->n0 >= ((int64_t)1 << 31) - 1;
+      for (const Part& p : h->parts)
+        if (p.ainv.p) tri = p.tri;
+      const int64_t one = nt * (nt + 1) / 2 * 64 * 64 * 8 + (16 * h->n0 + 2 * nt * nt * 64 * 8) * K;
+      tot += tri ? 2 * one : one;
     }
     *bytes = tot;
   });

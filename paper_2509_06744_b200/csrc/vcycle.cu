@@ -18,10 +18,12 @@
 
 namespace bmg {
 namespace kern {
-// K right-hand sides interleaved per scalar row; K = 1 is the plain symv
+// K right-hand sides interleaved per scalar row.  mode 0: symmetric tiles (row part
+// tile * x_J, column part tile^T * x_I for J < I); mode 1: lower-triangular T x (row
+// parts only); mode 2: T^T x (column parts, diagonal tiles included)
 __global__ void __launch_bounds__(256) symv_tiles_kernel(const double* __restrict__ tiles,
                                                          const double* __restrict__ x, int64_t N, int nt,
-                                                         double* __restrict__ part, int K) {
+                                                         double* __restrict__ part, int K, int mode) {
   __shared__ double tl[kTile][kTile + 1];
   __shared__ double xi[8][kTile], xj[8][kTile];
   int I, J;
@@ -40,7 +42,8 @@ __global__ void __launch_bounds__(256) symv_tiles_kernel(const double* __restric
     xj[v][t] = gj < N ? x[gj * K + v] : 0.0;
   }
   __syncthreads();
-  for (int it = threadIdx.x; it < 2 * kTile * K; it += blockDim.x) {
+  const int it0 = mode == 2 ? kTile * K : 0, it1 = mode == 1 ? kTile * K : 2 * kTile * K;
+  for (int it = it0 + threadIdx.x; it < it1; it += blockDim.x) {
     const int half = it / (kTile * K);
     const int rem = it - half * kTile * K;
     const int t = rem / K, v = rem - (rem / K) * K;
@@ -48,7 +51,7 @@ __global__ void __launch_bounds__(256) symv_tiles_kernel(const double* __restric
       double s = 0.0;
       for (int c = 0; c < kTile; ++c) s = __fma_rn(tl[t][c], xj[v][c], s);
       part[(((int64_t)I * nt + J) * kTile + t) * K + v] = s;
-    } else if (J < I) {  // column part: tile^T * x_I
+    } else if (J < I || mode == 2) {  // column part: tile^T * x_I
       double s = 0.0;
       for (int r = 0; r < kTile; ++r) s = __fma_rn(tl[r][t], xi[v][r], s);
       part[(((int64_t)J * nt + I) * kTile + t) * K + v] = s;
@@ -56,8 +59,10 @@ __global__ void __launch_bounds__(256) symv_tiles_kernel(const double* __restric
   }
 }
 
+// y of tile row R = sum over the second tile index S in ascending order: mode 0 all
+// S, mode 1 S <= R (lower row parts), mode 2 S >= R (transposed column parts)
 __global__ void symv_reduce_kernel(const double* __restrict__ part, int nt, int64_t N, double* __restrict__ y,
-                                   int K) {
+                                   int K, int mode) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= N * K) return;
   const int64_t i = K == 1 ? e : e / K;
@@ -66,15 +71,16 @@ __global__ void symv_reduce_kernel(const double* __restrict__ part, int nt, int6
   const double* __restrict__ pp = part + (((int64_t)I * nt) * kTile + r) * K + v;
   const int64_t stride = (int64_t)kTile * K;
   double s = 0.0;
-  int J = 0;
-  for (; J + 16 <= nt; J += 16) {  // sixteen loads in flight, additions in tile order
+  int J = mode == 2 ? I : 0;
+  const int J1 = mode == 1 ? I + 1 : nt;
+  for (; J + 16 <= J1; J += 16) {  // sixteen loads in flight, additions in tile order
     double t[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) t[u] = __ldg(pp + (int64_t)(J + u) * stride);
 #pragma unroll
     for (int u = 0; u < 16; ++u) s = __dadd_rn(s, t[u]);
   }
-  for (; J < nt; ++J) s = __dadd_rn(s, __ldg(pp + (int64_t)J * stride));
+  for (; J < J1; ++J) s = __dadd_rn(s, __ldg(pp + (int64_t)J * stride));
   y[e] = s;
 }
 
@@ -201,11 +207,21 @@ static void coarse_solve(Hier& h) {
     const int nt = (int)((N + kern::kTile - 1) / kern::kTile);
     const int64_t ntiles = (int64_t)nt * (nt + 1) / 2;
     const int K = h.nrhs;
-    kern::symv_tiles_kernel<<<(unsigned)ntiles, 256, 0, h.ctx->stream>>>(p.ainv.p, vec(h, p, 0, VB) + L.off(), N, nt,
-                                                                        p.cpart.p, K);
-    kern::symv_reduce_kernel<<<(unsigned)((N * K + 255) / 256), 256, 0, h.ctx->stream>>>(
-        p.cpart.p, nt, N, vec(h, p, 0, VX) + L.off(), K);
-    h.ctx->count(2);
+    const unsigned rgrid = (unsigned)((N * K + 255) / 256);
+    if (!p.tri) {  // x = A_0^{-1} b with the symmetric packed inverse
+      kern::symv_tiles_kernel<<<(unsigned)ntiles, 256, 0, h.ctx->stream>>>(p.ainv.p, vec(h, p, 0, VB) + L.off(), N,
+                                                                          nt, p.cpart.p, K, 0);
+      kern::symv_reduce_kernel<<<rgrid, 256, 0, h.ctx->stream>>>(p.cpart.p, nt, N, vec(h, p, 0, VX) + L.off(), K, 0);
+      h.ctx->count(2);
+    } else {  // x = W^T (W b), W = L^{-1}: y in the level's r buffer
+      double* y = vec(h, p, 0, VR) + L.off();
+      kern::symv_tiles_kernel<<<(unsigned)ntiles, 256, 0, h.ctx->stream>>>(p.ainv.p, vec(h, p, 0, VB) + L.off(), N,
+                                                                          nt, p.cpart.p, K, 1);
+      kern::symv_reduce_kernel<<<rgrid, 256, 0, h.ctx->stream>>>(p.cpart.p, nt, N, y, K, 1);
+      kern::symv_tiles_kernel<<<(unsigned)ntiles, 256, 0, h.ctx->stream>>>(p.ainv.p, y, N, nt, p.cpart.p, K, 2);
+      kern::symv_reduce_kernel<<<rgrid, 256, 0, h.ctx->stream>>>(p.cpart.p, nt, N, vec(h, p, 0, VX) + L.off(), K, 2);
+      h.ctx->count(4);
+    }
     BMG_LAUNCHED(h.ctx->stream, "symv_kernels");
   }
 }
