@@ -327,4 +327,36 @@ inline SolveReport solve(const Hierarchy& h, const CycleSpec& spec, const Device
   return r;
 }
 
+// RateReport / measure_rates (experiments.hpp:15-33, experiments.cpp:15-67); the
+// assembled system is passed as its parts (mass matrix, b, reference solution)
+enum class SolveStatus { Converged = 0, MaxIter = 1, Diverged = 2 };
+struct RateReport {
+  double rho_l2 = 0.0, rho_a = 0.0, rho_r = 0.0;
+  int iterations = 0;
+  SolveStatus status = SolveStatus::Converged;
+  int blowup_iteration = -1;
+  std::vector<double> l2_sq, energy_sq, residual;
+};
+inline RateReport measure_rates(const Hierarchy& h, const DeviceMatrix& mass, const DeviceVector& b,
+                                const DeviceVector& u_ref, const CycleSpec& spec, std::uint64_t seed, double tol,
+                                int max_iter) {
+  RateReport r;
+  r.l2_sq.assign((size_t)max_iter + 1, 0.0);
+  r.energy_sq.assign((size_t)max_iter + 1, 0.0);
+  r.residual.assign((size_t)max_iter + 1, 0.0);
+  int st = 0;
+  double rates[3];
+  check(bmg_measure_rates(h.get(), mass.get(), b.get(), u_ref.get(), spec.k_pre, spec.k_post, seed, tol, max_iter,
+                          r.l2_sq.data(), r.energy_sq.data(), r.residual.data(), &r.iterations, &st,
+                          &r.blowup_iteration, rates));
+  r.status = static_cast<SolveStatus>(st);
+  r.rho_l2 = rates[0];
+  r.rho_a = rates[1];
+  r.rho_r = rates[2];
+  r.l2_sq.resize((size_t)r.iterations + 1);
+  r.energy_sq.resize((size_t)r.iterations + 1);
+  r.residual.resize((size_t)r.iterations + 1);
+  return r;
+}
+
 }  // namespace bmg

@@ -203,6 +203,15 @@ int bmg_vcycle_batch(bmg_hier* h, int k_pre, int k_post, int nrhs, const bmg_vec
 int bmg_vcycle_batch_host(bmg_hier* h, int k_pre, int k_post, int nrhs, const double* b, double* x);
 int bmg_solve(bmg_hier* h, int k_pre, int k_post, const bmg_vec* b, bmg_vec* x, double tol,
               int max_iter, double* hist, int* iters, int* status);
+/* measure_rates (experiments.cpp:15-67): initial error e_i =
+ * CounterRng(seed).symmetric(i) normalised to unit M-norm, x = u_ref + e, V-cycles
+ * on b; after each: squared M- and A-norms of x - u_ref and ||b - A x||.  Stops
+ * when the squared M-norm < tol^2 (status 0), at max_iter (1), or on divergence
+ * (2, blowup = iteration).  Histories hold max_iter + 1 entries; rates =
+ * {rho_l2, rho_a, rho_r} (experiments.hpp:17-27).  Whole hierarchies. */
+int bmg_measure_rates(bmg_hier* h, const bmg_bsr* mass, const bmg_vec* b, const bmg_vec* u_ref, int k_pre,
+                      int k_post, uint64_t seed, double tol, int max_iter, double* l2_sq, double* energy_sq,
+                      double* residual, int* iterations, int* status, int* blowup_iteration, double* rates);
 
 /* ---- multi-GPU (row-partitioned V-cycle) ---------------
  * Every rank builds the same hierarchy (setup is deterministic), then keeps its

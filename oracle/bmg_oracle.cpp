@@ -1480,6 +1480,66 @@ int orc_solve(const orc_hier* h, int k_pre, int k_post, const double* b, double*
   });
 }
 
+// measure_rates: experiments.cpp:15-67.  Initial error e_i = CounterRng(seed)
+// .symmetric(i) normalised to unit M-norm, x = u_ref + e; after every cycle record
+// the squared M- and A-norms of x - u_ref and ||b - A((x - u_ref) + u_ref)||;
+// converged when the squared M-norm drops below tol^2; rates from the histories.
+int orc_measure_rates(const orc_hier* h, const orc_mat* mass, const double* b, const double* u_ref, int k_pre,
+                      int k_post, uint64_t seed, double tol, int max_iter, double* l2_sq, double* energy_sq,
+                      double* residual, int* iters, int* status, int* blowup, double* rates) {
+  return guard([&] {
+    const Mat& a = h->h.levels.back().A;
+    const Mat& m = mass->m;
+    const int n = a.rl.dim;
+    require(m.rl.dim == n && m.cl.dim == n, "measure_rates: mass matrix does not match the finest level");
+    std::vector<double> e(n), tmp(n), x(n), w(n);
+    for (int i = 0; i < n; ++i) e[i] = rng_symmetric(seed, (uint64_t)i);  // CounterRng::symmetric
+    spmv(m, e.data(), tmp.data());
+    const double s = std::sqrt(dot(e.data(), tmp.data(), n));
+    for (int i = 0; i < n; ++i) e[i] /= s;
+    for (int i = 0; i < n; ++i) x[i] = u_ref[i] + e[i];
+    int rec = 0;
+    auto record = [&](const double* err) {
+      spmv(m, err, tmp.data());
+      l2_sq[rec] = dot(err, tmp.data(), n);
+      spmv(a, err, tmp.data());
+      energy_sq[rec] = dot(err, tmp.data(), n);
+      for (int i = 0; i < n; ++i) w[i] = err[i] + u_ref[i];
+      spmv(a, w.data(), tmp.data());
+      for (int i = 0; i < n; ++i) tmp[i] = b[i] - tmp[i];
+      residual[rec] = norm2(tmp.data(), n);
+      ++rec;
+    };
+    record(e.data());
+    const double tol_sq = tol * tol;
+    int it = 0, st = 1;
+    *blowup = -1;
+    if (l2_sq[0] < tol_sq) st = 0;
+    while (st == 1 && it < max_iter) {
+      v_cycle(h->h, k_pre, k_post, h->h.finest(), b, x.data());
+      ++it;
+      for (int i = 0; i < n; ++i) e[i] = x[i] - u_ref[i];
+      record(e.data());
+      const double growth = residual[it] / std::max(residual[it - 1], 1e-300);
+      if (!std::isfinite(residual[it]) || growth > 1e6) {
+        st = 2;
+        *blowup = it;
+        break;
+      }
+      if (l2_sq[it] < tol_sq) st = 0;
+    }
+    *iters = it;
+    *status = st;
+    rates[0] = rates[1] = rates[2] = 0.0;
+    if (it > 0) {
+      const double ex = 1.0 / (2.0 * it);
+      rates[0] = std::pow(l2_sq[it] / l2_sq[0], ex);
+      rates[1] = std::pow(energy_sq[it] / energy_sq[0], ex);
+      rates[2] = std::pow(residual[it] / residual[0], 1.0 / it);
+    }
+  });
+}
+
 uint64_t orc_mix64(uint64_t z) { return mix64(z); }
 double orc_rng_uniform(uint64_t seed, uint64_t i) { return rng_uniform(seed, i); }
 

@@ -127,6 +127,12 @@ int orc_vcycle(const orc_hier* h, int k_pre, int k_post, int level, const double
 int orc_solve(const orc_hier* h, int k_pre, int k_post, const double* b, double* x, double tol,
               int max_iter, double* hist, int* iters, int* status);
 
+/* measure_rates (experiments.cpp:15-67): arrays hold max_iter + 1 entries;
+ * status 0 converged, 1 max_iter, 2 diverged; rates = {rho_l2, rho_a, rho_r} */
+int orc_measure_rates(const orc_hier* h, const orc_mat* mass, const double* b, const double* u_ref, int k_pre,
+                      int k_post, uint64_t seed, double tol, int max_iter, double* l2_sq, double* energy_sq,
+                      double* residual, int* iters, int* status, int* blowup, double* rates);
+
 /* ---- RNG (rng.hpp:12-57) ---- */
 uint64_t orc_mix64(uint64_t z);
 double orc_rng_uniform(uint64_t seed, uint64_t i);

@@ -68,6 +68,8 @@ _SIGS = {
     "orc_hier_coarse_l": (_I, [_P, _PD]),
     "orc_vcycle": (_I, [_P, _I, _I, _I, _PD, _PD]),
     "orc_solve": (_I, [_P, _I, _I, _PD, _PD, _D, _I, _PD, C.POINTER(_I), C.POINTER(_I)]),
+    "orc_measure_rates": (_I, [_P, _P, _PD, _PD, _I, _I, C.c_uint64, _D, _I, _PD, _PD, _PD, C.POINTER(_I),
+                               C.POINTER(_I), C.POINTER(_I), _PD]),
     "orc_mix64": (_U64, [_U64]),
     "orc_rng_uniform": (_D, [_U64, _U64]),
 }
@@ -393,6 +395,19 @@ class Hierarchy:
         check(lib().orc_solve(self.h, k_pre, k_post, _d(b), _d(x), tol, max_iter, _d(hist), C.byref(it),
                               C.byref(st)))
         return hist[:it.value + 1], it.value, st.value, x
+
+    def measure_rates(self, mass, b, u_ref, k_pre, k_post, seed=0, tol=1e-8, max_iter=50):
+        """measure_rates (experiments.cpp:15-67) -> dict of histories and rates."""
+        b = np.ascontiguousarray(b, np.float64)
+        u = np.ascontiguousarray(u_ref, np.float64)
+        l2, en, rs = np.zeros(max_iter + 1), np.zeros(max_iter + 1), np.zeros(max_iter + 1)
+        rates = np.zeros(3)
+        it, st, bl = C.c_int(), C.c_int(), C.c_int()
+        check(lib().orc_measure_rates(self.h, mass.h, _d(b), _d(u), k_pre, k_post, seed, tol, max_iter, _d(l2),
+                                      _d(en), _d(rs), C.byref(it), C.byref(st), C.byref(bl), _d(rates)))
+        n = it.value + 1
+        return dict(l2_sq=l2[:n], energy_sq=en[:n], residual=rs[:n], iterations=it.value, status=st.value,
+                    blowup_iteration=bl.value, rho_l2=rates[0], rho_a=rates[1], rho_r=rates[2])
 
     def __del__(self):
         try:

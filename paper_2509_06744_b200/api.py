@@ -480,6 +480,18 @@ class Hierarchy:
                               C.byref(st)))
         return hist[:it.value + 1], it.value, st.value
 
+    def measure_rates(self, mass: BlockSparseMatrix, b: Vector, u_ref: Vector, k_pre, k_post, seed=0, tol=1e-8,
+                      max_iter=50) -> dict:
+        """measure_rates (experiments.cpp:15-67): RateReport as a dict."""
+        l2, en, rs = np.zeros(max_iter + 1), np.zeros(max_iter + 1), np.zeros(max_iter + 1)
+        rates = np.zeros(3)
+        it, st, bl = C.c_int(), C.c_int(), C.c_int()
+        check(lib().bmg_measure_rates(self.h, mass.h, b.h, u_ref.h, k_pre, k_post, seed, tol, max_iter, dptr(l2),
+                                      dptr(en), dptr(rs), C.byref(it), C.byref(st), C.byref(bl), dptr(rates)))
+        n = it.value + 1
+        return dict(l2_sq=l2[:n], energy_sq=en[:n], residual=rs[:n], iterations=it.value, status=st.value,
+                    blowup_iteration=bl.value, rho_l2=rates[0], rho_a=rates[1], rho_r=rates[2])
+
     def close(self):
         if self.h:
             check(lib().bmg_hier_destroy(self.h))

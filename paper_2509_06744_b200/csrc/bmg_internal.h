@@ -213,6 +213,7 @@ struct StepScalars {
 };
 std::vector<StepScalars> smoother_schedule(const SmootherSpec& s, int k);
 double dot(Ctx* ctx, const double* a, const double* b, int64_t n);
+void rng_symmetric(Ctx* ctx, double* v, int64_t n, uint64_t seed);
 void fill(Ctx* ctx, double* p, int64_t n, double v);
 void copy(Ctx* ctx, double* dst, const double* src, int64_t n);
 void fsai_apply(const Fsai& m, const double* r, double* z, double* tmp1, double* tmp2);

@@ -163,6 +163,9 @@ void run_vcycle(Hier& h, int kpre, int kpost, const double* bf, double* xf);
 double finest_norm(Hier& h, const double* r_whole);
 void finest_residual(Hier& h, const double* b, double* x, double* rtmp);
 void coarse_factor(Hier& h, Part& p);
+void measure_rates(Hier& h, const Bsr& mass, const double* b, const double* u, int kpre, int kpost, uint64_t seed,
+                   double tol, int max_iter, double* l2_sq, double* energy_sq, double* resid, int* iters,
+                   int* status, int* blowup, double* rates);
 void alloc_vectors(Hier& h, PLevel& L, bool top);
 std::unique_ptr<Bsr> slice_rows(const Bsr& g, int lo, int hi, int col_lo, int ncols);
 SplitMat split_rows(const Bsr& g, int lo, int hi, int wlo, int nwin, int own_lo, int own_hi);

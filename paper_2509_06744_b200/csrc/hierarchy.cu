@@ -758,6 +758,22 @@ int bmg_solve(bmg_hier* hh, int kpre, int kpost, const bmg_vec* bh, bmg_vec* xh,
   });
 }
 
+// measure_rates (experiments.cpp:15-67)
+int bmg_measure_rates(bmg_hier* hh, const bmg_bsr* mass, const bmg_vec* b, const bmg_vec* u_ref, int kpre,
+                      int kpost, uint64_t seed, double tol, int max_iter, double* l2_sq, double* energy_sq,
+                      double* residual_hist, int* iters, int* status, int* blowup, double* rates) {
+  return guard([&] {
+    Hier* h = H_(hh);
+    h->ctx->activate();
+    if (max_iter < 0) fail(BMG_EINVAL, "measure_rates: max_iter must be >= 0");
+    const int64_t n = finest_len(*h);
+    need_len(V_(b), n, "measure_rates");
+    need_len(V_(u_ref), n, "measure_rates");
+    measure_rates(*h, *B_(mass), V_(b)->d.p, V_(u_ref)->d.p, kpre, kpost, seed, tol, max_iter, l2_sq, energy_sq,
+                  residual_hist, iters, status, blowup, rates);
+  });
+}
+
 int bmg_ctx_create_nccl(int device, int rank, int world, const unsigned char* id128, bmg_ctx** out) {
   return guard([&] {
     bmg_ctx* c = nullptr;

@@ -1094,6 +1094,13 @@ static void smooth_single(const Bsr& A, const Fsai& M, const SmootherSpec& spec,
   }
 }
 
+// CounterRng(seed).symmetric(i) for i < n (rng.hpp:20-35) into v
+void rng_symmetric(Ctx* ctx, double* v, int64_t n, uint64_t seed) {
+  kern::rng_symmetric_kernel<<<grid1d(n), 256, 0, ctx->stream>>>(v, n, seed);
+  ctx->count();
+  BMG_CUDA(cudaGetLastError());
+}
+
 }  // namespace bmg
 
 // ============================================================================ C ABI

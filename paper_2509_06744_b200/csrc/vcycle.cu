@@ -102,6 +102,16 @@ __global__ void __launch_bounds__(256) segment_sq_kernel(const double* __restric
   }
   if (threadIdx.x == 0) out[blockIdx.x] = sh[0];
 }
+// out = a + s * b   (s = +1 / -1: the reference's Vector sums and differences)
+__global__ void axpby_kernel(double* __restrict__ out, const double* __restrict__ a, const double* __restrict__ b,
+                             int64_t n, int sub) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = sub ? __dsub_rn(a[i], b[i]) : __dadd_rn(a[i], b[i]);
+}
+__global__ void scale_inv_kernel(double* v, int64_t n, double d) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = __ddiv_rn(v[i], d);
+}
 }  // namespace kern
 
 // ============================================================================ halo exchange
@@ -424,6 +434,83 @@ void finest_residual(Hier& h, const double* b, double* x, double* rtmp) {
              const int64_t o = L.off() + L.sc(sl.row0);
              residual(*sl.m, L.v[VB].p + o, L.v[VX].p, L.v[VR].p + o);
            });
+}
+
+}  // namespace bmg
+
+namespace bmg {
+
+// measure_rates (experiments.cpp:15-67) on a whole device hierarchy: the initial
+// error e_i = CounterRng(seed).symmetric(i) normalised to unit M-norm, x = u_ref + e;
+// after every cycle the squared M- and A-norms of x - u_ref and the residual
+// ||b - A((x - u_ref) + u_ref)||; converged when the squared M-norm < tol^2.
+void measure_rates(Hier& h, const Bsr& mass, const double* b, const double* u, int kpre, int kpost, uint64_t seed,
+                   double tol, int max_iter, double* l2_sq, double* energy_sq, double* resid, int* iters,
+                   int* status, int* blowup, double* rates) {
+  if (!h.whole()) fail(BMG_EINVAL, "measure_rates: whole (unpartitioned) hierarchies only");
+  set_nrhs(h, 1);
+  Ctx* ctx = h.ctx;
+  Part& P = h.parts[0];
+  const Bsr& a = *P.lv[h.finest()].A;
+  const int64_t n = a.dim_r;
+  if (mass.dim_r != n || mass.dim_c != n) fail(BMG_EINVAL, "measure_rates: mass matrix does not match the finest level");
+  DBuf<double> e(std::max<int64_t>(n, 1)), t(std::max<int64_t>(n, 1)), x(std::max<int64_t>(n, 1)),
+      w(std::max<int64_t>(n, 1));
+  rng_symmetric(ctx, e.p, n, seed);
+  spmv(mass, e.p, t.p);
+  const double s = std::sqrt(dot(ctx, e.p, t.p, n));
+  kern::scale_inv_kernel<<<grid1d(n), 256, 0, ctx->stream>>>(e.p, n, s);
+  kern::axpby_kernel<<<grid1d(n), 256, 0, ctx->stream>>>(x.p, u, e.p, n, 0);
+  ctx->count(2);
+  int rec = 0;
+  auto record = [&]() {  // e holds the error
+    spmv(mass, e.p, t.p);
+    l2_sq[rec] = dot(ctx, e.p, t.p, n);
+    spmv(a, e.p, t.p);
+    energy_sq[rec] = dot(ctx, e.p, t.p, n);
+    kern::axpby_kernel<<<grid1d(n), 256, 0, ctx->stream>>>(w.p, e.p, u, n, 0);
+    ctx->count();
+    residual(a, b, w.p, t.p);
+    resid[rec] = std::sqrt(dot(ctx, t.p, t.p, n));
+    ++rec;
+  };
+  record();
+  const double tol_sq = tol * tol;
+  int it = 0, st = 1;
+  *blowup = -1;
+  if (l2_sq[0] < tol_sq) st = 0;
+  while (st == 1 && it < max_iter) {
+    run_vcycle(h, kpre, kpost, b, x.p);
+    ++it;
+    kern::axpby_kernel<<<grid1d(n), 256, 0, ctx->stream>>>(e.p, x.p, u, n, 1);
+    ctx->count();
+    record();
+    const double growth = resid[it] / std::max(resid[it - 1], 1e-300);
+    if (!std::isfinite(resid[it]) || growth > 1e6) {
+      st = 2;
+      *blowup = it;
+      break;
+    }
+    if (l2_sq[it] < tol_sq) st = 0;
+  }
+  BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (auto g = h.graphs.begin(); g != h.graphs.end();) {  // graphs of the local iterate
+    if (g->first.x == x.p) {
+      cudaGraphExecDestroy(g->second.exec);
+      g = h.graphs.erase(g);
+    } else {
+      ++g;
+    }
+  }
+  *iters = it;
+  *status = st;
+  rates[0] = rates[1] = rates[2] = 0.0;
+  if (it > 0) {
+    const double ex = 1.0 / (2.0 * it);
+    rates[0] = std::pow(l2_sq[it] / l2_sq[0], ex);
+    rates[1] = std::pow(energy_sq[it] / energy_sq[0], ex);
+    rates[2] = std::pow(resid[it] / resid[0], 1.0 / it);
+  }
 }
 
 }  // namespace bmg

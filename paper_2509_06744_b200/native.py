@@ -145,6 +145,8 @@ _SIGS = {
     "bmg_vcycle": (_I, [_P, _I, _I, _P, _P]),
     "bmg_vcycle_host": (_I, [_P, _I, _I, _PD, _PD]),
     "bmg_solve": (_I, [_P, _I, _I, _P, _P, _D, _I, _PD, C.POINTER(_I), C.POINTER(_I)]),
+    "bmg_measure_rates": (_I, [_P, _P, _P, _P, _I, _I, C.c_uint64, _D, _I, _PD, _PD, _PD, C.POINTER(_I),
+                               C.POINTER(_I), C.POINTER(_I), _PD]),
     "bmg_time_residual": (_I, [_P, _P, _P, _P, _I, _PD]),
     "bmg_nccl_unique_id": (_I, [C.c_char_p]),
     "bmg_ctx_create_nccl": (_I, [_I, _I, _I, C.c_char_p, _PP]),

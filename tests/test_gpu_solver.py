@@ -347,3 +347,43 @@ def test_vcycle_smoother_kinds_and_v2k0(ctx, kind, kpre, kpost):
     hist_g, it_g, _ = dh.solve(kpre, kpost, Vector(ctx, b), Vector(ctx, b.size), 1e-8, 8)
     assert it_o == it_g
     assert np.all(np.abs(hist_g / hist_g[0] - hist_o / hist_o[0]) <= 1e-10)
+
+
+def _block_diag(host):
+    # the diagonal blocks of an s.p.d. block matrix: an s.p.d. stand-in for the PUM mass matrix
+    m = int(host.row_sizes[0])
+    n = host.nbr
+    vals = []
+    for i in range(n):
+        for p in range(host.row_ptr[i], host.row_ptr[i + 1]):
+            if host.col_idx[p] == i:
+                vals.append(host.vals[p * m * m:(p + 1) * m * m])
+    from paper_2509_06744_b200.api import HostBsr
+    return HostBsr(host.row_sizes, host.col_sizes, np.arange(n + 1, dtype=np.int64), np.arange(n, dtype=np.int32),
+                   np.concatenate(vals), True)
+
+
+@pytest.mark.parametrize("tol,max_iter", [(1e-3, 30), (1e-30, 6), (10.0, 5)])
+def test_measure_rates_matches_oracle(ctx, tol, max_iter):
+    # measure_rates (experiments.cpp:15-67): error histories in the M- and A-norms,
+    # residual history, iteration count, status and the three rates
+    cfg = pr.CONFIGS["C2"].scaled(16, 3)
+    A, T, _ = pr.make_problem(cfg)
+    Mh = _block_diag(A)
+    u = pr.normal_vector(A.dim_r, 0, 7)
+    b = O.Mat(A).spmv(u)
+    oh = O.Hierarchy(O.Mat(A), [O.Mat(p) for p in T], t_max=1, coarse_dim_cap=1 << 30, probe=False)
+    want = oh.measure_rates(O.Mat(Mh), b, u, 3, 3, seed=11, tol=tol, max_iter=max_iter)
+    dh = Hierarchy.setup(BlockSparseMatrix(ctx, A), [BlockSparseMatrix(ctx, p) for p in T],
+                         default_params(t_max=1, coarse_dim_cap=1 << 30))
+    got = dh.measure_rates(BlockSparseMatrix(ctx, Mh), Vector(ctx, b), Vector(ctx, u), 3, 3, seed=11, tol=tol,
+                           max_iter=max_iter)
+    assert got["iterations"] == want["iterations"] and got["status"] == want["status"]
+    assert got["blowup_iteration"] == want["blowup_iteration"]
+    for key in ("l2_sq", "energy_sq", "residual"):
+        g, w = got[key], want[key]
+        assert np.all(np.abs(g / w[0] - w / w[0]) <= 1e-10), key
+    for key in ("rho_l2", "rho_a", "rho_r"):
+        assert abs(got[key] - want[key]) <= 1e-9 * max(abs(want[key]), 1e-300), key
+    if tol == 10.0:
+        assert got["iterations"] == 0 and got["status"] == 0 and got["rho_l2"] == 0.0
