@@ -470,3 +470,24 @@ def test_rng_counter_stream():
     assert all(0.0 < v < 1.0 for v in u)
     assert lib.orc_rng_uniform(42, 17) == u[17]
     assert lib.orc_mix64(0) == 0
+
+
+def test_measure_rates_semantics():
+    # experiments.cpp:15-67: e normalised to unit M-norm (l2_sq[0] = 1), rates are
+    # (q_n / q_0)^(1/2n) for the quadratic forms and (r_n / r_0)^(1/n) for the residual
+    from paper_2509_06744_b200 import problems as pr
+    cfg = pr.CONFIGS["C2"].scaled(8, 2)
+    A, T, _ = pr.make_problem(cfg)
+    u = pr.normal_vector(A.dim_r, 0, 7)
+    om = O.Mat(A)
+    b = om.spmv(u)
+    oh = O.Hierarchy(om, [O.Mat(p) for p in T], t_max=1, coarse_dim_cap=1 << 30, probe=False)
+    r = oh.measure_rates(om, b, u, 2, 2, seed=3, tol=1e-30, max_iter=4)
+    assert abs(r["l2_sq"][0] - 1.0) < 1e-14
+    assert r["l2_sq"][0] == r["energy_sq"][0]  # M = A here
+    n = r["iterations"]
+    assert n == 4 and r["status"] == 1 and r["blowup_iteration"] == -1
+    assert abs(r["rho_l2"] - (r["l2_sq"][n] / r["l2_sq"][0]) ** (1 / (2 * n))) < 1e-15
+    assert abs(r["rho_r"] - (r["residual"][n] / r["residual"][0]) ** (1 / n)) < 1e-15
+    r0 = oh.measure_rates(om, b, u, 2, 2, seed=3, tol=2.0, max_iter=4)
+    assert r0["iterations"] == 0 and r0["status"] == 0 and r0["rho_a"] == 0.0
