@@ -296,6 +296,10 @@ inline Hierarchy setup(const DeviceMatrix& a_finest, const std::vector<const Dev
 inline void v_cycle(const Hierarchy& h, const CycleSpec& spec, const DeviceVector& b, DeviceVector& x) {
   check(bmg_vcycle(h.get(), spec.k_pre, spec.k_post, b.get(), x.get()));
 }
+// the reference signature: v_cycle(h, spec, level, b, x) (multilevel.hpp:65)
+inline void v_cycle(const Hierarchy& h, const CycleSpec& spec, int level, const DeviceVector& b, DeviceVector& x) {
+  check(bmg_vcycle_level(h.get(), spec.k_pre, spec.k_post, level, b.get(), x.get()));
+}
 inline void v_cycle(const Hierarchy& h, const CycleSpec& spec, const std::vector<double>& b,
                     std::vector<double>& x) {
   check(bmg_vcycle_host(h.get(), spec.k_pre, spec.k_post, b.data(), x.data()));

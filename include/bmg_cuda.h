@@ -192,6 +192,10 @@ int bmg_hier_cycle_bytes_batch(const bmg_hier* h, int k_pre, int k_post, int nrh
 /* 1 (default) = replay each cycle from a captured CUDA graph */
 int bmg_hier_use_graph(bmg_hier* h, int on);
 int bmg_vcycle(bmg_hier* h, int k_pre, int k_post, const bmg_vec* b, bmg_vec* x);
+/* v_cycle(h, spec, level, b, x) (multilevel.hpp:65) started on `level` (0 = the direct
+ * coarse solve); b, x have that level's length; levels below the finest need an
+ * unpartitioned hierarchy.  BMG_ERANGE for a level out of range. */
+int bmg_vcycle_level(bmg_hier* h, int k_pre, int k_post, int level, const bmg_vec* b, bmg_vec* x);
 /* end-to-end: host b, host x (in/out); H2D + cycle + D2H inside the call */
 int bmg_vcycle_host(bmg_hier* h, int k_pre, int k_post, const double* b, double* x);
 /* K right-hand sides in one cycle (K = 1, 2, 4, 8), interleaved per scalar row:

@@ -457,6 +457,10 @@ class Hierarchy:
     def v_cycle(self, k_pre, k_post, b: Vector, x: Vector):
         check(lib().bmg_vcycle(self.h, k_pre, k_post, b.h, x.h))
 
+    def v_cycle_level(self, k_pre, k_post, level: int, b: Vector, x: Vector):
+        """v_cycle(h, spec, level, b, x) (multilevel.hpp:65): start on `level`."""
+        check(lib().bmg_vcycle_level(self.h, k_pre, k_post, level, b.h, x.h))
+
     def v_cycle_batch(self, k_pre, k_post, nrhs: int, b: Vector, x: Vector):
         """K right-hand sides interleaved per scalar row (b[i*K + v]); bmg_vcycle_batch."""
         check(lib().bmg_vcycle_batch(self.h, k_pre, k_post, nrhs, b.h, x.h))

@@ -101,11 +101,11 @@ struct LevelStats {  // global byte model inputs (bmg_hier_cycle_bytes)
 };
 
 struct GraphKey {
-  int kpre, kpost, nrhs;
+  int kpre, kpost, nrhs, top;
   const double* b;
   double* x;
   bool operator<(const GraphKey& o) const {
-    return std::tie(kpre, kpost, nrhs, b, x) < std::tie(o.kpre, o.kpost, o.nrhs, o.b, o.x);
+    return std::tie(kpre, kpost, nrhs, top, b, x) < std::tie(o.kpre, o.kpost, o.nrhs, o.top, o.b, o.x);
   }
 };
 
@@ -140,6 +140,8 @@ struct Hier {
     if (comm) cudaStreamDestroy(comm);
   }
   int finest() const { return (int)nbr.size() - 1; }
+  int top = -1;  // level the current cycle starts on (v_cycle's `level`; -1: finest)
+  int cycle_top() const { return top >= 0 ? top : finest(); }
   bool whole() const { return world == 1; }
   void drop_graphs() {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
@@ -149,7 +151,7 @@ struct Hier {
 
 // vector of level l on part p; the unpartitioned top level uses the caller's b, x
 inline double* vec(Hier& h, Part& p, int l, Which w) {
-  if (h.whole() && l == h.finest()) {
+  if (h.whole() && l == h.cycle_top()) {
     if (w == VB) return const_cast<double*>(h.user_b);
     if (w == VX) return h.user_x;
   }

@@ -700,6 +700,31 @@ int bmg_vcycle_batch(bmg_hier* hh, int kpre, int kpost, int nrhs, const bmg_vec*
   });
 }
 
+// v_cycle(h, spec, level, b, x) (multilevel.cpp:77-103) started on any level of a
+// whole hierarchy; b and x have that level's length (level 0: the direct solve)
+int bmg_vcycle_level(bmg_hier* hh, int kpre, int kpost, int level, const bmg_vec* b, bmg_vec* x) {
+  return guard([&] {
+    Hier* h = H_(hh);
+    h->ctx->activate();
+    if (kpre + kpost < 1) fail(BMG_EINVAL, "v_cycle: cycle needs at least one smoothing step");
+    if (level < 0 || level > h->finest()) fail(BMG_ERANGE, "v_cycle: level out of range");
+    if (level != h->finest() && !h->whole())
+      fail(BMG_EINVAL, "v_cycle: levels below the finest need an unpartitioned hierarchy");
+    set_nrhs(*h, 1);
+    const int64_t n = h->parts[0].lv[level].n_own();
+    need_len(V_(b), n, "v_cycle");
+    need_len(V_(x), n, "v_cycle");
+    h->top = level;
+    try {
+      run_vcycle(*h, kpre, kpost, V_(b)->d.p, V_(x)->d.p);
+    } catch (...) {
+      h->top = -1;
+      throw;
+    }
+    h->top = -1;
+  });
+}
+
 int bmg_vcycle_host(bmg_hier* hh, int kpre, int kpost, const double* b, double* x) {
   return bmg_vcycle_batch_host(hh, kpre, kpost, 1, b, x);
 }

@@ -238,7 +238,7 @@ static void coarse_solve(Hier& h) {
 
 // v_cycle (multilevel.cpp:77-103), recursion unrolled: down, coarse solve, up
 static void enqueue_vcycle(Hier& h, int kpre, int kpost) {
-  const int top = h.finest();
+  const int top = h.cycle_top();
   for (int l = top; l >= 1; --l) {
     const bool xzero = l < top;
     Which r = VR;
@@ -342,7 +342,7 @@ void run_vcycle(Hier& h, int kpre, int kpost, const double* bf, double* xf) {
   Ctx* ctx = h.ctx;
   h.user_b = bf;
   h.user_x = xf;
-  if (h.finest() == 0) {
+  if (h.cycle_top() == 0) {  // multilevel.cpp:81-84: the coarsest level solves directly
     stage_in(h, bf, xf);
     coarse_solve(h);
     stage_out(h, xf);
@@ -354,7 +354,7 @@ void run_vcycle(Hier& h, int kpre, int kpost, const double* bf, double* xf) {
     stage_out(h, xf);
     return;
   }
-  GraphKey key{kpre, kpost, h.nrhs, bf, xf};
+  GraphKey key{kpre, kpost, h.nrhs, h.cycle_top(), bf, xf};
   auto it = h.graphs.find(key);
   if (it == h.graphs.end()) {
     cudaStream_t user = ctx->stream;

@@ -143,6 +143,7 @@ _SIGS = {
     "bmg_vcycle_batch_host": (_I, [_P, _I, _I, _I, _PD, _PD]),
     "bmg_hier_use_graph": (_I, [_P, _I]),
     "bmg_vcycle": (_I, [_P, _I, _I, _P, _P]),
+    "bmg_vcycle_level": (_I, [_P, _I, _I, _I, _P, _P]),
     "bmg_vcycle_host": (_I, [_P, _I, _I, _PD, _PD]),
     "bmg_solve": (_I, [_P, _I, _I, _P, _P, _D, _I, _PD, C.POINTER(_I), C.POINTER(_I)]),
     "bmg_measure_rates": (_I, [_P, _P, _P, _P, _I, _I, C.c_uint64, _D, _I, _PD, _PD, _PD, C.POINTER(_I),

@@ -387,3 +387,21 @@ def test_measure_rates_matches_oracle(ctx, tol, max_iter):
         assert abs(got[key] - want[key]) <= 1e-9 * max(abs(want[key]), 1e-300), key
     if tol == 10.0:
         assert got["iterations"] == 0 and got["status"] == 0 and got["rho_l2"] == 0.0
+
+
+def test_vcycle_from_every_level_matches_oracle(ctx, rng):
+    # v_cycle(h, spec, level, b, x) (multilevel.cpp:77-103) from each level, with a
+    # nonzero initial guess; level 0 is the dense direct solve
+    A, T, b, oh, dh = _small_hierarchies(ctx, 16, 3)
+    for level in range(dh.levels):
+        n = oh.A(level).export(symmetric=True).dim_r
+        bl = rng.standard_normal(n)
+        x0 = rng.standard_normal(n)
+        want = oh.v_cycle(2, 1, bl, x0.copy(), level=level)
+        xv = Vector(ctx, x0.copy())
+        dh.v_cycle_level(2, 1, level, Vector(ctx, bl), xv)
+        got = xv.download()
+        assert np.linalg.norm(got - want) <= 1e-11 * np.linalg.norm(want), level
+    from paper_2509_06744_b200.native import OutOfRange
+    with pytest.raises(OutOfRange):
+        dh.v_cycle_level(2, 2, dh.levels, Vector(ctx, 4), Vector(ctx, 4))
