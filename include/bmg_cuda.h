@@ -146,6 +146,10 @@ int bmg_triple_product(const bmg_bsr* f, const bmg_bsr* a, bmg_bsr** out);
 
 /* ---- block-FSAI (fsai.cpp) ---------------------------------------------- */
 int bmg_fsai_build(const bmg_bsr* a, int kind, int t_max, double tau, int nest, bmg_fsai** out);
+/* build_fsai(A, p) (fsai.hpp:25) for a caller's LowerPattern p: pat_ptr[n+1] /
+ * pat_col list each row's lower block columns (duplicates and the diagonal, always
+ * present, are ignored; j > i is BMG_EINVAL) */
+int bmg_fsai_build_pattern(const bmg_bsr* a, const int64_t* pat_ptr, const int32_t* pat_col, bmg_fsai** out);
 /* inject reference-built factors of a one-factor chain: F (unit-diagonal
  * lower BSR) and the row-major Cholesky factors of S-hat packed per block row */
 int bmg_fsai_from_factors(bmg_ctx* ctx, const bmg_bsr* F, const double* shat_l_packed,

@@ -281,6 +281,20 @@ class Fsai:
         self._owned = owned
 
     @classmethod
+    def from_pattern(cls, a: BlockSparseMatrix, pattern) -> "Fsai":
+        """build_fsai(A, LowerPattern p) (fsai.hpp:25); pattern[i] = iterable of j <= i."""
+        n = a.info()["nbr"]
+        pp = np.zeros(n + 1, np.int64)
+        cols = []
+        for i in range(n):
+            cols.extend(int(j) for j in pattern[i])
+            pp[i + 1] = len(cols)
+        pc = np.asarray(cols if cols else [0], np.int32)
+        h = C.c_void_p()
+        check(lib().bmg_fsai_build_pattern(a.h, i64ptr(pp), i32ptr(pc), C.byref(h)))
+        return cls(a.ctx, h)
+
+    @classmethod
     def build(cls, a: BlockSparseMatrix, kind=N.FSAI_ADAPTIVE, t_max=1, tau=1.0, nest=0) -> "Fsai":
         h = C.c_void_p()
         check(lib().bmg_fsai_build(a.h, kind, t_max, tau, nest, C.byref(h)))

@@ -218,6 +218,7 @@ void fill(Ctx* ctx, double* p, int64_t n, double v);
 void copy(Ctx* ctx, double* dst, const double* src, int64_t n);
 void fsai_apply(const Fsai& m, const double* r, double* z, double* tmp1, double* tmp2);
 std::unique_ptr<Fsai> fsai_build(const Bsr& a, int kind, int t_max, double tau, int nest);
+std::unique_ptr<Fsai> fsai_build_pattern(const Bsr& a, const int64_t* ptr, const int32_t* col);
 std::unique_ptr<Fsai> fsai_from_factors(Ctx* ctx, const Bsr& F, const double* shat_l_packed);
 double lanczos_lambda_max(const Bsr& a, const Fsai& m, int iters, double safety, uint64_t seed);
 std::unique_ptr<Bsr> galerkin(const Bsr& a, const Bsr& p);

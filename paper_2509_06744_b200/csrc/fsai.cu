@@ -694,6 +694,37 @@ std::unique_ptr<Fsai> fsai_build(const Bsr& a, int kind, int t_max, double tau, 
   return wrap(ctx, a.dim_r, std::move(fwd));
 }
 
+// build_fsai(A, p) (fsai.cpp:72-83) for a caller's lower pattern: per row the
+// strictly lower block columns (LowerPattern::add semantics: duplicates and the
+// diagonal, which is always present, are ignored; j > i is an error)
+std::unique_ptr<Fsai> fsai_build_pattern(const Bsr& a, const int64_t* ptr, const int32_t* col) {
+  if (!(a.rsz == a.csz)) fail(BMG_EINVAL, "fsai: matrix must be square");
+  if (!a.sym) fail(BMG_EINVAL, "fsai: matrix must be symmetric");
+  const int n = a.nbr;
+  std::vector<int64_t> pp(n + 1, 0);
+  std::vector<int32_t> pc;
+  if (ptr[0] != 0) fail(BMG_EINVAL, "LowerPattern: row_ptr[0] must be 0");
+  std::vector<int32_t> row;
+  for (int k = 0; k < n; ++k) {
+    if (ptr[k + 1] < ptr[k]) fail(BMG_EINVAL, "LowerPattern: row_ptr must be non-decreasing");
+    row.clear();
+    for (int64_t q = ptr[k]; q < ptr[k + 1]; ++q) {
+      const int c = col[q];
+      if (c == k) continue;
+      if (c < 0 || c > k) fail(BMG_EINVAL, "LowerPattern: entries must satisfy 0 <= j <= i");
+      row.push_back(c);
+    }
+    std::sort(row.begin(), row.end());
+    row.erase(std::unique(row.begin(), row.end()), row.end());
+    pc.insert(pc.end(), row.begin(), row.end());
+    pp[k + 1] = (int64_t)pc.size();
+  }
+  Aux aux = make_aux(a, true);
+  std::vector<std::unique_ptr<Bsr>> fwd;
+  fwd.push_back(factor_from_pattern(a, aux, pp, pc, false));
+  return wrap(a.ctx, a.dim_r, std::move(fwd));
+}
+
 std::unique_ptr<Fsai> fsai_from_factors(Ctx* ctx, const Bsr& F, const double* shat) {
   if (!(F.rsz == F.csz)) fail(BMG_EINVAL, "fsai: factor must be square");
   const int n = F.nbr;

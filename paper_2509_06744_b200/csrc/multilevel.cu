@@ -1145,6 +1145,12 @@ int bmg_fsai_build(const bmg_bsr* a, int kind, int t_max, double tau, int nest, 
     *out = reinterpret_cast<bmg_fsai*>(fsai_build(*B(a), kind, t_max, tau, nest).release());
   });
 }
+int bmg_fsai_build_pattern(const bmg_bsr* a, const int64_t* pat_ptr, const int32_t* pat_col, bmg_fsai** out) {
+  return guard([&] {
+    B(a)->ctx->activate();
+    *out = reinterpret_cast<bmg_fsai*>(fsai_build_pattern(*B(a), pat_ptr, pat_col).release());
+  });
+}
 int bmg_fsai_from_factors(bmg_ctx* ctx, const bmg_bsr* F, const double* shat, bmg_fsai** out) {
   return guard([&] {
     Ctx* c = reinterpret_cast<Ctx*>(ctx);

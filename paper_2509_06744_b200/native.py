@@ -119,6 +119,7 @@ _SIGS = {
     "bmg_dot": (_I, [_P, _P, _PD]),
     "bmg_galerkin": (_I, [_P, _P, _PP]),
     "bmg_fsai_build": (_I, [_P, _I, _I, _D, _I, _PP]),
+    "bmg_fsai_build_pattern": (_I, [_P, _PI64, _PI32, _PP]),
     "bmg_fsai_from_factors": (_I, [_P, _P, _PD, _PP]),
     "bmg_fsai_destroy": (_I, [_P]),
     "bmg_fsai_apply": (_I, [_P, _P, _P]),

@@ -405,3 +405,24 @@ def test_vcycle_from_every_level_matches_oracle(ctx, rng):
     from paper_2509_06744_b200.native import OutOfRange
     with pytest.raises(OutOfRange):
         dh.v_cycle_level(2, 2, dh.levels, Vector(ctx, 4), Vector(ctx, 4))
+
+
+@pytest.mark.parametrize("layout", ["stencil", "variable"])
+def test_fsai_user_pattern_bitwise(ctx, rng, layout):
+    # build_fsai(A, LowerPattern p) (fsai.hpp:25) with a caller's pattern: G bitwise
+    if layout == "stencil":
+        host = pr.stencil_matrix(2, 12, 2, 10)
+    else:
+        host = random_spd(rng, random_layout(rng, 14, 5), 0.5)
+    n = host.nbr
+    pattern = []
+    for i in range(n):
+        lower = [int(j) for j in host.col_idx[host.row_ptr[i]:host.row_ptr[i + 1]] if j < i]
+        extra = [int(j) for j in rng.integers(0, i + 1, size=2)] if i > 0 else []
+        pattern.append(sorted(set(lower[::2] + extra + [i])))
+    M = Fsai.from_pattern(BlockSparseMatrix(ctx, host), pattern)
+    want = O.fsai_with_pattern(O.Mat(host), [[j for j in row if j < i] for i, row in enumerate(pattern)])
+    _assert_same_bsr(M.G.download(host.row_sizes, host.col_sizes), want.G().export())
+    from paper_2509_06744_b200.native import InvalidArgument
+    with pytest.raises(InvalidArgument):
+        Fsai.from_pattern(BlockSparseMatrix(ctx, host), [[i + 1] if i + 1 < n else [] for i in range(n)])
