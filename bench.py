@@ -428,10 +428,20 @@ def run_ours(args, cfg):
             extra["C2x8"] = measure_batch(ctx, stream, H, b_own, k, 8, args.steps)
         except Exception as e:
             extra["C2x8"] = {"error": f"{type(e).__name__}: {e}"}
-        if not args.no_c4:
-            # largest single-GPU config (C4, ~110 GB): free the headline hierarchy first
+        if not args.no_c4 or not args.no_quarter:
+            # the large lines: free the headline hierarchy first
             del H, dA, dT, bv, xv, rv
             ctx.sync()
+        if not args.no_quarter:
+            # C3 and C5 do not fit one GPU; their shapes (C3: nested FSAI, m = 21, 25-pt,
+            # V(4,4), 5 levels; C5: m = 15, 6 levels) at a quarter of the rows do
+            for key, c in (("C3@512", pr.CONFIGS["C3"].scaled(512)), ("C5@1024", pr.CONFIGS["C5"].scaled(1024))):
+                try:
+                    extra[key] = measure_hierarchy(ctx, stream, c, min(args.steps, 10))
+                    extra[key]["note"] = "reduced size: a quarter of the named config's fine rows, same shape"
+                except Exception as e:
+                    extra[key] = {"error": f"{type(e).__name__}: {e}"}
+        if not args.no_c4:
             try:
                 free = torch.cuda.mem_get_info()[0]
                 if free < 125e9:
@@ -530,6 +540,7 @@ def main():
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of row strips")
     ap.add_argument("--no-c4", action="store_true", help="skip the extra C4 (largest single-GPU config) line")
     ap.add_argument("--no-single-core", action="store_true", help="skip the 1-thread oracle cycle")
+    ap.add_argument("--no-quarter", action="store_true", help="skip the quarter-size C3 / C5 shape lines")
     args = ap.parse_args()
     from paper_2509_06744_b200 import problems as pr
 
