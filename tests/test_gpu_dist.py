@@ -100,3 +100,23 @@ def test_dist_setup_rejects_underestimated_radius(ctx):
     with pytest.raises(InvalidArgument, match="radius"):
         Hierarchy.setup_dist(ctx, BlockSparseMatrix(ctx, A), [BlockSparseMatrix(ctx, p) for p in T], gran, bad, 1,
                              params)
+
+
+def test_dist_setup_batched_cycles_and_whole_only_apis(ctx):
+    # a distributed-setup hierarchy runs batched cycles bitwise like the single-device
+    # one; whole-only entry points refuse it cleanly
+    from paper_2509_06744_b200.native import InvalidArgument
+    cfg, params = _cfg("c2_like")
+    hw, b = _whole(ctx, cfg, params)
+    hd, _ = _dist(ctx, cfg, params, 3, 1)
+    K = 4
+    B = np.stack([np.roll(b, 3 * v) for v in range(K)], axis=1).ravel().copy()
+    x1, x2 = Vector(ctx, B.size), Vector(ctx, B.size)
+    for _ in range(2):
+        hw.v_cycle_batch(3, 3, K, Vector(ctx, B), x1)
+        hd.v_cycle_batch(3, 3, K, Vector(ctx, B), x2)
+    assert np.array_equal(x1.download(), x2.download())
+    with pytest.raises(InvalidArgument):
+        hd.v_cycle_level(3, 3, 1, Vector(ctx, 16), Vector(ctx, 16))
+    with pytest.raises(InvalidArgument):
+        hd.measure_rates(BlockSparseMatrix(ctx, pr.stencil_matrix(2, 32, 2, 4)), Vector(ctx, b), Vector(ctx, b), 3, 3)
