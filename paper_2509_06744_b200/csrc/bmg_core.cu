@@ -39,10 +39,20 @@ thread_local int g_last_pivot = -1;
 // ============================================================================ context
 Ctx::~Ctx() {
   comm.reset();
+  // at process exit the runtime may already be unloading: the driver reclaims
+  // everything, and library handles must not be torn down against a dead context
+  if (cudaFree(nullptr) == cudaErrorCudartUnloading) return;
   if (solver) cusolverDnDestroy(solver);
   if (blas) cublasDestroy(blas);
   if (h_red) cudaFreeHost(h_red);
   if (own) cudaStreamDestroy(own);
+}
+
+void ctx_retain(Ctx* c) {
+  if (c) c->refs.fetch_add(1, std::memory_order_relaxed);
+}
+void ctx_release(Ctx* c) {
+  if (c && c->refs.fetch_sub(1, std::memory_order_acq_rel) == 1) delete c;
 }
 
 cublasHandle_t Ctx::cublas() {
@@ -709,7 +719,7 @@ int bmg_ctx_destroy(bmg_ctx* ctx) {
   return guard([&] {
     Ctx* c = reinterpret_cast<Ctx*>(ctx);
     if (c) BMG_CUDA(cudaStreamSynchronize(c->stream));
-    delete c;
+    ctx_release(c);  // freed now, or when its last device object is destroyed
   });
 }
 int bmg_ctx_set_stream(bmg_ctx* ctx, void* s) {

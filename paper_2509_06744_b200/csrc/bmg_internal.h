@@ -4,6 +4,7 @@
 #include <cublas_v2.h>
 #include <cusolverDn.h>
 
+#include <atomic>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -78,6 +79,31 @@ std::unique_ptr<Comm> make_nccl_comm(int rank, int world, const unsigned char* i
 std::unique_ptr<Comm> make_loopback_comm(LoopGroup* g, int rank);
 void nccl_unique_id(unsigned char* id128);
 
+struct Ctx;
+void ctx_retain(Ctx* c);
+void ctx_release(Ctx* c);
+// A counted reference to the owning context: device objects keep their context
+// alive, so handles may be destroyed in any order (bmg_ctx_destroy drops the
+// caller's reference; the context goes when its last object does).
+struct CtxRef {
+  Ctx* p = nullptr;
+  CtxRef() = default;
+  CtxRef(Ctx* c) : p(c) { ctx_retain(p); }  // NOLINT(google-explicit-constructor)
+  CtxRef(const CtxRef& o) : p(o.p) { ctx_retain(p); }
+  CtxRef& operator=(const CtxRef& o) {
+    if (this != &o) {
+      ctx_retain(o.p);
+      ctx_release(p);
+      p = o.p;
+    }
+    return *this;
+  }
+  CtxRef& operator=(Ctx* c) { return *this = CtxRef(c); }
+  ~CtxRef() { ctx_release(p); }
+  Ctx* operator->() const { return p; }
+  operator Ctx*() const { return p; }  // NOLINT(google-explicit-constructor)
+};
+
 struct Ctx {
   int device = 0;
   int sms = 148;
@@ -95,6 +121,7 @@ struct Ctx {
   cusolverDnHandle_t cusolver();
   cublasHandle_t blas = nullptr;
   cublasHandle_t cublas();
+  std::atomic<int> refs{1};  // the creator's reference plus one per live object
   ~Ctx();
 };
 
@@ -116,7 +143,7 @@ struct Plan {
 // the sm_100a bulk-copy kernel.  Variable layouts use per-block value offsets
 // and a warp-per-block-row kernel.
 struct Bsr {
-  Ctx* ctx = nullptr;
+  CtxRef ctx;
   int nbr = 0, nbc = 0;
   std::vector<int> rsz, csz, roff, coff;  // host layouts
   int dim_r = 0, dim_c = 0;
@@ -162,7 +189,7 @@ BlkView blk_view(const struct Bsr& a);
 int max_block(const struct Bsr& a);
 
 struct Vec {
-  Ctx* ctx = nullptr;
+  CtxRef ctx;
   int64_t n = 0;
   DBuf<double> d;
 };
@@ -170,7 +197,7 @@ struct Vec {
 // M = G^T G with G = L-hat^{-1} F-hat; `fwd` holds the forward factors applied
 // in order (one for nest = 0: G itself), `bwd` their transposes (reverse order).
 struct Fsai {
-  Ctx* ctx = nullptr;
+  CtxRef ctx;
   int dim = 0;
   std::vector<std::unique_ptr<Bsr>> fwd, bwd;
   const Bsr& G() const { return *fwd.back(); }

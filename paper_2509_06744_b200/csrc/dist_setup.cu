@@ -181,6 +181,36 @@ static std::unique_ptr<Bsr> principal(const Bsr& a, int lo, int hi) {
   return out;
 }
 
+// A phase that only some ranks run (or that may fail on some ranks) followed by
+// collectives: with a transport, every rank learns whether any rank failed and all
+// of them throw together instead of leaving the others blocked in a collective.
+template <class F>
+static void collective_phase(Ctx* ctx, bool with_comm, F&& f) {
+  if (!with_comm) {
+    f();
+    return;
+  }
+  int st = BMG_OK;
+  std::string msg;
+  try {
+    f();
+  } catch (const Error& e) {
+    st = e.status;
+    msg = e.what();
+  } catch (const std::exception& e) {
+    st = BMG_ERUNTIME;
+    msg = e.what();
+  }
+  DBuf<int32_t> flag(1);
+  int32_t h = st != BMG_OK ? 1 : 0;
+  BMG_CUDA(cudaMemcpy(flag.p, &h, 4, cudaMemcpyHostToDevice));
+  ctx->comm->allreduce(flag.p, flag.p, 1, DType::I32, ROp::Max, ctx->stream);
+  BMG_CUDA(cudaMemcpyAsync(&h, flag.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (st != BMG_OK) fail(st, msg);
+  if (h) fail(BMG_ERUNTIME, "dist setup: another rank failed");
+}
+
 struct Kept {  // one rank's exact own rows of one level, global column indices
   std::unique_ptr<Bsr> A, P, R;
   std::vector<std::unique_ptr<Bsr>> F, Bt;
@@ -375,14 +405,17 @@ static std::vector<std::vector<Kept>> dist_build(Ctx* ctx, const DistPlan& P, bo
   std::vector<std::vector<Kept>> K(nh);
   for (auto& k : K) k.resize(L);
   std::vector<std::unique_ptr<Bsr>> aext(nh);
+  const bool with_comm = !emulated && world > 1;
   for (int l = top; l >= P.agg; --l) {
-    for (int i = 0; i < nh; ++i) {
-      const int r = emulated ? i : ctx->rank;
-      const Bsr* a = l == top ? a_top[i] : aext[i].get();
-      if (P.B[l][r + 1] <= P.B[l][r]) continue;
-      if (!a) fail(BMG_ERUNTIME, "dist setup: missing extended strip");
-      dist_level(ctx, P, r, l, *a, *pin[i][l], prm, K[i]);
-    }
+    collective_phase(ctx, with_comm, [&] {
+      for (int i = 0; i < nh; ++i) {
+        const int r = emulated ? i : ctx->rank;
+        const Bsr* a = l == top ? a_top[i] : aext[i].get();
+        if (P.B[l][r + 1] <= P.B[l][r]) continue;
+        if (!a) fail(BMG_ERUNTIME, "dist setup: missing extended strip");
+        dist_level(ctx, P, r, l, *a, *pin[i][l], prm, K[i]);
+      }
+    });
     for (auto& a : aext) a.reset();
     if (l == P.agg) break;
     // next level's extended strips from the owners' exact rows
@@ -528,6 +561,8 @@ static std::unique_ptr<Hier> dist_setup(Ctx* ctx, const DistPlan& P, int rank, s
   const bool have_root = h->emulated || ctx->rank == 0;
   std::vector<std::unique_ptr<Bsr>> whole_A(agg);
   std::vector<std::unique_ptr<Bsr>> whole_R(agg + 1);
+  const bool with_comm = !h->emulated && world > 1;
+  collective_phase(ctx, with_comm, [&] {
   if (have_root) {
     const Bsr* ak = a_agg.get();
     for (int l = agg; l >= 1; --l) {
@@ -546,6 +581,7 @@ static std::unique_ptr<Hier> dist_setup(Ctx* ctx, const DistPlan& P, int rank, s
     }
     k0[agg].R = std::move(whole_R[agg]);
   }
+  });
   // the parts
   const int nparts = h->emulated ? world : 1;
   for (int pi = 0; pi < nparts; ++pi) {
@@ -708,12 +744,14 @@ static std::unique_ptr<Hier> dist_setup(Ctx* ctx, const DistPlan& P, int rank, s
   h->user_b = nullptr;
   h->user_x = nullptr;
   // coarse direct solve on rank 0
-  for (Part& p : h->parts)
-    if (p.rank == 0) {
-      if (P.nbr[0] * (int64_t)h->msz[0] > prm.coarse_dim_cap)
-        fail(BMG_EINVAL, "setup: coarsest level exceeds the dense-solve cap");
-      coarse_factor(*h, p);
-    }
+  collective_phase(ctx, with_comm, [&] {
+    for (Part& p : h->parts)
+      if (p.rank == 0) {
+        if (P.nbr[0] * (int64_t)h->msz[0] > prm.coarse_dim_cap)
+          fail(BMG_EINVAL, "setup: coarsest level exceeds the dense-solve cap");
+        coarse_factor(*h, p);
+      }
+  });
   if (!h->emulated && world > 1) {
     int64_t n0 = h->n0;
     DBuf<int64_t> d(1);

@@ -110,7 +110,7 @@ struct GraphKey {
 };
 
 struct Hier {
-  Ctx* ctx = nullptr;
+  CtxRef ctx;
   int world = 1;          // ranks the rows are split over
   bool emulated = false;  // all virtual ranks live in this process
   std::vector<Part> parts;

@@ -85,3 +85,23 @@ def test_spmv_length_validation(ctx, rng):
     A = BlockSparseMatrix(ctx, host)
     with pytest.raises(InvalidArgument):
         spmv(A, Vector(ctx, 39), Vector(ctx, 40))
+
+
+def test_objects_outlive_their_context_handle():
+    # handles may be destroyed in any order (the C objects keep their context alive):
+    # closing the context first must neither crash nor break the objects still in use
+    import gc
+
+    from paper_2509_06744_b200 import BlockSparseMatrix, Context, Vector, spmv
+    from paper_2509_06744_b200 import problems as pr
+    c = Context(0)
+    host = pr.stencil_matrix(2, 8, 2, 10)
+    A = BlockSparseMatrix(c, host)
+    x = Vector(c, pr.normal_vector(host.dim_c, 0, 1))
+    y = Vector(c, host.dim_r)
+    c.close()
+    spmv(A, x, y)
+    assert np.isfinite(y.download()).all()
+    del A, x
+    gc.collect()
+    y.close()

@@ -105,3 +105,37 @@ def test_distributed_setup_through_transport(ctx, name, world, agg):
         return _rank_cycles(h, c, b_own)
 
     _check(ref, _run_ranks(world, rank), world)
+
+
+def test_distributed_setup_failure_on_one_rank_fails_all(ctx):
+    # rank 1 passes a strip that does not match the plan: it fails in its own phase,
+    # rank 0 must not block in the following row exchange but fail as well
+    import time
+    cfg = pr.Config("c2", 2, 32, 2, 4, 3, "adaptive", 3)
+    params = default_params(t_max=1, coarse_dim_cap=1 << 30)
+    _, _, gran, rad = pr.level_grid(cfg)
+    world = 2
+    group = LoopbackGroup(world)
+    errs = [None] * world
+
+    def body(r):
+        try:
+            c = Context(0, loopback=(group, r))
+            A, T, _, _ = pr.dist_inputs(cfg, world, r, 1, params)
+            if r == 1:
+                A, _, _, _ = pr.dist_inputs(cfg, world, 0, 1, params)  # rank 0's strip: wrong rows
+            Hierarchy.setup_dist(c, BlockSparseMatrix(c, A), [BlockSparseMatrix(c, p) for p in T], gran, rad, 1,
+                                 params)
+        except Exception as e:  # noqa: BLE001
+            errs[r] = e
+
+    t0 = time.time()
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not any(t.is_alive() for t in th)
+    assert time.time() - t0 < 100  # no transport timeout involved
+    assert errs[1] is not None and "dist setup" in str(errs[1])
+    assert errs[0] is not None and "another rank failed" in str(errs[0])
