@@ -48,6 +48,19 @@ Ctx::~Ctx() {
   if (own) cudaStreamDestroy(own);
 }
 
+void bsr_retain(const Bsr* a) {
+  if (a) a->refs.fetch_add(1, std::memory_order_relaxed);
+}
+void bsr_release(const Bsr* a) {
+  if (a && a->refs.fetch_sub(1, std::memory_order_acq_rel) == 1) delete a;
+}
+void fsai_retain(const Fsai* m) {
+  if (m) m->refs.fetch_add(1, std::memory_order_relaxed);
+}
+void fsai_release(const Fsai* m) {
+  if (m && m->refs.fetch_sub(1, std::memory_order_acq_rel) == 1) delete m;
+}
+
 void ctx_retain(Ctx* c) {
   if (c) c->refs.fetch_add(1, std::memory_order_relaxed);
 }
@@ -749,7 +762,7 @@ int bmg_bsr_destroy(bmg_bsr* a) {
   return guard([&] {
     Bsr* m = reinterpret_cast<Bsr*>(a);
     if (m) BMG_CUDA(cudaStreamSynchronize(m->ctx->stream));
-    delete m;
+    bsr_release(m);  // freed now, or when the last hierarchy holding it goes
   });
 }
 int bmg_bsr_info(const bmg_bsr* ah, int* nbr, int* nbc, int64_t* nnzb, int* dim_r, int* dim_c,

@@ -137,6 +137,26 @@ struct Plan {
   DBuf<int> cta_chunk;   // [nctas + 1]
 };
 
+// Counted references to matrices / preconditioners: every owner (a unique_ptr, or a
+// hierarchy holding the caller's inputs -- the reference's setup has value
+// semantics) drops one reference and the object goes with the last one.
+struct Bsr;
+struct Fsai;
+void bsr_retain(const Bsr* a);
+void bsr_release(const Bsr* a);
+void fsai_retain(const Fsai* m);
+void fsai_release(const Fsai* m);
+}  // namespace bmg
+template <>
+struct std::default_delete<bmg::Bsr> {
+  void operator()(bmg::Bsr* p) const { bmg::bsr_release(p); }
+};
+template <>
+struct std::default_delete<bmg::Fsai> {
+  void operator()(bmg::Fsai* p) const { bmg::fsai_release(p); }
+};
+namespace bmg {
+
 // ---- block-sparse matrix on the device ----------------------------------------
 // Uniform layouts (every block m_r x m_c) store blocks row-major with a padded
 // stride bs = m_r*m_c rounded up to even (16-byte aligned blocks), streamed by
@@ -144,6 +164,7 @@ struct Plan {
 // and a warp-per-block-row kernel.
 struct Bsr {
   CtxRef ctx;
+  mutable std::atomic<int> refs{1};  // the creator's reference + hierarchies holding it
   int nbr = 0, nbc = 0;
   std::vector<int> rsz, csz, roff, coff;  // host layouts
   int dim_r = 0, dim_c = 0;
@@ -188,6 +209,7 @@ struct BlkView {
 BlkView blk_view(const struct Bsr& a);
 int max_block(const struct Bsr& a);
 
+
 struct Vec {
   CtxRef ctx;
   int64_t n = 0;
@@ -198,6 +220,7 @@ struct Vec {
 // in order (one for nest = 0: G itself), `bwd` their transposes (reverse order).
 struct Fsai {
   CtxRef ctx;
+  mutable std::atomic<int> refs{1};
   int dim = 0;
   std::vector<std::unique_ptr<Bsr>> fwd, bwd;
   const Bsr& G() const { return *fwd.back(); }

@@ -133,7 +133,21 @@ struct Hier {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   const double* user_b = nullptr;
   double* user_x = nullptr;
+  std::vector<const Bsr*> held_bsr;    // caller objects the levels point to
+  std::vector<const Fsai*> held_fsai;
+  void hold(const Bsr* a) {
+    bsr_retain(a);
+    held_bsr.push_back(a);
+  }
+  void hold(const Fsai* m) {
+    fsai_retain(m);
+    held_fsai.push_back(m);
+  }
   ~Hier() {
+    if (ctx) cudaStreamSynchronize(ctx->stream);
+    parts.clear();  // level objects first, then the caller objects they point to
+    for (const Bsr* a : held_bsr) bsr_release(a);
+    for (const Fsai* m : held_fsai) fsai_release(m);
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);

@@ -484,10 +484,12 @@ int bmg_hier_setup(const bmg_bsr* a_finest, int ntransfers, const bmg_bsr* const
     const int depth = ntransfers;
     p.lv.resize(depth + 1);
     p.lv[depth].A = af;
+    h->hold(af);
     SetupClock clk(ctx);
     for (int l = depth; l >= 1; --l) {
       PLevel& L = p.lv[l];
       L.P = B_(transfers[l - 1]);
+      h->hold(L.P);
       L.R_own = bsr_transpose(*L.P);
       L.R = L.R_own.get();
       clk.mark("transpose P", l);
@@ -527,13 +529,16 @@ int bmg_hier_create(bmg_ctx* ctx, int nlevels, const bmg_bsr* const* A, const bm
     for (int l = 0; l < nlevels; ++l) {
       PLevel& L = p.lv[l];
       L.A = B_(A[l]);
+      h->hold(L.A);
       if (l >= 1) {
         L.P = B_(P[l]);
+        h->hold(L.P);
         if (L.P->dim_r != L.A->dim_r || L.P->dim_c != B_(A[l - 1])->dim_r)
           fail(BMG_EINVAL, "hierarchy: prolongation shape does not match the levels");
         L.R_own = bsr_transpose(*L.P);
         L.R = L.R_own.get();
         L.M = M_(Mh[l]);
+        h->hold(L.M);
         L.spec.kind = 2;
         L.spec.beta = beta[l];
         L.spec.alpha = beta[l] / 30.0;

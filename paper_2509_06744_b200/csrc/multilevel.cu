@@ -1162,7 +1162,7 @@ int bmg_fsai_destroy(bmg_fsai* m) {
   return guard([&] {
     Fsai* f = reinterpret_cast<Fsai*>(m);
     if (f) BMG_CUDA(cudaStreamSynchronize(f->ctx->stream));
-    delete f;
+    fsai_release(f);
   });
 }
 int bmg_fsai_apply(const bmg_fsai* mh, const bmg_vec* r, bmg_vec* z) {

@@ -426,3 +426,42 @@ def test_fsai_user_pattern_bitwise(ctx, rng, layout):
     from paper_2509_06744_b200.native import InvalidArgument
     with pytest.raises(InvalidArgument):
         Fsai.from_pattern(BlockSparseMatrix(ctx, host), [[i + 1] if i + 1 < n else [] for i in range(n)])
+
+
+def test_hierarchy_keeps_its_inputs_alive(ctx):
+    # setup (multilevel.hpp:59) has value semantics: destroying the caller's A and
+    # transfers (and, for create, the FSAI objects) afterwards must not affect cycles
+    cfg = pr.CONFIGS["C2"].scaled(16, 3)
+    A, T, b = pr.make_problem(cfg)
+    ref = Hierarchy.setup(BlockSparseMatrix(ctx, A), [BlockSparseMatrix(ctx, p) for p in T],
+                          default_params(t_max=1, coarse_dim_cap=1 << 30))
+    x_ref = Vector(ctx, b.size)
+    ref.v_cycle(3, 3, Vector(ctx, b), x_ref)
+    dA = BlockSparseMatrix(ctx, A)
+    dT = [BlockSparseMatrix(ctx, p) for p in T]
+    h = Hierarchy.setup(dA, dT, default_params(t_max=1, coarse_dim_cap=1 << 30))
+    dA.close()
+    for p in dT:
+        p.close()
+    h._keep.clear()
+    x = Vector(ctx, b.size)
+    h.v_cycle(3, 3, Vector(ctx, b), x)
+    assert np.array_equal(x.download(), x_ref.download())
+    # create(): levels, transfers and preconditioners taken from another hierarchy
+    L = ref.levels
+    As, Ps, Ms = [], [None], [None]
+    for l in range(L):
+        a, p, m = ref.level(l)
+        As.append(a)
+        if l:
+            Ps.append(p)
+            Ms.append(m)
+    betas = [0.0] + [ref.beta(l) for l in range(1, L)]
+    hc = Hierarchy.create(ctx, As, Ps, Ms, betas)
+    hc._keep.clear()
+    x2 = Vector(ctx, b.size)
+    hc.v_cycle(3, 3, Vector(ctx, b), x2)
+    ref.close()  # the level objects hc points to belonged to ref
+    x3 = Vector(ctx, b.size)
+    hc.v_cycle(3, 3, Vector(ctx, b), x3)
+    assert np.array_equal(x2.download(), x3.download())
