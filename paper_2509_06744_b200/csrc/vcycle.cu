@@ -14,47 +14,88 @@
 #include <tuple>
 
 #include "bmg_abi.h"
+#include "bsr_stream.cuh"
 #include "hier.h"
 
 namespace bmg {
 namespace kern {
-// K right-hand sides interleaved per scalar row.  mode 0: symmetric tiles (row part
-// tile * x_J, column part tile^T * x_I for J < I); mode 1: lower-triangular T x (row
-// parts only); mode 2: T^T x (column parts, diagonal tiles included)
-__global__ void __launch_bounds__(256) symv_tiles_kernel(const double* __restrict__ tiles,
-                                                         const double* __restrict__ x, int64_t N, int nt,
-                                                         double* __restrict__ part, int K, int mode) {
-  __shared__ double tl[kTile][kTile + 1];
-  __shared__ double xi[8][kTile], xj[8][kTile];
-  int I, J;
-  tile_of(blockIdx.x, &I, &J);
-  const double2* src = reinterpret_cast<const double2*>(tiles + (int64_t)blockIdx.x * kTile * kTile);
-  for (int e = threadIdx.x; e < kTile * kTile / 2; e += blockDim.x) {
-    const double2 v = __ldg(src + e);
-    const int r = (2 * e) / kTile, c = (2 * e) - r * kTile;
-    tl[r][c] = v.x;
-    tl[r][c + 1] = v.y;
-  }
-  for (int e = threadIdx.x; e < kTile * K; e += blockDim.x) {
-    const int t = e / K, v = e - (e / K) * K;
-    const int64_t gi = (int64_t)I * kTile + t, gj = (int64_t)J * kTile + t;
-    xi[v][t] = gi < N ? x[gi * K + v] : 0.0;
-    xj[v][t] = gj < N ? x[gj * K + v] : 0.0;
+// Coarse solve x = A_0^{-1} b from packed lower 64 x 64 tiles; K right-hand sides
+// interleaved per scalar row.  mode 0: symmetric tiles (row part tile * x_J, column
+// part tile^T * x_I for J < I); mode 1: lower-triangular T x (row parts only);
+// mode 2: T^T x (column parts, diagonal tiles included).  Partials go to
+// part[(out tile row, other tile, row, rhs)] and are summed by symv_reduce_kernel.
+// Persistent: each CTA walks tiles
+// blockIdx.x, +gridDim.x, ... and streams them through a two-stage shared-memory
+// ring with cp.async.bulk (mbarrier complete_tx), so the next tile lands while the
+// current one is used.  Row parts read the unpadded tile in a rotated column order
+// (c = (c' + t) mod 64: conflict-free banks); column parts read columns directly.
+constexpr int kSymvThreads = 256;
+constexpr size_t kSymvSmem = 2 * kTile * kTile * sizeof(double) + 2 * 8 * kTile * sizeof(double) + 16;
+__global__ void __launch_bounds__(kSymvThreads) symv_stream_kernel(const double* __restrict__ tiles,
+                                                                   const double* __restrict__ x, int64_t N, int nt,
+                                                                   int64_t ntiles, double* __restrict__ part, int K,
+                                                                   int mode) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  double* ring = reinterpret_cast<double*>(smem);                    // 2 x 64 x 64
+  double* xi = ring + 2 * kTile * kTile;                             // [8][64]
+  double* xj = xi + 8 * kTile;                                       // [8][64]
+  uint64_t* full = reinterpret_cast<uint64_t*>(xj + 8 * kTile);      // 2 barriers
+  const int tid = threadIdx.x;
+  constexpr uint32_t kBytes = kTile * kTile * sizeof(double);
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_fence_init();
   }
   __syncthreads();
+  const int64_t stride = gridDim.x;
+  if (tid == 0)
+    for (int st = 0; st < 2; ++st) {
+      const int64_t t = blockIdx.x + st * stride;
+      if (t < ntiles) {
+        mbar_arrive_expect_tx(&full[st], kBytes);
+        bulk_g2s(ring + st * kTile * kTile, tiles + t * kTile * kTile, kBytes, &full[st]);
+      }
+    }
   const int it0 = mode == 2 ? kTile * K : 0, it1 = mode == 1 ? kTile * K : 2 * kTile * K;
-  for (int it = it0 + threadIdx.x; it < it1; it += blockDim.x) {
-    const int half = it / (kTile * K);
-    const int rem = it - half * kTile * K;
-    const int t = rem / K, v = rem - (rem / K) * K;
-    if (half == 0) {  // row part: tile * x_J
-      double s = 0.0;
-      for (int c = 0; c < kTile; ++c) s = __fma_rn(tl[t][c], xj[v][c], s);
-      part[(((int64_t)I * nt + J) * kTile + t) * K + v] = s;
-    } else if (J < I || mode == 2) {  // column part: tile^T * x_I
-      double s = 0.0;
-      for (int r = 0; r < kTile; ++r) s = __fma_rn(tl[r][t], xi[v][r], s);
-      part[(((int64_t)J * nt + I) * kTile + t) * K + v] = s;
+  int it = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += stride, ++it) {
+    const int st = it & 1;
+    int I, J;
+    tile_of(t, &I, &J);
+    for (int e = tid; e < kTile * K; e += kSymvThreads) {
+      const int r = e / K, v = e - (e / K) * K;
+      const int64_t gi = (int64_t)I * kTile + r, gj = (int64_t)J * kTile + r;
+      xi[v * kTile + r] = gi < N ? x[gi * K + v] : 0.0;
+      xj[v * kTile + r] = gj < N ? x[gj * K + v] : 0.0;
+    }
+    __syncthreads();
+    mbar_wait(&full[st], (it >> 1) & 1);
+    const double* tl = ring + st * kTile * kTile;
+    for (int q = it0 + tid; q < it1; q += kSymvThreads) {
+      const int half = q / (kTile * K);
+      const int rem = q - half * kTile * K;
+      const int r = rem / K, v = rem - (rem / K) * K;
+      if (half == 0) {  // row part: tile * x_J
+        double sum = 0.0;
+        const double* row = tl + r * kTile;
+        const double* xv = xj + v * kTile;
+        for (int c0 = 0; c0 < kTile; ++c0) {
+          const int c = (c0 + r) & (kTile - 1);
+          sum = __fma_rn(row[c], xv[c], sum);
+        }
+        part[(((int64_t)I * nt + J) * kTile + r) * K + v] = sum;
+      } else if (J < I || mode == 2) {  // column part: tile^T * x_I
+        double sum = 0.0;
+        const double* xv = xi + v * kTile;
+        for (int rr = 0; rr < kTile; ++rr) sum = __fma_rn(tl[rr * kTile + r], xv[rr], sum);
+        part[(((int64_t)J * nt + I) * kTile + r) * K + v] = sum;
+      }
+    }
+    __syncthreads();  // tile and x segments consumed
+    if (tid == 0 && t + 2 * stride < ntiles) {
+      mbar_arrive_expect_tx(&full[st], kBytes);
+      bulk_g2s(ring + st * kTile * kTile, tiles + (t + 2 * stride) * kTile * kTile, kBytes, &full[st]);
     }
   }
 }
@@ -218,17 +259,26 @@ static void coarse_solve(Hier& h) {
     const int64_t ntiles = (int64_t)nt * (nt + 1) / 2;
     const int K = h.nrhs;
     const unsigned rgrid = (unsigned)((N * K + 255) / 256);
+    static const bool attr = [] {
+      BMG_CUDA(cudaFuncSetAttribute(kern::symv_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)kern::kSymvSmem));
+      return true;
+    }();
+    (void)attr;
+    const unsigned sgrid = (unsigned)std::min<int64_t>(ntiles, (int64_t)h.ctx->sms * 3);
+    auto tiles_pass = [&](const double* in, int mode) {
+      kern::symv_stream_kernel<<<sgrid, kern::kSymvThreads, kern::kSymvSmem, h.ctx->stream>>>(
+          p.ainv.p, in, N, nt, ntiles, p.cpart.p, K, mode);
+    };
     if (!p.tri) {  // x = A_0^{-1} b with the symmetric packed inverse
-      kern::symv_tiles_kernel<<<(unsigned)ntiles, 256, 0, h.ctx->stream>>>(p.ainv.p, vec(h, p, 0, VB) + L.off(), N,
-                                                                          nt, p.cpart.p, K, 0);
+      tiles_pass(vec(h, p, 0, VB) + L.off(), 0);
       kern::symv_reduce_kernel<<<rgrid, 256, 0, h.ctx->stream>>>(p.cpart.p, nt, N, vec(h, p, 0, VX) + L.off(), K, 0);
       h.ctx->count(2);
     } else {  // x = W^T (W b), W = L^{-1}: y in the level's r buffer
       double* y = vec(h, p, 0, VR) + L.off();
-      kern::symv_tiles_kernel<<<(unsigned)ntiles, 256, 0, h.ctx->stream>>>(p.ainv.p, vec(h, p, 0, VB) + L.off(), N,
-                                                                          nt, p.cpart.p, K, 1);
+      tiles_pass(vec(h, p, 0, VB) + L.off(), 1);
       kern::symv_reduce_kernel<<<rgrid, 256, 0, h.ctx->stream>>>(p.cpart.p, nt, N, y, K, 1);
-      kern::symv_tiles_kernel<<<(unsigned)ntiles, 256, 0, h.ctx->stream>>>(p.ainv.p, y, N, nt, p.cpart.p, K, 2);
+      tiles_pass(y, 2);
       kern::symv_reduce_kernel<<<rgrid, 256, 0, h.ctx->stream>>>(p.cpart.p, nt, N, vec(h, p, 0, VX) + L.off(), K, 2);
       h.ctx->count(4);
     }
