@@ -128,6 +128,7 @@ struct Hier {
     int64_t kernels;
   };
   std::map<GraphKey, Captured> graphs;
+  std::map<GraphKey, int> warm;  // transport hierarchies: keys already run once eagerly
   DBuf<double> io_b, io_x, seg;
   cudaStream_t comm = nullptr;  // halo exchanges overlap interior slices
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -160,6 +161,7 @@ struct Hier {
   void drop_graphs() {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
     graphs.clear();
+    warm.clear();
   }
 };
 

@@ -406,6 +406,15 @@ void run_vcycle(Hier& h, int kpre, int kpost, const double* bf, double* xf) {
   }
   GraphKey key{kpre, kpost, h.nrhs, h.cycle_top(), bf, xf};
   auto it = h.graphs.find(key);
+  if (it == h.graphs.end() && ctx->comm && !h.emulated && !h.warm.count(key)) {
+    // NCCL sets up peer connections on first use, which must not happen inside
+    // graph capture: the first cycle of every key runs eagerly
+    h.warm[key] = 1;
+    stage_in(h, bf, xf);
+    enqueue_vcycle(h, kpre, kpost);
+    stage_out(h, xf);
+    return;
+  }
   if (it == h.graphs.end()) {
     cudaStream_t user = ctx->stream;
     ctx->stream = ctx->own;
