@@ -38,10 +38,13 @@ thread_local int g_last_pivot = -1;
 
 // ============================================================================ context
 Ctx::~Ctx() {
-  comm.reset();
   // at process exit the runtime may already be unloading: the driver reclaims
-  // everything, and library handles must not be torn down against a dead context
-  if (cudaFree(nullptr) == cudaErrorCudartUnloading) return;
+  // everything, and communicators / library handles must not be torn down then
+  if (cudaFree(nullptr) == cudaErrorCudartUnloading) {
+    (void)comm.release();
+    return;
+  }
+  comm.reset();
   if (solver) cusolverDnDestroy(solver);
   if (blas) cublasDestroy(blas);
   if (h_red) cudaFreeHost(h_red);
