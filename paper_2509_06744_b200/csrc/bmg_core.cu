@@ -383,6 +383,9 @@ static void finish_layouts(Bsr& a, int nbr, const int* rsz, int nbc, const int* 
   a.uniform = nbr > 0 && nbc > 0;
   for (int i = 1; i < nbr && a.uniform; ++i) a.uniform = rsz[i] == rsz[0];
   for (int j = 1; j < nbc && a.uniform; ++j) a.uniform = csz[j] == csz[0];
+  a.mmax = 1;
+  for (int i = 0; i < nbr; ++i) a.mmax = std::max(a.mmax, rsz[i]);
+  for (int j = 0; j < nbc; ++j) a.mmax = std::max(a.mmax, csz[j]);
   a.mr = a.uniform ? rsz[0] : 0;
   a.mc = a.uniform ? csz[0] : 0;
   a.bs = a.uniform ? ((a.mr * a.mc + 1) & ~1) : 0;
@@ -451,12 +454,7 @@ BlkView blk_view(const Bsr& a) {
   return v;
 }
 
-int max_block(const Bsr& a) {
-  int m = 1;
-  for (int x : a.rsz) m = std::max(m, x);
-  for (int x : a.csz) m = std::max(m, x);
-  return m;
-}
+int max_block(const Bsr& a) { return a.mmax; }
 
 std::unique_ptr<Bsr> make_bsr_structure(Ctx* ctx, int nbr, const int* rsz, int nbc, const int* csz,
                                         std::vector<int64_t> row_ptr, std::vector<int32_t> col,

@@ -170,6 +170,7 @@ struct Bsr {
   int dim_r = 0, dim_c = 0;
   bool uniform = false;
   int mr = 0, mc = 0, bs = 0;  // uniform sizes / padded stride (doubles)
+  int mmax = 1;                // largest block dimension
   int64_t nnzb = 0;
   bool sym = false;
   std::vector<int64_t> h_row_ptr;
