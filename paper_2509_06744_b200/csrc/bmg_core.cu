@@ -289,10 +289,12 @@ static int occupancy_for(int mr, int mc, size_t smem, int K = 1) {
 
 // Partition block rows into per-CTA ranges balanced by blocks; cut each
 // range's contiguous block span into chunks of cb_max blocks (bsr_stream.cuh).
-static void build_plan_into(const Bsr& a, Plan& P, int K) {
+// plan for streaming `a` as uniform mr x mr blocks of stride bs (the real layout,
+// or a variable layout's padded copy)
+static void build_plan_into(const Bsr& a, Plan& P, int K, int mr, int bs) {
   P = Plan();
-  if (!(a.uniform && stream_supported(a.mr, a.mc)) || a.nbr == 0) return;
-  P.cb_max = chunk_blocks(a.mr, a.bs, K);
+  if (!stream_supported(mr, mr) || a.nbr == 0) return;
+  P.cb_max = chunk_blocks(mr, bs, K);
   P.stages = ring_stages();
   const auto& rp = a.h_row_ptr;
   // chunk list per CTA range
@@ -300,8 +302,8 @@ static void build_plan_into(const Bsr& a, Plan& P, int K) {
   std::vector<int> cta;
   int rmax = 1;
   // first pass with a provisional rmax to size smem and query occupancy
-  const size_t smem0 = kern::SmemLayout(a.bs, P.cb_max, P.cb_max + 2, a.mr, P.stages, K).total;
-  const int occ = occupancy_for(a.mr, a.mc, smem0, K);
+  const size_t smem0 = kern::SmemLayout(bs, P.cb_max, P.cb_max + 2, mr, P.stages, K).total;
+  const int occ = occupancy_for(mr, mr, smem0, K);
   const int64_t gmax = (int64_t)a.ctx->sms * occ;
   const int64_t per = std::max<int64_t>(1, (a.nnzb + gmax - 1) / gmax);
   int row = 0;
@@ -337,23 +339,73 @@ static void build_plan_into(const Bsr& a, Plan& P, int K) {
   P.rmax = rmax;
   P.nctas = (int)cta.size() - 1;
   P.nchunks = (int)chunks.size();
-  P.smem = kern::SmemLayout(a.bs, P.cb_max, P.rmax, a.mr, P.stages, K).total;
+  P.smem = kern::SmemLayout(bs, P.cb_max, P.rmax, mr, P.stages, K).total;
   if (P.smem > 227 * 1024) fail(BMG_EINVAL, "plan: chunk does not fit in shared memory");
-  occupancy_for(a.mr, a.mc, P.smem, K);  // sets the shared-memory attributes
+  occupancy_for(mr, mr, P.smem, K);  // sets the shared-memory attributes
   P.chunks.alloc(chunks.size());
   P.cta_chunk.alloc(cta.size());
   BMG_CUDA(cudaMemcpy(P.chunks.p, chunks.data(), chunks.size() * sizeof(int4), cudaMemcpyHostToDevice));
   BMG_CUDA(cudaMemcpy(P.cta_chunk.p, cta.data(), cta.size() * sizeof(int), cudaMemcpyHostToDevice));
 }
 
-void build_plan(Bsr& a) { build_plan_into(a, a.plan, 1); }
+void build_plan(Bsr& a) {
+  if (a.uniform && a.mr == a.mc) build_plan_into(a, a.plan, 1, a.mr, a.bs);
+}
+
+bool var_streamed(const Bsr& a) {
+  static const bool off = [] {
+    const char* e = std::getenv("BMG_VAR_STREAM");
+    return e && e[0] == '0';
+  }();
+  return !off && !a.uniform && a.nnzb > 0 && stream_supported(a.mmax, a.mmax);
+}
+
+namespace kern {
+// block b of a variable layout -> its mmax x mmax zero-padded slot (warp per block row)
+__global__ void pad_blocks_kernel(const double* __restrict__ vals, const int64_t* __restrict__ voff,
+                                  const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                                  const int* __restrict__ rsz, const int* __restrict__ csz, int nbr, int M, int pbs,
+                                  double* __restrict__ out) {
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= nbr) return;
+  const int mi = rsz[i];
+  for (int64_t b = row_ptr[i]; b < row_ptr[i + 1]; ++b) {
+    const int mj = csz[col[b]];
+    const double* src = vals + voff[b];
+    double* dst = out + b * pbs;
+    for (int e = lane; e < pbs; e += 32) {
+      const int r = e / M, c = e - (e / M) * M;
+      dst[e] = (r < mi && c < mj) ? src[r * mj + c] : 0.0;
+    }
+  }
+}
+}  // namespace kern
 
 const Plan& plan_for(const Bsr& a, int nrhs) {
+  const int idx = nrhs <= 1 ? 0 : nrhs == 2 ? 1 : nrhs == 4 ? 2 : 3;
+  if (var_streamed(a)) {
+    if (!a.pvals.p) {
+      const int M = a.mmax;
+      a.pbs = (M * M + 1) & ~1;
+      a.pvals.alloc((size_t)a.nnzb * a.pbs);
+      kern::pad_blocks_kernel<<<(unsigned)(((int64_t)a.nbr * 32 + 255) / 256), 256, 0, a.ctx->stream>>>(
+          a.vals.p, a.voff.p, a.row_ptr.p, a.col.p, a.d_rsz.p, a.d_csz.p, a.nbr, M, a.pbs, a.pvals.p);
+      a.ctx->count();
+      BMG_CUDA(cudaGetLastError());
+      BMG_CUDA(cudaStreamSynchronize(a.ctx->stream));
+    }
+    if (!a.pplan[idx]) {
+      auto p = std::make_unique<Plan>();
+      build_plan_into(a, *p, std::max(nrhs, 1), a.mmax, a.pbs);
+      a.pplan[idx] = std::move(p);
+    }
+    return *a.pplan[idx];
+  }
   if (nrhs <= 1) return a.plan;
-  const int idx = nrhs == 2 ? 1 : nrhs == 4 ? 2 : 3;
   if (!a.kplan[idx]) {
     auto p = std::make_unique<Plan>();
-    build_plan_into(a, *p, nrhs);
+    build_plan_into(a, *p, nrhs, a.mr, a.bs);
     a.kplan[idx] = std::move(p);
   }
   return *a.kplan[idx];
@@ -613,23 +665,29 @@ static bool pdl_enabled() {
   return on;
 }
 
-template <int MR, int MC, int K, class Epi>
+template <int MR, int MC, int K, class Epi, bool VAR = false>
 static void launch_stream_t(const Bsr& a, const double* x, Epi epi) {
   const Plan& P = plan_for(a, K);
   kern::StreamArgs s;
-  s.vals = a.vals.p;
+  s.vals = VAR ? a.pvals.p : a.vals.p;
   s.col = a.col.p;
   s.row_ptr = a.row_ptr.p;
   s.chunks = P.chunks.p;
   s.cta_chunk = P.cta_chunk.p;
   s.x = x;
-  s.bs = a.bs;
+  s.bs = VAR ? a.pbs : a.bs;
+  if (VAR) {
+    s.coff = a.d_coff.p;
+    s.roff = a.d_roff.p;
+    s.rsz = a.d_rsz.p;
+    s.xlen = a.dim_c;
+  }
   s.cb_max = P.cb_max;
   s.rmax = P.rmax;
   s.stages = P.stages;
   // one attribute per template instantiation (covers the largest plan)
   static const bool attr_set = [] {  // thread-safe one-time init (contexts may live on several threads)
-    stream_attrs(kern::bsr_stream_kernel<MR, MC, K, Epi>, K);
+    stream_attrs(kern::bsr_stream_kernel<MR, MC, K, Epi, VAR>, K);
     return true;
   }();
   (void)attr_set;
@@ -643,18 +701,18 @@ static void launch_stream_t(const Bsr& a, const double* x, Epi epi) {
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  BMG_CUDA(cudaLaunchKernelEx(&cfg, kern::bsr_stream_kernel<MR, MC, K, Epi>, s, epi));
+  BMG_CUDA(cudaLaunchKernelEx(&cfg, kern::bsr_stream_kernel<MR, MC, K, Epi, VAR>, s, epi));
   a.ctx->count();
   BMG_LAUNCHED(a.ctx->stream, "bsr_stream_kernel");
 }
 
-template <int MR, int MC, class Epi>
+template <int MR, int MC, class Epi, bool VAR = false>
 static void launch_stream_k(const Bsr& a, const double* x, Epi epi, int nrhs) {
   switch (nrhs) {
-    case 1: return launch_stream_t<MR, MC, 1>(a, x, epi);
-    case 2: return launch_stream_t<MR, MC, 2>(a, x, epi);
-    case 4: return launch_stream_t<MR, MC, 4>(a, x, epi);
-    case 8: return launch_stream_t<MR, MC, 8>(a, x, epi);
+    case 1: return launch_stream_t<MR, MC, 1, Epi, VAR>(a, x, epi);
+    case 2: return launch_stream_t<MR, MC, 2, Epi, VAR>(a, x, epi);
+    case 4: return launch_stream_t<MR, MC, 4, Epi, VAR>(a, x, epi);
+    case 8: return launch_stream_t<MR, MC, 8, Epi, VAR>(a, x, epi);
   }
   fail(BMG_EINVAL, "right-hand-side batch must be 1, 2, 4 or 8");
 }
@@ -668,6 +726,14 @@ static void launch(const Bsr& a, const double* x, Epi epi, int nrhs) {
       case 15: return launch_stream_k<15, 15>(a, x, epi, nrhs);
       case 20: return launch_stream_k<20, 20>(a, x, epi, nrhs);
       case 21: return launch_stream_k<21, 21>(a, x, epi, nrhs);
+    }
+  }
+  if (var_streamed(a)) {
+    switch (a.mmax) {
+      case 10: return launch_stream_k<10, 10, Epi, true>(a, x, epi, nrhs);
+      case 15: return launch_stream_k<15, 15, Epi, true>(a, x, epi, nrhs);
+      case 20: return launch_stream_k<20, 20, Epi, true>(a, x, epi, nrhs);
+      case 21: return launch_stream_k<21, 21, Epi, true>(a, x, epi, nrhs);
     }
   }
   if (nrhs < 1 || nrhs > 8) fail(BMG_EINVAL, "right-hand-side batch must be 1..8");

@@ -183,6 +183,11 @@ struct Bsr {
   DBuf<int> d_roff, d_coff, d_rsz, d_csz;
   Plan plan;                              // single right-hand side
   mutable std::unique_ptr<Plan> kplan[4];  // batched: index log2(nrhs), built on first use
+  // variable layouts with a streamed block size: values padded to mmax x mmax
+  // (zeros) for the streaming kernel, and its plans; built on first use
+  mutable DBuf<double> pvals;
+  mutable int pbs = 0;
+  mutable std::unique_ptr<Plan> pplan[4];
   std::unique_ptr<Bsr> tcache;  // device transpose (spmv_t)
   int64_t pass_bytes() const;
   int64_t device_bytes() const;
@@ -240,6 +245,8 @@ void build_plan(Bsr& a);
 // launch plan for nrhs right-hand sides (shared-memory size and CTA count depend
 // on it); call outside graph capture before the first batched launch
 const Plan& plan_for(const Bsr& a, int nrhs);
+// whether a variable layout runs on the streaming kernel through padded blocks
+bool var_streamed(const Bsr& a);
 
 // ---- device operations (all enqueue on ctx->stream) --------------------------
 // nrhs > 1: right-hand sides interleaved per scalar row (x[i * nrhs + v]); every

@@ -145,6 +145,12 @@ struct StreamArgs {
   int cb_max;  // blocks per chunk
   int rmax;    // rows per chunk
   int stages;  // shared-memory ring depth (<= kMaxStages)
+  // variable layouts streamed as MR x MC padded blocks (VAR kernels): block
+  // offsets / sizes of the real layout, x length for clamped gathers
+  const int* coff = nullptr;
+  const int* roff = nullptr;
+  const int* rsz = nullptr;
+  int64_t xlen = 0;
 };
 
 // column-index slots per stage: cb_max + 8, rounded to 16 bytes (bulk-copy
@@ -173,7 +179,10 @@ struct SmemLayout {
 
 // K right-hand sides interleaved per scalar row (x[i * K + v]): one matrix stream
 // serves K vectors; each RHS keeps the single-vector arithmetic order.
-template <int MR, int MC, int K, class Epi>
+// VAR: a variable layout whose blocks are stored padded to MR x MC with zeros; the
+// zero padding adds exact zeros to every fma chain, so each real entry keeps the
+// oracle's arithmetic order; padded rows are computed and never stored.
+template <int MR, int MC, int K, class Epi, bool VAR = false>
 __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi epi) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int kStages = s.stages;
@@ -247,9 +256,15 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
     typename Epi::Pre pre0{};
     if (tid < ritems) {
       const int rr = tid / (MR * K);
+      const int rv = tid - rr * MR * K;
       rlo0 = __ldg(s.row_ptr + d.z + rr);
       rhi0 = __ldg(s.row_ptr + d.z + rr + 1);
-      pre0 = epi.load((int64_t)(d.z + rr) * MR * K + (tid - rr * MR * K));
+      if constexpr (VAR) {
+        if (rv / K < __ldg(s.rsz + d.z + rr))
+          pre0 = epi.load(((int64_t)__ldg(s.roff + d.z + rr) + rv / K) * K + (rv - (rv / K) * K));
+      } else {
+        pre0 = epi.load((int64_t)(d.z + rr) * MR * K + rv);
+      }
     }
     mbar_wait(&full[st], (it / kStages) & 1);
 
@@ -269,8 +284,14 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
         const int v = rem / RG, g = rem - (rem / RG) * RG;
         const double* __restrict__ xj = s.x + (int64_t)cs[b] * MC * K + v;
         double xv[MC];
+        if constexpr (VAR) {
+          const int64_t x0 = (int64_t)__ldg(s.coff + cs[b]);
 #pragma unroll
-        for (int q = 0; q < MC; ++q) xv[q] = __ldg(xj + q * K);
+          for (int q = 0; q < MC; ++q) xv[q] = __ldg(s.x + min(x0 + q, s.xlen - 1) * K + v);
+        } else {
+#pragma unroll
+          for (int q = 0; q < MC; ++q) xv[q] = __ldg(xj + q * K);
+        }
         const double* ab = vs + b * s.bs;
 #pragma unroll
         for (int rr = 0; rr < RPG; ++rr) {
@@ -306,7 +327,11 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
         continue;
       }
       double xv[MC];
-      if constexpr (MC % 2 == 0) {
+      if constexpr (VAR) {
+        const int64_t x0 = (int64_t)__ldg(s.coff + j);
+#pragma unroll
+        for (int q = 0; q < MC; ++q) xv[q] = __ldg(s.x + min(x0 + q, s.xlen - 1));
+      } else if constexpr (MC % 2 == 0) {
 #pragma unroll
         for (int q = 0; q < MC / 2; ++q) {
           const double2 t2 = __ldg(reinterpret_cast<const double2*>(xj) + q);
@@ -342,10 +367,16 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
       const int rv = item - rr * MR * K;  // r * K + v
       int64_t rlo = rlo0, rhi = rhi0;
       typename Epi::Pre pre = pre0;
+      int64_t oi = (int64_t)(d.z + rr) * MR * K + rv;  // output index
+      bool real = true;
+      if constexpr (VAR) {
+        real = rv / K < __ldg(s.rsz + d.z + rr);
+        oi = ((int64_t)__ldg(s.roff + d.z + rr) + rv / K) * K + (rv - (rv / K) * K);
+      }
       if (item != tid) {
         rlo = __ldg(s.row_ptr + d.z + rr);
         rhi = __ldg(s.row_ptr + d.z + rr + 1);
-        pre = epi.load((int64_t)(d.z + rr) * MR * K + rv);
+        if (real) pre = epi.load(oi);
       }
       const int lo = (int)(max(rlo, (int64_t)d.x) - d.x);
       const int hi = (int)(min(rhi, (int64_t)(d.x + d.y)) - d.x);
@@ -354,8 +385,8 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
       for (int b = lo; b < hi; ++b) acc = __dadd_rn(acc, part[(b * MR + r) * KP + v]);
       if (rr == nrows - 1 && cout)
         carry_out[rv] = acc;
-      else
-        epi.store((int64_t)(d.z + rr) * MR * K + rv, acc, pre);
+      else if (real)
+        epi.store(oi, acc, pre);
     }
   }
 }

@@ -349,15 +349,11 @@ static void stage_out(Hier& h, double* x) {
 
 // batch size of the following cycles: every level's vectors hold K interleaved
 // right-hand sides (grown on demand; setup, Lanczos and solve run at K = 1)
-void set_nrhs(Hier& h, int K) {
-  if (K != 1 && K != 2 && K != 4 && K != 8) fail(BMG_EINVAL, "v_cycle batch: nrhs must be 1, 2, 4 or 8");
-  if (K == h.nrhs) return;
-  BMG_CUDA(cudaStreamSynchronize(h.ctx->stream));
-  h.nrhs = K;
-  bool moved = false;  // captured graphs of every batch size point at the old buffers
-  for (Part& p : h.parts) {
+// launch plans (and padded copies of variable layouts) for every matrix the cycle
+// streams with K right-hand sides: built here, never inside graph capture
+static void prepare_plans(Hier& h, int K) {
+  for (Part& p : h.parts)
     for (PLevel& L : p.lv) {
-      // launch plans for this batch size (built here, never inside graph capture)
       auto plans = [&](const SplitMat& sm) {
         for (const Slice& sl : sm.s) plan_for(*sl.m, K);
       };
@@ -366,6 +362,17 @@ void set_nrhs(Hier& h, int K) {
       plans(L.sP);
       for (auto& f : L.sF) plans(f);
       for (auto& f : L.sB) plans(f);
+    }
+}
+
+void set_nrhs(Hier& h, int K) {
+  if (K != 1 && K != 2 && K != 4 && K != 8) fail(BMG_EINVAL, "v_cycle batch: nrhs must be 1, 2, 4 or 8");
+  if (K == h.nrhs) return;
+  BMG_CUDA(cudaStreamSynchronize(h.ctx->stream));
+  h.nrhs = K;
+  bool moved = false;  // captured graphs of every batch size point at the old buffers
+  for (Part& p : h.parts) {
+    for (PLevel& L : p.lv) {
       L.k = K;
       for (int w = 0; w < VNUM; ++w) {
         if (!L.v[w].p || L.v[w].n >= (size_t)std::max<int64_t>(L.n_win(), 1)) continue;
@@ -384,6 +391,7 @@ void set_nrhs(Hier& h, int K) {
     }
   }
   if (moved) h.drop_graphs();
+  prepare_plans(h, K);
   BMG_CUDA(cudaStreamSynchronize(h.ctx->stream));
 }
 
@@ -416,6 +424,7 @@ void run_vcycle(Hier& h, int kpre, int kpost, const double* bf, double* xf) {
     return;
   }
   if (it == h.graphs.end()) {
+    prepare_plans(h, h.nrhs);
     cudaStream_t user = ctx->stream;
     ctx->stream = ctx->own;
     const int64_t before = ctx->launches;
