@@ -97,8 +97,10 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower().startswith("active")})
         under_load = [s for s in sm if s > 0.5 * (max(sm) if sm else 1)]
+        pw = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
         return {"sm_mhz": statistics.median(under_load) if under_load else None,
-                "sm_max_mhz": max(smax) if smax else None, "reasons": reasons, "samples": len(self.rows)}
+                "sm_max_mhz": max(smax) if smax else None, "reasons": reasons, "samples": len(self.rows),
+                "power_w": statistics.median(pw) if pw else None}
 
 
 def cpu_info():
@@ -227,19 +229,23 @@ def measure_hierarchy(ctx, stream, cfg, steps):
     for _ in range(3):
         H.v_cycle(cfg.k, cfg.k, bv, xv)
     torch.cuda.synchronize()
+    sampler = ClockSampler(torch.cuda.current_device())
+    sampler.start()
+    time.sleep(0.3)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(steps):
         H.v_cycle(cfg.k, cfg.k, bv, xv)
     e1.record(stream)
     torch.cuda.synchronize()
+    clocks = sampler.stop()
     ms = e0.elapsed_time(e1) / steps
     cb = H.cycle_bytes(cfg.k, cfg.k)
     peak, _ = hbm_peak()
     out = {"workload": f"{cfg.name}: {cfg.n}^{cfg.dim} patches, m={cfg.m}, {cfg.levels} levels, V({cfg.k},{cfg.k})",
            "value": 1e3 / ms, "unit": "V-cycles/s", "ms_per_step": ms, "cycle_bytes": cb,
            "effective_gbs": cb / ms / 1e6, "frac_of_roofline": cb / ms / 1e6 / peak,
-           "device_gb": H.device_bytes / 1e9, "setup_s": round(setup_s, 1)}
+           "device_gb": H.device_bytes / 1e9, "setup_s": round(setup_s, 1), "clocks": clocks}
     del H, dA, dT, bv, xv
     ctx.sync()
     return out
