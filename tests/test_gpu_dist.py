@@ -18,6 +18,10 @@ CASES = {
     "c4_like_3d": (3, 16, 2, 3, 3, 0, 1, FSAI_ADAPTIVE),
     "tmax2": (2, 32, 2, 3, 3, 0, 2, FSAI_ADAPTIVE),
     "static": (2, 32, 2, 3, 3, 0, 1, FSAI_STATIC_LOWER),
+    # streamed block sizes (the BASELINE shapes)
+    "c2_m10": (2, 32, 2, 10, 3, 0, 1, FSAI_ADAPTIVE),
+    "c5_m15": (2, 32, 2, 15, 3, 0, 1, FSAI_ADAPTIVE),
+    "c3_m21_nested": (2, 64, 3, 21, 3, 1, 1, FSAI_ADAPTIVE),
 }
 
 
@@ -51,6 +55,7 @@ def _dist(ctx, cfg, params, world, agg):
     ("c2_like", 2, 1), ("c2_like", 3, 2), ("c2_like", 4, 1),
     ("c3_like_nested", 2, 1), ("c4_like_3d", 2, 1), ("c4_like_3d", 3, 2),
     ("tmax2", 2, 1), ("static", 3, 1),
+    ("c2_m10", 4, 1), ("c5_m15", 2, 2), ("c3_m21_nested", 2, 1),
 ])
 def test_dist_setup_bitwise_equal_to_single_device(ctx, name, world, agg):
     cfg, params = _cfg(name)
