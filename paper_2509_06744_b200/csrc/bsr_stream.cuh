@@ -14,14 +14,19 @@
 //     balanced by blocks; the rows' value span is contiguous in HBM and is cut
 //     into chunks of cb_max blocks (rows may straddle chunks; a per-CTA carry
 //     holds the partial row sum).
-//   * One producer thread streams chunks into a 4-stage shared-memory ring with
-//     cp.async.bulk (TMA bulk copy, mbarrier complete_tx): values and the
-//     chunk's column indices.  HBM sees large sequential transfers; nothing is
-//     re-read.
-//   * Consumers (4 warps) compute per-(block, scalar row) dot products from
-//     shared memory against x gathered through L2 (phase A), release the
+//   * One producer thread streams chunks into a 2-stage (BMG_STAGES) shared-
+//     memory ring with cp.async.bulk (TMA bulk copy, mbarrier complete_tx):
+//     values and the chunk's column indices.  HBM sees large sequential
+//     transfers; nothing is re-read.
+//   * Consumers (8 warps) compute per-(block, scalar row) dot products from
+//     shared memory against x gathered through L1/L2 (phase A), release the
 //     stage, then sum each row's partials in ascending block order and run the
-//     fused epilogue with coalesced vector traffic (phase B).
+//     fused epilogue with coalesced vector traffic (phase B).  Partials and the
+//     row carry are double-buffered: one named barrier per chunk.
+//   * Programmatic dependent launch: dependents are released at entry, vector
+//     accesses wait for the predecessor (griddepcontrol).
+//   * K > 1 right-hand sides interleaved per scalar row share each staged block;
+//     VAR streams a variable layout through zero-padded MR x MC block copies.
 //   * Arithmetic order matches the oracle exactly: t = fma-chain over columns
 //     from 0.0, then y += t per block in ascending column order, so results
 //     are bitwise identical to oracle/bmg_oracle.cpp spmv.
