@@ -1,0 +1,37 @@
+"""Randomized campaign: variable-layout SpMV through the padded streaming kernel
+(K = 1 and batched) bitwise vs the oracle.  Usage: python tools/fuzz_spmv_variable.py SEED SECONDS"""
+import os
+import sys
+import time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+from oracle import pyoracle as O
+from paper_2509_06744_b200 import BlockSparseMatrix, Context, Vector, spmv, spmv_batch
+from tests.helpers import random_bsr
+ctx = Context(0)
+rng = np.random.default_rng(int(sys.argv[1]) if len(sys.argv) > 1 else 0)
+t0 = time.time(); cases = 0; fails = 0
+while time.time() - t0 < float(sys.argv[2] if len(sys.argv) > 2 else 60):
+    mmax = int(rng.choice([10, 15, 20, 21]))
+    nbr = int(rng.integers(1, 300)); nbc = int(rng.integers(1, 300))
+    rs = rng.integers(1, mmax + 1, size=nbr).astype(np.int32); rs[rng.integers(nbr)] = mmax
+    cs = rng.integers(1, mmax + 1, size=nbc).astype(np.int32); cs[rng.integers(nbc)] = mmax
+    dens = float(rng.choice([0.005, 0.03, 0.2]))
+    h = random_bsr(rng, rs, cs, dens)
+    A = BlockSparseMatrix(ctx, h)
+    x = rng.standard_normal(h.dim_c)
+    y = Vector(ctx, h.dim_r)
+    spmv(A, Vector(ctx, x), y)
+    ok = np.array_equal(y.download(), O.Mat(h).spmv(x))
+    K = int(rng.choice([2, 4, 8]))
+    X = rng.standard_normal((h.dim_c, K))
+    Y = Vector(ctx, h.dim_r * K)
+    spmv_batch(A, K, Vector(ctx, X.ravel().copy()), Y)
+    Yg = Y.download().reshape(-1, K)
+    for v in range(K):
+        ok &= np.array_equal(Yg[:, v], O.Mat(h).spmv(X[:, v].copy()))
+    cases += 1
+    if not ok:
+        fails += 1
+        print("FAIL", mmax, nbr, nbc, dens, K, flush=True)
+print("cases", cases, "fails", fails)
