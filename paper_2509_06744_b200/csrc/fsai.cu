@@ -18,6 +18,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "bmg_abi.h"
@@ -678,20 +681,40 @@ std::unique_ptr<Fsai> fsai_build(const Bsr& a, int kind, int t_max, double tau, 
   // applies F_0 .. F_{n-1} and G_n = L-hat^{-1} F_n
   const Bsr* ak = &a;
   std::unique_ptr<Bsr> ak_own;
+  static const bool timing = [] {
+    const char* e = std::getenv("BMG_SETUP_TIMING");
+    return e && e[0] == '1';
+  }();
+  auto t = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what, int level) {
+    if (!timing) return;
+    cudaStreamSynchronize(ctx->stream);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[bmg setup]   fsai %d: %-22s %8.3f s\n", level, what,
+                 std::chrono::duration<double>(now - t).count());
+    t = now;
+  };
   for (int level = 0; level <= nest; ++level) {
     Aux aux = make_aux(*ak, true);
+    mark("aux", level);
     adaptive_pattern(*ak, aux, t_max, tau, pp, pc);
+    mark("adaptive pattern", level);
     if (level < nest) {
       auto F = factor_from_pattern(*ak, aux, pp, pc, true);
+      mark("factor", level);
       auto next = triple_product(*F, *ak);
+      mark("triple product", level);
       fwd.push_back(std::move(F));
       ak_own = std::move(next);
       ak = ak_own.get();
     } else {
       fwd.push_back(factor_from_pattern(*ak, aux, pp, pc, false));
+      mark("factor", level);
     }
   }
-  return wrap(ctx, a.dim_r, std::move(fwd));
+  auto out = wrap(ctx, a.dim_r, std::move(fwd));
+  mark("transposes", nest);
+  return out;
 }
 
 // build_fsai(A, p) (fsai.cpp:72-83) for a caller's lower pattern: per row the

@@ -699,12 +699,12 @@ __global__ void sym_diag_sqnorm_kernel(double* __restrict__ L, const int64_t* __
       for (int e = threadIdx.x; e < rows * rows; e += blockDim.x) b[e] = tmp[e];
       __syncthreads();
     }
-    if (threadIdx.x == 0) {
-      double sq = 0.0;
-      for (int e = 0; e < rows * cols; ++e) sq = __dadd_rn(sq, __dmul_rn(b[e], b[e]));
-      nonzero[o] = sq != 0.0;
-    }
-    __syncthreads();
+    // squaredNorm() == 0 (kernels.cpp:110-113): squares cannot cancel, so the sum is
+    // zero exactly when every square is -- any summation order decides the same
+    int any = 0;
+    for (int e = threadIdx.x; e < rows * cols; e += blockDim.x) any |= __dmul_rn(b[e], b[e]) != 0.0;
+    any = __syncthreads_or(any);
+    if (threadIdx.x == 0) nonzero[o] = any;
   }
 }
 // out block o (row i, col j) = lower block from[o] (or its transpose)
@@ -732,6 +732,7 @@ std::unique_ptr<Bsr> triple_product(const Bsr& f, const Bsr& a) {
   const bool uni = a.uniform && f.uniform;
   const int m = a.mr, bs = a.bs, n = a.nbr;
   if (max_block(a) > 32) fail(BMG_EINVAL, "device triple_product: block sizes above 32 are not supported");
+  PhaseTimer tm(ctx);
   // H = F A
   Product h = symbolic(
       n,
@@ -739,6 +740,7 @@ std::unique_ptr<Bsr> triple_product(const Bsr& f, const Bsr& a) {
         for (int64_t q = f.h_row_ptr[i]; q < f.h_row_ptr[i + 1]; ++q) emit(f.h_col[q], q);
       },
       a.h_row_ptr, a.h_col);
+  tm.mark("triple: H = F A symbolic (host)");
   auto up64v = [&](const std::vector<int64_t>& v, DBuf<int64_t>& d) {
     d.alloc(std::max<size_t>(v.size(), 1));
     if (!v.empty()) BMG_CUDA(cudaMemcpy(d.p, v.data(), v.size() * 8, cudaMemcpyHostToDevice));
@@ -751,6 +753,7 @@ std::unique_ptr<Bsr> triple_product(const Bsr& f, const Bsr& a) {
   }
   DBuf<double> hv(std::max<int64_t>(uni ? (int64_t)h.col.size() * bs : hoff.back(), 2));
   pair_gemm(ctx, {f.vals.p, f.voff.p}, f.col.p, {a.vals.p, a.voff.p}, h, {hv.p, d_hoff.p}, a, 0);
+  tm.mark("triple: H numeric (device)");
   // F column index: column k -> rows j (ascending) holding F_jk
   std::vector<int64_t> fc_ptr(n + 1, 0);
   for (int64_t q = 0; q < f.nnzb; ++q) fc_ptr[f.h_col[q] + 1]++;
@@ -817,6 +820,7 @@ std::unique_ptr<Bsr> triple_product(const Bsr& f, const Bsr& a) {
     std::copy(rpr[i].begin(), rpr[i].end(), lo.pairs.begin() + pbase[i]);
   }
   lo.pair_ptr[nl] = pbase[n];
+  tm.mark("triple: lower pairs (host)");
   std::vector<int64_t> loff;
   DBuf<int64_t> d_loff;
   DBuf<int32_t> d_hcol, d_lrow, d_lcol;
@@ -841,6 +845,7 @@ std::unique_ptr<Bsr> triple_product(const Bsr& f, const Bsr& a) {
   DBuf<double> lv(std::max<int64_t>(uni ? (int64_t)nl * bs : loff.back(), 2));
   pair_gemm(ctx, {hv.p, d_hoff.p}, d_hcol.p, {f.vals.p, f.voff.p}, lo, {lv.p, d_loff.p}, a, 2);
   hv.release();
+  tm.mark("triple: lower numeric (device)");
   DBuf<int64_t> ddiag(std::max<int64_t>(nl, 1));
   DBuf<int> dnz(std::max<int64_t>(nl, 1));
   if (nl) {
@@ -853,27 +858,47 @@ std::unique_ptr<Bsr> triple_product(const Bsr& f, const Bsr& a) {
   std::vector<int> nz(nl);
   if (nl) BMG_CUDA(cudaMemcpy(nz.data(), dnz.p, nl * 4, cudaMemcpyDeviceToHost));
   // insert_symmetric of the kept lower blocks: row i gets (i, j) and row j gets (j, i)^T
-  std::vector<std::vector<std::tuple<int32_t, int64_t, int>>> rows(n);
+  // (counting placement, then each row sorted by column)
+  std::vector<int64_t> rp(n + 1, 0);
   for (int i = 0; i < n; ++i)
     for (int64_t q = lo.row_ptr[i]; q < lo.row_ptr[i + 1]; ++q) {
       if (!nz[q]) continue;
       const int j = lo.col[q];
-      rows[i].emplace_back(j, q, 0);
-      if (j != i) rows[j].emplace_back(i, q, 1);
+      ++rp[i + 1];
+      if (j != i) ++rp[j + 1];
     }
-  std::vector<int64_t> rp(n + 1, 0);
-  std::vector<int32_t> col;
-  std::vector<int64_t> from;
-  std::vector<int> trans;
-  for (int i = 0; i < n; ++i) {
-    std::sort(rows[i].begin(), rows[i].end());
-    for (auto& [j, q, t] : rows[i]) {
-      col.push_back(j);
-      from.push_back(q);
-      trans.push_back(t);
-    }
-    rp[i + 1] = (int64_t)col.size();
+  for (int i = 0; i < n; ++i) rp[i + 1] += rp[i];
+  const int64_t nout = rp[n];
+  struct Ent {
+    int32_t col;
+    int32_t trans;
+    int64_t from;
+  };
+  std::vector<Ent> ent(nout);
+  {
+    std::vector<int64_t> cur(rp.begin(), rp.end() - 1);
+    for (int i = 0; i < n; ++i)
+      for (int64_t q = lo.row_ptr[i]; q < lo.row_ptr[i + 1]; ++q) {
+        if (!nz[q]) continue;
+        const int j = lo.col[q];
+        ent[cur[i]++] = {j, 0, q};
+        if (j != i) ent[cur[j]++] = {i, 1, q};
+      }
   }
+#pragma omp parallel for schedule(dynamic, 256)
+  for (int i = 0; i < n; ++i)
+    std::sort(ent.begin() + rp[i], ent.begin() + rp[i + 1], [](const Ent& x, const Ent& y) { return x.col < y.col; });
+  std::vector<int32_t> col(nout);
+  std::vector<int64_t> from(nout);
+  std::vector<int> trans(nout);
+#pragma omp parallel for schedule(static)
+  for (int64_t q = 0; q < nout; ++q) {
+    col[q] = ent[q].col;
+    from[q] = ent[q].from;
+    trans[q] = ent[q].trans;
+  }
+  ent.clear();
+  ent.shrink_to_fit();
   std::vector<int32_t> orow_h(col.size());
   for (int i = 0; i < n; ++i)
     for (int64_t q = rp[i]; q < rp[i + 1]; ++q) orow_h[q] = i;
@@ -892,6 +917,7 @@ std::unique_ptr<Bsr> triple_product(const Bsr& f, const Bsr& a) {
     BMG_CUDA(cudaGetLastError());
     BMG_CUDA(cudaStreamSynchronize(ctx->stream));
   }
+  tm.mark("triple: drop + assemble");
   return out;
 }
 
