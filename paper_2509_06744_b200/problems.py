@@ -3,6 +3,7 @@
 The generator itself is host C++ inside libbmgcuda.so (csrc/generator.cpp); this
 module only sizes the arrays and names the configs.  Inputs are data, not the
 solver path: the reference's PUM discretiser is out of scope.
+The reference's FD test problem (experiments.cpp:104-195) is restated at the end.
 """
 from __future__ import annotations
 
@@ -176,3 +177,99 @@ def make_variable_problem(cfg: Config, m_bnd: int):
     Tv = [truncate_blocks(T[l - 1], sizes[l], sizes[l - 1], symmetric=False) for l in range(1, L)]
     b = normal_vector(int(sizes[-1].sum()), cfg.seed, 0)
     return Av, Tv, b
+
+
+# ---------------------------------------------------------------------------
+# the reference's finite-difference test problem (proj/src/experiments.cpp:104-195):
+# the problem its own multilevel tests run on (proj/tests/test_multilevel.cpp:20-23)
+@dataclass
+class FdProblem:
+    A: HostBsr                # 13-point biharmonic, scalar blocks
+    transfers: list           # transfers[l-1]: bilinear prolongation level l-1 -> l
+    b: np.ndarray             # A @ reference
+    reference: np.ndarray     # samples of the manufactured field
+    mass: HostBsr             # h^2 I
+    h: float
+
+
+def _scalar_csr(nr: int, nc: int, rows, cols, vals, symmetric: bool) -> HostBsr:
+    order = np.lexsort((cols, rows))
+    rows, cols, vals = rows[order], cols[order], vals[order]
+    rp = np.zeros(nr + 1, np.int64)
+    np.add.at(rp, rows + 1, 1)
+    return HostBsr(np.ones(nr, np.int32), np.ones(nc, np.int32), np.cumsum(rp), cols, vals, symmetric)
+
+
+def fd_biharmonic_matrix(ng: int) -> HostBsr:
+    """13-point bilaplacian on the (ng-1)^2 interior nodes of the unit square,
+    h = 1/ng, clamped boundary (experiments.cpp:110-144): Dirichlet values drop,
+    the distance-2 ghost reflects onto the first interior line (+s on the
+    diagonal per boundary direction).  Node (i, j) is row j*(ng-1) + i."""
+    m = ng - 1
+    h = 1.0 / ng
+    s = 1.0 / (h * h * h * h)
+    j, i = np.divmod(np.arange(m * m), m)
+    rows, cols, vals = [], [], []
+
+    def put(di, dj, w):
+        i1, j1 = i + di, j + dj
+        ok = (i1 >= 0) & (i1 < m) & (j1 >= 0) & (j1 < m)
+        rows.append((j * m + i)[ok])
+        cols.append((j1 * m + i1)[ok])
+        vals.append(np.broadcast_to(w, i.shape)[ok])
+
+    put(0, 0, 20.0 * s + s * ((i == 0) | (i == m - 1)) + s * ((j == 0) | (j == m - 1)))
+    for di, dj in ((1, 0), (-1, 0), (0, 1), (0, -1)):
+        put(di, dj, -8.0 * s)
+        put(2 * di, 2 * dj, 1.0 * s)
+    for di, dj in ((1, 1), (1, -1), (-1, 1), (-1, -1)):
+        put(di, dj, 2.0 * s)
+    return _scalar_csr(m * m, m * m, np.concatenate(rows), np.concatenate(cols).astype(np.int32),
+                       np.concatenate(vals).astype(np.float64), True)
+
+
+def fd_prolongation(ng_fine: int) -> HostBsr:
+    """Bilinear interpolation from the (ng/2 - 1)^2 coarse interior nodes to the
+    (ng - 1)^2 fine ones (experiments.cpp:146-167): weight
+    (1 - |i+1 - 2(ci+1)|/2)(1 - |j+1 - 2(cj+1)|/2) from the surrounding coarse nodes."""
+    mf, mc = ng_fine - 1, ng_fine // 2 - 1
+    j, i = np.divmod(np.arange(mf * mf), mf)
+    rows, cols, vals = [], [], []
+    for dcj in (-1, 0, 1):
+        for dci in (-1, 0, 1):
+            ci, cj = i // 2 + dci, j // 2 + dcj
+            wx = 1.0 - 0.5 * np.abs(i + 1 - 2 * (ci + 1))
+            wy = 1.0 - 0.5 * np.abs(j + 1 - 2 * (cj + 1))
+            ok = (ci >= 0) & (ci < mc) & (cj >= 0) & (cj < mc) & (wx > 0) & (wy > 0)
+            rows.append((j * mf + i)[ok])
+            cols.append((cj * mc + ci)[ok])
+            vals.append((wx * wy)[ok])
+    return _scalar_csr(mf * mf, mc * mc, np.concatenate(rows), np.concatenate(cols).astype(np.int32),
+                       np.concatenate(vals), False)
+
+
+def fd_biharmonic(n_grid: int, levels: int) -> FdProblem:
+    """experiments.cpp:104-195: finest grid n_grid (a power of two), `levels`
+    nested grids n_grid / 2^k, manufactured field cos(2 pi x) sin(2 pi y)."""
+    if levels < 1:
+        raise ValueError("fd_biharmonic: need at least one level")
+    if n_grid & (n_grid - 1):
+        raise ValueError("fd_biharmonic: n_grid must be 2^l")
+    if (n_grid >> (levels - 1)) < 4:
+        raise ValueError("fd_biharmonic: grid too small for the level count")
+    A = fd_biharmonic_matrix(n_grid)
+    m = n_grid - 1
+    h = 1.0 / n_grid
+    mass = _scalar_csr(m * m, m * m, np.arange(m * m), np.arange(m * m, dtype=np.int32),
+                       np.full(m * m, h * h), True)
+    j, i = np.divmod(np.arange(m * m), m)
+    ref = np.cos(2.0 * np.pi * (i + 1) * h) * np.sin(2.0 * np.pi * (j + 1) * h)
+    b = np.zeros(m * m)
+    for r in range(m * m):  # spmv: ascending columns within the row
+        lo, hi = A.row_ptr[r], A.row_ptr[r + 1]
+        acc = 0.0
+        for p in range(lo, hi):
+            acc += A.vals[p] * ref[A.col_idx[p]]
+        b[r] = acc
+    transfers = [fd_prolongation(n_grid >> (levels - 1 - l)) for l in range(1, levels)]
+    return FdProblem(A, transfers, b, ref, mass, h)

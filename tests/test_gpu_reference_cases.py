@@ -1,6 +1,7 @@
 """Device twins of the reference's own test cases for this path
 (proj/tests/test_multilevel.cpp, test_fsai.cpp, test_chebyshev.cpp), on the
-synthetic problems (the FD biharmonic / PUM generators are out of scope)."""
+synthetic problems (the same cases on the reference's FD biharmonic problem:
+test_gpu_fd_problem.py; the PUM generator is out of scope)."""
 import numpy as np
 import pytest
 
