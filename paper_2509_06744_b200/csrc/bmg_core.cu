@@ -287,23 +287,95 @@ static int occupancy_for(int mr, int mc, size_t smem, int K = 1) {
   return 1;
 }
 
+// ---- batched (K > 1) streaming kernel: RHS groups and occupancy
+template <int MR, int K, int U>
+static int batch_occupancy(size_t smem) {
+  auto kfn = kern::bsr_batch_kernel<MR, MR, K, U, kern::EpiStore>;
+  stream_attrs(kfn, K);
+  int occ = 0;
+  BMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kern::kThreads, smem));
+  return std::max(occ, 1);
+}
+template <int MR>
+static int batch_occupancy_m(size_t smem, int K, int U) {
+  if (K == 2) return batch_occupancy<MR, 2, 1>(smem);
+  if (K == 4) return U == 1 ? batch_occupancy<MR, 4, 1>(smem) : batch_occupancy<MR, 4, 2>(smem);
+  return U == 1 ? batch_occupancy<MR, 8, 1>(smem) : batch_occupancy<MR, 8, 2>(smem);
+}
+static int batch_occupancy_for(int mr, size_t smem, int K, int U) {
+  switch (mr) {
+    case 10: return batch_occupancy_m<10>(smem, K, U);
+    case 15: return batch_occupancy_m<15>(smem, K, U);
+    case 20: return batch_occupancy_m<20>(smem, K, U);
+    case 21: return batch_occupancy_m<21>(smem, K, U);
+  }
+  return 1;
+}
+// Which kernel streams K > 1 right-hand sides, with its RHS groups U (V = K / U
+// per thread) and blocks per chunk, from measured sweeps on B200
+// (profiles/r01_batched_kernel_sweep.txt).  The staged-x kernel wins where blocks
+// are large (m = 15 for K <= 4, m = 20, 21: up to 2x); for m = 10 the chunk
+// count per byte is high and the per-chunk staging latency loses to the L1
+// gathers of bsr_stream_kernel.  BMG_BATCH_KERNEL=old|new, BMG_BATCH_U and
+// BMG_BATCH_CB override (sweeps).
+struct BatchChoice {
+  int u = 0;   // 0: bsr_stream_kernel<K>; else bsr_batch_kernel with U groups
+  int cb = 0;  // blocks per chunk (0: kConsumers / (mr U))
+};
+static BatchChoice batch_choice(int mr, int K) {
+  static const int env_k = [] {
+    const char* e = std::getenv("BMG_BATCH_KERNEL");
+    return !e ? -1 : (e[0] == 'n' ? 1 : 0);
+  }();
+  static const int env_u = [] {
+    const char* e = std::getenv("BMG_BATCH_U");
+    return e ? std::atoi(e) : 0;
+  }();
+  static const int env_cb = [] {
+    const char* e = std::getenv("BMG_BATCH_CB");
+    return e ? std::atoi(e) : 0;
+  }();
+  BatchChoice c;
+  switch (mr) {
+    case 15: if (K == 2) c = {1, 16}; else if (K == 4) c = {2, 20}; break;
+    case 20:
+    case 21: c = {1, 8}; break;
+    default: break;
+  }
+  if (env_k == 0) c = {};
+  if (env_k == 1 && c.u == 0) c = {1, 0};
+  auto valid = [&](int u) { return (u == 1 || u == 2) && (K / u) % 2 == 0; };
+  if (c.u && valid(env_u)) c.u = env_u;
+  if (c.u && env_cb > 0) c.cb = env_cb;
+  return c;
+}
+
 // Partition block rows into per-CTA ranges balanced by blocks; cut each
 // range's contiguous block span into chunks of cb_max blocks (bsr_stream.cuh).
 // plan for streaming `a` as uniform mr x mr blocks of stride bs (the real layout,
 // or a variable layout's padded copy)
-static void build_plan_into(const Bsr& a, Plan& P, int K, int mr, int bs) {
+static void build_plan_into(const Bsr& a, Plan& P, int K, int mr, int bs, bool var = false) {
   P = Plan();
   if (!stream_supported(mr, mr) || a.nbr == 0) return;
-  P.cb_max = chunk_blocks(mr, bs, K);
   P.stages = ring_stages();
+  const BatchChoice bc = (K > 1 && !var) ? batch_choice(mr, K) : BatchChoice{};
+  if (bc.u) {
+    // bsr_batch_kernel: phase-A items (block, row, RHS group); the producer warp
+    // stages one x segment per lane, so a chunk holds at most 32 blocks
+    P.u = bc.u;
+    P.cb_max = std::min(32, bc.cb > 0 ? bc.cb : std::max(1, kern::kConsumers / (mr * P.u)));
+  } else {
+    P.cb_max = chunk_blocks(mr, bs, K);
+  }
   const auto& rp = a.h_row_ptr;
   // chunk list per CTA range
   std::vector<int4> chunks;
   std::vector<int> cta;
   int rmax = 1;
   // first pass with a provisional rmax to size smem and query occupancy
-  const size_t smem0 = kern::SmemLayout(bs, P.cb_max, P.cb_max + 2, mr, P.stages, K).total;
-  const int occ = occupancy_for(mr, mr, smem0, K);
+  const size_t smem0 = P.u ? kern::BatchSmem(bs, P.cb_max, mr, mr, K, P.stages).total
+                           : kern::SmemLayout(bs, P.cb_max, P.cb_max + 2, mr, P.stages, K).total;
+  const int occ = P.u ? batch_occupancy_for(mr, smem0, K, P.u) : occupancy_for(mr, mr, smem0, K);
   const int64_t gmax = (int64_t)a.ctx->sms * occ;
   const int64_t per = std::max<int64_t>(1, (a.nnzb + gmax - 1) / gmax);
   int row = 0;
@@ -339,9 +411,13 @@ static void build_plan_into(const Bsr& a, Plan& P, int K, int mr, int bs) {
   P.rmax = rmax;
   P.nctas = (int)cta.size() - 1;
   P.nchunks = (int)chunks.size();
-  P.smem = kern::SmemLayout(bs, P.cb_max, P.rmax, mr, P.stages, K).total;
+  P.smem = P.u ? kern::BatchSmem(bs, P.cb_max, mr, mr, K, P.stages).total
+               : kern::SmemLayout(bs, P.cb_max, P.rmax, mr, P.stages, K).total;
   if (P.smem > 227 * 1024) fail(BMG_EINVAL, "plan: chunk does not fit in shared memory");
-  occupancy_for(mr, mr, P.smem, K);  // sets the shared-memory attributes
+  if (P.u)  // sets the shared-memory attributes
+    batch_occupancy_for(mr, P.smem, K, P.u);
+  else
+    occupancy_for(mr, mr, P.smem, K);
   P.chunks.alloc(chunks.size());
   P.cta_chunk.alloc(cta.size());
   BMG_CUDA(cudaMemcpy(P.chunks.p, chunks.data(), chunks.size() * sizeof(int4), cudaMemcpyHostToDevice));
@@ -397,7 +473,7 @@ const Plan& plan_for(const Bsr& a, int nrhs) {
     }
     if (!a.pplan[idx]) {
       auto p = std::make_unique<Plan>();
-      build_plan_into(a, *p, std::max(nrhs, 1), a.mmax, a.pbs);
+      build_plan_into(a, *p, std::max(nrhs, 1), a.mmax, a.pbs, true);
       a.pplan[idx] = std::move(p);
     }
     return *a.pplan[idx];
@@ -706,8 +782,57 @@ static void launch_stream_t(const Bsr& a, const double* x, Epi epi) {
   BMG_LAUNCHED(a.ctx->stream, "bsr_stream_kernel");
 }
 
+template <int MR, int K, int U, class Epi>
+static void launch_batch_t(const Bsr& a, const Plan& P, const double* x, Epi epi) {
+  if (reinterpret_cast<uintptr_t>(x) & 15)
+    fail(BMG_EINVAL, "batched pass: x must be 16-byte aligned");
+  kern::StreamArgs s;
+  s.vals = a.vals.p;
+  s.col = a.col.p;
+  s.row_ptr = a.row_ptr.p;
+  s.chunks = P.chunks.p;
+  s.cta_chunk = P.cta_chunk.p;
+  s.x = x;
+  s.bs = a.bs;
+  s.cb_max = P.cb_max;
+  s.rmax = P.rmax;
+  s.stages = P.stages;
+  static const bool attr_set = [] {
+    stream_attrs(kern::bsr_batch_kernel<MR, MR, K, U, Epi>, K);
+    return true;
+  }();
+  (void)attr_set;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(P.nctas);
+  cfg.blockDim = dim3(kern::kThreads);
+  cfg.dynamicSmemBytes = P.smem;
+  cfg.stream = a.ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  BMG_CUDA(cudaLaunchKernelEx(&cfg, kern::bsr_batch_kernel<MR, MR, K, U, Epi>, s, epi));
+  a.ctx->count();
+  BMG_LAUNCHED(a.ctx->stream, "bsr_batch_kernel");
+}
+
+template <int MR, class Epi>
+static void launch_batch(const Bsr& a, const double* x, Epi epi, int nrhs) {
+  const Plan& P = plan_for(a, nrhs);
+  if (nrhs == 2) return launch_batch_t<MR, 2, 1>(a, P, x, epi);
+  if (nrhs == 4) return P.u == 1 ? launch_batch_t<MR, 4, 1>(a, P, x, epi) : launch_batch_t<MR, 4, 2>(a, P, x, epi);
+  if (nrhs == 8) {
+    return P.u == 1 ? launch_batch_t<MR, 8, 1>(a, P, x, epi) : launch_batch_t<MR, 8, 2>(a, P, x, epi);
+  }
+  fail(BMG_EINVAL, "right-hand-side batch must be 1, 2, 4 or 8");
+}
+
 template <int MR, int MC, class Epi, bool VAR = false>
 static void launch_stream_k(const Bsr& a, const double* x, Epi epi, int nrhs) {
+  if constexpr (!VAR) {
+    if (nrhs > 1 && plan_for(a, nrhs).u) return launch_batch<MR>(a, x, epi, nrhs);
+  }
   switch (nrhs) {
     case 1: return launch_stream_t<MR, MC, 1, Epi, VAR>(a, x, epi);
     case 2: return launch_stream_t<MR, MC, 2, Epi, VAR>(a, x, epi);

@@ -396,6 +396,221 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
   }
 }
 
+// ------------------------------------------------ batched right-hand sides
+// K > 1 right-hand sides on uniform layouts.  The producer warp stages, per
+// block, both the block (one bulk copy per chunk) and the block's x segment
+// x[j*MC*K, (j+1)*MC*K) -- contiguous because the K right-hand sides are
+// interleaved per scalar row -- so phase A reads only shared memory and the x
+// gathers' L2 latency sits in the async ring instead of the consumers.  A
+// phase-A item is (block, scalar row, RHS group of V = K / U): the block row is
+// read from shared memory U times in total (not K times), the staged x segment
+// is read by the MR row threads of the block together (broadcast), and every
+// (row, RHS) keeps the single-vector fma chain over columns from 0.0.
+// Partials are stored unpadded at stride K per (block, row) slot with the
+// 16-byte pieces XOR-swizzled by slot, so the phase-A stores and the phase-B
+// reads are bank-conflict free.
+// staged x segment stride (doubles): +2 shifts consecutive segments by 16 bytes of banks
+__host__ __device__ inline int batch_xstride(int mc, int K) { return mc * K + 2; }
+
+struct BatchSmem {
+  uint32_t vals, xs, part, carry, bars, total;
+  __host__ __device__ BatchSmem(int bs, int cb_max, int mr, int mc, int K, int kStages) {
+    uint32_t o = 0;
+    auto al = [](uint32_t v, uint32_t a) { return (v + a - 1) / a * a; };
+    vals = o;
+    o += al((uint32_t)kStages * cb_max * bs * 8, 128);
+    xs = o;
+    o += al((uint32_t)kStages * cb_max * batch_xstride(mc, K) * 8, 128);
+    part = o;
+    o += al((uint32_t)2 * cb_max * mr * K * 8, 16);
+    carry = o;
+    o += al((uint32_t)2 * mr * K * 8, 16);
+    bars = o;
+    o += 2 * kStages * 8;
+    total = al(o, 128);
+  }
+};
+
+// physical double index of (slot, v) in the swizzled partials
+template <int K>
+__device__ __forceinline__ int batch_part_idx(int slot, int v) {
+  constexpr int P = K / 2;        // 16-byte pieces per slot
+  constexpr int RPL = 8 / P;      // slots per 128-byte line
+  return slot * K + ((((v >> 1) ^ ((slot / RPL) % P))) << 1) + (v & 1);
+}
+
+template <int MR, int MC, int K, int U, class Epi>
+__global__ void __launch_bounds__(kThreads, K / U >= 8 ? 2 : 3) bsr_batch_kernel(StreamArgs s, Epi epi) {
+  static_assert(K % 2 == 0 && K <= 8 && K % U == 0 && (K / U) % 2 == 0, "batch shape");
+  constexpr int V = K / U;  // right-hand sides per thread
+  constexpr int XS = MC * K + 2;  // == batch_xstride(MC, K)
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int kStages = s.stages;
+  const BatchSmem L(s.bs, s.cb_max, MR, MC, K, kStages);
+  double* vals_s = reinterpret_cast<double*>(smem + L.vals);
+  double* xs_s = reinterpret_cast<double*>(smem + L.xs);
+  double* part_s = reinterpret_cast<double*>(smem + L.part);
+  double* carry_s = reinterpret_cast<double*>(smem + L.carry);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
+  uint64_t* empty = full + kStages;
+
+  const int c0 = s.cta_chunk[blockIdx.x];
+  const int c1 = s.cta_chunk[blockIdx.x + 1];
+  const int tid = threadIdx.x;
+  pdl_launch_dependents();
+  if (tid == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  const int stage_vals = s.cb_max * s.bs;
+  const int stage_xs = s.cb_max * XS;
+
+  if (tid >= kConsumers) {
+    // ------------------------------------------------------ producer warp
+    // chunks hold at most 32 blocks (host plan: cb_max = kConsumers / (MR U) <= 25),
+    // so lane b owns block b's x segment; the next chunk's descriptor and column
+    // indices are loaded one chunk ahead, off the empty-slot wait
+    const int lane = tid - kConsumers;
+    constexpr uint32_t xbytes = (uint32_t)MC * K * 8u;
+    bool waited = false;
+    int4 dn = c0 < c1 ? s.chunks[c0] : make_int4(0, 0, 0, 0);
+    int jn = lane < dn.y ? __ldg(s.col + dn.x + lane) : 0;
+    for (int c = c0, it = 0; c < c1; ++c, ++it) {
+      const int st = it % kStages;
+      const int4 d = dn;
+      const int j = jn;
+      if (c + 1 < c1) dn = s.chunks[c + 1];
+      if (lane == 0 && it >= kStages) mbar_wait(&empty[st], ((it / kStages) - 1) & 1);
+      __syncwarp();
+      if (d.y == 0) {
+        if (lane == 0) mbar_arrive_expect_tx(&full[st], 0);
+      } else {
+        if (lane == 0) {
+          const uint32_t vbytes = (uint32_t)d.y * (uint32_t)s.bs * 8u;
+          mbar_arrive_expect_tx(&full[st], vbytes + (uint32_t)d.y * xbytes);
+          bulk_g2s(vals_s + (size_t)st * stage_vals, s.vals + (int64_t)d.x * s.bs, vbytes, &full[st]);
+        }
+        if (!waited) {  // x belongs to the predecessor pass (the matrix does not)
+          pdl_wait();
+          waited = true;
+        }
+        __syncwarp();
+        if (lane < d.y)
+          bulk_g2s(xs_s + (size_t)st * stage_xs + lane * XS, s.x + (int64_t)j * MC * K, xbytes, &full[st]);
+      }
+      jn = (c + 1 < c1 && lane < dn.y) ? __ldg(s.col + dn.x + lane) : 0;
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------ consumers
+  pdl_wait();
+  for (int c = c0, it = 0; c < c1; ++c, ++it) {
+    const int st = it % kStages;
+    const int pb = it & 1;
+    const int4 d = s.chunks[c];
+    const int nrows = (int)((unsigned)d.w & kRowMask);
+    const bool cin = ((unsigned)d.w & kCarryIn) != 0;
+    const bool cout = ((unsigned)d.w & kCarryOut) != 0;
+    double* part = part_s + pb * s.cb_max * MR * K;
+
+    const int ritems = nrows * MR * K;
+    int64_t rlo0 = 0, rhi0 = 0;
+    typename Epi::Pre pre0{};
+    if (tid < ritems) {
+      const int rr = tid / (MR * K);
+      const int rv = tid - rr * MR * K;
+      rlo0 = __ldg(s.row_ptr + d.z + rr);
+      rhi0 = __ldg(s.row_ptr + d.z + rr + 1);
+      pre0 = epi.load((int64_t)(d.z + rr) * MR * K + rv);
+    }
+    mbar_wait(&full[st], (it / kStages) & 1);
+
+    // phase A: item = (block, rhs group, row), row fastest
+    const double* vs = vals_s + (size_t)st * stage_vals;
+    const double* xs = xs_s + (size_t)st * stage_xs;
+    const int items = d.y * MR * U;
+    for (int item = tid; item < items; item += kConsumers) {
+      const int b = item / (MR * U);
+      const int rem = item - b * (MR * U);
+      const int u = rem / MR;
+      const int r = rem - u * MR;
+      const double* a = vs + b * s.bs + r * MC;
+      const double* xb = xs + b * XS + u * V;
+      double acc[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) acc[v] = 0.0;
+      if constexpr (MC % 2 == 0) {
+#pragma unroll
+        for (int q2 = 0; q2 < MC / 2; ++q2) {
+          const double2 a2 = reinterpret_cast<const double2*>(a)[q2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const double aq = h ? a2.y : a2.x;
+            const double2* xq = reinterpret_cast<const double2*>(xb + (2 * q2 + h) * K);
+#pragma unroll
+            for (int v2 = 0; v2 < V / 2; ++v2) {
+              const double2 x2 = xq[v2];
+              acc[2 * v2] = __fma_rn(aq, x2.x, acc[2 * v2]);
+              acc[2 * v2 + 1] = __fma_rn(aq, x2.y, acc[2 * v2 + 1]);
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < MC; ++q) {
+          const double aq = a[q];
+          const double2* xq = reinterpret_cast<const double2*>(xb + q * K);
+#pragma unroll
+          for (int v2 = 0; v2 < V / 2; ++v2) {
+            const double2 x2 = xq[v2];
+            acc[2 * v2] = __fma_rn(aq, x2.x, acc[2 * v2]);
+            acc[2 * v2 + 1] = __fma_rn(aq, x2.y, acc[2 * v2 + 1]);
+          }
+        }
+      }
+      const int slot = b * MR + r;
+#pragma unroll
+      for (int v2 = 0; v2 < V / 2; ++v2) {
+        const int v = u * V + 2 * v2;
+        *reinterpret_cast<double2*>(part + batch_part_idx<K>(slot, v)) = make_double2(acc[2 * v2], acc[2 * v2 + 1]);
+      }
+    }
+    consumer_bar();
+    if (tid == 0) mbar_arrive(&empty[st]);
+
+    // phase B: ordered row sums + fused epilogue (same order as the K = 1 kernel)
+    const double* carry_in = carry_s + (pb ^ 1) * MR * K;
+    double* carry_out = carry_s + pb * MR * K;
+    for (int item = tid; item < ritems; item += kConsumers) {
+      const int rr = item / (MR * K);
+      const int rv = item - rr * MR * K;  // r * K + v
+      int64_t rlo = rlo0, rhi = rhi0;
+      typename Epi::Pre pre = pre0;
+      const int64_t oi = (int64_t)(d.z + rr) * MR * K + rv;
+      if (item != tid) {
+        rlo = __ldg(s.row_ptr + d.z + rr);
+        rhi = __ldg(s.row_ptr + d.z + rr + 1);
+        pre = epi.load(oi);
+      }
+      const int lo = (int)(max(rlo, (int64_t)d.x) - d.x);
+      const int hi = (int)(min(rhi, (int64_t)(d.x + d.y)) - d.x);
+      double acc = (rr == 0 && cin) ? carry_in[rv] : 0.0;
+      const int r = rv / K, v = rv - (rv / K) * K;
+      for (int b = lo; b < hi; ++b) acc = __dadd_rn(acc, part[batch_part_idx<K>(b * MR + r, v)]);
+      if (rr == nrows - 1 && cout)
+        carry_out[rv] = acc;
+      else
+        epi.store(oi, acc, pre);
+    }
+  }
+}
+
 // ------------------------------------------------------ variable block sizes
 // Warp per block row, lane per scalar row (looping for m_i > 32); same
 // arithmetic order as the streaming kernel and the oracle.
