@@ -210,8 +210,9 @@ def measure_c1(ctx, stream, steps):
             "gbs": per / ms / 1e6, "l2": "L2-resident (0.09 GB working set < 126 MB L2)"}
 
 
-def measure_hierarchy(ctx, stream, cfg, steps):
-    """Extra line: V(k,k) cycles/s of another config's full device hierarchy."""
+def measure_hierarchy(ctx, stream, cfg, steps, batch=0):
+    """Extra line: V(k,k) cycles/s of another config's full device hierarchy (and,
+    with batch=K, the same hierarchy on K right-hand sides per cycle)."""
     import torch
 
     from paper_2509_06744_b200 import BlockSparseMatrix, Hierarchy, Vector, default_params
@@ -246,6 +247,11 @@ def measure_hierarchy(ctx, stream, cfg, steps):
            "value": 1e3 / ms, "unit": "V-cycles/s", "ms_per_step": ms, "cycle_bytes": cb,
            "effective_gbs": cb / ms / 1e6, "frac_of_roofline": cb / ms / 1e6 / peak,
            "device_gb": H.device_bytes / 1e9, "setup_s": round(setup_s, 1), "clocks": clocks}
+    if batch > 1:
+        try:
+            out[f"x{batch}"] = measure_batch(ctx, stream, H, b, cfg.k, batch, max(steps // 2, 3), cfg.name)
+        except Exception as e:
+            out[f"x{batch}"] = {"error": f"{type(e).__name__}: {e}"}
     del H, dA, dT, bv, xv
     ctx.sync()
     return out
@@ -455,7 +461,7 @@ def run_ours(args, cfg):
                 if free < 125e9:
                     extra["C4"] = {"skipped": f"needs ~115 GB free, {free / 1e9:.0f} GB available"}
                 else:
-                    extra["C4"] = measure_hierarchy(ctx, stream, pr.CONFIGS["C4"], min(args.steps, 10))
+                    extra["C4"] = measure_hierarchy(ctx, stream, pr.CONFIGS["C4"], min(args.steps, 10), batch=4)
             except Exception as e:
                 extra["C4"] = {"error": f"{type(e).__name__}: {e}"}
 
@@ -513,7 +519,7 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
 
 
-def measure_batch(ctx, stream, H, b, k, K, steps):
+def measure_batch(ctx, stream, H, b, k, K, steps, name="C2"):
     """K independent right-hand sides per cycle, interleaved per scalar row: one
     stream of every matrix serves all K (each RHS bitwise the single cycle)."""
     import torch
@@ -532,7 +538,7 @@ def measure_batch(ctx, stream, H, b, k, K, steps):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
     by = H.cycle_bytes(k, k, K)
-    return {"workload": f"C2 hierarchy, {K} right-hand sides per V({k},{k}) cycle (bmg_vcycle_batch)",
+    return {"workload": f"{name} hierarchy, {K} right-hand sides per V({k},{k}) cycle (bmg_vcycle_batch)",
             "value": K * 1e3 / ms, "unit": "right-hand-side V-cycles/s", "ms_per_batch": ms,
             "batch_bytes": by, "effective_gbs": by / ms / 1e6}
 
