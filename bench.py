@@ -160,7 +160,7 @@ def run_reference(args, cfg):
         "impl": "reference",
         "metric": f"V-cycles/s ({cfg.name}, V({cfg.k},{cfg.k}))",
         "value": rate, "unit": unit, "n_gpus": args.gpus, "steps": steps, "warmup": warm,
-        "ms_per_step": 1e3 * dt / steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * dt / steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE.md §3 generator, seed 0)",
         "config": {"workload": f"{cfg.name}: {cfg.n}^{cfg.dim} patches, m={cfg.m}, {cfg.levels} levels, "
                                f"V({cfg.k},{cfg.k}), {cfg.fsai} block-FSAI t_max=1"},
