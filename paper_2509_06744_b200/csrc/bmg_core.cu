@@ -314,9 +314,9 @@ static int batch_occupancy_for(int mr, size_t smem, int K, int U) {
 // Which kernel streams K > 1 right-hand sides, with its RHS groups U (V = K / U
 // per thread) and blocks per chunk, from measured sweeps on B200
 // (profiles/r01_batched_kernel_sweep.txt).  The staged-x kernel wins where blocks
-// are large (m = 15 for K <= 4, m = 20, 21: up to 2x); for m = 10 the chunk
-// count per byte is high and the per-chunk staging latency loses to the L1
-// gathers of bsr_stream_kernel.  BMG_BATCH_KERNEL=old|new, BMG_BATCH_U and
+// are large (m = 15 for K <= 4, m = 20, 21: up to 2x) and for m = 10 at K = 8;
+// for m = 10 at K <= 4 the chunk count per byte is high and the per-chunk
+// staging latency loses to the L1 gathers of bsr_stream_kernel.  BMG_BATCH_KERNEL=old|new, BMG_BATCH_U and
 // BMG_BATCH_CB override (sweeps).
 struct BatchChoice {
   int u = 0;   // 0: bsr_stream_kernel<K>; else bsr_batch_kernel with U groups
@@ -337,6 +337,7 @@ static BatchChoice batch_choice(int mr, int K) {
   }();
   BatchChoice c;
   switch (mr) {
+    case 10: if (K == 8) c = {1, 16}; break;
     case 15: if (K == 2) c = {1, 16}; else if (K == 4) c = {2, 20}; break;
     case 20:
     case 21: c = {1, 8}; break;

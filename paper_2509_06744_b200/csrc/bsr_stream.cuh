@@ -440,7 +440,7 @@ __device__ __forceinline__ int batch_part_idx(int slot, int v) {
 }
 
 template <int MR, int MC, int K, int U, class Epi>
-__global__ void __launch_bounds__(kThreads, K / U >= 8 ? 2 : 3) bsr_batch_kernel(StreamArgs s, Epi epi) {
+__global__ void __launch_bounds__(kThreads, (MR <= 10 || K / U < 8) ? 3 : 2) bsr_batch_kernel(StreamArgs s, Epi epi) {
   static_assert(K % 2 == 0 && K <= 8 && K % U == 0 && (K / U) % 2 == 0, "batch shape");
   constexpr int V = K / U;  // right-hand sides per thread
   constexpr int XS = MC * K + 2;  // == batch_xstride(MC, K)
