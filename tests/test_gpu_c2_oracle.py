@@ -1,0 +1,43 @@
+"""The headline configuration itself against the oracle (BASELINE C2: 256^2
+patches, m = 10, 4 levels, adaptive block-FSAI t_max = 1, V(3,3), seed 0): the
+full device setup and solve loop against the CPU restatement of the reference on
+identical inputs.  Criteria: beta per level to
+1e-10, residual history |rho_n^gpu - rho_n^cpu| <= 1e-10 for every n and relative
+1e-10 while rho_n >= 1e-2, identical iteration counts and status, the iterate
+after the last cycle to 1e-10 relative.  About 40 s of host time for the oracle's
+setup and cycles (all host threads)."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import pyoracle as O
+from paper_2509_06744_b200 import BlockSparseMatrix, Hierarchy, Vector, default_params
+from paper_2509_06744_b200 import problems as pr
+
+pytestmark = pytest.mark.gpu
+
+CYCLES = 6
+
+
+def test_c2_full_size_matches_oracle(ctx):
+    cfg = pr.CONFIGS["C2"]
+    A, T, b = pr.make_problem(cfg)
+    O.set_threads(os.cpu_count() or 1)
+    oh = O.Hierarchy(O.Mat(A), [O.Mat(p) for p in T], t_max=1, coarse_dim_cap=1 << 30, probe=False)
+    dh = Hierarchy.setup(BlockSparseMatrix(ctx, A), [BlockSparseMatrix(ctx, p) for p in T],
+                         default_params(t_max=1, coarse_dim_cap=1 << 30))
+    assert dh.levels == oh.levels() == cfg.levels
+    for l in range(1, dh.levels):
+        assert abs(dh.beta(l) - oh.beta(l)) <= 1e-10 * oh.beta(l), l
+    # fixed cycle count (a random P contracts slowly, ~0.95 per cycle): tol far below reach
+    hist_o, it_o, st_o, x_o = oh.solve(cfg.k, cfg.k, b, np.zeros_like(b), 1e-30, CYCLES)
+    bv, xv = Vector(ctx, b), Vector(ctx, np.zeros_like(b))
+    hist_g, it_g, st_g = dh.solve(cfg.k, cfg.k, bv, xv, 1e-30, CYCLES)
+    assert it_g == it_o == CYCLES and st_g == st_o
+    rho_o, rho_g = hist_o / hist_o[0], hist_g / hist_g[0]
+    assert np.all(np.abs(rho_g - rho_o) <= 1e-10), np.abs(rho_g - rho_o).max()
+    big = rho_o >= 1e-2
+    assert np.all(np.abs(rho_g[big] / rho_o[big] - 1) <= 1e-10), np.abs(rho_g[big] / rho_o[big] - 1).max()
+    xg = xv.download()
+    assert np.linalg.norm(xg - x_o) <= 1e-10 * np.linalg.norm(x_o)
