@@ -734,6 +734,14 @@ std::unique_ptr<Bsr> bsr_transpose(const Bsr& a) {
 }
 
 // ============================================================================ launches
+static int l2_hint_enabled() {
+  static int on = [] {
+    const char* e = std::getenv("BMG_L2_HINT");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return on;
+}
+
 static bool pdl_enabled() {
   static bool on = [] {
     const char* e = std::getenv("BMG_PDL");
@@ -762,6 +770,7 @@ static void launch_stream_t(const Bsr& a, const double* x, Epi epi) {
   s.cb_max = P.cb_max;
   s.rmax = P.rmax;
   s.stages = P.stages;
+  s.l2hint = l2_hint_enabled();
   // one attribute per template instantiation (covers the largest plan)
   static const bool attr_set = [] {  // thread-safe one-time init (contexts may live on several threads)
     stream_attrs(kern::bsr_stream_kernel<MR, MC, K, Epi, VAR>, K);
@@ -798,6 +807,7 @@ static void launch_batch_t(const Bsr& a, const Plan& P, const double* x, Epi epi
   s.cb_max = P.cb_max;
   s.rmax = P.rmax;
   s.stages = P.stages;
+  s.l2hint = l2_hint_enabled();
   static const bool attr_set = [] {
     stream_attrs(kern::bsr_batch_kernel<MR, MR, K, U, Epi>, K);
     return true;

@@ -82,6 +82,31 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// Streamed-once data (matrix blocks and column indices, the coarse inverse's
+// tiles) is copied with an L2 evict-first policy, so the stream does not push the
+// gathered vectors (x, a few MB, re-read by every block row's neighbours) out of
+// the 126 MB L2 while hundreds of MB pass through it.  BMG_L2_HINT=0 disables.
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+// stream copy: evict-first when `hint`, else the default policy
+__device__ __forceinline__ void bulk_stream(void* dst, const void* src, uint32_t bytes, uint64_t* bar, bool hint,
+                                            uint64_t pol) {
+  if (hint)
+    bulk_g2s_hint(dst, src, bytes, bar, pol);
+  else
+    bulk_g2s(dst, src, bytes, bar);
+}
 // Programmatic dependent launch (sm_90+): the next pass may start streaming its
 // matrix while this one drains; vector reads/writes wait for the predecessor.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
@@ -156,6 +181,7 @@ struct StreamArgs {
   const int* roff = nullptr;
   const int* rsz = nullptr;
   int64_t xlen = 0;
+  int l2hint = 1;  // matrix stream with the L2 evict-first policy
 };
 
 // column-index slots per stage: cb_max + 8, rounded to 16 bytes (bulk-copy
@@ -222,6 +248,7 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
   if (tid >= kConsumers) {
     // ------------------------------------------------------------ producer
     if (tid == kConsumers) {
+      const uint64_t pol = l2_evict_first_policy();
       for (int c = c0, it = 0; c < c1; ++c, ++it) {
         const int st = it % kStages;
         if (it >= kStages) mbar_wait(&empty[st], ((it / kStages) - 1) & 1);
@@ -235,8 +262,8 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
         const int ch = (d.x + d.y + 3) & ~3;
         const uint32_t cbytes = (uint32_t)(ch - cl) * 4u;
         mbar_arrive_expect_tx(&full[st], vbytes + cbytes);
-        bulk_g2s(vals_s + (size_t)st * stage_vals, s.vals + (int64_t)d.x * s.bs, vbytes, &full[st]);
-        bulk_g2s(cols_s + st * stage_cols, s.col + cl, cbytes, &full[st]);
+        bulk_stream(vals_s + (size_t)st * stage_vals, s.vals + (int64_t)d.x * s.bs, vbytes, &full[st], s.l2hint, pol);
+        bulk_stream(cols_s + st * stage_cols, s.col + cl, cbytes, &full[st], s.l2hint, pol);
       }
     }
     return;
@@ -476,6 +503,7 @@ __global__ void __launch_bounds__(kThreads, (MR <= 10 || K / U < 8) ? 3 : 2) bsr
     // so lane b owns block b's x segment; the next chunk's descriptor and column
     // indices are loaded one chunk ahead, off the empty-slot wait
     const int lane = tid - kConsumers;
+    const uint64_t pol = l2_evict_first_policy();
     constexpr uint32_t xbytes = (uint32_t)MC * K * 8u;
     bool waited = false;
     int4 dn = c0 < c1 ? s.chunks[c0] : make_int4(0, 0, 0, 0);
@@ -493,7 +521,8 @@ __global__ void __launch_bounds__(kThreads, (MR <= 10 || K / U < 8) ? 3 : 2) bsr
         if (lane == 0) {
           const uint32_t vbytes = (uint32_t)d.y * (uint32_t)s.bs * 8u;
           mbar_arrive_expect_tx(&full[st], vbytes + (uint32_t)d.y * xbytes);
-          bulk_g2s(vals_s + (size_t)st * stage_vals, s.vals + (int64_t)d.x * s.bs, vbytes, &full[st]);
+          bulk_stream(vals_s + (size_t)st * stage_vals, s.vals + (int64_t)d.x * s.bs, vbytes, &full[st], s.l2hint,
+                      pol);
         }
         if (!waited) {  // x belongs to the predecessor pass (the matrix does not)
           pdl_wait();

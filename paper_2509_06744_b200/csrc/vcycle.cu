@@ -49,12 +49,13 @@ __global__ void __launch_bounds__(kSymvThreads) symv_stream_kernel(const double*
   }
   __syncthreads();
   const int64_t stride = gridDim.x;
+  const uint64_t pol = l2_evict_first_policy();
   if (tid == 0)
     for (int st = 0; st < 2; ++st) {
       const int64_t t = blockIdx.x + st * stride;
       if (t < ntiles) {
         mbar_arrive_expect_tx(&full[st], kBytes);
-        bulk_g2s(ring + st * kTile * kTile, tiles + t * kTile * kTile, kBytes, &full[st]);
+        bulk_g2s_hint(ring + st * kTile * kTile, tiles + t * kTile * kTile, kBytes, &full[st], pol);
       }
     }
   const int it0 = mode == 2 ? kTile * K : 0, it1 = mode == 1 ? kTile * K : 2 * kTile * K;
@@ -95,7 +96,7 @@ __global__ void __launch_bounds__(kSymvThreads) symv_stream_kernel(const double*
     __syncthreads();  // tile and x segments consumed
     if (tid == 0 && t + 2 * stride < ntiles) {
       mbar_arrive_expect_tx(&full[st], kBytes);
-      bulk_g2s(ring + st * kTile * kTile, tiles + (t + 2 * stride) * kTile * kTile, kBytes, &full[st]);
+      bulk_g2s_hint(ring + st * kTile * kTile, tiles + (t + 2 * stride) * kTile * kTile, kBytes, &full[st], pol);
     }
   }
 }
