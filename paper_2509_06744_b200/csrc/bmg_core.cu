@@ -355,9 +355,13 @@ static BatchChoice batch_choice(int mr, int K) {
 // range's contiguous block span into chunks of cb_max blocks (bsr_stream.cuh).
 // plan for streaming `a` as uniform mr x mr blocks of stride bs (the real layout,
 // or a variable layout's padded copy)
-static void build_plan_into(const Bsr& a, Plan& P, int K, int mr, int bs, bool var = false) {
+// rows [row0, row1) only when row1 > 0 (a row-range plan over the whole matrix's
+// storage: chunk descriptors keep absolute block and row indices)
+static void build_plan_into(const Bsr& a, Plan& P, int K, int mr, int bs, bool var = false, int row0 = 0,
+                            int row1 = 0) {
   P = Plan();
-  if (!stream_supported(mr, mr) || a.nbr == 0) return;
+  if (row1 <= 0) row1 = a.nbr;
+  if (!stream_supported(mr, mr) || a.nbr == 0 || row1 <= row0) return;
   P.stages = ring_stages();
   const BatchChoice bc = (K > 1 && !var) ? batch_choice(mr, K) : BatchChoice{};
   if (bc.u) {
@@ -378,15 +382,16 @@ static void build_plan_into(const Bsr& a, Plan& P, int K, int mr, int bs, bool v
                            : kern::SmemLayout(bs, P.cb_max, P.cb_max + 2, mr, P.stages, K).total;
   const int occ = P.u ? batch_occupancy_for(mr, smem0, K, P.u) : occupancy_for(mr, mr, smem0, K);
   const int64_t gmax = (int64_t)a.ctx->sms * occ;
-  const int64_t per = std::max<int64_t>(1, (a.nnzb + gmax - 1) / gmax);
-  int row = 0;
-  while (row < a.nbr) {
+  const int64_t nnzb_range = a.h_row_ptr[row1] - a.h_row_ptr[row0];
+  const int64_t per = std::max<int64_t>(1, (nnzb_range + gmax - 1) / gmax);
+  int row = row0;
+  while (row < row1) {
     const int rlo = row;
     const int64_t b0 = rp[rlo];
-    while (row < a.nbr && rp[row + 1] - b0 < per) ++row;
-    if (row < a.nbr) ++row;  // include the row that reaches the target
+    while (row < row1 && rp[row + 1] - b0 < per) ++row;
+    if (row < row1) ++row;  // include the row that reaches the target
     // rows that are empty right after the cut stay with this CTA
-    while (row < a.nbr && rp[row + 1] == rp[row]) ++row;
+    while (row < row1 && rp[row + 1] == rp[row]) ++row;
     const int rhi = row;
     const int64_t B0 = rp[rlo], B1 = rp[rhi];
     cta.push_back((int)chunks.size());
@@ -751,8 +756,13 @@ static bool pdl_enabled() {
 }
 
 template <int MR, int MC, int K, class Epi, bool VAR = false>
+static void launch_stream_plan(const Bsr& a, const Plan& P, const double* x, Epi epi);
+template <int MR, int MC, int K, class Epi, bool VAR = false>
 static void launch_stream_t(const Bsr& a, const double* x, Epi epi) {
-  const Plan& P = plan_for(a, K);
+  launch_stream_plan<MR, MC, K, Epi, VAR>(a, plan_for(a, K), x, epi);
+}
+template <int MR, int MC, int K, class Epi, bool VAR>
+static void launch_stream_plan(const Bsr& a, const Plan& P, const double* x, Epi epi) {
   kern::StreamArgs s;
   s.vals = VAR ? a.pvals.p : a.vals.p;
   s.col = a.col.p;
@@ -889,6 +899,24 @@ static void launch(const Bsr& a, const double* x, Epi epi, int nrhs) {
   kern::bsr_var_kernel<Epi><<<blocks, 256, 0, a.ctx->stream>>>(s, epi);
   a.ctx->count();
   BMG_LAUNCHED(a.ctx->stream, "bsr_var_kernel");
+}
+
+std::unique_ptr<Plan> plan_rows(const Bsr& a, int row0, int row1) {
+  if (!a.uniform || !stream_supported(a.mr, a.mc)) return nullptr;
+  auto p = std::make_unique<Plan>();
+  build_plan_into(a, *p, 1, a.mr, a.bs, false, row0, row1);
+  if (p->nctas == 0) return nullptr;
+  return p;
+}
+void residual_rows(const Bsr& a, const Plan& P, const double* b, const double* x, double* r) {
+  const kern::EpiResidual epi{b, r};
+  switch (a.mr) {
+    case 10: return launch_stream_plan<10, 10, 1>(a, P, x, epi);
+    case 15: return launch_stream_plan<15, 15, 1>(a, P, x, epi);
+    case 20: return launch_stream_plan<20, 20, 1>(a, P, x, epi);
+    case 21: return launch_stream_plan<21, 21, 1>(a, P, x, epi);
+  }
+  fail(BMG_EINVAL, "residual_rows: streamed block sizes only");
 }
 
 void spmv(const Bsr& a, const double* x, double* y, int nrhs) { launch(a, x, kern::EpiStore{y}, nrhs); }

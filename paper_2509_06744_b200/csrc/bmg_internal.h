@@ -246,6 +246,11 @@ void build_plan(Bsr& a);
 // launch plan for nrhs right-hand sides (shared-memory size and CTA count depend
 // on it); call outside graph capture before the first batched launch
 const Plan& plan_for(const Bsr& a, int nrhs);
+// a single-RHS plan over block rows [row0, row1) of a uniform streamed matrix (no
+// data copy; outputs land at their absolute rows); nullptr if not streamable
+std::unique_ptr<Plan> plan_rows(const Bsr& a, int row0, int row1);
+// r = b - A x on the rows of a plan_rows plan
+void residual_rows(const Bsr& a, const Plan& P, const double* b, const double* x, double* r);
 // whether a variable layout runs on the streaming kernel through padded blocks
 bool var_streamed(const Bsr& a);
 

@@ -104,8 +104,25 @@ struct GraphKey {
   int kpre, kpost, nrhs, top;
   const double* b;
   double* x;
+  bool hostio = false;  // b, x are the caller's host buffers (copies inside the graph)
   bool operator<(const GraphKey& o) const {
-    return std::tie(kpre, kpost, nrhs, top, b, x) < std::tie(o.kpre, o.kpost, o.nrhs, o.top, o.b, o.x);
+    return std::tie(kpre, kpost, nrhs, top, b, x, hostio) < std::tie(o.kpre, o.kpost, o.nrhs, o.top, o.b, o.x, o.hostio);
+  }
+};
+
+// Host-buffer cycles (bmg_vcycle_host): b and x go up in row slices on a copy
+// stream and the first residual r = b - A x runs per slice as soon as the rows it
+// reads have landed, so the upload overlaps the first pass.
+struct HostIo {
+  std::vector<std::unique_ptr<Plan>> plans;  // row-range plans of the finest A
+  std::vector<int> row0, row1, need;         // slice rows; last slice whose x it reads
+  cudaStream_t cs = nullptr;
+  cudaEvent_t fork = nullptr;
+  std::vector<cudaEvent_t> ev;               // slice s landed
+  ~HostIo() {
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    if (fork) cudaEventDestroy(fork);
+    if (cs) cudaStreamDestroy(cs);
   }
 };
 
@@ -134,6 +151,8 @@ struct Hier {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   const double* user_b = nullptr;
   double* user_x = nullptr;
+  std::unique_ptr<HostIo> hio;
+  bool skip_top_res = false;  // the top level's first residual is already in its r
   std::vector<const Bsr*> held_bsr;    // caller objects the levels point to
   std::vector<const Fsai*> held_fsai;
   void hold(const Bsr* a) {
@@ -178,6 +197,9 @@ inline double* vec(Hier& h, Part& p, int l, Which w) {
 void exchange(Hier& h, int l, Which w);
 void set_nrhs(Hier& h, int K);
 void run_vcycle(Hier& h, int kpre, int kpost, const double* bf, double* xf);
+// whole single-RHS hierarchies with pinned host b, x and kpre > 0: the pipelined
+// host-buffer cycle; false if it does not apply (the caller copies around run_vcycle)
+bool run_vcycle_hostio(Hier& h, int kpre, int kpost, const double* hb, double* hx);
 double finest_norm(Hier& h, const double* r_whole);
 void finest_residual(Hier& h, const double* b, double* x, double* rtmp);
 void coarse_factor(Hier& h, Part& p);

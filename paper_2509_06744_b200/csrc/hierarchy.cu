@@ -745,10 +745,13 @@ int bmg_vcycle_batch_host(bmg_hier* hh, int kpre, int kpost, int nrhs, const dou
       h->io_b.alloc(std::max<int64_t>(n, 1));
       h->io_x.alloc(std::max<int64_t>(n, 1));
     }
-    BMG_CUDA(cudaMemcpyAsync(h->io_b.p, b, n * 8, cudaMemcpyHostToDevice, ctx->stream));
-    BMG_CUDA(cudaMemcpyAsync(h->io_x.p, x, n * 8, cudaMemcpyHostToDevice, ctx->stream));
-    run_vcycle(*h, kpre, kpost, h->io_b.p, h->io_x.p);
-    BMG_CUDA(cudaMemcpyAsync(x, h->io_x.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    if (kpre + kpost < 1) fail(BMG_EINVAL, "v_cycle: cycle needs at least one smoothing step");
+    if (!run_vcycle_hostio(*h, kpre, kpost, b, x)) {
+      BMG_CUDA(cudaMemcpyAsync(h->io_b.p, b, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+      BMG_CUDA(cudaMemcpyAsync(h->io_x.p, x, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+      run_vcycle(*h, kpre, kpost, h->io_b.p, h->io_x.p);
+      BMG_CUDA(cudaMemcpyAsync(x, h->io_x.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    }
     BMG_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }

@@ -217,6 +217,9 @@ static void smooth(Hier& h, int l, int k, bool xzero) {
     const bool zero_x = (s == 0 && xzero);
     if (zero_x) {
       src = VB;  // A * 0 = 0: r = b exactly
+    } else if (s == 0 && h.skip_top_res && l == h.cycle_top()) {
+      src = VR;  // computed by the host-buffer slices (run_vcycle_hostio); pre-smoothing only
+      h.skip_top_res = false;
     } else {
       run_pass(h, l, VX, l, [&](Part& p) { return &p.lv[l].sA; },
                [&](Part& p, PLevel& L, const Slice& sl) {
@@ -453,6 +456,120 @@ void run_vcycle(Hier& h, int kpre, int kpost, const double* bf, double* xf) {
   }
   BMG_CUDA(cudaGraphLaunch(it->second.exec, ctx->stream));
   ctx->launches += it->second.kernels;
+}
+
+bool run_vcycle_hostio(Hier& h, int kpre, int kpost, const double* hb, double* hx) {
+  static const bool off = [] {
+    const char* e = std::getenv("BMG_HOSTIO_PIPELINE");
+    return e && e[0] == '0';
+  }();
+  if (off || !h.whole() || h.nrhs != 1 || kpre < 1 || !h.use_graph || h.cycle_top() != h.finest() ||
+      h.finest() == 0)
+    return false;
+  Ctx* ctx = h.ctx;
+  Part& P0 = h.parts[0];
+  PLevel& L = P0.lv[h.finest()];
+  const Bsr& A = *L.A;
+  if (!A.uniform || L.m == 0) return false;
+  auto pinned = [](const void* p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+  };
+  if (!pinned(hb) || !pinned(hx)) return false;
+  const int64_t n = L.n_own();
+  const int m = L.m;
+  if (!h.hio) {  // slices, plans, copy stream and events: built once, outside capture
+    auto io = std::make_unique<HostIo>();
+    static const int nslice = [] {
+      const char* e = std::getenv("BMG_HOSTIO_SLICES");
+      return e ? std::max(1, std::min(64, std::atoi(e))) : 4;
+    }();
+    const int S = (int)std::min<int64_t>(nslice, std::max(1, A.nbr / 64));
+    for (int s = 0; s < S; ++s) {
+      const int r0 = (int)((int64_t)A.nbr * s / S), r1 = (int)((int64_t)A.nbr * (s + 1) / S);
+      auto pl = plan_rows(A, r0, r1);
+      if (!pl) return false;
+      int maxc = -1;
+      for (int i = r0; i < r1; ++i)
+        if (A.h_row_ptr[i + 1] > A.h_row_ptr[i]) maxc = std::max(maxc, A.h_col[A.h_row_ptr[i + 1] - 1]);
+      io->plans.push_back(std::move(pl));
+      io->row0.push_back(r0);
+      io->row1.push_back(r1);
+      io->need.push_back(maxc);
+    }
+    for (int s = 0; s < S; ++s) {  // column -> the slice whose copy brings it
+      int t = s;
+      while (t + 1 < S && io->need[s] >= io->row1[t]) ++t;
+      io->need[s] = t;
+    }
+    BMG_CUDA(cudaStreamCreateWithFlags(&io->cs, cudaStreamNonBlocking));
+    BMG_CUDA(cudaEventCreateWithFlags(&io->fork, cudaEventDisableTiming));
+    io->ev.resize(S, nullptr);
+    for (auto& e : io->ev) BMG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    h.hio = std::move(io);
+  }
+  HostIo& io = *h.hio;
+  if (h.io_b.n < (size_t)n) {
+    BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+    h.io_b.alloc(std::max<int64_t>(n, 1));
+    h.io_x.alloc(std::max<int64_t>(n, 1));
+    h.drop_graphs();
+  }
+  GraphKey key{kpre, kpost, 1, h.cycle_top(), hb, hx, true};
+  auto it = h.graphs.find(key);
+  if (it == h.graphs.end()) {
+    prepare_plans(h, 1);
+    cudaStream_t user = ctx->stream;
+    ctx->stream = ctx->own;
+    const int64_t before = ctx->launches;
+    BMG_CUDA(cudaStreamBeginCapture(ctx->own, cudaStreamCaptureModeThreadLocal));
+    try {
+      double* r = L.v[VR].p;
+      BMG_CUDA(cudaEventRecord(io.fork, ctx->own));
+      BMG_CUDA(cudaStreamWaitEvent(io.cs, io.fork, 0));
+      const int S = (int)io.plans.size();
+      for (int s = 0; s < S; ++s) {
+        const int64_t o = (int64_t)io.row0[s] * m, len = (int64_t)(io.row1[s] - io.row0[s]) * m;
+        BMG_CUDA(cudaMemcpyAsync(h.io_b.p + o, hb + o, len * 8, cudaMemcpyHostToDevice, io.cs));
+        BMG_CUDA(cudaMemcpyAsync(h.io_x.p + o, hx + o, len * 8, cudaMemcpyHostToDevice, io.cs));
+        BMG_CUDA(cudaEventRecord(io.ev[s], io.cs));
+      }
+      for (int s = 0; s < S; ++s) {
+        BMG_CUDA(cudaStreamWaitEvent(ctx->own, io.ev[io.need[s]], 0));
+        residual_rows(A, *io.plans[s], h.io_b.p, h.io_x.p, r);
+      }
+      BMG_CUDA(cudaStreamWaitEvent(ctx->own, io.ev[S - 1], 0));  // join the copy stream
+      h.user_b = h.io_b.p;
+      h.user_x = h.io_x.p;
+      h.skip_top_res = true;
+      enqueue_vcycle(h, kpre, kpost);
+      h.skip_top_res = false;
+      BMG_CUDA(cudaMemcpyAsync(hx, h.io_x.p, n * 8, cudaMemcpyDeviceToHost, ctx->own));
+    } catch (...) {
+      h.skip_top_res = false;
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(ctx->own, &g);
+      if (g) cudaGraphDestroy(g);
+      ctx->stream = user;
+      ctx->launches = before;
+      throw;
+    }
+    cudaGraph_t g;
+    BMG_CUDA(cudaStreamEndCapture(ctx->own, &g));
+    ctx->stream = user;
+    cudaGraphExec_t ex;
+    BMG_CUDA(cudaGraphInstantiate(&ex, g, 0));
+    cudaGraphDestroy(g);
+    it = h.graphs.emplace(key, Hier::Captured{ex, ctx->launches - before}).first;
+    ctx->launches = before;
+  }
+  BMG_CUDA(cudaGraphLaunch(it->second.exec, ctx->stream));
+  ctx->launches += it->second.kernels;
+  return true;
 }
 
 // partition-invariant ||r||_2 of the finest level (segments = granules)
