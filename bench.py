@@ -174,7 +174,7 @@ def run_reference(args, cfg):
 
 
 # ------------------------------------------------------------------ GPU arm
-def measure_c1(ctx, stream, steps):
+def measure_c1(ctx, stream, steps, with_cpu=False):
     """BASELINE configs[0] (C1): one fourth-kind smoother application, k = 3, static
     block-FSAI lower(P(A)) on the 64^2 m = 10 operator.  Working set ~0.09 GB, so
     the number is L2-resident by construction (labelled so)."""
@@ -205,9 +205,27 @@ def measure_c1(ctx, stream, steps):
     n = A.dim_r
     g, gt = M.G, M.G.transpose()
     per = c1.k * (dA.info()["pass_bytes"] + 24 * n + g.info()["pass_bytes"] + gt.info()["pass_bytes"] + 56 * n)
-    return {"workload": "C1: 64^2 patches, m=10, static block-FSAI lower(P(A)), one cheb4 application k=3",
-            "value": 1e3 / ms, "unit": "smoother applications/s", "ms": ms, "bytes_per_application": per,
-            "gbs": per / ms / 1e6, "l2": "L2-resident (0.09 GB working set < 126 MB L2)"}
+    out = {"workload": "C1: 64^2 patches, m=10, static block-FSAI lower(P(A)), one cheb4 application k=3",
+           "value": 1e3 / ms, "unit": "smoother applications/s", "ms": ms, "bytes_per_application": per,
+           "gbs": per / ms / 1e6, "l2": "L2-resident (0.09 GB working set < 126 MB L2)"}
+    if with_cpu:  # the same application on the CPU oracle (the reference's own CPU-runnable case)
+        from oracle import pyoracle as O
+        om = O.Mat(A)
+        of = O.Fsai(om, O.Fsai.STATIC)
+        bh, xh = b.download(), x.download()
+        for threads in (os.cpu_count() or 1, 1):
+            O.set_threads(threads)
+            O.smoother_apply(om, of, O.CHEB_FOURTH, bh, xh, c1.k, beta=beta)
+            t0 = time.perf_counter()
+            reps_c = 0
+            while time.perf_counter() - t0 < 1.0:
+                O.smoother_apply(om, of, O.CHEB_FOURTH, bh, xh, c1.k, beta=beta)
+                reps_c += 1
+            rate = reps_c / (time.perf_counter() - t0)
+            out["cpu_oracle_threads" if threads > 1 else "cpu_oracle_1_thread"] = {
+                "value": rate, "unit": "smoother applications/s", "cores": threads}
+        O.set_threads(os.cpu_count() or 1)
+    return out
 
 
 def measure_hierarchy(ctx, stream, cfg, steps, batch=0):
@@ -435,7 +453,7 @@ def run_ours(args, cfg):
     if rank == 0 and ws == 1:
         extra = {}
         try:
-            extra["C1"] = measure_c1(ctx, stream, args.steps)
+            extra["C1"] = measure_c1(ctx, stream, args.steps, with_cpu=not args.no_cpu_baseline)
         except Exception as e:  # secondary lines never fail the headline run
             extra["C1"] = {"error": f"{type(e).__name__}: {e}"}
         try:  # the same hierarchy on 8 right-hand sides per cycle (bmg_vcycle_batch)
