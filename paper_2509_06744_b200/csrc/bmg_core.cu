@@ -312,8 +312,9 @@ static int batch_occupancy_for(int mr, size_t smem, int K, int U) {
   return 1;
 }
 // Which kernel streams K > 1 right-hand sides, with its RHS groups U (V = K / U
-// per thread) and blocks per chunk, from measured sweeps on B200
-// (profiles/r01_batched_kernel_sweep.txt).  The staged-x kernel wins where blocks
+// per thread), blocks per chunk and x path (bulk copies or XL consumer gathers),
+// from measured sweeps on B200 (profiles/r01_batched_kernel_sweep.txt,
+// r01_batched_xl_sweep.txt).  The staged-x kernel wins where blocks
 // are large (m = 15 for K <= 4, m = 20, 21: up to 2x) and for m = 10 at K = 8;
 // for m = 10 at K <= 4 the chunk count per byte is high and the per-chunk
 // staging latency loses to the L1 gathers of bsr_stream_kernel.  BMG_BATCH_KERNEL=old|new, BMG_BATCH_U and
@@ -321,6 +322,7 @@ static int batch_occupancy_for(int mr, size_t smem, int K, int U) {
 struct BatchChoice {
   int u = 0;   // 0: bsr_stream_kernel<K>; else bsr_batch_kernel with U groups
   int cb = 0;  // blocks per chunk (0: kConsumers / (mr U))
+  int xl = 0;  // x segments gathered by the consumers through L1 (else bulk-copied)
 };
 static BatchChoice batch_choice(int mr, int K) {
   static const int env_k = [] {
@@ -337,9 +339,9 @@ static BatchChoice batch_choice(int mr, int K) {
   }();
   BatchChoice c;
   switch (mr) {
-    case 10: if (K == 8) c = {1, 16}; break;
+    case 10: if (K == 8) c = {1, 16}; else if (K == 2) c = {1, 25, 1}; break;
     case 15: if (K == 2) c = {1, 16}; else if (K == 4) c = {2, 20}; break;
-    case 20:
+    case 20: c = K == 2 ? BatchChoice{1, 8, 1} : BatchChoice{1, 8}; break;
     case 21: c = {1, 8}; break;
     default: break;
   }
@@ -348,6 +350,16 @@ static BatchChoice batch_choice(int mr, int K) {
   auto valid = [&](int u) { return (u == 1 || u == 2) && (K / u) % 2 == 0; };
   if (c.u && valid(env_u)) c.u = env_u;
   if (c.u && env_cb > 0) c.cb = env_cb;
+  static const int env_xl = [] {
+    const char* e = std::getenv("BMG_BATCH_XL");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (c.u && env_xl >= 0) c.xl = env_xl ? 1 : 0;
+  if (K != 2) c.xl = 0;  // instantiated for K = 2 only
+  if (c.xl) {
+    const int cap = kern::batch_xl_cb(mr);
+    if (c.cb <= 0 || c.cb > cap) c.cb = std::min(cap, std::max(1, kern::kConsumers / (mr * c.u)));
+  }
   return c;
 }
 
@@ -368,6 +380,7 @@ static void build_plan_into(const Bsr& a, Plan& P, int K, int mr, int bs, bool v
     // bsr_batch_kernel: phase-A items (block, row, RHS group); the producer warp
     // stages one x segment per lane, so a chunk holds at most 32 blocks
     P.u = bc.u;
+    P.xl = bc.xl;
     P.cb_max = std::min(32, bc.cb > 0 ? bc.cb : std::max(1, kern::kConsumers / (mr * P.u)));
   } else {
     P.cb_max = chunk_blocks(mr, bs, K);
@@ -802,8 +815,8 @@ static void launch_stream_plan(const Bsr& a, const Plan& P, const double* x, Epi
   BMG_LAUNCHED(a.ctx->stream, "bsr_stream_kernel");
 }
 
-template <int MR, int K, int U, class Epi>
-static void launch_batch_t(const Bsr& a, const Plan& P, const double* x, Epi epi) {
+template <int MR, int K, int U, class Epi, bool XL>
+static void launch_batch_x(const Bsr& a, const Plan& P, const double* x, Epi epi) {
   if (reinterpret_cast<uintptr_t>(x) & 15)
     fail(BMG_EINVAL, "batched pass: x must be 16-byte aligned");
   kern::StreamArgs s;
@@ -819,7 +832,7 @@ static void launch_batch_t(const Bsr& a, const Plan& P, const double* x, Epi epi
   s.stages = P.stages;
   s.l2hint = l2_hint_enabled();
   static const bool attr_set = [] {
-    stream_attrs(kern::bsr_batch_kernel<MR, MR, K, U, Epi>, K);
+    stream_attrs(kern::bsr_batch_kernel<MR, MR, K, U, Epi, XL>, K);
     return true;
   }();
   (void)attr_set;
@@ -833,9 +846,17 @@ static void launch_batch_t(const Bsr& a, const Plan& P, const double* x, Epi epi
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  BMG_CUDA(cudaLaunchKernelEx(&cfg, kern::bsr_batch_kernel<MR, MR, K, U, Epi>, s, epi));
+  BMG_CUDA(cudaLaunchKernelEx(&cfg, kern::bsr_batch_kernel<MR, MR, K, U, Epi, XL>, s, epi));
   a.ctx->count();
   BMG_LAUNCHED(a.ctx->stream, "bsr_batch_kernel");
+}
+
+template <int MR, int K, int U, class Epi>
+static void launch_batch_t(const Bsr& a, const Plan& P, const double* x, Epi epi) {
+  if constexpr (K == 2) {  // the only batch size where XL measured faster (batch_choice)
+    if (P.xl) return launch_batch_x<MR, K, U, Epi, true>(a, P, x, epi);
+  }
+  launch_batch_x<MR, K, U, Epi, false>(a, P, x, epi);
 }
 
 template <int MR, class Epi>

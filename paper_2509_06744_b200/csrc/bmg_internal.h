@@ -134,6 +134,7 @@ struct Plan {
   int nchunks = 0;
   size_t smem = 0;
   int u = 0;             // K > 1 on a uniform layout: bsr_batch_kernel with U RHS groups
+  int xl = 0;            // ... with x gathered by the consumers (XL)
   DBuf<int4> chunks;     // {blk_lo, nblk, row_lo, nrows | carry flags}
   DBuf<int> cta_chunk;   // [nctas + 1]
 };

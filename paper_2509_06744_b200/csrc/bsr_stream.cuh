@@ -466,7 +466,15 @@ __device__ __forceinline__ int batch_part_idx(int slot, int v) {
   return slot * K + ((((v >> 1) ^ ((slot / RPL) % P))) << 1) + (v & 1);
 }
 
-template <int MR, int MC, int K, int U, class Epi>
+// XL: the x segments do not go through the TMA engine (which the matrix stream
+// already keeps busy) but are gathered by the consumer threads with read-only
+// 16-byte loads through L1 -- consecutive chunks of a CTA reuse most segments, so
+// L1 serves them -- one chunk ahead into registers, and stored to a
+// parity-indexed shared buffer at the end of the previous chunk's phase A (before
+// the chunk's one barrier).  Chunks hold at most batch_xl_cb(MR) blocks then.
+__host__ __device__ constexpr int batch_xl_cb(int mr) { return mr <= 10 ? 32 : (mr <= 15 ? 16 : 8); }
+
+template <int MR, int MC, int K, int U, class Epi, bool XL = false>
 __global__ void __launch_bounds__(kThreads, (MR <= 10 || K / U < 8) ? 3 : 2) bsr_batch_kernel(StreamArgs s, Epi epi) {
   static_assert(K % 2 == 0 && K <= 8 && K % U == 0 && (K / U) % 2 == 0, "batch shape");
   constexpr int V = K / U;  // right-hand sides per thread
@@ -520,7 +528,7 @@ __global__ void __launch_bounds__(kThreads, (MR <= 10 || K / U < 8) ? 3 : 2) bsr
       } else {
         if (lane == 0) {
           const uint32_t vbytes = (uint32_t)d.y * (uint32_t)s.bs * 8u;
-          mbar_arrive_expect_tx(&full[st], vbytes + (uint32_t)d.y * xbytes);
+          mbar_arrive_expect_tx(&full[st], vbytes + (XL ? 0u : (uint32_t)d.y * xbytes));
           bulk_stream(vals_s + (size_t)st * stage_vals, s.vals + (int64_t)d.x * s.bs, vbytes, &full[st], s.l2hint,
                       pol);
         }
@@ -529,7 +537,7 @@ __global__ void __launch_bounds__(kThreads, (MR <= 10 || K / U < 8) ? 3 : 2) bsr
           waited = true;
         }
         __syncwarp();
-        if (lane < d.y)
+        if (!XL && lane < d.y)
           bulk_g2s(xs_s + (size_t)st * stage_xs + lane * XS, s.x + (int64_t)j * MC * K, xbytes, &full[st]);
       }
       jn = (c + 1 < c1 && lane < dn.y) ? __ldg(s.col + dn.x + lane) : 0;
@@ -539,6 +547,40 @@ __global__ void __launch_bounds__(kThreads, (MR <= 10 || K / U < 8) ? 3 : 2) bsr
 
   // ------------------------------------------------------------ consumers
   pdl_wait();
+  // XL staging: pieces (16 bytes) of the chunk's x segments, thread t takes pieces
+  // t, t + kConsumers, ...
+  constexpr int PPB = MC * K / 2;
+  constexpr int NP = XL ? (batch_xl_cb(MR) * PPB + kConsumers - 1) / kConsumers : 1;
+  double2 xr[NP];
+  int xo[NP];
+  auto xload = [&](int c) {
+#pragma unroll
+    for (int k = 0; k < NP; ++k) xo[k] = -1;
+    if (c >= c1) return;
+    const int4 d = s.chunks[c];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      const int p = tid + k * kConsumers;
+      if (p < d.y * PPB) {
+        const int b = p / PPB;
+        const int o = p - b * PPB;
+        const int j = __ldg(s.col + d.x + b);
+        xr[k] = __ldg(reinterpret_cast<const double2*>(s.x + (int64_t)j * MC * K) + o);
+        xo[k] = b * XS + 2 * o;
+      }
+    }
+  };
+  auto xstore = [&](double* dst) {
+#pragma unroll
+    for (int k = 0; k < NP; ++k)
+      if (xo[k] >= 0) *reinterpret_cast<double2*>(dst + xo[k]) = xr[k];
+  };
+  if constexpr (XL) {
+    xload(c0);
+    xstore(xs_s);
+    xload(c0 + 1);
+    consumer_bar();
+  }
   for (int c = c0, it = 0; c < c1; ++c, ++it) {
     const int st = it % kStages;
     const int pb = it & 1;
@@ -562,7 +604,7 @@ __global__ void __launch_bounds__(kThreads, (MR <= 10 || K / U < 8) ? 3 : 2) bsr
 
     // phase A: item = (block, rhs group, row), row fastest
     const double* vs = vals_s + (size_t)st * stage_vals;
-    const double* xs = xs_s + (size_t)st * stage_xs;
+    const double* xs = xs_s + (size_t)(XL ? pb : st) * stage_xs;
     const int items = d.y * MR * U;
     for (int item = tid; item < items; item += kConsumers) {
       const int b = item / (MR * U);
@@ -609,6 +651,10 @@ __global__ void __launch_bounds__(kThreads, (MR <= 10 || K / U < 8) ? 3 : 2) bsr
         const int v = u * V + 2 * v2;
         *reinterpret_cast<double2*>(part + batch_part_idx<K>(slot, v)) = make_double2(acc[2 * v2], acc[2 * v2 + 1]);
       }
+    }
+    if constexpr (XL) {  // the next chunk's x into the other buffer, then the one after into registers
+      xstore(xs_s + (size_t)(pb ^ 1) * stage_xs);
+      xload(c + 2);
     }
     consumer_bar();
     if (tid == 0) mbar_arrive(&empty[st]);
