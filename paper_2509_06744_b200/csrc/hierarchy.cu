@@ -774,7 +774,7 @@ int bmg_solve(bmg_hier* hh, int kpre, int kpost, const bmg_vec* bh, bmg_vec* xh,
     };
     hist[0] = resid();
     int it = 0, st = 1;
-    if (hist[0] == 0.0) st = 0;
+    if (hist[0] == 0.0 || hist[0] / hist[0] < tol) st = 0;  // as the oracle (orc_solve) and measure_rates
     while (st == 1 && it < max_iter) {
       run_vcycle(*h, kpre, kpost, b, x);
       ++it;

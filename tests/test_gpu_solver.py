@@ -487,3 +487,14 @@ def test_vcycle_pinned_host_pipelined_equals_device(ctx, n, levels, kpre, kpost)
         assert np.array_equal(hx.numpy(), xv.download())
     # the caller's b is untouched
     assert np.array_equal(hb.numpy(), b)
+
+
+def test_solve_stopping_edge_cases_match_oracle(ctx):
+    """tol above 1 (converged before any cycle), zero right-hand side (zero residual),
+    max_iter 0: iteration counts, status and histories as the oracle's loop."""
+    A, T, b, oh, dh = _small_hierarchies(ctx, 16, 2)
+    for bb, tol, mi in ((b, 2.0, 10), (np.zeros_like(b), 1e-8, 10), (b, 1e-8, 0)):
+        hist_o, it_o, st_o, _ = oh.solve(3, 3, bb, np.zeros_like(bb), tol, mi)
+        hist_g, it_g, st_g = dh.solve(3, 3, Vector(ctx, bb), Vector(ctx, np.zeros_like(bb)), tol, mi)
+        assert (it_g, st_g) == (it_o, st_o), (tol, mi, it_g, st_g, it_o, st_o)
+        assert np.allclose(hist_g, hist_o, rtol=1e-12, atol=0.0)
