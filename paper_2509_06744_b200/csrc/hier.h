@@ -104,9 +104,11 @@ struct GraphKey {
   int kpre, kpost, nrhs, top;
   const double* b;
   double* x;
-  bool hostio = false;  // b, x are the caller's host buffers (copies inside the graph)
+  int kind = 0;  // 0 cycle on device vectors; 1 cycle on the caller's host buffers
+                // (copies inside the graph); bmg_solve steps: 2 residual norm, 3 cycle +
+                // residual norm (segment sums copied to pinned memory inside the graph)
   bool operator<(const GraphKey& o) const {
-    return std::tie(kpre, kpost, nrhs, top, b, x, hostio) < std::tie(o.kpre, o.kpost, o.nrhs, o.top, o.b, o.x, o.hostio);
+    return std::tie(kpre, kpost, nrhs, top, b, x, kind) < std::tie(o.kpre, o.kpost, o.nrhs, o.top, o.b, o.x, o.kind);
   }
 };
 
@@ -144,6 +146,8 @@ struct Hier {
     cudaGraphExec_t exec;
     int64_t kernels;
   };
+  double* h_seg = nullptr;  // pinned copy of the residual's segment sums (bmg_solve)
+  int h_seg_n = 0;
   std::map<GraphKey, Captured> graphs;
   std::map<GraphKey, int> warm;  // transport hierarchies: keys already run once eagerly
   DBuf<double> io_b, io_x, seg;
@@ -172,6 +176,7 @@ struct Hier {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (comm) cudaStreamDestroy(comm);
+    if (h_seg) cudaFreeHost(h_seg);
   }
   int finest() const { return (int)nbr.size() - 1; }
   int top = -1;  // level the current cycle starts on (v_cycle's `level`; -1: finest)
@@ -200,6 +205,12 @@ void run_vcycle(Hier& h, int kpre, int kpost, const double* bf, double* xf);
 // whole single-RHS hierarchies with pinned host b, x and kpre > 0: the pipelined
 // host-buffer cycle; false if it does not apply (the caller copies around run_vcycle)
 bool run_vcycle_hostio(Hier& h, int kpre, int kpost, const double* hb, double* hx);
+// bmg_solve on whole single-RHS hierarchies: each iteration (cycle, residual,
+// segment sums to pinned memory) is one graph launch; the stopping test stays on
+// the host in the oracle's order; false if it does not apply (the caller runs the
+// eager loop)
+bool solve_device(Hier& h, int kpre, int kpost, const double* b, double* x, double tol, int max_iter, double* hist,
+                  int* iters, int* status);
 double finest_norm(Hier& h, const double* r_whole);
 void finest_residual(Hier& h, const double* b, double* x, double* rtmp);
 void coarse_factor(Hier& h, Part& p);

@@ -767,6 +767,7 @@ int bmg_solve(bmg_hier* hh, int kpre, int kpost, const bmg_vec* bh, bmg_vec* xh,
     need_len(V_(xh), n, "solve");
     const double* b = V_(bh)->d.p;
     double* x = V_(xh)->d.p;
+    if (solve_device(*h, kpre, kpost, b, x, tol, max_iter, hist, iters, status)) return;
     PLevel& F = h->parts[0].lv[h->finest()];
     auto resid = [&]() {
       finest_residual(*h, b, x, F.v[VR].p);

@@ -519,7 +519,7 @@ bool run_vcycle_hostio(Hier& h, int kpre, int kpost, const double* hb, double* h
     h.io_x.alloc(std::max<int64_t>(n, 1));
     h.drop_graphs();
   }
-  GraphKey key{kpre, kpost, 1, h.cycle_top(), hb, hx, true};
+  GraphKey key{kpre, kpost, 1, h.cycle_top(), hb, hx, 1};
   auto it = h.graphs.find(key);
   if (it == h.graphs.end()) {
     prepare_plans(h, 1);
@@ -569,6 +569,109 @@ bool run_vcycle_hostio(Hier& h, int kpre, int kpost, const double* hb, double* h
   }
   BMG_CUDA(cudaGraphLaunch(it->second.exec, ctx->stream));
   ctx->launches += it->second.kernels;
+  return true;
+}
+
+// residual r = b - A x of the whole finest level, then its segment sums (the
+// enqueue half of finest_residual + finest_norm, no host read)
+static int enqueue_residual_segments(Hier& h, const double* b, const double* x) {
+  Ctx* ctx = h.ctx;
+  const int top = h.finest();
+  PLevel& L = h.parts[0].lv[top];
+  residual(*L.A, b, x, L.v[VR].p);
+  const int m = h.msz[top];
+  const int gran = h.granule_top;
+  const int nseg = m ? (h.nbr[top] + gran - 1) / gran : (int)((L.dim + 255) / 256);
+  BMG_CUDA(cudaMemsetAsync(h.seg.p, 0, nseg * sizeof(double), ctx->stream));
+  kern::segment_sq_kernel<<<nseg, 256, 0, ctx->stream>>>(L.v[VR].p, L.n_own(), m ? (int64_t)gran * m : 256, h.seg.p);
+  ctx->count();
+  BMG_CUDA(cudaGetLastError());
+  return nseg;
+}
+
+bool solve_device(Hier& h, int kpre, int kpost, const double* b, double* x, double tol, int max_iter, double* hist,
+                  int* iters, int* status) {
+  static const bool off = [] {
+    const char* e = std::getenv("BMG_DEVICE_SOLVE");
+    return e && e[0] == '0';
+  }();
+  if (off || !h.whole() || h.nrhs != 1 || !h.use_graph || h.top >= 0 || h.finest() == 0 || max_iter < 0)
+    return false;
+  Ctx* ctx = h.ctx;
+  const int top = h.finest();
+  const int m = h.msz[top];
+  const int nseg = m ? (h.nbr[top] + h.granule_top - 1) / h.granule_top
+                     : (int)((h.parts[0].lv[top].dim + 255) / 256);
+  if (h.seg.n < (size_t)nseg) {
+    BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+    h.seg.alloc(std::max(nseg, 1));
+    h.drop_graphs();
+  }
+  if (!h.h_seg || h.h_seg_n < nseg) {
+    if (h.h_seg) cudaFreeHost(h.h_seg);
+    BMG_CUDA(cudaMallocHost(&h.h_seg, (size_t)nseg * sizeof(double)));
+    h.h_seg_n = nseg;
+    h.drop_graphs();
+  }
+  // one graph per step: [cycle,] residual, segment sums, their copy to pinned memory
+  auto step_graph = [&](int kind, int kp, int kq) -> Hier::Captured& {
+    GraphKey key{kp, kq, 1, top, b, x, kind};
+    auto it = h.graphs.find(key);
+    if (it != h.graphs.end()) return it->second;
+    prepare_plans(h, 1);
+    h.user_b = b;
+    h.user_x = x;
+    cudaStream_t user = ctx->stream;
+    ctx->stream = ctx->own;
+    const int64_t before = ctx->launches;
+    BMG_CUDA(cudaStreamBeginCapture(ctx->own, cudaStreamCaptureModeThreadLocal));
+    try {
+      if (kind == 3) enqueue_vcycle(h, kp, kq);
+      enqueue_residual_segments(h, b, x);
+      BMG_CUDA(cudaMemcpyAsync(h.h_seg, h.seg.p, nseg * sizeof(double), cudaMemcpyDeviceToHost, ctx->own));
+    } catch (...) {
+      cudaGraph_t junk = nullptr;
+      cudaStreamEndCapture(ctx->own, &junk);
+      if (junk) cudaGraphDestroy(junk);
+      ctx->stream = user;
+      ctx->launches = before;
+      throw;
+    }
+    cudaGraph_t g;
+    BMG_CUDA(cudaStreamEndCapture(ctx->own, &g));
+    ctx->stream = user;
+    cudaGraphExec_t ex;
+    BMG_CUDA(cudaGraphInstantiate(&ex, g, 0));
+    cudaGraphDestroy(g);
+    auto ins = h.graphs.emplace(key, Hier::Captured{ex, ctx->launches - before});
+    ctx->launches = before;
+    return ins.first->second;
+  };
+  auto norm = [&](Hier::Captured& c) {  // the host's sequential sum, as finest_norm
+    BMG_CUDA(cudaGraphLaunch(c.exec, ctx->stream));
+    ctx->launches += c.kernels;
+    BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+    double s = 0.0;
+    for (int i = 0; i < nseg; ++i) s += h.h_seg[i];
+    return std::sqrt(s);
+  };
+  Hier::Captured& head = step_graph(2, 0, 0);
+  Hier::Captured& step = step_graph(3, kpre, kpost);
+  hist[0] = norm(head);
+  int it = 0, st = 1;
+  if (hist[0] == 0.0 || hist[0] / hist[0] < tol) st = 0;
+  while (st == 1 && it < max_iter) {
+    ++it;
+    hist[it] = norm(step);
+    const double growth = hist[it] / std::max(hist[it - 1], 1e-300);
+    if (!std::isfinite(hist[it]) || growth > 1e6) {
+      st = 2;
+      break;
+    }
+    if (hist[it] / hist[0] < tol) st = 0;
+  }
+  *iters = it;
+  *status = st;
   return true;
 }
 

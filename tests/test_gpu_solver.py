@@ -498,3 +498,23 @@ def test_solve_stopping_edge_cases_match_oracle(ctx):
         hist_g, it_g, st_g = dh.solve(3, 3, Vector(ctx, bb), Vector(ctx, np.zeros_like(bb)), tol, mi)
         assert (it_g, st_g) == (it_o, st_o), (tol, mi, it_g, st_g, it_o, st_o)
         assert np.allclose(hist_g, hist_o, rtol=1e-12, atol=0.0)
+
+
+@pytest.mark.parametrize("tol,max_iter", [(1e-8, 25), (1e-2, 200), (1e-30, 0), (5.0, 10)])
+def test_graph_solve_loop_equals_eager_loop(ctx, tol, max_iter):
+    """bmg_solve with one graph launch per iteration (cycle, residual, segment sums
+    to pinned memory) against the eager loop (use_graph off): bitwise histories and
+    iterates, iteration counts and status as the oracle's."""
+    A, T, b, oh, dh = _small_hierarchies(ctx, 32, 3)
+    out = []
+    for graph in (False, True, True):  # eager loop, graph loop, graph loop from its cache
+        dh.use_graph(graph)
+        x = Vector(ctx, np.zeros_like(b))
+        hist, it, st = dh.solve(3, 3, Vector(ctx, b), x, tol, max_iter)
+        out.append((hist.copy(), it, st, x.download()))
+    dh.use_graph(True)
+    for o in out[1:]:
+        assert o[1:3] == out[0][1:3]
+        assert np.array_equal(o[0], out[0][0]) and np.array_equal(o[3], out[0][3])
+    hist_o, it_o, st_o, _ = oh.solve(3, 3, b, np.zeros_like(b), tol, max_iter)
+    assert (out[1][1], out[1][2]) == (it_o, st_o)

@@ -23,7 +23,7 @@ H = Hierarchy.setup(BlockSparseMatrix(ctx, A), [BlockSparseMatrix(ctx, p) for p 
                     default_params(t_max=1, nest=cfg.nest, coarse_dim_cap=1 << 30))
 bv = Vector(ctx, b)
 x = Vector(ctx, b.size)
-H.solve(cfg.k, cfg.k, bv, x, 1e-30, 3)
+H.solve(cfg.k, cfg.k, bv, x, 1e-30, iters)  # warm-up with the same shape (graph captured here)
 torch.cuda.synchronize()
 x = Vector(ctx, b.size)
 t0 = time.perf_counter()
