@@ -212,7 +212,7 @@ int64_t Bsr::device_bytes() const {
 }
 
 static bool stream_supported(int mr, int mc) {
-  return mr == mc && (mr == 10 || mr == 15 || mr == 20 || mr == 21);
+  return mr == mc && (mr == 3 || mr == 6 || mr == 10 || mr == 15 || mr == 20 || mr == 21);
 }
 
 static int ring_stages() {
@@ -243,7 +243,14 @@ static int chunk_blocks(int mr, int bs, int K = 1) {
   if (K > 1 && mr == 20) kb = 48;
   if (K == 8 && mr == 10) kb = 16;
   const int cap = env_cap ? env_cap : kb * 1024;
-  const int by_items = std::max(1, kern::kConsumers / mr);
+  // small blocks: several phase-A items per consumer thread, so a chunk still
+  // carries enough bytes per barrier (BMG_SMALL_ITEMS overrides the factor)
+  static const int env_items = [] {
+    const char* e = std::getenv("BMG_SMALL_ITEMS");
+    return e ? std::max(1, std::atoi(e)) : 0;
+  }();
+  const int per_thread = mr >= 10 ? 1 : (env_items ? env_items : 3);  // measured: m = 3 3.1 -> 4.2, m = 6 5.9 -> 6.1 TB/s
+  const int by_items = std::max(1, per_thread * kern::kConsumers / mr);
   const int by_bytes = std::max(1, cap / (bs * 8));
   return std::min(by_items, by_bytes);
 }
@@ -279,6 +286,8 @@ static int occupancy_k(size_t smem, int K) {
 
 static int occupancy_for(int mr, int mc, size_t smem, int K = 1) {
   switch (mr) {
+    case 3: return occupancy_k<3, 3>(smem, K);
+    case 6: return occupancy_k<6, 6>(smem, K);
     case 10: return occupancy_k<10, 10>(smem, K);
     case 15: return occupancy_k<15, 15>(smem, K);
     case 20: return occupancy_k<20, 20>(smem, K);
@@ -338,6 +347,7 @@ static BatchChoice batch_choice(int mr, int K) {
     return e ? std::atoi(e) : 0;
   }();
   BatchChoice c;
+  if (mr < 10) return c;  // small blocks (m = 3, 6): the gather kernel only
   switch (mr) {
     case 10: if (K == 8) c = {1, 16}; else if (K == 2) c = {1, 25, 1}; break;
     case 15: if (K == 2) c = {1, 16}; else if (K == 4) c = {2, 20}; break;
@@ -880,7 +890,7 @@ static void launch_batch(const Bsr& a, const double* x, Epi epi, int nrhs) {
 
 template <int MR, int MC, class Epi, bool VAR = false>
 static void launch_stream_k(const Bsr& a, const double* x, Epi epi, int nrhs) {
-  if constexpr (!VAR) {
+  if constexpr (!VAR && MR >= 10) {  // the staged batch kernel serves m >= 10 (batch_choice)
     if (nrhs > 1 && plan_for(a, nrhs).u) return launch_batch<MR>(a, x, epi, nrhs);
   }
   switch (nrhs) {
@@ -897,6 +907,8 @@ static void launch(const Bsr& a, const double* x, Epi epi, int nrhs) {
   if (a.nbr == 0) return;
   if (a.uniform && stream_supported(a.mr, a.mc)) {
     switch (a.mr) {
+      case 3: return launch_stream_k<3, 3>(a, x, epi, nrhs);
+      case 6: return launch_stream_k<6, 6>(a, x, epi, nrhs);
       case 10: return launch_stream_k<10, 10>(a, x, epi, nrhs);
       case 15: return launch_stream_k<15, 15>(a, x, epi, nrhs);
       case 20: return launch_stream_k<20, 20>(a, x, epi, nrhs);
@@ -905,6 +917,8 @@ static void launch(const Bsr& a, const double* x, Epi epi, int nrhs) {
   }
   if (var_streamed(a)) {
     switch (a.mmax) {
+      case 3: return launch_stream_k<3, 3, Epi, true>(a, x, epi, nrhs);
+      case 6: return launch_stream_k<6, 6, Epi, true>(a, x, epi, nrhs);
       case 10: return launch_stream_k<10, 10, Epi, true>(a, x, epi, nrhs);
       case 15: return launch_stream_k<15, 15, Epi, true>(a, x, epi, nrhs);
       case 20: return launch_stream_k<20, 20, Epi, true>(a, x, epi, nrhs);
@@ -940,6 +954,8 @@ std::unique_ptr<Plan> plan_rows(const Bsr& a, int row0, int row1) {
 void residual_rows(const Bsr& a, const Plan& P, const double* b, const double* x, double* r) {
   const kern::EpiResidual epi{b, r};
   switch (a.mr) {
+    case 3: return launch_stream_plan<3, 3, 1>(a, P, x, epi);
+    case 6: return launch_stream_plan<6, 6, 1>(a, P, x, epi);
     case 10: return launch_stream_plan<10, 10, 1>(a, P, x, epi);
     case 15: return launch_stream_plan<15, 15, 1>(a, P, x, epi);
     case 20: return launch_stream_plan<20, 20, 1>(a, P, x, epi);

@@ -24,7 +24,7 @@ def _dev_spmv(ctx, host, x):
     return yv.download()
 
 
-@pytest.mark.parametrize("m", [10, 15, 20, 21])
+@pytest.mark.parametrize("m", [3, 6, 10, 15, 20, 21])
 @pytest.mark.parametrize("density", [0.05, 0.4, 1.0])
 def test_spmv_uniform_bitwise(ctx, rng, m, density):
     # density 1.0 gives rows far longer than one chunk (carry across chunks)
@@ -55,7 +55,7 @@ def test_spmv_variable_layout_bitwise(ctx, rng):
         assert np.array_equal(_dev_spmv(ctx, host, x), O.Mat(host).spmv(x))
 
 
-@pytest.mark.parametrize("m", [10, 15, 3])
+@pytest.mark.parametrize("m", [10, 15, 3, 6])
 def test_spmv_transpose_and_residual_bitwise(ctx, rng, m):
     host = random_bsr(rng, np.full(29, m, np.int32), np.full(23, m, np.int32), 0.3)
     A = BlockSparseMatrix(ctx, host)

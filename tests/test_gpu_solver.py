@@ -518,3 +518,34 @@ def test_graph_solve_loop_equals_eager_loop(ctx, tol, max_iter):
         assert np.array_equal(o[0], out[0][0]) and np.array_equal(o[3], out[0][3])
     hist_o, it_o, st_o, _ = oh.solve(3, 3, b, np.zeros_like(b), tol, max_iter)
     assert (out[1][1], out[1][2]) == (it_o, st_o)
+
+
+@pytest.mark.parametrize("m", [3, 6])
+def test_small_uniform_blocks_stream_and_match_oracle(ctx, m):
+    """Uniform linear / quadratic PUM-size blocks (m = 3, 6) on the streaming kernel:
+    setup, cycles (graph), batched cycles and the solve loop against the oracle."""
+    import dataclasses
+
+    cfg = dataclasses.replace(pr.CONFIGS["C2"].scaled(32, 3), m=m)
+    A, T, b = pr.make_problem(cfg)
+    oh = O.Hierarchy(O.Mat(A), [O.Mat(p) for p in T], t_max=1, coarse_dim_cap=1 << 30, probe=False)
+    dh = Hierarchy.setup(BlockSparseMatrix(ctx, A), [BlockSparseMatrix(ctx, p) for p in T],
+                         default_params(t_max=1, coarse_dim_cap=1 << 30))
+    for l in range(1, dh.levels):
+        assert abs(dh.beta(l) - oh.beta(l)) <= 1e-10 * oh.beta(l)
+    hist_o, it_o, st_o, x_o = oh.solve(3, 3, b, np.zeros_like(b), 1e-8, 20)
+    xv = Vector(ctx, np.zeros_like(b))
+    hist_g, it_g, st_g = dh.solve(3, 3, Vector(ctx, b), xv, 1e-8, 20)
+    assert (it_g, st_g) == (it_o, st_o)
+    rho_o, rho_g = hist_o / hist_o[0], hist_g / hist_g[0]
+    assert np.all(np.abs(rho_g - rho_o) <= 1e-10)
+    # K = 4 batched cycle, each RHS bitwise the single cycle
+    K = 4
+    B = np.stack([np.roll(b, 5 * v) for v in range(K)], axis=1).ravel().copy()
+    xb = Vector(ctx, B.size)
+    dh.v_cycle_batch(3, 3, K, Vector(ctx, B), xb)
+    xbk = xb.download().reshape(-1, K)
+    for v in range(K):
+        xs = Vector(ctx, b.size)
+        dh.v_cycle(3, 3, Vector(ctx, np.ascontiguousarray(B.reshape(-1, K)[:, v])), xs)
+        assert np.array_equal(xbk[:, v], xs.download())
