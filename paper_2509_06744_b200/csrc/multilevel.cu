@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(128) ap_chunk_kernel(const double* __restrict_
                                                        const int32_t* __restrict__ APcol, int f0, int f1,
                                                        int64_t apbase, const int64_t* __restrict__ APoff, int bs_o,
                                                        double* __restrict__ APv) {
-  __shared__ double tiles[4][32 * 32];  // one block tile per warp (128 threads)
+  __shared__ __align__(16) double tiles[4][32 * 32];  // one block tile per warp (128 threads)
   double* tile = tiles[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   const int64_t q0 = APrp[f0], q1 = APrp[f1];
@@ -351,17 +351,33 @@ __global__ void __launch_bounds__(128) ap_chunk_kernel(const double* __restrict_
       double t[MAXR];
 #pragma unroll
       for (int j = 0; j < MAXR; ++j) t[j] = 0.0;
+      const bool zpair = (mk & 1) == 0;  // tile row r: z, z+1 adjacent
       for (int z0 = 0; z0 < mk; z0 += 8) {
         double bc[8];
 #pragma unroll
         for (int zz = 0; zz < 8; ++zz)
           if (z0 + zz < mk) bc[zz] = b[(z0 + zz) * cols + L.c];
+        if (zpair) {  // one 16-byte load: (z, z+1) of row j, the chain order kept
 #pragma unroll
-        for (int zz = 0; zz < 8; ++zz) {
-          if (z0 + zz < mk) {
+          for (int zz = 0; zz < 8; zz += 2) {
+            if (z0 + zz < mk) {
 #pragma unroll
-            for (int j = 0; j < MAXR; ++j)
-              if (j < L.nr) t[j] = __fma_rn(tile[L.row(j) * mk + z0 + zz], bc[zz], t[j]);
+              for (int j = 0; j < MAXR; ++j)
+                if (j < L.nr) {
+                  const double2 tv = *reinterpret_cast<const double2*>(tile + L.row(j) * mk + z0 + zz);
+                  t[j] = __fma_rn(tv.x, bc[zz], t[j]);
+                  t[j] = __fma_rn(tv.y, bc[zz + 1], t[j]);
+                }
+            }
+          }
+        } else {
+#pragma unroll
+          for (int zz = 0; zz < 8; ++zz) {
+            if (z0 + zz < mk) {
+#pragma unroll
+              for (int j = 0; j < MAXR; ++j)
+                if (j < L.nr) t[j] = __fma_rn(tile[L.row(j) * mk + z0 + zz], bc[zz], t[j]);
+            }
           }
         }
       }
@@ -389,7 +405,7 @@ __global__ void __launch_bounds__(128) c_accum_kernel(const double* __restrict__
                                                       const int64_t* __restrict__ Crp,
                                                       const int32_t* __restrict__ Ccol, int I0, int I1, int f0,
                                                       int f1, double* __restrict__ Cv, BlkView Cl) {
-  __shared__ double tiles[4][32 * 32];
+  __shared__ __align__(16) double tiles[4][32 * 32];
   double* tile = tiles[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   const int64_t o0 = Crp[I0], o1 = Crp[I1];
@@ -442,17 +458,34 @@ __global__ void __launch_bounds__(128) c_accum_kernel(const double* __restrict__
       double sm[MAXR];
 #pragma unroll
       for (int j = 0; j < MAXR; ++j) sm[j] = 0.0;
+      const bool pair = L.G == 1 && (rows & 1) == 0;  // lane rows j, j+1 adjacent in the tile
       for (int z0 = 0; z0 < mi; z0 += 8) {
         double ac[8];
 #pragma unroll
         for (int zz = 0; zz < 8; ++zz)
           if (z0 + zz < mi) ac[zz] = ap[(z0 + zz) * cols + L.c];
+        if (pair) {  // one 16-byte broadcast load feeds two fma chains
 #pragma unroll
-        for (int zz = 0; zz < 8; ++zz) {
-          if (z0 + zz < mi) {
+          for (int zz = 0; zz < 8; ++zz) {
+            if (z0 + zz < mi) {
+              const double2* tr = reinterpret_cast<const double2*>(tile + (z0 + zz) * rows);
 #pragma unroll
-            for (int j = 0; j < MAXR; ++j)
-              if (j < L.nr) sm[j] = __fma_rn(tile[(z0 + zz) * rows + L.row(j)], ac[zz], sm[j]);
+              for (int j2 = 0; j2 < MAXR / 2; ++j2)
+                if (2 * j2 + 1 < L.nr) {
+                  const double2 tv = tr[j2];
+                  sm[2 * j2] = __fma_rn(tv.x, ac[zz], sm[2 * j2]);
+                  sm[2 * j2 + 1] = __fma_rn(tv.y, ac[zz], sm[2 * j2 + 1]);
+                }
+            }
+          }
+        } else {
+#pragma unroll
+          for (int zz = 0; zz < 8; ++zz) {
+            if (z0 + zz < mi) {
+#pragma unroll
+              for (int j = 0; j < MAXR; ++j)
+                if (j < L.nr) sm[j] = __fma_rn(tile[(z0 + zz) * rows + L.row(j)], ac[zz], sm[j]);
+            }
           }
         }
       }
