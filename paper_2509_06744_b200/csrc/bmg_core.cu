@@ -37,6 +37,11 @@ thread_local std::string g_last_error;
 thread_local int g_last_pivot = -1;
 
 // ============================================================================ context
+uint64_t next_object_uid() {
+  static std::atomic<uint64_t> n{1};
+  return n++;
+}
+
 Ctx::~Ctx() {
   // at process exit the runtime may already be unloading: the driver reclaims
   // everything, and communicators / library handles must not be torn down then
@@ -44,6 +49,7 @@ Ctx::~Ctx() {
     (void)comm.release();
     return;
   }
+  for (auto& kv : smoother_graphs) cudaGraphExecDestroy(kv.second);
   comm.reset();
   if (solver) cusolverDnDestroy(solver);
   if (blas) cublasDestroy(blas);

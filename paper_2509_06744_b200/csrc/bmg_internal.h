@@ -6,6 +6,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -122,6 +123,8 @@ struct Ctx {
   cublasHandle_t blas = nullptr;
   cublasHandle_t cublas();
   std::atomic<int> refs{1};  // the creator's reference plus one per live object
+  // captured standalone smoother applications (bmg_cheb4_apply / bmg_smoother_apply)
+  std::map<std::vector<uint64_t>, cudaGraphExec_t> smoother_graphs;
   ~Ctx();
 };
 
@@ -164,9 +167,13 @@ namespace bmg {
 // stride bs = m_r*m_c rounded up to even (16-byte aligned blocks), streamed by
 // the sm_100a bulk-copy kernel.  Variable layouts use per-block value offsets
 // and a warp-per-block-row kernel.
+// process-unique object ids (graph cache keys must not alias a freed object's address)
+uint64_t next_object_uid();
+
 struct Bsr {
   CtxRef ctx;
   mutable std::atomic<int> refs{1};  // the creator's reference + hierarchies holding it
+  const uint64_t uid = next_object_uid();
   int nbr = 0, nbc = 0;
   std::vector<int> rsz, csz, roff, coff;  // host layouts
   int dim_r = 0, dim_c = 0;
@@ -229,6 +236,7 @@ struct Vec {
 struct Fsai {
   CtxRef ctx;
   mutable std::atomic<int> refs{1};
+  const uint64_t uid = next_object_uid();
   int dim = 0;
   std::vector<std::unique_ptr<Bsr>> fwd, bwd;
   const Bsr& G() const { return *fwd.back(); }

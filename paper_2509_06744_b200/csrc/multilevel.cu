@@ -1274,9 +1274,67 @@ static void smoother_abi(const bmg_bsr* ah, const bmg_fsai* mh, const SmootherSp
   if (ctx->work.n < (size_t)(4 * n)) {
     BMG_CUDA(cudaStreamSynchronize(ctx->stream));
     ctx->work.alloc(4 * n);
+    // captured applications point at the old work buffer
+    for (auto& kv : ctx->smoother_graphs) cudaGraphExecDestroy(kv.second);
+    ctx->smoother_graphs.clear();
   }
   double* w0 = ctx->work.p;
-  smooth_single(*a, *M(mh), spec, k, V(b)->d.p, V(x)->d.p, w0, w0 + n, w0 + 2 * n, w0 + 3 * n);
+  const Fsai& m = *M(mh);
+  // repeated applications with the same operands replay one captured graph
+  // (the C1 configuration: 9 launches per application)
+  static const bool use_graph = [] {
+    const char* e = std::getenv("BMG_SMOOTHER_GRAPH");
+    return !(e && e[0] == '0');
+  }();
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  BMG_CUDA(cudaStreamIsCapturing(ctx->stream, &cap));
+  if (!use_graph || ctx->comm || cap != cudaStreamCaptureStatusNone) {  // a caller's capture records the launches
+    smooth_single(*a, m, spec, k, V(b)->d.p, V(x)->d.p, w0, w0 + n, w0 + 2 * n, w0 + 3 * n);
+    return;
+  }
+  auto bits = [](double v) {
+    uint64_t u;
+    std::memcpy(&u, &v, 8);
+    return u;
+  };
+  const std::vector<uint64_t> key = {a->uid, m.uid, (uint64_t)(uintptr_t)V(b)->d.p, (uint64_t)(uintptr_t)V(x)->d.p,
+                                     (uint64_t)(uintptr_t)w0, (uint64_t)spec.kind, bits(spec.alpha),
+                                     bits(spec.beta), bits(spec.omega), (uint64_t)k};
+  auto it = ctx->smoother_graphs.find(key);
+  if (it == ctx->smoother_graphs.end()) {
+    if (ctx->smoother_graphs.size() >= 64) {  // bounded cache
+      BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+      for (auto& kv : ctx->smoother_graphs) cudaGraphExecDestroy(kv.second);
+      ctx->smoother_graphs.clear();
+    }
+    plan_for(*a, 1);  // lazily built plans / padded copies: never inside capture
+    for (const auto& f : m.fwd) plan_for(*f, 1);
+    for (const auto& f : m.bwd) plan_for(*f, 1);
+    cudaStream_t user = ctx->stream;
+    ctx->stream = ctx->own;
+    const int64_t before = ctx->launches;
+    BMG_CUDA(cudaStreamBeginCapture(ctx->own, cudaStreamCaptureModeThreadLocal));
+    try {
+      smooth_single(*a, m, spec, k, V(b)->d.p, V(x)->d.p, w0, w0 + n, w0 + 2 * n, w0 + 3 * n);
+    } catch (...) {
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(ctx->own, &g);
+      if (g) cudaGraphDestroy(g);
+      ctx->stream = user;
+      ctx->launches = before;
+      throw;
+    }
+    cudaGraph_t g;
+    BMG_CUDA(cudaStreamEndCapture(ctx->own, &g));
+    ctx->stream = user;
+    cudaGraphExec_t ex;
+    BMG_CUDA(cudaGraphInstantiate(&ex, g, 0));
+    cudaGraphDestroy(g);
+    it = ctx->smoother_graphs.emplace(key, ex).first;
+    ctx->launches = before;
+  }
+  BMG_CUDA(cudaGraphLaunch(it->second, ctx->stream));
+  ctx->count((int)(k * (1 + m.fwd.size() + m.bwd.size())));
 }
 
 int bmg_cheb4_apply(const bmg_bsr* ah, const bmg_fsai* mh, const bmg_vec* b, bmg_vec* x, double beta, int k) {
