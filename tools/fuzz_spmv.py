@@ -13,7 +13,7 @@ ctx = Context(0)
 rng = np.random.default_rng(int(sys.argv[1]) if len(sys.argv) > 1 else 0)
 t0 = time.time(); cases = 0; fails = 0
 while time.time() - t0 < float(sys.argv[2] if len(sys.argv) > 2 else 120):
-    m = int(rng.choice([10, 15, 20, 21, 3, 7]))
+    m = int(rng.choice([10, 15, 20, 21, 3, 6, 7]))
     nbr = int(rng.integers(1, 400)); nbc = int(rng.integers(1, 400))
     dens = float(rng.choice([0.002, 0.02, 0.1, 0.5]))
     h = random_bsr(rng, np.full(nbr, m, np.int32), np.full(nbc, m, np.int32), dens)
