@@ -245,7 +245,9 @@ static int chunk_blocks(int mr, int bs, int K = 1) {
   }();
   // measured sweeps (profiles/r01_kernel_sweep.jsonl, r01_batched_spmv_sweep.jsonl):
   // batched 3-D m = 20 wants more blocks per barrier, batched m = 10 fewer
-  int kb = (mr == 15 || mr == 21) ? 32 : 24;
+  // m = 20: 32 KB measured on whole C4 cycles (72.5 ms against 73.8 at 24 KB;
+  // the coarse levels' 285 / 462-block rows gain most)
+  int kb = (mr == 15 || mr == 21 || mr == 20) ? 32 : 24;
   if (K > 1 && mr == 20) kb = 48;
   if (K == 8 && mr == 10) kb = 16;
   const int cap = env_cap ? env_cap : kb * 1024;

@@ -6,6 +6,7 @@ mode=residual: profile 3 launches of the finest-level residual pass
 import os
 import sys
 
+import numpy as np
 import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -43,6 +44,18 @@ elif mode in ("gpass", "gtpass"):
     torch.cuda.profiler.start()
     for _ in range(3):
         spmv(G, bv, rv)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
+elif mode.startswith("residual@"):  # residual pass of level l (residual@2)
+    lvl = int(mode.split("@")[1])
+    Al, _, _ = H.level(lvl)
+    nl = Al.info()["dim_r"]
+    xl, bl, rl = Vector(ctx, np.ones(nl)), Vector(ctx, np.ones(nl)), Vector(ctx, nl)
+    residual(Al, bl, xl, rl)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
+    for _ in range(3):
+        residual(Al, bl, xl, rl)
     torch.cuda.synchronize()
     torch.cuda.profiler.stop()
 else:
