@@ -409,8 +409,10 @@ static void build_plan_into(const Bsr& a, Plan& P, int K, int mr, int bs, bool v
   std::vector<int> cta;
   int rmax = 1;
   // first pass with a provisional rmax to size smem and query occupancy
+  // bsr_stream_kernel's SKEW layout (m = 20, K = 1, uniform): block pitch bs + 2 in shared memory
+  const int spitch = (K == 1 && mr == 20 && !var) ? bs + 2 : bs;
   const size_t smem0 = P.u ? kern::BatchSmem(bs, P.cb_max, mr, mr, K, P.stages).total
-                           : kern::SmemLayout(bs, P.cb_max, P.cb_max + 2, mr, P.stages, K).total;
+                           : kern::SmemLayout(spitch, P.cb_max, P.cb_max + 2, mr, P.stages, K).total;
   const int occ = P.u ? batch_occupancy_for(mr, smem0, K, P.u) : occupancy_for(mr, mr, smem0, K);
   const int64_t gmax = (int64_t)a.ctx->sms * occ;
   const int64_t nnzb_range = a.h_row_ptr[row1] - a.h_row_ptr[row0];
@@ -449,7 +451,7 @@ static void build_plan_into(const Bsr& a, Plan& P, int K, int mr, int bs, bool v
   P.nctas = (int)cta.size() - 1;
   P.nchunks = (int)chunks.size();
   P.smem = P.u ? kern::BatchSmem(bs, P.cb_max, mr, mr, K, P.stages).total
-               : kern::SmemLayout(bs, P.cb_max, P.rmax, mr, P.stages, K).total;
+               : kern::SmemLayout(spitch, P.cb_max, P.rmax, mr, P.stages, K).total;
   if (P.smem > 227 * 1024) fail(BMG_EINVAL, "plan: chunk does not fit in shared memory");
   if (P.u)  // sets the shared-memory attributes
     batch_occupancy_for(mr, P.smem, K, P.u);

@@ -217,7 +217,13 @@ template <int MR, int MC, int K, class Epi, bool VAR = false>
 __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi epi) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int kStages = s.stages;
-  const SmemLayout L(s.bs, s.cb_max, s.rmax, MR, kStages, K);
+  // SKEW (m = 20): blocks land in shared memory at a pitch of bs + 2 doubles (one
+  // bulk copy per block) and a quarter-warp takes rows 4k..4k+3 of two adjacent
+  // blocks: the 160-byte row pitch alone maps rows r and r + 4 of a block to the
+  // same banks (2-way conflicts on every 16-byte load, 2.5e8 per C4 coarse pass)
+  constexpr bool SKEW = (MR == 20 && MC == 20 && K == 1 && !VAR);
+  const int pitch = SKEW ? s.bs + 2 : s.bs;
+  const SmemLayout L(pitch, s.cb_max, s.rmax, MR, kStages, K);
   // partials of one (block, row) item for K > 1 sit at stride K + 1 (bank spread)
   constexpr int KP = K > 1 ? K + 1 : 1;
   double* vals_s = reinterpret_cast<double*>(smem + L.vals);
@@ -242,7 +248,7 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
   }
   __syncthreads();
 
-  const int stage_vals = s.cb_max * s.bs;
+  const int stage_vals = s.cb_max * pitch;
   const int stage_cols = stage_cols_of(s.cb_max);
 
   if (tid >= kConsumers) {
@@ -262,7 +268,14 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
         const int ch = (d.x + d.y + 3) & ~3;
         const uint32_t cbytes = (uint32_t)(ch - cl) * 4u;
         mbar_arrive_expect_tx(&full[st], vbytes + cbytes);
-        bulk_stream(vals_s + (size_t)st * stage_vals, s.vals + (int64_t)d.x * s.bs, vbytes, &full[st], s.l2hint, pol);
+        if constexpr (SKEW) {
+          for (int b = 0; b < d.y; ++b)
+            bulk_stream(vals_s + (size_t)st * stage_vals + b * pitch, s.vals + (int64_t)(d.x + b) * s.bs,
+                        (uint32_t)s.bs * 8u, &full[st], s.l2hint, pol);
+        } else {
+          bulk_stream(vals_s + (size_t)st * stage_vals, s.vals + (int64_t)d.x * s.bs, vbytes, &full[st], s.l2hint,
+                      pol);
+        }
         bulk_stream(cols_s + st * stage_cols, s.col + cl, cbytes, &full[st], s.l2hint, pol);
       }
     }
@@ -349,11 +362,19 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
     }
     const int items = K > 1 ? 0 : d.y * MR;
     for (int item = tid; item < items; item += kConsumers) {
-      const int b = item / MR;
-      const int r = item - b * MR;
+      int b = item / MR;
+      int r = item - b * MR;
+      if constexpr (SKEW) {  // pairs of blocks: quarter k of a pair = rows 4k..4k+3 of both
+        const int pair = item / (2 * MR);
+        if (2 * pair + 1 < d.y) {
+          const int w = item - pair * 2 * MR;
+          b = 2 * pair + ((w & 7) >> 2);
+          r = 4 * (w >> 3) + (w & 3);
+        }
+      }
       const int j = cs[b];
       const double* __restrict__ xj = s.x + (int64_t)j * MC * K;
-      const double* a = vs + b * s.bs + r * MC;
+      const double* a = vs + b * pitch + r * MC;
       if constexpr (K > 1) {
         // unreachable: K > 1 uses the (block, row group, rhs) items below
         continue;
@@ -386,7 +407,7 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
 #pragma unroll
         for (int q = 0; q < MC; ++q) t = __fma_rn(a[q], xv[q], t);
       }
-      part[item] = t;
+      part[b * MR + r] = t;
     }
     consumer_bar();
     if (tid == 0) mbar_arrive(&empty[st]);
