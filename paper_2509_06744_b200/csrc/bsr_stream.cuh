@@ -16,8 +16,12 @@
 //     holds the partial row sum).
 //   * One producer thread streams chunks into a 2-stage (BMG_STAGES) shared-
 //     memory ring with cp.async.bulk (TMA bulk copy, mbarrier complete_tx):
-//     values and the chunk's column indices.  HBM sees large sequential
-//     transfers; nothing is re-read.
+//     values and the chunk's column indices, with an L2 evict-first policy so
+//     the gathered vectors stay in L2.  HBM sees large sequential transfers;
+//     nothing is re-read (DRAM bytes = algorithmic bytes under ncu).
+//   * m = 20: blocks are copied one by one to a shared-memory pitch of bs + 2
+//     doubles and quarter-warps span two blocks (SKEW), which removes the bank
+//     conflicts of the 160-byte row pitch.
 //   * Consumers (8 warps) compute per-(block, scalar row) dot products from
 //     shared memory against x gathered through L1/L2 (phase A), release the
 //     stage, then sum each row's partials in ascending block order and run the
@@ -25,7 +29,9 @@
 //     row carry are double-buffered: one named barrier per chunk.
 //   * Programmatic dependent launch: dependents are released at entry, vector
 //     accesses wait for the predecessor (griddepcontrol).
-//   * K > 1 right-hand sides interleaved per scalar row share each staged block;
+//   * K > 1 right-hand sides interleaved per scalar row share each staged block
+//     (this kernel's gather form, or bsr_batch_kernel below: staged x segments,
+//     row-per-thread items; the host picks per (m, K) from measured sweeps);
 //     VAR streams a variable layout through zero-padded MR x MC block copies.
 //   * Arithmetic order matches the oracle exactly: t = fma-chain over columns
 //     from 0.0, then y += t per block in ascending column order, so results
