@@ -258,7 +258,9 @@ static int chunk_blocks(int mr, int bs, int K = 1) {
     return e ? std::max(1, std::atoi(e)) : 0;
   }();
   const int per_thread = mr >= 10 ? 1 : (env_items ? env_items : 3);  // measured: m = 3 3.1 -> 4.2, m = 6 5.9 -> 6.1 TB/s
-  const int by_items = std::max(1, per_thread * kern::kConsumers / mr);
+  // m = 15 takes 16 lanes per block in bsr_stream_kernel (bank-conflict-free rows)
+  const int lanes = (K == 1 && mr == 15) ? 16 : mr;
+  const int by_items = std::max(1, per_thread * kern::kConsumers / lanes);
   const int by_bytes = std::max(1, cap / (bs * 8));
   return std::min(by_items, by_bytes);
 }

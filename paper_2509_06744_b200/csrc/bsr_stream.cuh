@@ -366,10 +366,16 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
         }
       }
     }
-    const int items = K > 1 ? 0 : d.y * MR;
+    // HALF (m = 15): 16 lanes per block (one idle), so a half-warp -- one wavefront
+    // of 8-byte loads -- reads the 15 rows of one block: the 120-byte row pitch
+    // spreads them over distinct bank pairs, while two blocks in one half-warp collide
+    constexpr bool HALF = (MR == 15 && MC == 15 && K == 1 && !VAR);
+    constexpr int LPB = HALF ? 16 : MR;
+    const int items = K > 1 ? 0 : d.y * LPB;
     for (int item = tid; item < items; item += kConsumers) {
-      int b = item / MR;
-      int r = item - b * MR;
+      int b = item / LPB;
+      int r = item - b * LPB;
+      if (HALF && r >= MR) continue;
       if constexpr (SKEW) {  // pairs of blocks: quarter k of a pair = rows 4k..4k+3 of both
         const int pair = item / (2 * MR);
         if (2 * pair + 1 < d.y) {

@@ -15,6 +15,8 @@ from paper_2509_06744_b200 import BlockSparseMatrix, Context, Hierarchy, Vector,
 from paper_2509_06744_b200 import problems as pr  # noqa
 
 cfg = pr.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "C2"]
+if len(sys.argv) > 2:  # reduced grid (C3 / C5 do not fit one GPU at full size)
+    cfg = cfg.scaled(int(sys.argv[2]))
 ctx = Context(0)
 stream = torch.cuda.current_stream()
 ctx.set_stream(stream.cuda_stream)
