@@ -59,18 +59,43 @@ __global__ void __launch_bounds__(kSymvThreads) symv_stream_kernel(const double*
       }
     }
   const int it0 = mode == 2 ? kTile * K : 0, it1 = mode == 1 ? kTile * K : 2 * kTile * K;
+  // the x segments of a tile (64 K values each for its row and column ranges) are
+  // loaded into registers one tile ahead, so their latency overlaps the current
+  // tile's work instead of preceding it (K <= 8: at most two per thread)
+  constexpr int kXPer = 8 * kTile / kSymvThreads;
+  double pxi[kXPer], pxj[kXPer];
+  auto xload = [&](int64_t tt) {
+    if (tt >= ntiles) return;
+    int I, J;
+    tile_of(tt, &I, &J);
+#pragma unroll
+    for (int u = 0; u < kXPer; ++u) {
+      const int e = tid + u * kSymvThreads;
+      if (e < kTile * K) {
+        const int r = e / K, v = e - (e / K) * K;
+        const int64_t gi = (int64_t)I * kTile + r, gj = (int64_t)J * kTile + r;
+        pxi[u] = gi < N ? x[gi * K + v] : 0.0;
+        pxj[u] = gj < N ? x[gj * K + v] : 0.0;
+      }
+    }
+  };
+  xload(blockIdx.x);
   int it = 0;
   for (int64_t t = blockIdx.x; t < ntiles; t += stride, ++it) {
     const int st = it & 1;
     int I, J;
     tile_of(t, &I, &J);
-    for (int e = tid; e < kTile * K; e += kSymvThreads) {
-      const int r = e / K, v = e - (e / K) * K;
-      const int64_t gi = (int64_t)I * kTile + r, gj = (int64_t)J * kTile + r;
-      xi[v * kTile + r] = gi < N ? x[gi * K + v] : 0.0;
-      xj[v * kTile + r] = gj < N ? x[gj * K + v] : 0.0;
+#pragma unroll
+    for (int u = 0; u < kXPer; ++u) {
+      const int e = tid + u * kSymvThreads;
+      if (e < kTile * K) {
+        const int r = e / K, v = e - (e / K) * K;
+        xi[v * kTile + r] = pxi[u];
+        xj[v * kTile + r] = pxj[u];
+      }
     }
     __syncthreads();
+    xload(t + stride);
     mbar_wait(&full[st], (it >> 1) & 1);
     const double* tl = ring + st * kTile * kTile;
     for (int q = it0 + tid; q < it1; q += kSymvThreads) {
