@@ -22,6 +22,7 @@
 //     contraction disabled (-ffp-contract=off).
 #include "bmg_oracle.h"
 
+#include <immintrin.h>
 #include <omp.h>
 
 #include <algorithm>
@@ -187,32 +188,66 @@ static void spmv_t(const Mat& a, const double* x, double* y) {
   }
 }
 
+// Block products.  Every output element keeps its own chain
+//   t = fma(a_rk, b_kc, t) over k ascending from 0.0, then acc_rc += t
+// (the convention above); the loops below only evaluate up to 16 such chains
+// side by side (4-wide vectors over c), which changes no rounding.
+// a_rk = a[r * ars + k * aks], b row k = b + k * C (contiguous over c).
+static inline void gemm_rows(int R, int K, int C, const double* a, int ars, int aks, const double* b,
+                             double* acc) {
+  for (int r = 0; r < R; ++r) {
+    const double* ar = a + (size_t)r * ars;
+    double* accr = acc + (size_t)r * C;
+    int c0 = 0;
+    for (; c0 + 16 <= C; c0 += 16) {
+      __m256d t0 = _mm256_setzero_pd(), t1 = t0, t2 = t0, t3 = t0;
+      for (int k = 0; k < K; ++k) {
+        const __m256d av = _mm256_set1_pd(ar[(size_t)k * aks]);
+        const double* bk = b + (size_t)k * C + c0;
+        t0 = _mm256_fmadd_pd(av, _mm256_loadu_pd(bk), t0);
+        t1 = _mm256_fmadd_pd(av, _mm256_loadu_pd(bk + 4), t1);
+        t2 = _mm256_fmadd_pd(av, _mm256_loadu_pd(bk + 8), t2);
+        t3 = _mm256_fmadd_pd(av, _mm256_loadu_pd(bk + 12), t3);
+      }
+      _mm256_storeu_pd(accr + c0, _mm256_add_pd(_mm256_loadu_pd(accr + c0), t0));
+      _mm256_storeu_pd(accr + c0 + 4, _mm256_add_pd(_mm256_loadu_pd(accr + c0 + 4), t1));
+      _mm256_storeu_pd(accr + c0 + 8, _mm256_add_pd(_mm256_loadu_pd(accr + c0 + 8), t2));
+      _mm256_storeu_pd(accr + c0 + 12, _mm256_add_pd(_mm256_loadu_pd(accr + c0 + 12), t3));
+    }
+    for (; c0 + 4 <= C; c0 += 4) {
+      __m256d t0 = _mm256_setzero_pd();
+      for (int k = 0; k < K; ++k)
+        t0 = _mm256_fmadd_pd(_mm256_set1_pd(ar[(size_t)k * aks]), _mm256_loadu_pd(b + (size_t)k * C + c0), t0);
+      _mm256_storeu_pd(accr + c0, _mm256_add_pd(_mm256_loadu_pd(accr + c0), t0));
+    }
+    for (; c0 < C; ++c0) {
+      double t = 0.0;
+      for (int k = 0; k < K; ++k) t = fma_(ar[(size_t)k * aks], b[(size_t)k * C + c0], t);
+      accr[c0] += t;
+    }
+  }
+}
 // acc (r x c) += a (r x k) * b (k x c)
 static void gemm_acc(int R, int K, int C, const double* a, const double* b, double* acc) {
-  for (int r = 0; r < R; ++r)
-    for (int c = 0; c < C; ++c) {
-      double t = 0.0;
-      for (int k = 0; k < K; ++k) t = fma_(a[r * K + k], b[k * C + c], t);
-      acc[r * C + c] += t;
-    }
+  gemm_rows(R, K, C, a, K, 1, b, acc);
 }
 // acc (r x c) += a^T * b with a (k x r), b (k x c)
 static void gemm_tn_acc(int R, int K, int C, const double* a, const double* b, double* acc) {
-  for (int r = 0; r < R; ++r)
-    for (int c = 0; c < C; ++c) {
-      double t = 0.0;
-      for (int k = 0; k < K; ++k) t = fma_(a[k * R + r], b[k * C + c], t);
-      acc[r * C + c] += t;
-    }
+  gemm_rows(R, K, C, a, 1, R, b, acc);
 }
-// acc (r x c) += a * b^T with a (r x k), b (c x k)
+// acc (r x c) += a * b^T with a (r x k), b (c x k): b is transposed into a
+// (k x c) scratch first, the chains are the same
 static void gemm_nt_acc(int R, int K, int C, const double* a, const double* b, double* acc) {
-  for (int r = 0; r < R; ++r)
-    for (int c = 0; c < C; ++c) {
-      double t = 0.0;
-      for (int k = 0; k < K; ++k) t = fma_(a[r * K + k], b[c * K + k], t);
-      acc[r * C + c] += t;
-    }
+  double bt_small[64 * 64];
+  std::vector<double> bt_big;
+  double* bt = bt_small;
+  if ((size_t)K * C > sizeof(bt_small) / sizeof(double)) {
+    bt_big.resize((size_t)K * C);
+    bt = bt_big.data();
+  }
+  for (int c = 0; c < C; ++c)
+    for (int k = 0; k < K; ++k) bt[(size_t)k * C + c] = b[(size_t)c * K + k];
+  gemm_rows(R, K, C, a, K, 1, bt, acc);
 }
 
 // multiply: kernels.cpp:66-75 (per output block, ascending k)
@@ -958,33 +993,143 @@ static double poly_eval(int kind, int degree, double alpha, double beta, double 
 
 // ----------------------------------------------------------------------------
 // multilevel.cpp
+// C = P^T (A P) exactly as transpose_multiply(p, multiply(a, p)), without holding
+// the whole A P (C4's 3-D fine level: ~105 GB).  A P is formed for a range of
+// fine rows at a time; every coarse block C_kj is created at its first term and
+// accumulates its terms P_ik^T (AP)_ij in ascending i across the ranges, the same
+// sequence of `acc += tmp` as the one-shot product.
+static Mat galerkin_product(const Mat& a, const Mat& p) {
+  require(a.cl == p.rl && a.rl == p.rl, "galerkin_coarsen: layouts do not match");
+  const int nf = a.nbr(), nc = p.nbc();
+  const auto& pc = p.colindex();
+  std::vector<RowMap> crow(nc);
+  std::vector<size_t> cursor(nc, 0);
+  const size_t chunk_bytes = size_t(2) << 30;
+  int i0 = 0;
+  while (i0 < nf) {
+    // fine rows [i0, i1): estimate A P bytes from the row's A-by-P block counts
+    int i1 = i0;
+    size_t bytes = 0;
+    // (block products per row / 8 approximates the distinct blocks of an A P row;
+    // at least 4096 rows per range keep every thread busy)
+    while (i1 < nf && (i1 - i0 < 4096 || bytes < chunk_bytes)) {
+      size_t blocks = 0;
+      for (int k : a.cols[i1]) blocks += p.cols[k].size();
+      bytes += blocks / 8 * (size_t)a.rl.sz[i1] * 8 * 24;
+      ++i1;
+    }
+    std::vector<std::vector<int>> apc(i1 - i0);
+    std::vector<std::vector<size_t>> apo(i1 - i0);
+    std::vector<std::vector<double>> apv(i1 - i0);
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int i = i0; i < i1; ++i) {  // multiply(a, p) row i (kernels.cpp:66-75)
+      RowMap row;
+      const int mi = a.rl.sz[i];
+      for (size_t q = 0; q < a.cols[i].size(); ++q) {
+        const int k = a.cols[i][q];
+        const int mk = a.cl.sz[k];
+        for (size_t s = 0; s < p.cols[k].size(); ++s) {
+          const int j = p.cols[k][s];
+          auto& acc = row[j];
+          if (acc.empty()) acc.assign((size_t)mi * p.cl.sz[j], 0.0);
+          gemm_acc(mi, mk, p.cl.sz[j], a.blk(i, (int)q), p.blk(k, (int)s), acc.data());
+        }
+      }
+      auto& cc = apc[i - i0];
+      auto& oo = apo[i - i0];
+      auto& vv = apv[i - i0];
+      for (auto& [j, b] : row) {
+        cc.push_back(j);
+        oo.push_back(vv.size());
+        vv.insert(vv.end(), b.begin(), b.end());
+      }
+    }
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int k = 0; k < nc; ++k) {  // transpose_multiply(p, ap) row k (kernels.cpp:77-86)
+      const int mk = p.cl.sz[k];
+      auto& row = crow[k];
+      size_t t = cursor[k];
+      for (; t < pc[k].size() && pc[k][t].first < i1; ++t) {
+        const int i = pc[k][t].first;
+        const double* pik = pc[k][t].second;
+        const int mi = p.rl.sz[i];
+        const auto& cc = apc[i - i0];
+        for (size_t q = 0; q < cc.size(); ++q) {
+          const int j = cc[q];
+          const int mj = p.cl.sz[j];
+          auto& acc = row[j];
+          if (acc.empty()) acc.assign((size_t)mk * mj, 0.0);
+          gemm_tn_acc(mk, mi, mj, pik, apv[i - i0].data() + apo[i - i0][q], acc.data());
+        }
+      }
+      cursor[k] = t;
+    }
+    i0 = i1;
+  }
+  Mat c(p.cl, p.cl, false);
+  for (int k = 0; k < nc; ++k) {
+    c.set_row(k, crow[k]);
+    RowMap().swap(crow[k]);
+  }
+  c.tidx_ok = false;
+  return c;
+}
+
 // galerkin_coarsen: multilevel.cpp:11-28
 static Mat galerkin(const Mat& a, const Mat& p) {
   if (!(a.square() && a.rl == p.rl))
     throw std::invalid_argument("galerkin_coarsen: layouts do not match");
-  const Mat c = transpose_multiply(p, multiply(a, p));
+  const Mat c = galerkin_product(a, p);
   const int n = c.nbr();
-  std::vector<RowMap> rows(n);
+  // The reference visits every stored (i, j), j <= i, and inserts
+  // S = (C_ij + C_ji^T) / 2 (or C_ij / 2 without a mirror block) at (i, j) and S^T
+  // at (j, i) (insert_symmetric).  No two visits write the same block, so row i of
+  // the result is assembled independently: its lower blocks from C's row i, its
+  // upper blocks (i, j > i) as the transposes of the S made for C's (j, i).
+  const auto& ccol = c.colindex();
+  Mat out(c.rl, c.cl, true);
+  auto sym_block = [&](int i, int q, std::vector<double>& s) {  // S for stored (i, cols[i][q])
+    const int j = c.cols[i][q];
+    const int mi = c.rl.sz[i], mj = c.cl.sz[j];
+    const double* blk = c.blk(i, q);
+    s.assign(blk, blk + (size_t)mi * mj);
+    const int pj = c.find(j, i);
+    if (pj >= 0) {
+      const double* bt = c.blk(j, pj);  // mj x mi
+      for (int r = 0; r < mi; ++r)
+        for (int t = 0; t < mj; ++t) s[(size_t)r * mj + t] = 0.5 * (blk[r * mj + t] + bt[t * mi + r]);
+    } else {
+      for (auto& v : s) v *= 0.5;
+    }
+  };
+#pragma omp parallel for schedule(dynamic, 16)
   for (int i = 0; i < n; ++i) {
-    const int mi = c.rl.sz[i];
+    RowMap row;
+    std::vector<double> s;
     for (size_t q = 0; q < c.cols[i].size(); ++q) {
-      const int j = c.cols[i][q];
-      if (j > i) continue;
-      const int mj = c.cl.sz[j];
-      const double* blk = c.blk(i, (int)q);
-      std::vector<double> sym(blk, blk + (size_t)mi * mj);
-      const int pj = c.find(j, i);
-      if (pj >= 0) {
-        const double* bt = c.blk(j, pj);  // mj x mi
-        for (int r = 0; r < mi; ++r)
-          for (int s = 0; s < mj; ++s) sym[(size_t)r * mj + s] = 0.5 * (blk[r * mj + s] + bt[s * mi + r]);
-      } else {
-        for (auto& v : sym) v *= 0.5;
-      }
-      insert_sym(rows, c.rl, i, j, sym);
+      if (c.cols[i][q] > i) continue;
+      sym_block(i, (int)q, s);
+      row[c.cols[i][q]] = s;
+    }
+    for (const auto& [j, ptr] : ccol[i]) {  // stored (j, i) with j > i
+      if (j <= i) continue;
+      const int q = c.find(j, i);
+      sym_block(j, q, s);
+      std::vector<double> t(s.size());
+      transpose_block(c.rl.sz[j], c.cl.sz[i], s.data(), t.data());
+      row[j] = std::move(t);
+    }
+    out.cols[i].clear();
+    out.boff[i].clear();
+    out.vals[i].clear();
+    for (const auto& [j, b] : row) {
+      out.cols[i].push_back(j);
+      out.boff[i].push_back(out.vals[i].size());
+      out.vals[i].insert(out.vals[i].end(), b.begin(), b.end());
     }
   }
-  return from_rowmaps(c.rl, c.cl, true, rows);
+  out.tidx_ok = false;
+  return out;
 }
 
 struct Level {
