@@ -1,5 +1,9 @@
 // generator.cpp -- synthetic BASELINE problems (BASELINE.json configs).
 //
+// Built as its own library, bmggen/libbmggen.so (C ABI in include/bmg_gen.h),
+// shared by both benchmark arms and the tests: it is input data, not the
+// solver, so neither the product (libbmgcuda.so) nor the CPU oracle contains it.
+//
 // Input data only (the reference's PUM discretiser is out of scope):
 //   A_ij = (S_p)_ij C            i != j
 //   A_ii = (S_p)_ii C + reg D_i
@@ -16,7 +20,10 @@
 #include <stdexcept>
 #include <vector>
 
-#include "bmg_internal.h"
+#include <exception>
+#include <string>
+
+#include "../include/bmg_gen.h"
 
 namespace bmg {
 namespace gen {
@@ -268,3 +275,40 @@ void gen_normal(uint64_t seed, uint64_t tag, int64_t n, double* out) {
 }
 
 }  // namespace bmg
+
+// ---- C ABI (include/bmg_gen.h) ------------------------------------------
+namespace {
+thread_local std::string g_gen_err;
+template <class F>
+int gen_guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_gen_err = e.what();
+    return 1;  // BMG_EINVAL
+  } catch (const std::exception& e) {
+    g_gen_err = e.what();
+    return 4;  // BMG_ERUNTIME
+  }
+}
+}  // namespace
+
+extern "C" {
+const char* bmg_gen_last_error(void) { return g_gen_err.c_str(); }
+int bmg_gen_stencil(int dim, int n, int power, int m, uint64_t seed, double reg, int64_t row_lo, int64_t row_hi,
+                    int64_t* nnzb, int64_t* row_ptr, int32_t* col_idx, double* vals) {
+  return gen_guard([&] {
+    *nnzb = bmg::gen_stencil(dim, n, power, m, seed, reg, row_lo, row_hi, row_ptr, col_idx, vals);
+  });
+}
+int bmg_gen_prolongation(int dim, int n_fine, int m, uint64_t seed, int level, int64_t row_lo, int64_t row_hi,
+                         int64_t* nnzb, int64_t* row_ptr, int32_t* col_idx, double* vals) {
+  return gen_guard([&] {
+    *nnzb = bmg::gen_prolongation(dim, n_fine, m, seed, level, row_lo, row_hi, row_ptr, col_idx, vals);
+  });
+}
+int bmg_gen_normal(uint64_t seed, uint64_t tag, int64_t n, double* out) {
+  return gen_guard([&] { bmg::gen_normal(seed, tag, n, out); });
+}
+}  // extern "C"

@@ -4,6 +4,15 @@
 // the same function names, argument meaning and exception types, so a caller of
 // the reference's spmv / nested_build / cheb_fourth_apply / lanczos_lambda_max /
 // setup / v_cycle can switch by replacing the matrix type with a device handle.
+//
+// Everything lives in namespace bmg::cuda, so this header can be included in
+// the same translation unit as the reference's own headers (namespace bmg):
+// bmg::BlockLayout / bmg::Hierarchy stay the reference's, bmg::cuda::* are the
+// device counterparts (tests/cpp/ref_mock + tests/cpp/adapter_compile_test.cpp
+// compile both side by side).  The reference's exception types are thrown
+// (std::invalid_argument, std::out_of_range, std::runtime_error); the two the
+// reference defines itself (NotPositiveDefinite, IoError) have device
+// counterparts here with the same members (pivot, line).
 //   BlockLayout              block_layout.hpp:8-28
 //   NotPositiveDefinite      small_cholesky.hpp:10-13
 //   spmv / spmv_transpose    kernels.hpp:15,19
@@ -17,6 +26,7 @@
 #pragma once
 
 #include <cstdint>
+#include <initializer_list>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -26,6 +36,7 @@
 #include "../bmg_cuda.h"
 
 namespace bmg {
+namespace cuda {
 
 struct NotPositiveDefinite : std::runtime_error {
   int pivot;
@@ -105,6 +116,8 @@ struct HostBsr {
   bool symmetric = false;
 };
 
+class DeviceVector;
+
 class DeviceMatrix {
  public:
   DeviceMatrix(Context& ctx, const HostBsr& h) : rows_(h.rows), cols_(h.cols) {
@@ -124,6 +137,8 @@ class DeviceMatrix {
   const bmg_bsr* get() const { return h_; }
   const BlockLayout& row_layout() const { return rows_; }
   const BlockLayout& col_layout() const { return cols_; }
+  // the operator callable of the reference's smoothers: a(x, y) is y = A x
+  inline void operator()(const DeviceVector& x, DeviceVector& y) const;
 
  private:
   friend DeviceMatrix galerkin_coarsen(const DeviceMatrix&, const DeviceMatrix&);
@@ -132,14 +147,42 @@ class DeviceMatrix {
   bool owned_ = true;
 };
 
+// A device FP64 vector with the reference's Vector value semantics
+// (types.hpp:10): copies are device copies, moves transfer the buffer.
 class DeviceVector {
  public:
   DeviceVector(Context& ctx, int64_t n) { check(bmg_vec_create(ctx.get(), n, &h_)); }
   DeviceVector(Context& ctx, const std::vector<double>& v) : DeviceVector(ctx, (int64_t)v.size()) { upload(v); }
+  // a zero vector of o's length on o's context (Vector r(x.size()))
+  static DeviceVector zeros_like(const DeviceVector& o) {
+    bmg_vec* h = nullptr;
+    check(bmg_vec_create_like(o.h_, &h));
+    return DeviceVector(h);
+  }
   ~DeviceVector() {
     if (h_) bmg_vec_destroy(h_);
   }
-  DeviceVector(const DeviceVector&) = delete;
+  DeviceVector(const DeviceVector& o) : h_(nullptr) {
+    check(bmg_vec_create_like(o.h_, &h_));
+    check(bmg_vec_copy(o.h_, h_));
+  }
+  DeviceVector(DeviceVector&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
+  DeviceVector& operator=(const DeviceVector& o) {
+    if (this != &o) {
+      if (size() != o.size()) {
+        DeviceVector t(o);
+        std::swap(h_, t.h_);
+      } else {
+        check(bmg_vec_copy(o.h_, h_));
+      }
+    }
+    return *this;
+  }
+  DeviceVector& operator=(DeviceVector&& o) noexcept {
+    std::swap(h_, o.h_);
+    return *this;
+  }
+  int64_t size() const { return h_ ? bmg_vec_size(h_) : 0; }
   void upload(const std::vector<double>& v) { check(bmg_vec_upload(h_, v.data())); }
   std::vector<double> download() const {
     std::vector<double> out((size_t)bmg_vec_size(h_));
@@ -149,8 +192,15 @@ class DeviceVector {
   bmg_vec* get() const { return h_; }
 
  private:
+  explicit DeviceVector(bmg_vec* h) : h_(h) {}
   bmg_vec* h_ = nullptr;
 };
+
+// z = alpha x + beta y with separately rounded products (the reference's Eigen
+// vector expressions, see bmg_vec_axpby); z may alias x or y
+inline void axpby(double alpha, const DeviceVector& x, double beta, const DeviceVector& y, DeviceVector& z) {
+  check(bmg_vec_axpby(alpha, x.get(), beta, y.get(), z.get()));
+}
 
 // y = A x (kernels.hpp:15); y = A^T x (kernels.hpp:19)
 inline void spmv(const DeviceMatrix& a, const DeviceVector& x, DeviceVector& y) {
@@ -162,6 +212,8 @@ inline void spmv_batch(const DeviceMatrix& a, int nrhs, const DeviceVector& x, D
 inline void spmv_transpose(const DeviceMatrix& a, const DeviceVector& x, DeviceVector& y) {
   check(bmg_spmv_t(a.get(), x.get(), y.get()));
 }
+
+inline void DeviceMatrix::operator()(const DeviceVector& x, DeviceVector& y) const { spmv(*this, x, y); }
 
 // P^T A P, symmetrised (multilevel.hpp:50)
 inline DeviceMatrix galerkin_coarsen(const DeviceMatrix& a, const DeviceMatrix& p) {
@@ -181,7 +233,21 @@ class NestedFsai {
   }
   NestedFsai(NestedFsai&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
   NestedFsai(const NestedFsai&) = delete;
+  // Vector apply(const Vector& r) const -- M r (fsai.hpp:62)
+  DeviceVector apply(const DeviceVector& r) const {
+    DeviceVector z = DeviceVector::zeros_like(r);
+    apply(r, z);
+    return z;
+  }
+  // Vector apply_transformed(a, x) const -- L^-1 F A F^T L^-T x (fsai.hpp:65)
+  DeviceVector apply_transformed(const DeviceMatrix& a, const DeviceVector& x) const {
+    DeviceVector y = DeviceVector::zeros_like(x);
+    check(bmg_fsai_apply_transformed(h_, a.get(), x.get(), y.get()));
+    return y;
+  }
   void apply(const DeviceVector& r, DeviceVector& z) const { check(bmg_fsai_apply(h_, r.get(), z.get())); }
+  // the preconditioner callable of the reference's smoothers: m(r, z) is z = M r
+  void operator()(const DeviceVector& r, DeviceVector& z) const { apply(r, z); }
   const bmg_fsai* get() const { return h_; }
 
  private:
@@ -199,10 +265,87 @@ inline NestedFsai build_fsai_static(const DeviceMatrix& a) {  // build_fsai(A, L
   return NestedFsai(out);
 }
 
-// x <- cheb_fourth_apply(A, M, b, x, beta, k) (chebyshev.hpp:48-69), in place
-inline void cheb_fourth_apply(const DeviceMatrix& a, const NestedFsai& m, const DeviceVector& b, DeviceVector& x,
-                              double beta, int k) {
+inline double fourth_kind_mu(int n) { return (2.0 * n + 1.0) / (2.0 * n + 3.0); }  // chebyshev.hpp:42
+
+// Vector cheb_fourth_apply(a, m, b, Vector x, beta, k) (chebyshev.hpp:48-69)
+// for any operator callables a(x, t), m(r, z) on device vectors, step for step
+// as the reference (separately rounded vector updates, closed-form mu).
+template <class OpA, class OpM>
+DeviceVector cheb_fourth_apply(const OpA& a, const OpM& m, const DeviceVector& b, DeviceVector x, double beta,
+                               int k) {
+  if (!(beta > 0.0)) throw std::invalid_argument("cheb_fourth_apply: beta must be positive");
+  if (k < 1) throw std::invalid_argument("cheb_fourth_apply: degree must be >= 1");
+  const double d = 4.0 / beta;
+  DeviceVector r = DeviceVector::zeros_like(x), p = DeviceVector::zeros_like(x), t = DeviceVector::zeros_like(x);
+  a(x, t);
+  axpby(1.0, b, -1.0, t, r);  // r = b - t
+  m(r, p);
+  double mu = fourth_kind_mu(0);
+  axpby(1.0, x, d * mu, p, x);  // x += d * mu * p
+  for (int i = 2; i <= k; ++i) {
+    a(x, t);
+    axpby(1.0, b, -1.0, t, r);
+    m(r, t);
+    axpby(mu * mu, p, 1.0, t, p);  // p = mu * mu * p + t
+    mu = fourth_kind_mu(i - 1);
+    axpby(1.0, x, d * mu, p, x);
+  }
+  return x;
+}
+// The device operators themselves: the same recurrence as fused streaming
+// passes (residual, G, G^T + update epilogue; bmg_cheb4_apply), bitwise equal
+// to the generic template above on the same operands.
+inline DeviceVector cheb_fourth_apply(const DeviceMatrix& a, const NestedFsai& m, const DeviceVector& b,
+                                      DeviceVector x, double beta, int k) {
   check(bmg_cheb4_apply(a.get(), m.get(), b.get(), x.get(), beta, k));
+  return x;
+}
+// in-place form (no copy of x)
+inline void cheb_fourth_apply_inplace(const DeviceMatrix& a, const NestedFsai& m, const DeviceVector& b,
+                                      DeviceVector& x, double beta, int k) {
+  check(bmg_cheb4_apply(a.get(), m.get(), b.get(), x.get(), beta, k));
+}
+
+// cheb_first_apply (chebyshev.hpp:74-98) and richardson_apply (:101-115) for
+// generic callables, step for step as the reference
+template <class OpA, class OpM>
+DeviceVector cheb_first_apply(const OpA& a, const OpM& m, const DeviceVector& b, DeviceVector x, double alpha,
+                              double beta, int k) {
+  if (!(alpha > 0.0) || !(alpha < beta))
+    throw std::invalid_argument("cheb_first_apply: interval must satisfy 0 < alpha < beta");
+  if (k < 1) throw std::invalid_argument("cheb_first_apply: degree must be >= 1");
+  const double c = 0.5 * (alpha + beta);
+  const double d = 0.5 * (beta - alpha);
+  DeviceVector r = DeviceVector::zeros_like(x), p = DeviceVector::zeros_like(x), t = DeviceVector::zeros_like(x);
+  a(x, t);
+  axpby(1.0, b, -1.0, t, r);
+  m(r, p);
+  double omega = 1.0 / c;
+  double psi = 0.5 * (d * omega) * (d * omega);
+  axpby(1.0, x, omega, p, x);
+  for (int i = 2; i <= k; ++i) {
+    a(x, t);
+    axpby(1.0, b, -1.0, t, r);
+    m(r, t);
+    axpby(1.0, t, psi, p, p);  // p = t + psi * p
+    omega = 1.0 / (c - psi / omega);
+    psi = 0.25 * (d * omega) * (d * omega);
+    axpby(1.0, x, omega, p, x);
+  }
+  return x;
+}
+template <class OpA, class OpM>
+DeviceVector richardson_apply(const OpA& a, const OpM& m, const DeviceVector& b, DeviceVector x, double omega,
+                              int k) {
+  if (k < 1) throw std::invalid_argument("richardson_apply: step count must be >= 1");
+  DeviceVector r = DeviceVector::zeros_like(x), t = DeviceVector::zeros_like(x);
+  for (int i = 0; i < k; ++i) {
+    a(x, t);
+    axpby(1.0, b, -1.0, t, r);
+    m(r, t);
+    axpby(1.0, x, omega, t, x);
+  }
+  return x;
 }
 
 struct SmootherSpec {  // chebyshev.hpp:12-18
@@ -210,9 +353,25 @@ struct SmootherSpec {  // chebyshev.hpp:12-18
   int degree = 1;
   double alpha = 0.0, beta = 1.0, omega = 1.0;
 };
-// x <- apply_smoother(spec, degree, A, M, b, x) (chebyshev.hpp:117-129), in place
-inline void apply_smoother(const SmootherSpec& s, int degree, const DeviceMatrix& a, const NestedFsai& m,
-                           const DeviceVector& b, DeviceVector& x) {
+// Vector apply_smoother(spec, degree, a, m, b, Vector x) (chebyshev.hpp:117-129)
+template <class OpA, class OpM>
+DeviceVector apply_smoother(const SmootherSpec& s, int degree, const OpA& a, const OpM& m, const DeviceVector& b,
+                            DeviceVector x) {
+  switch (s.kind) {
+    case SmootherKind::Richardson: return richardson_apply(a, m, b, std::move(x), s.omega, degree);
+    case SmootherKind::ChebFirst: return cheb_first_apply(a, m, b, std::move(x), s.alpha, s.beta, degree);
+    case SmootherKind::ChebFourth: return cheb_fourth_apply(a, m, b, std::move(x), s.beta, degree);
+  }
+  throw std::logic_error("apply_smoother: unknown kind");
+}
+// the device operators: one fused-epilogue pass sequence (bmg_smoother_apply)
+inline DeviceVector apply_smoother(const SmootherSpec& s, int degree, const DeviceMatrix& a, const NestedFsai& m,
+                                   const DeviceVector& b, DeviceVector x) {
+  check(bmg_smoother_apply(a.get(), m.get(), (int)s.kind, s.alpha, s.beta, s.omega, degree, b.get(), x.get()));
+  return x;
+}
+inline void apply_smoother_inplace(const SmootherSpec& s, int degree, const DeviceMatrix& a, const NestedFsai& m,
+                                   const DeviceVector& b, DeviceVector& x) {
   check(bmg_smoother_apply(a.get(), m.get(), (int)s.kind, s.alpha, s.beta, s.omega, degree, b.get(), x.get()));
 }
 
@@ -292,6 +451,18 @@ inline Hierarchy setup(const DeviceMatrix& a_finest, const std::vector<const Dev
   return Hierarchy(h);
 }
 
+inline Hierarchy setup(const DeviceMatrix& a_finest, std::initializer_list<const DeviceMatrix*> transfers,
+                       const SetupParams& p) {
+  return setup(a_finest, std::vector<const DeviceMatrix*>(transfers), p);
+}
+// the reference's signature, transfers by value (multilevel.hpp:59-60); the
+// hierarchy keeps what it needs alive, so the caller's matrices may go away
+inline Hierarchy setup(const DeviceMatrix& a_finest, std::vector<DeviceMatrix> transfers, const SetupParams& p) {
+  std::vector<const DeviceMatrix*> t;
+  for (auto& m : transfers) t.push_back(&m);
+  return setup(a_finest, t, p);
+}
+
 // v_cycle on the finest level (multilevel.hpp:65); x is updated in place
 inline void v_cycle(const Hierarchy& h, const CycleSpec& spec, const DeviceVector& b, DeviceVector& x) {
   check(bmg_vcycle(h.get(), spec.k_pre, spec.k_post, b.get(), x.get()));
@@ -363,4 +534,5 @@ inline RateReport measure_rates(const Hierarchy& h, const DeviceMatrix& mass, co
   return r;
 }
 
+}  // namespace cuda
 }  // namespace bmg

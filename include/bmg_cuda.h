@@ -129,6 +129,15 @@ int bmg_vec_destroy(bmg_vec* v);
 int bmg_vec_upload(bmg_vec* v, const double* host);
 int bmg_vec_download(const bmg_vec* v, double* host);
 int bmg_vec_fill(bmg_vec* v, double value);
+/* a zero vector of v's length on v's context */
+int bmg_vec_create_like(const bmg_vec* v, bmg_vec** out);
+/* dst = src (device to device, same context and length) */
+int bmg_vec_copy(const bmg_vec* src, bmg_vec* dst);
+/* z = alpha x + beta y, products and sum rounded separately (no fma): the
+ * reference's vector expressions r = b - t, p = mu*mu*p + t, x += d*mu*p
+ * (chebyshev.hpp:55-66) for the generic-operator cheb_fourth_apply of the C++
+ * facade; z may alias x or y */
+int bmg_vec_axpby(double alpha, const bmg_vec* x, double beta, const bmg_vec* y, bmg_vec* z);
 void* bmg_vec_device_ptr(bmg_vec* v);
 int64_t bmg_vec_size(const bmg_vec* v);
 
@@ -289,19 +298,7 @@ int bmg_time_residual(const bmg_bsr* a, const bmg_vec* b, const bmg_vec* x, bmg_
 /* symmetric tridiagonal eigenvalues (ascending), the host step of Lanczos */
 int bmg_tridiag_eigs(int n, const double* d, const double* e, double* out);
 
-/* ---- synthetic BASELINE problems (host generator) -------- */
-/* S_p = L_D^p block stencil on an n^dim patch grid (dim 2 or 3), blocks
- * A_ij = S_ij C (+ reg D_i on the diagonal); block rows [row_lo, row_hi)
- * (row_hi < 0: all) with global column indices.  Two calls: arrays NULL to
- * query nnzb, then filled. */
-int bmg_gen_stencil(int dim, int n, int power, int m, uint64_t seed, double reg, int64_t row_lo,
-                    int64_t row_hi, int64_t* nnzb, int64_t* row_ptr, int32_t* col_idx, double* vals);
-/* prolongation from an (n/2)^dim coarse grid to the n^dim fine grid, rows as above */
-int bmg_gen_prolongation(int dim, int n_fine, int m, uint64_t seed, int level, int64_t row_lo,
-                         int64_t row_hi, int64_t* nnzb, int64_t* row_ptr, int32_t* col_idx,
-                         double* vals);
-/* N(0,1) vector (Box-Muller on the counter RNG), stream `tag` */
-int bmg_gen_normal(uint64_t seed, uint64_t tag, int64_t n, double* out);
+/* the synthetic BASELINE input generator is a separate library: include/bmg_gen.h */
 
 #ifdef __cplusplus
 }

@@ -105,6 +105,17 @@ __global__ void copy_kernel(double* __restrict__ d, const double* __restrict__ s
     d[i] = s[i];
 }
 
+// z = alpha x + beta y, each product and the sum rounded separately (no fma):
+// the reference's Eigen vector expressions r = b - t, p = mu*mu*p + t and
+// x += d*mu*p (chebyshev.hpp:55-66, built with -ffp-contract=off in the oracle)
+// are this with (alpha, beta) = (1, -1), (mu*mu, 1), (1, d*mu) -- exact scalings
+// by +-1 leave the other operand unchanged.
+__global__ void axpby_kernel(double* z, double alpha, const double* x, double beta,
+                             const double* y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    z[i] = __dadd_rn(__dmul_rn(alpha, x[i]), __dmul_rn(beta, y[i]));
+}
+
 constexpr int kDotBlocks = 592;
 constexpr int kDotThreads = 256;
 
@@ -183,6 +194,13 @@ void fill(Ctx* ctx, double* p, int64_t n, double v) {
 void copy(Ctx* ctx, double* dst, const double* src, int64_t n) {
   if (n <= 0 || dst == src) return;
   kern::copy_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(dst, src, n);
+  ctx->count();
+  BMG_CUDA(cudaGetLastError());
+}
+
+void axpby(Ctx* ctx, double* z, double alpha, const double* x, double beta, const double* y, int64_t n) {
+  if (n <= 0) return;
+  kern::axpby_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(z, alpha, x, beta, y, n);
   ctx->count();
   BMG_CUDA(cudaGetLastError());
 }
@@ -1132,6 +1150,38 @@ int bmg_vec_fill(bmg_vec* vh, double value) {
     fill(v->ctx, v->d.p, v->n, value);
   });
 }
+int bmg_vec_create_like(const bmg_vec* like, bmg_vec** out) {
+  return guard([&] {
+    const Vec* v = reinterpret_cast<const Vec*>(like);
+    if (!v) fail(BMG_EINVAL, "bmg_vec_create_like: null vector");
+    v->ctx->activate();
+    auto w = std::make_unique<Vec>();
+    w->ctx = v->ctx;
+    w->n = v->n;
+    w->d.alloc(std::max<int64_t>(v->n, 1));
+    BMG_CUDA(cudaMemsetAsync(w->d.p, 0, w->d.bytes(), v->ctx->stream));
+    *out = reinterpret_cast<bmg_vec*>(w.release());
+  });
+}
+int bmg_vec_copy(const bmg_vec* srch, bmg_vec* dsth) {
+  return guard([&] {
+    const Vec* s = reinterpret_cast<const Vec*>(srch);
+    Vec* d = reinterpret_cast<Vec*>(dsth);
+    if (s->n != d->n) fail(BMG_EINVAL, "bmg_vec_copy: length mismatch");
+    if (s->ctx != d->ctx) fail(BMG_EINVAL, "bmg_vec_copy: vectors belong to different contexts");
+    copy(d->ctx, d->d.p, s->d.p, s->n);
+  });
+}
+int bmg_vec_axpby(double alpha, const bmg_vec* xh, double beta, const bmg_vec* yh, bmg_vec* zh) {
+  return guard([&] {
+    const Vec* x = reinterpret_cast<const Vec*>(xh);
+    const Vec* y = reinterpret_cast<const Vec*>(yh);
+    Vec* z = reinterpret_cast<Vec*>(zh);
+    if (x->n != z->n || y->n != z->n) fail(BMG_EINVAL, "bmg_vec_axpby: length mismatch");
+    if (x->ctx != z->ctx || y->ctx != z->ctx) fail(BMG_EINVAL, "bmg_vec_axpby: vectors belong to different contexts");
+    axpby(z->ctx, z->d.p, alpha, x->d.p, beta, y->d.p, z->n);
+  });
+}
 void* bmg_vec_device_ptr(bmg_vec* v) { return reinterpret_cast<Vec*>(v)->d.p; }
 int64_t bmg_vec_size(const bmg_vec* v) { return reinterpret_cast<const Vec*>(v)->n; }
 
@@ -1215,20 +1265,6 @@ int bmg_time_residual(const bmg_bsr* ah, const bmg_vec* bh, const bmg_vec* xh, b
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
   });
-}
-
-int bmg_gen_stencil(int dim, int n, int power, int m, uint64_t seed, double reg, int64_t row_lo, int64_t row_hi,
-                    int64_t* nnzb, int64_t* row_ptr, int32_t* col_idx, double* vals) {
-  return guard([&] { *nnzb = gen_stencil(dim, n, power, m, seed, reg, row_lo, row_hi, row_ptr, col_idx, vals); });
-}
-int bmg_gen_prolongation(int dim, int n_fine, int m, uint64_t seed, int level, int64_t row_lo, int64_t row_hi,
-                         int64_t* nnzb, int64_t* row_ptr, int32_t* col_idx, double* vals) {
-  return guard([&] {
-    *nnzb = gen_prolongation(dim, n_fine, m, seed, level, row_lo, row_hi, row_ptr, col_idx, vals);
-  });
-}
-int bmg_gen_normal(uint64_t seed, uint64_t tag, int64_t n, double* out) {
-  return guard([&] { gen_normal(seed, tag, n, out); });
 }
 
 }  // extern "C"

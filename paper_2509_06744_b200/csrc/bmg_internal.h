@@ -289,6 +289,7 @@ double dot(Ctx* ctx, const double* a, const double* b, int64_t n);
 void rng_symmetric(Ctx* ctx, double* v, int64_t n, uint64_t seed);
 void fill(Ctx* ctx, double* p, int64_t n, double v);
 void copy(Ctx* ctx, double* dst, const double* src, int64_t n);
+void axpby(Ctx* ctx, double* z, double alpha, const double* x, double beta, const double* y, int64_t n);
 void fsai_apply(const Fsai& m, const double* r, double* z, double* tmp1, double* tmp2);
 std::unique_ptr<Fsai> fsai_build(const Bsr& a, int kind, int t_max, double tau, int nest);
 std::unique_ptr<Fsai> fsai_build_pattern(const Bsr& a, const int64_t* ptr, const int32_t* col);
@@ -307,11 +308,5 @@ void row_window(const int64_t* row_ptr, const int32_t* col, int lo, int hi, int 
 // host helpers
 std::vector<double> tridiag_eigenvalues(std::vector<double> d, std::vector<double> e);
 
-// generator (generator.cpp)
-int64_t gen_stencil(int dim, int n, int power, int m, uint64_t seed, double reg, int64_t row_lo,
-                    int64_t row_hi, int64_t* row_ptr, int32_t* col_idx, double* vals);
-int64_t gen_prolongation(int dim, int n_fine, int m, uint64_t seed, int level, int64_t row_lo, int64_t row_hi,
-                         int64_t* row_ptr, int32_t* col_idx, double* vals);
-void gen_normal(uint64_t seed, uint64_t tag, int64_t n, double* out);
 
 }  // namespace bmg

@@ -110,6 +110,9 @@ _SIGS = {
     "bmg_vec_upload": (_I, [_P, _PD]),
     "bmg_vec_download": (_I, [_P, _PD]),
     "bmg_vec_fill": (_I, [_P, _D]),
+    "bmg_vec_create_like": (_I, [_P, _PP]),
+    "bmg_vec_copy": (_I, [_P, _P]),
+    "bmg_vec_axpby": (_I, [_D, _P, _D, _P, _P]),
     "bmg_vec_device_ptr": (_P, [_P]),
     "bmg_vec_size": (_I64, [_P]),
     "bmg_spmv": (_I, [_P, _P, _P]),
@@ -167,9 +170,6 @@ _SIGS = {
     "bmg_io_write_matrix": (_I, [_P, C.c_char_p]),
     "bmg_io_read_vector": (_I, [_P, C.c_char_p, _PP]),
     "bmg_io_write_vector": (_I, [_P, C.c_char_p]),
-    "bmg_gen_stencil": (_I, [_I, _I, _I, _I, _U64, _D, _I64, _I64, _PI64, _PI64, _PI32, _PD]),
-    "bmg_gen_prolongation": (_I, [_I, _I, _I, _U64, _I, _I64, _I64, _PI64, _PI64, _PI32, _PD]),
-    "bmg_gen_normal": (_I, [_U64, _U64, _I64, _PD]),
 }
 
 _lib = None

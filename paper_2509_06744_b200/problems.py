@@ -1,7 +1,9 @@
 """Synthetic BASELINE problems (BASELINE.json configs).
 
-The generator itself is host C++ inside libbmgcuda.so (csrc/generator.cpp); this
-module only sizes the arrays and names the configs.  Inputs are data, not the
+The generator itself is host C++ in its own library, bmggen/libbmggen.so
+(bmggen/generator.cpp, include/bmg_gen.h) -- input data shared by the product
+tests, both benchmark arms and the oracle fixtures; this module only sizes the
+arrays and names the configs, and it loads neither libbmgcuda.so nor the oracle.  Inputs are data, not the
 solver path: the reference's PUM discretiser is out of scope.
 The reference's FD test problem (experiments.cpp:104-195) is restated at the end.
 """
@@ -12,8 +14,16 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+import os
+import sys
+
 from .api import HostBsr
-from .native import check, dptr, i32ptr, i64ptr, lib
+from .native import dptr, i32ptr, i64ptr
+
+_ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if _ROOT not in sys.path:
+    sys.path.insert(0, _ROOT)
+from bmggen import check, lib  # noqa: E402  (the generator library, not libbmgcuda.so)
 
 
 @dataclass

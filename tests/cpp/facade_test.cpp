@@ -3,32 +3,40 @@
 // reference's exception types.  Exit code 0 = pass.  Needs a B200.
 #include <cmath>
 #include <cstdio>
+#include <stdexcept>
 #include <vector>
 
 #include "bmg/blockmg.hpp"
+#include "bmg_gen.h"
 
-static bmg::HostBsr stencil(int n, int m) {
+namespace bmg_c = bmg::cuda;
+
+static void gen_check(int st) {
+  if (st != 0) throw std::runtime_error(bmg_gen_last_error());
+}
+
+static bmg_c::HostBsr stencil(int n, int m) {
   int64_t nnzb = 0;
-  bmg::check(bmg_gen_stencil(2, n, 2, m, 0, 0.01, 0, -1, &nnzb, nullptr, nullptr, nullptr));
-  bmg::HostBsr h;
-  h.rows = h.cols = bmg::BlockLayout::uniform(n * n, m);
+  gen_check(bmg_gen_stencil(2, n, 2, m, 0, 0.01, 0, -1, &nnzb, nullptr, nullptr, nullptr));
+  bmg_c::HostBsr h;
+  h.rows = h.cols = bmg_c::BlockLayout::uniform(n * n, m);
   h.row_ptr.resize((size_t)n * n + 1);
   h.col_idx.resize((size_t)nnzb);
   h.vals.resize((size_t)nnzb * m * m);
-  bmg::check(bmg_gen_stencil(2, n, 2, m, 0, 0.01, 0, -1, &nnzb, h.row_ptr.data(), h.col_idx.data(), h.vals.data()));
+  gen_check(bmg_gen_stencil(2, n, 2, m, 0, 0.01, 0, -1, &nnzb, h.row_ptr.data(), h.col_idx.data(), h.vals.data()));
   h.symmetric = true;
   return h;
 }
-static bmg::HostBsr prolong(int nf, int m, int level) {
+static bmg_c::HostBsr prolong(int nf, int m, int level) {
   int64_t nnzb = 0;
-  bmg::check(bmg_gen_prolongation(2, nf, m, 0, level, 0, -1, &nnzb, nullptr, nullptr, nullptr));
-  bmg::HostBsr h;
-  h.rows = bmg::BlockLayout::uniform(nf * nf, m);
-  h.cols = bmg::BlockLayout::uniform(nf * nf / 4, m);
+  gen_check(bmg_gen_prolongation(2, nf, m, 0, level, 0, -1, &nnzb, nullptr, nullptr, nullptr));
+  bmg_c::HostBsr h;
+  h.rows = bmg_c::BlockLayout::uniform(nf * nf, m);
+  h.cols = bmg_c::BlockLayout::uniform(nf * nf / 4, m);
   h.row_ptr.resize((size_t)nf * nf + 1);
   h.col_idx.resize((size_t)nnzb);
   h.vals.resize((size_t)nnzb * m * m);
-  bmg::check(bmg_gen_prolongation(2, nf, m, 0, level, 0, -1, &nnzb, h.row_ptr.data(), h.col_idx.data(), h.vals.data()));
+  gen_check(bmg_gen_prolongation(2, nf, m, 0, level, 0, -1, &nnzb, h.row_ptr.data(), h.col_idx.data(), h.vals.data()));
   return h;
 }
 
@@ -41,49 +49,85 @@ static bmg::HostBsr prolong(int nf, int m, int level) {
   } while (0)
 
 int main() {
-  bmg::Context ctx(0);
+  bmg_c::Context ctx(0);
   const int n = 32, m = 10;
-  bmg::HostBsr ah = stencil(n, m);
-  bmg::DeviceMatrix A(ctx, ah);
-  bmg::DeviceMatrix P2(ctx, prolong(32, m, 2)), P1(ctx, prolong(16, m, 1));
-  bmg::SetupParams prm;
+  bmg_c::HostBsr ah = stencil(n, m);
+  bmg_c::DeviceMatrix A(ctx, ah);
+  bmg_c::DeviceMatrix P2(ctx, prolong(32, m, 2)), P1(ctx, prolong(16, m, 1));
+  bmg_c::SetupParams prm;
   prm.t_max = 1;
   prm.coarse_dim_cap = 1 << 30;
-  bmg::Hierarchy h = bmg::setup(A, {&P1, &P2}, prm);
+  bmg_c::Hierarchy h = bmg_c::setup(A, {&P1, &P2}, prm);
   EXPECT(h.levels() == 3);
   EXPECT(h.beta(2) > 0.0 && h.beta(1) > 0.0);
   std::vector<double> b((size_t)ah.rows.dim());
-  bmg::check(bmg_gen_normal(0, 0, (int64_t)b.size(), b.data()));
-  bmg::DeviceVector bv(ctx, b), xv(ctx, (int64_t)b.size());
-  auto rep = bmg::solve(h, bmg::CycleSpec::vkk(3), bv, xv, 5e-2, 200);
+  gen_check(bmg_gen_normal(0, 0, (int64_t)b.size(), b.data()));
+  bmg_c::DeviceVector bv(ctx, b), xv(ctx, (int64_t)b.size());
+  auto rep = bmg_c::solve(h, bmg_c::CycleSpec::vkk(3), bv, xv, 5e-2, 200);
   EXPECT(rep.status == 0);
   EXPECT(rep.residual.back() < 5e-2 * rep.residual.front());
   // host-buffer v_cycle matches the device-vector one bitwise
   std::vector<double> x1(b.size(), 0.0);
-  bmg::v_cycle(h, bmg::CycleSpec::vkk(3), b, x1);
-  bmg::DeviceVector x2(ctx, (int64_t)b.size());
-  bmg::v_cycle(h, bmg::CycleSpec::vkk(3), bv, x2);
+  bmg_c::v_cycle(h, bmg_c::CycleSpec::vkk(3), b, x1);
+  bmg_c::DeviceVector x2(ctx, (int64_t)b.size());
+  bmg_c::v_cycle(h, bmg_c::CycleSpec::vkk(3), bv, x2);
   EXPECT(x1 == x2.download());
+  // reference-shaped entry points (chebyshev.hpp:48-50, fsai.hpp:62): x by value,
+  // result returned; generic operator callables take the step-for-step path, the
+  // device handles the fused passes -- bitwise the same numbers
+  {
+    bmg_c::NestedFsai M = bmg_c::nested_build(A, 1, 1.0, 0);
+    const double beta = bmg_c::lanczos_lambda_max(A, M);
+    std::vector<double> x0h(b.size());
+    gen_check(bmg_gen_normal(0, 3, (int64_t)x0h.size(), x0h.data()));
+    bmg_c::DeviceVector x0(ctx, x0h);
+    bmg_c::DeviceVector xf = bmg_c::cheb_fourth_apply(A, M, bv, x0, beta, 3);
+    auto a_op = [&](const bmg_c::DeviceVector& in, bmg_c::DeviceVector& out) { bmg_c::spmv(A, in, out); };
+    auto m_op = [&](const bmg_c::DeviceVector& in, bmg_c::DeviceVector& out) { M.apply(in, out); };
+    bmg_c::DeviceVector xg = bmg_c::cheb_fourth_apply(a_op, m_op, bv, x0, beta, 3);
+    EXPECT(xf.download() == xg.download());
+    EXPECT(x0.download() == x0h);  // the caller's x is untouched (by-value)
+    for (int kind = 0; kind < 3; ++kind) {
+      bmg_c::SmootherSpec s;
+      s.kind = static_cast<bmg_c::SmootherKind>(kind);
+      s.alpha = beta / 30.0;
+      s.beta = beta;
+      s.omega = 1.0 / beta;
+      bmg_c::DeviceVector y1 = bmg_c::apply_smoother(s, 3, A, M, bv, x0);
+      bmg_c::DeviceVector y2 = bmg_c::apply_smoother(s, 3, a_op, m_op, bv, x0);
+      EXPECT(y1.download() == y2.download());
+    }
+    bmg_c::DeviceVector z1 = M.apply(bv);  // Vector NestedFsai::apply(const Vector&) const
+    bmg_c::DeviceVector z2(ctx, (int64_t)b.size());
+    M.apply(bv, z2);
+    EXPECT(z1.download() == z2.download());
+    // setup with transfers by value (multilevel.hpp:59-60); the inputs may go away
+    std::vector<bmg_c::DeviceMatrix> tv;
+    tv.emplace_back(ctx, prolong(16, m, 1));
+    tv.emplace_back(ctx, prolong(32, m, 2));
+    bmg_c::Hierarchy h2 = bmg_c::setup(A, std::move(tv), prm);
+    EXPECT(h2.beta(2) == h.beta(2) && h2.beta(1) == h.beta(1));
+  }
   // exception mapping (kernels.cpp:9-11, small_cholesky.cpp:19)
   bool threw = false;
   try {
-    bmg::DeviceVector bad(ctx, 3);
-    bmg::spmv(A, bad, xv);
+    bmg_c::DeviceVector bad(ctx, 3);
+    bmg_c::spmv(A, bad, xv);
   } catch (const std::invalid_argument&) {
     threw = true;
   }
   EXPECT(threw);
-  bmg::HostBsr ind;
-  ind.rows = ind.cols = bmg::BlockLayout({2});
+  bmg_c::HostBsr ind;
+  ind.rows = ind.cols = bmg_c::BlockLayout({2});
   ind.row_ptr = {0, 1};
   ind.col_idx = {0};
   ind.vals = {1.0, 2.0, 2.0, 1.0};
   ind.symmetric = true;
-  bmg::DeviceMatrix I(ctx, ind);
+  bmg_c::DeviceMatrix I(ctx, ind);
   threw = false;
   try {
-    bmg::build_fsai_static(I);
-  } catch (const bmg::NotPositiveDefinite& e) {
+    bmg_c::build_fsai_static(I);
+  } catch (const bmg_c::NotPositiveDefinite& e) {
     threw = e.pivot == 1;
   }
   EXPECT(threw);

@@ -24,6 +24,24 @@ def test_library_exports_every_header_symbol():
     assert set(syms) <= set(N._SIGS), set(syms) - set(N._SIGS)
 
 
+def test_generator_is_a_separate_library():
+    # the synthetic inputs come from bmggen/libbmggen.so (include/bmg_gen.h), so the
+    # reference arm of bench.py maps neither the product nor its kernels
+    import re
+
+    import bmggen
+
+    hdr = open(os.path.join(os.path.dirname(N.HEADER_PATH), "bmg_gen.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    gen_syms = sorted(set(re.findall(r"\b(bmg_gen_[a-z_]+)\s*\(", hdr)))
+    assert len(gen_syms) == 4
+    g = bmggen.lib()
+    assert all(hasattr(g, s) for s in gen_syms)
+    assert set(gen_syms) == set(bmggen._SIGS)
+    nm = subprocess.run(["nm", "-D", "--defined-only", N.LIB_PATH], capture_output=True, text=True).stdout
+    assert "bmg_gen_" not in nm, "libbmgcuda.so must not carry the generator"
+
+
 def test_library_is_sm100a_only():
     out = subprocess.run(["cuobjdump", "--list-elf", N.LIB_PATH], capture_output=True, text=True).stdout
     archs = {line.split(".")[-2] for line in out.splitlines() if ".sm_" in line}

@@ -16,7 +16,8 @@ while time.time() - t0 < float(sys.argv[2] if len(sys.argv) > 2 else 120):
     dim = int(rng.choice([2, 2, 3]))
     levels = int(rng.integers(2, 4))
     n = int(rng.choice([8, 16])) if dim == 2 else 8
-    m = int(rng.choice([3, 4, 6, 10]))
+    # the BASELINE block sizes (C2 10, C5 15, C4 20, C3 21) and small ones
+    m = int(rng.choice([3, 4, 6, 10, 15, 20, 21]))
     power = int(rng.choice([1, 2])) if dim == 3 else int(rng.choice([2, 3]))
     nest = int(rng.choice([0, 0, 1]))
     t_max = int(rng.choice([1, 2]))
