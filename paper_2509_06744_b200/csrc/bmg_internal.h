@@ -57,6 +57,44 @@ struct DBuf {
   size_t bytes() const { return n * sizeof(T); }
 };
 
+// A device buffer whose physical memory can be returned from the tail while the
+// front stays in place (CUDA virtual memory management: one reserved address
+// range, physical memory mapped in chunks).  The coarse solve factorises A_0 in
+// an N0 x N0 buffer and packs the lower 64x64 tiles of the inverse into the front
+// of the same buffer, then unmaps the rest: the dense matrix and the packed tiles
+// are never held at the same time (C3's N0 = 86,016: 59 GB dense, 30 GB packed).
+struct ShrinkBuf {
+  double* p = nullptr;
+  size_t n = 0;  // doubles currently backed
+  ShrinkBuf() = default;
+  ShrinkBuf(const ShrinkBuf&) = delete;
+  ShrinkBuf& operator=(const ShrinkBuf&) = delete;
+  ShrinkBuf(ShrinkBuf&& o) noexcept { swap(o); }
+  ShrinkBuf& operator=(ShrinkBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      swap(o);
+    }
+    return *this;
+  }
+  ~ShrinkBuf() { release(); }
+  void alloc(size_t count, int device);  // reserve + map (ceil to the chunk size)
+  void shrink(size_t count);             // unmap and free the chunks beyond `count`
+  void release();
+  size_t bytes() const { return n * sizeof(double); }
+
+ private:
+  void swap(ShrinkBuf& o) {
+    std::swap(p, o.p);
+    std::swap(n, o.n);
+    std::swap(reserved, o.reserved);
+    std::swap(chunk, o.chunk);
+    std::swap(handles, o.handles);
+  }
+  size_t reserved = 0, chunk = 0;  // bytes
+  std::vector<unsigned long long> handles;  // CUmemGenericAllocationHandle per mapped chunk
+};
+
 // ---- context ------------------------------------------------------------------
 // ---- rank-to-rank transport ---------------------------------------------------
 // NCCL over NVLink for real multi-GPU runs (bmg_ctx_create_nccl); a loopback

@@ -28,6 +28,9 @@ namespace kern {
 // contributes tile * x_J to rows of I and (J < I) tile^T * x_I to rows of J;
 // partials are summed per row in ascending tile order (deterministic).
 constexpr int kTile = 64;
+// right-hand sides per batched cycle: 1, 2, 4 or kMaxRhs (set_nrhs enforces it; the
+// coarse solve's x staging in symv_stream_kernel is sized by it)
+constexpr int kMaxRhs = 8;
 
 __device__ __forceinline__ void tile_of(int64_t t, int* I, int* J) {
   int i = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
@@ -90,7 +93,7 @@ struct PLevel {  // one (virtual) rank's share of one level
 struct Part {
   int rank = 0;
   std::vector<PLevel> lv;
-  DBuf<double> ainv;  // A_0^{-1} as packed lower 64x64 tiles (rank owning level 0), or
+  ShrinkBuf ainv;  // A_0^{-1} as packed lower 64x64 tiles (rank owning level 0), or
                       // W = L^{-1} (A_0 = L L^T) when the coarse level is triangular
   bool tri = false;   // coarse solve as x = W^T (W b): N0^2 >= 2^31 (no 64-bit potri)
   DBuf<double> cpart; // per-(tile row, tile) partial sums of the coarse solve
@@ -205,6 +208,7 @@ void run_vcycle(Hier& h, int kpre, int kpost, const double* bf, double* xf);
 // whole single-RHS hierarchies with pinned host b, x and kpre > 0: the pipelined
 // host-buffer cycle; false if it does not apply (the caller copies around run_vcycle)
 bool run_vcycle_hostio(Hier& h, int kpre, int kpost, const double* hb, double* hx);
+void ensure_host_io(Hier& h, int64_t n);
 // bmg_solve on whole single-RHS hierarchies: each iteration (cycle, residual,
 // segment sums to pinned memory) is one graph launch; the stopping test stays on
 // the host in the oracle's order; false if it does not apply (the caller runs the

@@ -16,6 +16,9 @@
 #include <tuple>
 
 #include "bmg_abi.h"
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "hier.h"
 
 namespace bmg {
@@ -59,6 +62,26 @@ __global__ void pack_lower_tiles_kernel(const double* __restrict__ full, int64_t
   }
 }
 
+// tile row I of the packed lower tiles: block J (0..I) writes tile (I, J) to
+// dst + J * 64 * 64 from `src`, which holds dense rows [row0, row0 + 64) with
+// leading dimension ld (entries beyond N are zero; `strict` as above)
+__global__ void pack_tile_row_kernel(const double* __restrict__ src, int64_t ld, int64_t row0, int I, int64_t N,
+                                     double* __restrict__ dst, int strict) {
+  const int J = blockIdx.x;
+  double* d = dst + (int64_t)J * kTile * kTile;
+  for (int e = threadIdx.x; e < kTile * kTile; e += blockDim.x) {
+    const int r = e / kTile, c = e - r * kTile;
+    const int64_t gr = (int64_t)I * kTile + r, gc = (int64_t)J * kTile + c;
+    d[e] = (gr < N && gc < N && (!strict || gc <= gr)) ? src[(gr - row0) * ld + gc] : 0.0;
+  }
+}
+// rows [0, nrows) x columns [0, ncols) of a row-major matrix with leading dimension ld
+__global__ void copy_rows_kernel(const double* __restrict__ a, int64_t ld, int64_t nrows, double* __restrict__ out,
+                                 int ncols) {
+  for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x)
+    for (int c = threadIdx.x; c < ncols; c += blockDim.x) out[r * ncols + c] = c < ld ? a[r * ld + c] : 0.0;
+}
+
 }  // namespace kern
 
 // BMG_SETUP_TIMING=1: per-phase wall time of the setup on stderr (device synced)
@@ -86,6 +109,44 @@ struct SetupClock {
 // dimension lda).  cuSOLVER's Xtrtri rejects n^2 >= 2^31, so larger blocks recurse on
 // their diagonal halves and finish the off-diagonal block with two in-place 64-bit
 // TRMMs: W21 = -W22 L21 W11.
+// Lower Cholesky (column-major, in place) of an n x n matrix with n^2 beyond what
+// cuSOLVER's dense factorisations handle (C3's N0 = 86,016: 7.4e9 elements; the
+// 64-bit Xpotrf fails there): right-looking blocked algorithm, the diagonal
+// blocks by Dpotrf (nb x nb, 32-bit safe), the panel by a 64-bit TRSM and the
+// trailing update by a 64-bit SYRK.
+static void blocked_potrf(Ctx* ctx, double* a, int64_t n, int64_t lda) {
+  constexpr int64_t nb = 2048;
+  cusolverDnHandle_t s = ctx->cusolver();
+  cublasHandle_t b = ctx->cublas();
+  int lwork = 0;
+  if (cusolverDnDpotrf_bufferSize(s, CUBLAS_FILL_MODE_LOWER, (int)nb, a, (int)lda, &lwork) != CUSOLVER_STATUS_SUCCESS)
+    fail(BMG_ECUDA, "cusolverDnDpotrf_bufferSize failed");
+  DBuf<double> work(std::max(lwork, 1));
+  DBuf<int> info(1);
+  const double one = 1.0, minus = -1.0;
+  for (int64_t k = 0; k < n; k += nb) {
+    const int64_t kb = std::min(nb, n - k);
+    double* a11 = a + k + k * lda;
+    if (cusolverDnDpotrf(s, CUBLAS_FILL_MODE_LOWER, (int)kb, a11, (int)lda, work.p, lwork, info.p) !=
+        CUSOLVER_STATUS_SUCCESS)
+      fail(BMG_ECUDA, "cusolverDnDpotrf (diagonal block) failed");
+    int hinfo = 0;
+    BMG_CUDA(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (hinfo != 0) fail(BMG_ERUNTIME, "setup: coarsest operator is not positive definite");
+    const int64_t rest = n - k - kb;
+    if (rest <= 0) break;
+    double* a21 = a11 + kb;
+    double* a22 = a21 + kb * lda;
+    if (cublasDtrsm_v2_64(b, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, rest, kb,
+                          &one, a11, lda, a21, lda) != CUBLAS_STATUS_SUCCESS)
+      fail(BMG_ECUDA, "cublasDtrsm (Cholesky panel) failed");
+    if (cublasDsyrk_v2_64(b, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, rest, kb, &minus, a21, lda, &one, a22, lda) !=
+        CUBLAS_STATUS_SUCCESS)
+      fail(BMG_ECUDA, "cublasDsyrk (Cholesky update) failed");
+  }
+}
+
 static void tri_inverse(Ctx* ctx, double* a, int64_t n, int64_t lda, DBuf<double>& scratch) {
   constexpr int64_t kMax = ((int64_t)1 << 31) - 1;
   if (n * n < kMax) {
@@ -131,13 +192,112 @@ static void tri_inverse(Ctx* ctx, double* a, int64_t n, int64_t lda, DBuf<double
     fail(BMG_ECUDA, "cublasDtrmm (W22 L21 W11) failed");
 }
 
+// ---- ShrinkBuf (bmg_internal.h) ------------------------------------------------
+// The driver's virtual-memory calls are resolved through the runtime
+// (cudaGetDriverEntryPoint), so the library does not link libcuda and still loads
+// on a GPU-less host (where every compute entry reports BMG_ECUDA).
+struct VmmApi {
+  PFN_cuMemGetAllocationGranularity granularity = nullptr;
+  PFN_cuMemAddressReserve reserve = nullptr;
+  PFN_cuMemAddressFree addr_free = nullptr;
+  PFN_cuMemCreate create = nullptr;
+  PFN_cuMemRelease release = nullptr;
+  PFN_cuMemMap map = nullptr;
+  PFN_cuMemUnmap unmap = nullptr;
+  PFN_cuMemSetAccess set_access = nullptr;
+};
+static const VmmApi& vmm() {
+  static const VmmApi api = [] {
+    VmmApi a;
+    auto get = [](const char* name, void** fn) {
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess ||
+          !*fn)
+        fail(BMG_ECUDA, std::string("driver entry point unavailable: ") + name);
+    };
+    get("cuMemGetAllocationGranularity", reinterpret_cast<void**>(&a.granularity));
+    get("cuMemAddressReserve", reinterpret_cast<void**>(&a.reserve));
+    get("cuMemAddressFree", reinterpret_cast<void**>(&a.addr_free));
+    get("cuMemCreate", reinterpret_cast<void**>(&a.create));
+    get("cuMemRelease", reinterpret_cast<void**>(&a.release));
+    get("cuMemMap", reinterpret_cast<void**>(&a.map));
+    get("cuMemUnmap", reinterpret_cast<void**>(&a.unmap));
+    get("cuMemSetAccess", reinterpret_cast<void**>(&a.set_access));
+    return a;
+  }();
+  return api;
+}
+static void cu_check(CUresult r, const char* what) {
+  if (r != CUDA_SUCCESS) fail(BMG_ECUDA, std::string(what) + " failed (CUresult " + std::to_string((int)r) + ")");
+}
+
+void ShrinkBuf::alloc(size_t count, int device) {
+  release();
+  CUmemAllocationProp prop = {};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = device;
+  size_t gran = 0;
+  cu_check(vmm().granularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED), "cuMemGetAllocationGranularity");
+  const size_t want = std::max<size_t>(count, 1) * sizeof(double);
+  chunk = ((std::max<size_t>(want / 64, (size_t)256 << 20) + gran - 1) / gran) * gran;  // <= 64 chunks, >= 256 MB
+  reserved = (want + chunk - 1) / chunk * chunk;
+  CUdeviceptr base = 0;
+  cu_check(vmm().reserve(&base, reserved, 0, 0, 0), "cuMemAddressReserve");
+  p = reinterpret_cast<double*>(base);
+  try {
+    for (size_t off = 0; off < reserved; off += chunk) {
+      CUmemGenericAllocationHandle hd;
+      cu_check(vmm().create(&hd, chunk, &prop, 0), "cuMemCreate");
+      handles.push_back(hd);
+      cu_check(vmm().map(base + off, chunk, 0, hd, 0), "cuMemMap");
+    }
+    CUmemAccessDesc acc = {};
+    acc.location = prop.location;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    cu_check(vmm().set_access(base, reserved, &acc, 1), "cuMemSetAccess");
+  } catch (...) {
+    release();
+    throw;
+  }
+  n = count;
+}
+
+void ShrinkBuf::shrink(size_t count) {
+  if (!p || count >= n) return;
+  const size_t keep = (std::max<size_t>(count, 1) * sizeof(double) + chunk - 1) / chunk;  // chunks kept
+  const CUdeviceptr base = reinterpret_cast<CUdeviceptr>(p);
+  while (handles.size() > keep) {
+    const size_t i = handles.size() - 1;
+    cu_check(vmm().unmap(base + i * chunk, chunk), "cuMemUnmap");
+    cu_check(vmm().release(handles[i]), "cuMemRelease");
+    handles.pop_back();
+  }
+  n = count;
+}
+
+void ShrinkBuf::release() {
+  if (p) {
+    const CUdeviceptr base = reinterpret_cast<CUdeviceptr>(p);
+    for (size_t i = 0; i < handles.size(); ++i) {
+      vmm().unmap(base + i * chunk, chunk);
+      vmm().release(handles[i]);
+    }
+    vmm().addr_free(base, reserved);
+  }
+  handles.clear();
+  p = nullptr;
+  n = 0;
+  reserved = chunk = 0;
+}
+
 void coarse_factor(Hier& h, Part& p) {
   Ctx* ctx = h.ctx;
   const Bsr& a0 = *p.lv[0].A;
   if (!(a0.rsz == a0.csz)) fail(BMG_EINVAL, "coarse solve: square block layout required");
   const int64_t N = a0.dim_r;
   h.n0 = N;
-  p.ainv.alloc(std::max<int64_t>(N * N, 1));
+  p.ainv.alloc((size_t)std::max<int64_t>(N * N, 1), ctx->device);
   BMG_CUDA(cudaMemsetAsync(p.ainv.p, 0, p.ainv.bytes(), ctx->stream));
   kern::bsr_to_dense_kernel<<<std::max(1, std::min(a0.nbr, ctx->sms * 8)), 128, 0, ctx->stream>>>(
       a0.vals.p, blk_view(a0), a0.row_ptr.p, a0.col.p, a0.nbr, p.ainv.p, N);
@@ -176,23 +336,7 @@ void coarse_factor(Hier& h, Part& p) {
       fail(BMG_ECUDA, "cusolverDnDpotri failed");
     check_info("setup: coarse inverse failed");
   } else {
-    cusolverDnParams_t prm = nullptr;
-    if (cusolverDnCreateParams(&prm) != CUSOLVER_STATUS_SUCCESS) fail(BMG_ECUDA, "cusolverDnCreateParams failed");
-    size_t dws = 0, hws = 0;
-    if (cusolverDnXpotrf_bufferSize(s, prm, CUBLAS_FILL_MODE_LOWER, N, CUDA_R_64F, p.ainv.p, N, CUDA_R_64F, &dws,
-                                    &hws) != CUSOLVER_STATUS_SUCCESS) {
-      cusolverDnDestroyParams(prm);
-      fail(BMG_ECUDA, "cusolverDnXpotrf_bufferSize failed");
-    }
-    {
-      DBuf<unsigned char> dwork(std::max<size_t>(dws, 1));
-      std::vector<unsigned char> hwork(std::max<size_t>(hws, 1));
-      const auto st = cusolverDnXpotrf(s, prm, CUBLAS_FILL_MODE_LOWER, N, CUDA_R_64F, p.ainv.p, N, CUDA_R_64F,
-                                       dwork.p, dws, hwork.data(), hws, info.p);
-      cusolverDnDestroyParams(prm);
-      if (st != CUSOLVER_STATUS_SUCCESS) fail(BMG_ECUDA, "cusolverDnXpotrf failed");
-      check_info("setup: coarsest operator is not positive definite");
-    }
+    blocked_potrf(ctx, p.ainv.p, N, N);
     DBuf<double> scratch;
     tri_inverse(ctx, p.ainv.p, N, N, scratch);
     BMG_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -201,15 +345,40 @@ void coarse_factor(Hier& h, Part& p) {
   kern::symmetrize_dense_kernel<<<grid1d(N * N), 256, 0, ctx->stream>>>(p.ainv.p, N);
   ctx->count();
   BMG_CUDA(cudaGetLastError());
-  // keep only the lower 64x64 tiles (packed); the dense copy is released
+  // keep only the lower 64x64 tiles, packed into the front of the same buffer, one
+  // tile row at a time in ascending order: tile row I's packed range ends before
+  // the first dense row it reads (I >= 1, N >= 256), and every later row reads
+  // behind it, so no unread entry is overwritten; row 0 overlaps its own source
+  // and goes through a 64 x 64 staging copy.  The tail is then unmapped.
   const int nt = (int)((N + kern::kTile - 1) / kern::kTile);
   const int64_t ntiles = (int64_t)nt * (nt + 1) / 2;
-  DBuf<double> tiles((size_t)ntiles * kern::kTile * kern::kTile);
-  kern::pack_lower_tiles_kernel<<<(unsigned)ntiles, 256, 0, ctx->stream>>>(p.ainv.p, N, tiles.p, p.tri ? 1 : 0);
-  ctx->count();
-  BMG_CUDA(cudaGetLastError());
-  BMG_CUDA(cudaStreamSynchronize(ctx->stream));
-  p.ainv = std::move(tiles);
+  const int64_t T2 = (int64_t)kern::kTile * kern::kTile;
+  if (N >= 4 * kern::kTile) {
+    DBuf<double> stage((size_t)T2);
+    kern::copy_rows_kernel<<<kern::kTile, 128, 0, ctx->stream>>>(p.ainv.p, N, std::min<int64_t>(N, kern::kTile),
+                                                                 stage.p, kern::kTile);
+    kern::pack_tile_row_kernel<<<1, 256, 0, ctx->stream>>>(stage.p, kern::kTile, 0, 0, N, p.ainv.p, p.tri ? 1 : 0);
+    ctx->count(2);
+    for (int I = 1; I < nt; ++I) {
+      kern::pack_tile_row_kernel<<<I + 1, 256, 0, ctx->stream>>>(p.ainv.p + (int64_t)I * kern::kTile * N, N,
+                                                                   (int64_t)I * kern::kTile, I, N,
+                                                                   p.ainv.p + ((int64_t)I * (I + 1) / 2) * T2,
+                                                                   p.tri ? 1 : 0);
+      ctx->count();
+    }
+    BMG_CUDA(cudaGetLastError());
+    BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+    p.ainv.shrink((size_t)(ntiles * T2));
+  } else {  // tiny coarse levels: a separate packed copy
+    DBuf<double> tiles((size_t)(ntiles * T2));
+    kern::pack_lower_tiles_kernel<<<(unsigned)ntiles, 256, 0, ctx->stream>>>(p.ainv.p, N, tiles.p, p.tri ? 1 : 0);
+    ctx->count();
+    BMG_CUDA(cudaGetLastError());
+    BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+    p.ainv.alloc((size_t)(ntiles * T2), ctx->device);
+    BMG_CUDA(cudaMemcpyAsync(p.ainv.p, tiles.p, tiles.bytes(), cudaMemcpyDeviceToDevice, ctx->stream));
+    BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
   p.cpart.alloc((size_t)nt * nt * kern::kTile);
   BMG_CUDA(cudaMemsetAsync(p.cpart.p, 0, p.cpart.bytes(), ctx->stream));
 }
@@ -741,11 +910,8 @@ int bmg_vcycle_batch_host(bmg_hier* hh, int kpre, int kpost, int nrhs, const dou
     ctx->activate();
     set_nrhs(*h, nrhs);
     const int64_t n = finest_len(*h);
-    if (h->io_b.n < (size_t)n) {
-      h->io_b.alloc(std::max<int64_t>(n, 1));
-      h->io_x.alloc(std::max<int64_t>(n, 1));
-    }
     if (kpre + kpost < 1) fail(BMG_EINVAL, "v_cycle: cycle needs at least one smoothing step");
+    ensure_host_io(*h, n);
     if (!run_vcycle_hostio(*h, kpre, kpost, b, x)) {
       BMG_CUDA(cudaMemcpyAsync(h->io_b.p, b, n * 8, cudaMemcpyHostToDevice, ctx->stream));
       BMG_CUDA(cudaMemcpyAsync(h->io_x.p, x, n * 8, cudaMemcpyHostToDevice, ctx->stream));

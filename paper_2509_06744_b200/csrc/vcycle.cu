@@ -30,16 +30,16 @@ namespace kern {
 // current one is used.  Row parts read the unpadded tile in a rotated column order
 // (c = (c' + t) mod 64: conflict-free banks); column parts read columns directly.
 constexpr int kSymvThreads = 256;
-constexpr size_t kSymvSmem = 2 * kTile * kTile * sizeof(double) + 2 * 8 * kTile * sizeof(double) + 16;
+constexpr size_t kSymvSmem = 2 * kTile * kTile * sizeof(double) + 2 * kMaxRhs * kTile * sizeof(double) + 16;
 __global__ void __launch_bounds__(kSymvThreads) symv_stream_kernel(const double* __restrict__ tiles,
                                                                    const double* __restrict__ x, int64_t N, int nt,
                                                                    int64_t ntiles, double* __restrict__ part, int K,
                                                                    int mode) {
   extern __shared__ __align__(128) unsigned char smem[];
   double* ring = reinterpret_cast<double*>(smem);                    // 2 x 64 x 64
-  double* xi = ring + 2 * kTile * kTile;                             // [8][64]
-  double* xj = xi + 8 * kTile;                                       // [8][64]
-  uint64_t* full = reinterpret_cast<uint64_t*>(xj + 8 * kTile);      // 2 barriers
+  double* xi = ring + 2 * kTile * kTile;                             // [kMaxRhs][64]
+  double* xj = xi + kMaxRhs * kTile;                                 // [kMaxRhs][64]
+  uint64_t* full = reinterpret_cast<uint64_t*>(xj + kMaxRhs * kTile);  // 2 barriers
   const int tid = threadIdx.x;
   constexpr uint32_t kBytes = kTile * kTile * sizeof(double);
   if (tid == 0) {
@@ -61,8 +61,9 @@ __global__ void __launch_bounds__(kSymvThreads) symv_stream_kernel(const double*
   const int it0 = mode == 2 ? kTile * K : 0, it1 = mode == 1 ? kTile * K : 2 * kTile * K;
   // the x segments of a tile (64 K values each for its row and column ranges) are
   // loaded into registers one tile ahead, so their latency overlaps the current
-  // tile's work instead of preceding it (K <= 8: at most two per thread)
-  constexpr int kXPer = 8 * kTile / kSymvThreads;
+  // tile's work instead of preceding it (K <= kMaxRhs: at most two per thread)
+  constexpr int kXPer = (kMaxRhs * kTile + kSymvThreads - 1) / kSymvThreads;
+  static_assert(kXPer * kSymvThreads >= kMaxRhs * kTile, "x prefetch must cover kTile * K values for K <= kMaxRhs");
   double pxi[kXPer], pxj[kXPer];
   auto xload = [&](int64_t tt) {
     if (tt >= ntiles) return;
@@ -395,7 +396,8 @@ static void prepare_plans(Hier& h, int K) {
 }
 
 void set_nrhs(Hier& h, int K) {
-  if (K != 1 && K != 2 && K != 4 && K != 8) fail(BMG_EINVAL, "v_cycle batch: nrhs must be 1, 2, 4 or 8");
+  static_assert(kern::kMaxRhs == 8, "nrhs set below and the batch kernels' instantiations");
+  if (K != 1 && K != 2 && K != 4 && K != kern::kMaxRhs) fail(BMG_EINVAL, "v_cycle batch: nrhs must be 1, 2, 4 or 8");
   if (K == h.nrhs) return;
   BMG_CUDA(cudaStreamSynchronize(h.ctx->stream));
   h.nrhs = K;
@@ -483,6 +485,17 @@ void run_vcycle(Hier& h, int kpre, int kpost, const double* bf, double* xf) {
   ctx->launches += it->second.kernels;
 }
 
+// The host-buffer cycles stage b and x in io_b / io_x, whose device addresses
+// are baked into every captured graph that uses them: growing them frees the old
+// buffers, so the stream is drained and every captured graph dropped first.
+void ensure_host_io(Hier& h, int64_t n) {
+  if (h.io_b.n >= (size_t)n && h.io_x.n >= (size_t)n) return;
+  BMG_CUDA(cudaStreamSynchronize(h.ctx->stream));
+  h.drop_graphs();
+  h.io_b.alloc(std::max<int64_t>(n, 1));
+  h.io_x.alloc(std::max<int64_t>(n, 1));
+}
+
 bool run_vcycle_hostio(Hier& h, int kpre, int kpost, const double* hb, double* hx) {
   static const bool off = [] {
     const char* e = std::getenv("BMG_HOSTIO_PIPELINE");
@@ -538,12 +551,7 @@ bool run_vcycle_hostio(Hier& h, int kpre, int kpost, const double* hb, double* h
     h.hio = std::move(io);
   }
   HostIo& io = *h.hio;
-  if (h.io_b.n < (size_t)n) {
-    BMG_CUDA(cudaStreamSynchronize(ctx->stream));
-    h.io_b.alloc(std::max<int64_t>(n, 1));
-    h.io_x.alloc(std::max<int64_t>(n, 1));
-    h.drop_graphs();
-  }
+  ensure_host_io(h, n);
   GraphKey key{kpre, kpost, 1, h.cycle_top(), hb, hx, 1};
   auto it = h.graphs.find(key);
   if (it == h.graphs.end()) {

@@ -145,3 +145,35 @@ def test_batch_rejects_bad_sizes(ctx):
         h.v_cycle_batch(3, 3, 4, Vector(ctx, b.size * 2), Vector(ctx, b.size * 2))
     with pytest.raises(InvalidArgument):
         h.v_cycle_batch(0, 0, 2, Vector(ctx, b.size * 2), Vector(ctx, b.size * 2))
+
+
+def test_host_buffer_cycles_after_batch_sizes_change(ctx):
+    # the host-buffer staging grows with K; graphs captured with the old
+    # staging buffers must not be replayed.  Sequence: device batch K = 4, host
+    # single (pinned, captured graph), host batch K = 2 (grows the staging), host
+    # single again -- every result equal to the device-vector cycles.
+    import torch
+
+    h, A, T, b = _hier(ctx, pr.CONFIGS["C2"].scaled(32, 3))
+    n = b.size
+    B4, X4 = _rhs(n, 4, 7)
+    got4 = _batched(ctx, h, B4, X4, 1)
+    assert np.array_equal(got4, _single(ctx, h, B4, X4, 1))
+
+    hb = torch.from_numpy(b.copy()).pin_memory()  # the same pinned buffers every call:
+    hx = torch.zeros(n, dtype=torch.float64).pin_memory()  # the captured graph is reused
+
+    def host_single(x0):
+        hx.numpy()[:] = x0
+        h.v_cycle_host_ptr(3, 3, hb.data_ptr(), hx.data_ptr())
+        return hx.numpy().copy()
+
+    x0 = np.random.default_rng(3).standard_normal(n)
+    want = _single(ctx, h, b[:, None], x0[:, None], 1)[:, 0]
+    assert np.array_equal(host_single(x0), want)
+    B2, X2 = _rhs(n, 2, 9)
+    xb = X2.ravel().copy()
+    h.v_cycle_batch_host(3, 3, 2, B2.ravel().copy(), xb)
+    assert np.array_equal(xb.reshape(n, 2), _single(ctx, h, B2, X2, 1))
+    for _ in range(2):
+        assert np.array_equal(host_single(x0), want)

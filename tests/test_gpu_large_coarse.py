@@ -25,6 +25,29 @@ def test_coarse_solve_above_2_31_elements(ctx):
     assert rel < 1e-8, rel
 
 
+@pytest.mark.parametrize("m", [15, 21])
+def test_coarse_solve_at_the_c5_and_c3_coarse_sizes(ctx, m):
+    # the coarsest levels of C5 (64^2 patches, m = 15: N0 = 61,440) and C3 (64^2,
+    # m = 21: N0 = 86,016) themselves: factor, W = L^-1, packed tiles built in place
+    # in the factor's buffer and its tail released (no dense + packed peak)
+    host = pr.stencil_matrix(2, 64, 2, m)
+    N = host.dim_r
+    assert N == 64 * 64 * m
+    A = BlockSparseMatrix(ctx, host)
+    h = Hierarchy.setup(A, [], default_params(t_max=1, coarse_dim_cap=1 << 30))
+    nt = (N + 63) // 64
+    packed = nt * (nt + 1) // 2 * 64 * 64 * 8
+    assert h.device_bytes < packed + 2 * 2 ** 30, (h.device_bytes, packed)  # not the 8 N^2 dense buffer
+    b = pr.normal_vector(N, 0, 0)
+    x = Vector(ctx, N)
+    bv = Vector(ctx, b)
+    h.v_cycle(1, 1, bv, x)
+    r = Vector(ctx, N)
+    residual(A, bv, x, r)
+    rel = np.linalg.norm(r.download()) / np.linalg.norm(b)
+    assert rel < 1e-8, rel
+
+
 def test_triangular_coarse_path_matches_symmetric(ctx):
     # the W^T (W b) path (used when N0^2 >= 2^31), forced on a small hierarchy by a
     # child process with BMG_COARSE_TRIANGULAR=1, against the default symmetric inverse
