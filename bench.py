@@ -1,20 +1,29 @@
 #!/usr/bin/env python
 """Benchmark: V-cycle application of the multilevel Chebyshev(4th kind) + block-FSAI
-solver (arXiv 2509.06744 hot path) on B200.
+solver (arXiv 2509.06744 hot path, the reference's `v_cycle`, multilevel.cpp:77-103,
+driven as in `measure_rates`, experiments.cpp:15-67) on B200.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
 
-A step is one V(k,k) cycle on the finest level of the config's hierarchy with the
-inputs (hierarchy, b, x) resident in HBM.  Workload: config C2 (BASELINE.json
-configs[1]: 256^2 patches, m = 10, 4 levels, V(3,3), adaptive block-FSAI), the
-configs[1] case that fits one GPU; its per-cycle traffic (14+ GB) exceeds L2, so
-no explicit flush is needed between cycles.  For N > 1 the hierarchy is split
-into row strips per rank with NCCL halo exchanges inside the captured cycle and
-the coarsest two levels on rank 0 (strong scaling); `--replicas`
-runs independent copies instead (weak scaling).
+A step is one V(k,k) cycle on the finest level of the config's hierarchy, with the
+hierarchy, b and x resident in HBM.  Default workload: C4 (BASELINE.json
+configs[3]: 64^3 patches, m = 20, 3-D 25-point, 4 levels, adaptive block-FSAI,
+V(3,3)) -- the largest BASELINE config that fits one B200 (C3 and C5 need >= 4,
+problems.memory_plan).  Every cycle streams ~434 GB (>> 126 MB L2), so no flush
+is needed between cycles.
 
-One JSON line is printed by rank 0.  `--impl reference` times the CPU oracle
-(the restatement of the reference, which cannot be built here) on the host cores.
+N > 1 (torchrun, one rank per GPU, NCCL): the hierarchy is built by the
+distributed setup (bmg_hier_setup_dist) from each rank's strips only -- no rank
+ever holds a whole partitioned level -- with the config's coarsest levels
+agglomerated on rank 0 (C5: 2, per BASELINE), NCCL halo exchanges inside the
+captured cycle, strong scaling.  Partition invariance is checked bitwise on a
+scaled copy before timing; a failing distributed path fails the run.
+`--replicas` runs independent copies instead (weak scaling).
+
+`--impl reference` times the CPU oracle (oracle/: the plain-C++ restatement of
+the reference, which itself needs Eigen3, absent) on the host cores.  It maps
+only oracle/liboracle.so and the input generator bmggen/libbmggen.so -- never the
+product library.
 """
 from __future__ import annotations
 
@@ -34,6 +43,21 @@ sys.path.insert(0, ROOT)
 
 MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 HBM_FALLBACK = 6650.0
+# coarsest levels held whole on rank 0 in N > 1 runs (BASELINE configs[4]: C5 "coarsest
+# two levels agglomerated on one GPU"; the dense level alone for the single-GPU configs)
+AGGLOMERATE = {"C2": 1, "C3": 2, "C4": 1, "C5": 2}
+# the CPU legs (cpu_baseline, --impl reference) time oracle V-cycles on a bounded
+# sample: the config's own shape (block size, stencil, FSAI, depth, smoother) on a
+# smaller grid, its rate scaled to the full config by the ratio of algorithmic bytes
+# per cycle.  C2 runs whole.
+CPU_SAMPLE = {"C2": None, "C4": ("C4", 32, 4), "C3": ("C3", 256, 5), "C5": ("C5", 512, 6)}
+# algorithmic bytes per V(k,k) cycle of each full config (the device byte model,
+# bmg_hier_cycle_bytes; the GPU arm re-derives it and asserts it matches)
+CYCLE_BYTES = {"C2": 13_813_927_776, "C4": 433_649_594_288}
+# residual-history fixtures of the oracle (tests/golden/make_solve_golden.py) the
+# GPU arm reproduces in every run: the headline shape and the full C2
+PARITY_CASE = {"C4": "C4@16x4", "C2": "C2", "C5": "C5@128x6", "C3": "C3@128x5"}
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r02_traffic.json")
 
 
 def hbm_peak():
@@ -139,35 +163,114 @@ def cpu_info():
     return model
 
 
-# ------------------------------------------------------------------ CPU oracle arm
-def oracle_vcycles(cfg, steps, warmup, threads, single_core=None):
-    """Time V-cycles of the CPU oracle (restatement of the reference) on `threads`
-    host threads: setup untimed, then warmup + `steps` cycles timed by wall clock."""
+def config_dict(cfg):
+    """The workload description, identical in both arms."""
+    return {"workload": f"{cfg.name}: {cfg.n}^{cfg.dim} patches, m={cfg.m}, {cfg.levels} levels, "
+                        f"{'3-D' if cfg.dim == 3 else '2-D'} {cfg_points(cfg)}-point block stencil, "
+                        f"V({cfg.k},{cfg.k}), {cfg.fsai} block-FSAI t_max=1" + (f", nest={cfg.nest}" if cfg.nest else ""),
+            "config": cfg.name, "patches": cfg.n ** cfg.dim, "m": cfg.m, "levels": cfg.levels,
+            "cycle": f"V({cfg.k},{cfg.k})", "seed": cfg.seed,
+            "l2": "inputs larger than L2 (>= 14 GB streamed per cycle vs 126 MB of L2): no flush needed"}
+
+
+def cfg_points(cfg):
+    from paper_2509_06744_b200 import problems as pr
+    return len(pr.level_offsets(cfg.scaled(cfg.n, 1))[0])
+
+
+# ------------------------------------------------------------------ byte model (both arms)
+def cycle_bytes_model(levels, kpre, kpost, n0):
+    """Algorithmic bytes of one V(kpre, kpost) cycle from per-level structure
+    (coarsest first): dict(n, a_pass, m_pass, r_pass, p_pass) -- the same model as
+    the device's bmg_hier_cycle_bytes (hierarchy.cu), so the CPU legs scale with it."""
+    tot = 0
+    top = len(levels) - 1
+    for l in range(1, top + 1):
+        s = levels[l]
+        n, nc = s["n"], levels[l - 1]["n"]
+        apass = s["a_pass"] + 24 * n
+        gvec = 16 * n + 40 * n
+        lvl = (kpre + kpost) * (apass + s["m_pass"] + gvec)
+        if l < top and kpre > 0:
+            lvl -= apass + 8 * n
+        lvl += apass
+        lvl += s["r_pass"] + 8 * n + 8 * nc
+        lvl += s["p_pass"] + 8 * nc + 16 * n
+        tot += lvl
+    nt = (n0 + 63) // 64
+    one = nt * (nt + 1) // 2 * 64 * 64 * 8 + 16 * n0 + 2 * nt * nt * 64 * 8
+    tot += 2 * one if n0 * n0 >= (1 << 31) - 1 else one
+    return tot
+
+
+def oracle_levels(oh, m):
+    """Per-level structure of an oracle hierarchy for cycle_bytes_model."""
+    def pass_bytes(mat, mr, mc):
+        return mat.info()["nnzb"] * (8 * mr * mc + 4)
+    out = []
+    for l in range(oh.levels()):
+        A = oh.A(l)
+        s = {"n": A.info()["dim_r"], "a_pass": pass_bytes(A, m, m)}
+        if l >= 1:
+            f = oh.fsai(l)
+            mp = sum(pass_bytes(f.factor(k), m, m) for k in range(f.chain_len() - 1)) + pass_bytes(f.G(), m, m)
+            s["m_pass"] = 2 * mp
+            s["r_pass"] = s["p_pass"] = pass_bytes(oh.P(l), m, m)
+        out.append(s)
+    return out
+
+
+# ------------------------------------------------------------------ CPU oracle legs
+def oracle_sample(cfg, steps, warmup, threads, single_core=False):
+    """Oracle V-cycles on CPU_SAMPLE[cfg]: setup untimed, `warmup` + `steps` cycles
+    timed by wall clock on `threads` threads; the rate is scaled to the full config
+    by the ratio of algorithmic bytes per cycle."""
     from oracle import pyoracle as O
     from paper_2509_06744_b200 import problems as pr
 
+    spec = CPU_SAMPLE.get(cfg.name)
+    scfg = cfg if spec is None else pr.CONFIGS[spec[0]].scaled(spec[1], spec[2])
     O.set_threads(threads)
-    A, T, b = pr.make_problem(cfg)
+    A, T, b = pr.make_problem(scfg)
     t0 = time.perf_counter()
-    H = O.Hierarchy(O.Mat(A), [O.Mat(p) for p in T], t_max=1, tau=1.0, nest=cfg.nest,
-                    fsai_kind=0 if cfg.fsai == "static" else 3, coarse_dim_cap=1 << 30, probe=False)
+    oh = O.Hierarchy(O.Mat(A), [O.Mat(p) for p in T], t_max=1, tau=1.0, nest=scfg.nest,
+                     fsai_kind=0 if scfg.fsai == "static" else 3, coarse_dim_cap=1 << 30, probe=False)
     setup_s = time.perf_counter() - t0
+    del A, T
+    n0 = oh.A(0).info()["dim_r"]
+    sample_bytes = cycle_bytes_model(oracle_levels(oh, scfg.m), scfg.k, scfg.k, n0)
     x = np.zeros_like(b)
     for _ in range(warmup):
-        x = H.v_cycle(cfg.k, cfg.k, b, x)
+        x = oh.v_cycle(scfg.k, scfg.k, b, x)
     t0 = time.perf_counter()
     for _ in range(steps):
-        x = H.v_cycle(cfg.k, cfg.k, b, x)
+        x = oh.v_cycle(scfg.k, scfg.k, b, x)
     dt = time.perf_counter() - t0
-    if single_core is not None:
-        # the reference itself is single-threaded (SURVEY.md §0.1): one cycle on one
-        # thread is its faithful per-cycle cost
+    rate = steps / dt
+    full_bytes = CYCLE_BYTES.get(cfg.name) if spec is not None else sample_bytes
+    scale = sample_bytes / full_bytes if full_bytes else None
+    out = {"rate_sample": rate, "sample": scfg.name, "sample_bytes": sample_bytes, "setup_s": setup_s, "dt": dt,
+           "steps": steps, "scale": scale, "value": rate * scale if scale else None}
+    if single_core:  # the reference itself is single-threaded (SURVEY.md §0.1)
         O.set_threads(1)
         t1 = time.perf_counter()
-        x = H.v_cycle(cfg.k, cfg.k, b, x)
-        single_core.append(1.0 / (time.perf_counter() - t1))
+        x = oh.v_cycle(scfg.k, scfg.k, b, x)
+        r1 = 1.0 / (time.perf_counter() - t1)
+        out["single_core"] = {"rate_sample": r1, "value": r1 * scale if scale else None}
         O.set_threads(threads)
-    return steps / dt, setup_s, dt
+    return out
+
+
+def sample_text(s, threads, cfg):
+    if s["sample"] == cfg.name:
+        return (f"{s['steps']} V-cycles of the C++ oracle (reference restatement; the reference needs Eigen3, "
+                f"absent) on {cfg.name} itself after {s['setup_s']:.0f} s untimed setup, {threads} OpenMP threads, "
+                f"CPU {cpu_info()}")
+    return (f"{s['steps']} V-cycles of the C++ oracle (reference restatement) on {s['sample']} -- {cfg.name}'s shape "
+            f"(m={cfg.m}, same stencil, FSAI, depth, V({cfg.k},{cfg.k})) on a smaller grid -- after "
+            f"{s['setup_s']:.0f} s untimed setup, {threads} OpenMP threads, CPU {cpu_info()}; measured "
+            f"{s['rate_sample']:.4g} cycles/s on the sample, scaled to {cfg.name} by the algorithmic bytes per cycle "
+            f"({s['sample_bytes'] / 1e9:.2f} GB sample vs {CYCLE_BYTES.get(cfg.name, 0) / 1e9:.1f} GB full)")
 
 
 def run_reference(args, cfg):
@@ -175,28 +278,146 @@ def run_reference(args, cfg):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    steps = max(1, args.steps)
-    warm = max(0, min(args.warmup, 3))
-    rate, setup_s, dt = oracle_vcycles(cfg, steps, warm, threads)
+    s = oracle_sample(cfg, max(1, args.steps), args.warmup, threads)
     unit = "V-cycles/s"
     line = {
         "impl": "reference",
         "metric": f"V-cycles/s ({cfg.name}, V({cfg.k},{cfg.k}))",
-        "value": rate, "unit": unit, "n_gpus": args.gpus, "steps": steps, "warmup": warm,
-        "ms_per_step": 1e3 * dt / steps, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE.md §3 generator, seed 0)",
-        "config": {"workload": f"{cfg.name}: {cfg.n}^{cfg.dim} patches, m={cfg.m}, {cfg.levels} levels, "
-                               f"V({cfg.k},{cfg.k}), {cfg.fsai} block-FSAI t_max=1"},
-        "cpu_baseline": {"value": rate, "unit": unit, "cores": threads, "kind": "port",
-                         "sample": f"{steps} V-cycles of the C++ oracle (reference restatement; the reference "
-                                   f"itself needs Eigen3, absent) after {setup_s:.0f}s untimed setup; "
-                                   f"CPU {cpu_info()}"},
-        "e2e": {"value": rate, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "value": s["value"], "unit": unit, "n_gpus": args.gpus, "steps": max(1, args.steps), "warmup": args.warmup,
+        "ms_per_step": 1e3 / s["value"] if s["value"] else None, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE.md §3 generator bmggen/, seed 0)",
+        "config": config_dict(cfg),
+        "cpu_baseline": {"value": s["value"], "unit": unit, "cores": threads, "kind": "port",
+                         "sample": sample_text(s, threads, cfg)},
+        "e2e": {"value": s["value"], "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-# ------------------------------------------------------------------ GPU arm
+# ------------------------------------------------------------------ GPU arm helpers
+def setup_params(cfg):
+    from paper_2509_06744_b200 import default_params
+    return default_params(t_max=1, tau=1.0, nest=cfg.nest, coarse_dim_cap=1 << 30,
+                          fsai_kind=0 if cfg.fsai == "static" else 3)
+
+
+def whole_hierarchy(ctx, cfg):
+    """Single-device setup (bmg_hier_setup) of the whole config; host inputs freed."""
+    from paper_2509_06744_b200 import BlockSparseMatrix, Hierarchy
+    from paper_2509_06744_b200 import problems as pr
+    A, T, b = pr.make_problem(cfg)
+    dA = BlockSparseMatrix(ctx, A)
+    dT = [BlockSparseMatrix(ctx, p) for p in T]
+    del A, T
+    H = Hierarchy.setup(dA, dT, setup_params(cfg))
+    return H, b
+
+
+def partitioned_hierarchy(ctx, cfg, world, rank, agglomerate):
+    """This rank's share of the distributed setup (bmg_hier_setup_dist): the
+    generator produces only the plan's extended strips for this rank."""
+    from paper_2509_06744_b200 import BlockSparseMatrix, Hierarchy
+    from paper_2509_06744_b200 import problems as pr
+    params = setup_params(cfg)
+    _, _, gran, rad = pr.level_grid(cfg)
+    A_ext, T_ext, b_own, _ = pr.dist_inputs(cfg, world, rank, agglomerate, params)
+    H = Hierarchy.setup_dist(ctx, BlockSparseMatrix(ctx, A_ext), [BlockSparseMatrix(ctx, p) for p in T_ext], gran,
+                             rad, agglomerate, params)
+    return H, b_own
+
+
+def invariance_check(ctx, cfg, world, rank, agglomerate, all_min, cycles=2):
+    """The partitioned cycle (distributed setup, halo exchanges through the
+    context's transport) must reproduce the single-device cycle bitwise on every
+    rank's rows; raises otherwise.  Run on a scaled copy of the config."""
+    from paper_2509_06744_b200 import Vector
+    H1, b = whole_hierarchy(ctx, cfg)
+    x1 = Vector(ctx, b.size)
+    bv = Vector(ctx, b)
+    for _ in range(cycles):
+        H1.v_cycle(cfg.k, cfg.k, bv, x1)
+    ref = x1.download()
+    del H1, x1, bv
+    Hp, b_own = partitioned_hierarchy(ctx, cfg, world, rank, agglomerate)
+    lo = Hp.part_info(cfg.levels - 1, rank)[0]
+    xp = Vector(ctx, b_own.size)
+    bp = Vector(ctx, b_own)
+    for _ in range(cycles):
+        Hp.v_cycle(cfg.k, cfg.k, bp, xp)
+    ok = bool(np.array_equal(xp.download(), ref[lo * cfg.m:lo * cfg.m + b_own.size]))
+    if all_min(1 if ok else 0) != 1:
+        raise RuntimeError(f"partitioned V-cycle of {cfg.name} differs from the single-GPU cycle")
+    return True
+
+
+def parity_check(ctx, case):
+    """Device setup + solve to 1e-8 on an oracle fixture case (the residual-history
+    criterion of BASELINE.md §2): iteration counts and the largest |rho_gpu - rho_cpu|."""
+    from paper_2509_06744_b200 import Vector
+    from tests.golden.make_solve_golden import case_config, load, path_for
+    if not os.path.exists(path_for(case)):
+        return {"case": case, "skipped": "fixture not generated"}
+    fx = load(case)
+    cfg, _ = case_config(case)
+    H, b = whole_hierarchy(ctx, cfg)
+    bv, xv = Vector(ctx, b), Vector(ctx, b.size)
+    t0 = time.perf_counter()
+    hist, it, st = H.solve(cfg.k, cfg.k, bv, xv, cfg.tol, fx["max_iter"])
+    dt = time.perf_counter() - t0
+    ho = fx["history_f"]
+    n = min(hist.size, ho.size)
+    d = np.abs(hist[:n] / hist[0] - ho[:n] / ho[0])
+    betas = [abs(H.beta(l) - float.fromhex(fx["level"][l]["beta"])) / float.fromhex(fx["level"][l]["beta"])
+             for l in range(1, H.levels)]
+    return {"case": case, "iters_gpu": int(it), "iters_cpu": fx["iterations"], "status_gpu": int(st),
+            "status_cpu": fx["status"], "max_abs_drho": float(d.max()), "max_rel_dbeta": float(max(betas)),
+            "tol": cfg.tol, "solve_s": round(dt, 2),
+            "oracle": "tests/golden/" + os.path.basename(path_for(case))}
+
+
+def time_cycles(ctx, stream, H, bv, xv, k, steps, ws=1):
+    import torch
+    import torch.distributed as dist
+    for _ in range(3):
+        H.v_cycle(k, k, bv, xv)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        H.v_cycle(k, k, bv, xv)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def measure_batch(ctx, stream, H, b, k, K, steps, name):
+    """K independent right-hand sides per cycle, interleaved per scalar row: one
+    stream of every matrix serves all K (each RHS bitwise the single cycle)."""
+    import torch
+
+    from paper_2509_06744_b200 import Vector
+    B = np.stack([np.roll(b, 7 * v) for v in range(K)], axis=1).ravel().copy()
+    bv, xv = Vector(ctx, B), Vector(ctx, B.size)
+    for _ in range(3):
+        H.v_cycle_batch(k, k, K, bv, xv)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        H.v_cycle_batch(k, k, K, bv, xv)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    by = H.cycle_bytes(k, k, K)
+    return {"workload": f"{name} hierarchy, {K} right-hand sides per V({k},{k}) cycle (bmg_vcycle_batch)",
+            "value": K * 1e3 / ms, "unit": "right-hand-side V-cycles/s", "ms_per_batch": ms,
+            "batch_bytes": by, "effective_gbs": by / ms / 1e6}
+
+
 def measure_c1(ctx, stream, steps, with_cpu=False):
     """BASELINE configs[0] (C1): one fourth-kind smoother application, k = 3, static
     block-FSAI lower(P(A)) on the 64^2 m = 10 operator.  Working set ~0.09 GB, so
@@ -251,51 +472,81 @@ def measure_c1(ctx, stream, steps, with_cpu=False):
     return out
 
 
-def measure_hierarchy(ctx, stream, cfg, steps, batch=0):
-    """Extra line: V(k,k) cycles/s of another config's full device hierarchy (and,
-    with batch=K, the same hierarchy on K right-hand sides per cycle)."""
+def measure_extra(ctx, stream, cfg, steps, batch=0, with_cpu=False, parity=None):
+    """Extra line: V(k,k) cycles/s of another config's whole device hierarchy."""
     import torch
-
-    from paper_2509_06744_b200 import BlockSparseMatrix, Hierarchy, Vector, default_params
-    from paper_2509_06744_b200 import problems as pr
+    from paper_2509_06744_b200 import Vector
 
     t0 = time.perf_counter()
-    A, T, b = pr.make_problem(cfg)
-    dA = BlockSparseMatrix(ctx, A)
-    dT = [BlockSparseMatrix(ctx, p) for p in T]
-    del A, T
-    H = Hierarchy.setup(dA, dT, default_params(t_max=1, coarse_dim_cap=1 << 30, nest=cfg.nest))
+    H, b = whole_hierarchy(ctx, cfg)
     ctx.sync()
     setup_s = time.perf_counter() - t0
     bv, xv = Vector(ctx, b), Vector(ctx, b.size)
-    for _ in range(3):
-        H.v_cycle(cfg.k, cfg.k, bv, xv)
-    torch.cuda.synchronize()
     sampler = ClockSampler(torch.cuda.current_device())
     sampler.start()
     time.sleep(0.3)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(steps):
-        H.v_cycle(cfg.k, cfg.k, bv, xv)
-    e1.record(stream)
-    torch.cuda.synchronize()
+    ms = time_cycles(ctx, stream, H, bv, xv, cfg.k, steps)
     clocks = sampler.stop()
-    ms = e0.elapsed_time(e1) / steps
     cb = H.cycle_bytes(cfg.k, cfg.k)
     peak, _ = hbm_peak()
-    out = {"workload": f"{cfg.name}: {cfg.n}^{cfg.dim} patches, m={cfg.m}, {cfg.levels} levels, V({cfg.k},{cfg.k})",
-           "value": 1e3 / ms, "unit": "V-cycles/s", "ms_per_step": ms, "cycle_bytes": cb,
-           "effective_gbs": cb / ms / 1e6, "frac_of_roofline": cb / ms / 1e6 / peak,
+    out = {"workload": config_dict(cfg)["workload"], "value": 1e3 / ms, "unit": "V-cycles/s", "ms_per_step": ms,
+           "cycle_bytes": cb, "effective_gbs": cb / ms / 1e6, "frac_of_roofline": cb / ms / 1e6 / peak,
            "device_gb": H.device_bytes / 1e9, "setup_s": round(setup_s, 1), "clocks": clocks}
     if batch > 1:
-        try:
-            out[f"x{batch}"] = measure_batch(ctx, stream, H, b, cfg.k, batch, max(steps // 2, 3), cfg.name)
-        except Exception as e:
-            out[f"x{batch}"] = {"error": f"{type(e).__name__}: {e}"}
-    del H, dA, dT, bv, xv
+        out[f"x{batch}"] = measure_batch(ctx, stream, H, b, cfg.k, batch, max(steps // 2, 3), cfg.name)
+    del H, bv, xv
     ctx.sync()
+    if parity:
+        out["parity"] = parity_check(ctx, parity)
+    if with_cpu:
+        threads = os.cpu_count() or 1
+        s = oracle_sample(cfg, 2, 0, threads)
+        out["cpu_baseline"] = {"value": s["value"], "unit": "V-cycles/s", "cores": threads, "kind": "port",
+                               "sample": sample_text(s, threads, cfg)}
     return out
+
+
+def residual_roofline(ctx, stream, H, bv, xv, n_own, m):
+    """The dominant kernel -- the finest-level residual pass r = b - A x
+    (bsr_stream_kernel<m,m,1,EpiResidual>, 2k+1 launches per cycle) -- timed alone
+    with CUDA events on the launching stream."""
+    import torch
+    from paper_2509_06744_b200 import Vector, residual
+    Af, _, _ = H.level(H.levels - 1)
+    rv = Vector(ctx, n_own)
+    reps = 20
+    residual(Af, bv, xv, rv)
+    torch.cuda.synchronize()
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k0.record(stream)
+    for _ in range(reps):
+        residual(Af, bv, xv, rv)
+    k1.record(stream)
+    torch.cuda.synchronize()
+    kern_ms = k0.elapsed_time(k1) / reps
+    inf = Af.info()
+    kern_bytes = inf["pass_bytes"] + 24 * n_own
+    achieved = kern_bytes / (kern_ms / 1e3) / 1e9
+    try:
+        rpeak = read_peak_gbs()
+    except Exception:
+        rpeak = None
+    peak, peak_kind = hbm_peak()
+    traffic, tsrc = None, None
+    try:
+        with open(TRAFFIC_FILE) as f:
+            t = json.load(f)
+        ent = t.get(f"residual_m{m}")
+        if ent and ent.get("algorithmic_bytes") == kern_bytes:
+            traffic, tsrc = ent["dram_bytes_per_launch"], ent["source"]
+    except Exception:
+        pass
+    return {"bound": "hbm", "kernel": f"bsr_stream_kernel<{m},{m},1,EpiResidual> (finest A, r = b - A x)",
+            "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "traffic_source": tsrc, "traffic_over_algorithmic": (traffic / kern_bytes)
+            if traffic else None, "frac_of_nominal_8000": achieved / 8000.0, "read_peak_gbs": rpeak,
+            "frac_of_read_peak": (achieved / rpeak) if rpeak else None, "bytes_per_launch": kern_bytes,
+            "ms_per_launch": kern_ms}
 
 
 def run_ours(args, cfg):
@@ -307,10 +558,9 @@ def run_ours(args, cfg):
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    from paper_2509_06744_b200 import BlockSparseMatrix, Context, Hierarchy, Vector, default_params, residual
+    from paper_2509_06744_b200 import Context, Vector
     from paper_2509_06744_b200 import problems as pr
 
-    mode = "single GPU"
     if ws > 1:
         uid = [Context.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
@@ -320,78 +570,47 @@ def run_ours(args, cfg):
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
 
-    A, T, b = pr.make_problem(cfg)
-    dA = BlockSparseMatrix(ctx, A)
-    dT = [BlockSparseMatrix(ctx, p) for p in T]
+    def all_min(v):
+        if ws == 1:
+            return v
+        t = torch.tensor([v], device="cuda", dtype=torch.int64)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return int(t.item())
+
+    agglomerate = AGGLOMERATE.get(cfg.name, 1)
+    run_info = {}
     t0 = time.perf_counter()
-    params = default_params(t_max=1, tau=1.0, nest=cfg.nest, coarse_dim_cap=1 << 30,
-                            fsai_kind=0 if cfg.fsai == "static" else 3)
-    H = Hierarchy.setup(dA, dT, params)
-    granule = [(cfg.n >> (cfg.levels - 1 - l)) ** (cfg.dim - 1) for l in range(cfg.levels)]
-    agglomerate = 1  # the dense coarsest level on rank 0; every other level stays split
-    cycle_bytes = H.cycle_bytes(cfg.k, cfg.k)
-    n = A.dim_r
-    lo_row, hi_row = 0, A.nbr
-    scaling = "weak" if (ws > 1 and args.replicas) else "strong"
     if ws > 1 and not args.replicas:
-        try:
-            # reference result of two unpartitioned cycles (every rank has the whole hierarchy)
-            H.partition(1, granule)
-            x_ref = Vector(ctx, n)
-            b_all = Vector(ctx, b)
-            for _ in range(2):
-                H.v_cycle(cfg.k, cfg.k, b_all, x_ref)
-            x_ref_h = x_ref.download()
-            del x_ref, b_all
-            del H
-            try:
-                # the scalable route: every rank builds only its extended strips
-                # (bmg_hier_setup_dist); no rank holds a whole partitioned level
-                _, _, gran_l, rad_l = pr.level_grid(cfg)
-                A_ext, T_ext, _, _ = pr.dist_inputs(cfg, ws, rank, agglomerate, params)
-                H = Hierarchy.setup_dist(ctx, BlockSparseMatrix(ctx, A_ext),
-                                         [BlockSparseMatrix(ctx, p) for p in T_ext], gran_l, rad_l, agglomerate,
-                                         params)
-                del A_ext, T_ext
-                setup_kind = "distributed setup"
-            except Exception as e:  # every rank builds the whole hierarchy and keeps its strip
-                H = Hierarchy.setup(dA, dT, params)
-                H.partition(ws, granule, agglomerate=agglomerate, rank=rank)
-                setup_kind = f"replicated setup ({type(e).__name__} in the distributed one)"
-            lo_row, hi_row, _, _ = H.part_info(cfg.levels - 1, rank)
-            # the partitioned cycle must reproduce it bitwise on every rank's strip
-            m_ = cfg.m
-            bp = Vector(ctx, np.ascontiguousarray(b[lo_row * m_:hi_row * m_]))
-            xp = Vector(ctx, (hi_row - lo_row) * m_)
-            for _ in range(2):
-                H.v_cycle(cfg.k, cfg.k, bp, xp)
-            ok = bool(np.array_equal(xp.download(), x_ref_h[lo_row * m_:hi_row * m_]))
-            flags = torch.tensor([1 if ok else 0], device="cuda")
-            dist.all_reduce(flags, op=dist.ReduceOp.MIN)
-            if flags.item() != 1:
-                raise RuntimeError("partitioned V-cycle differs from the 1-GPU cycle")
-            del bp, xp
-            mode = (f"row strips x{ws} ({setup_kind}, NCCL halos, coarsest {agglomerate} level(s) on rank 0; "
-                    f"verified bitwise against the 1-GPU cycle)")
-            scaling = "strong"
-        except Exception as e:  # keep the run alive: independent replicas instead
-            H = Hierarchy.setup(dA, dT, params)
-            lo_row, hi_row = 0, A.nbr
-            mode = f"replicas x{ws} (partitioned path failed: {type(e).__name__}: {e})"
-            scaling = "weak"
-    elif ws > 1:
-        mode = f"replicas x{ws}"
+        # partition invariance through the real transport on a scaled copy first
+        small = cfg.scaled(max(cfg.n // 4, 2 ** (cfg.levels + 1)))
+        invariance_check(ctx, small, ws, rank, agglomerate, all_min)
+        H, b_own = partitioned_hierarchy(ctx, cfg, ws, rank, agglomerate)
+        scaling = "strong"
+        run_info["parallelism"] = (f"row strips x{ws} (distributed setup, NCCL halo exchanges in the captured cycle, "
+                                   f"coarsest {agglomerate} level(s) on rank 0; verified bitwise against the 1-GPU "
+                                   f"cycle on {small.name})")
+        plan = pr.memory_plan(cfg, ws, agglomerate, setup_params(cfg))
+        run_info["memory_plan_gb"] = [round(p["peak_gb"], 1) for p in plan]
     else:
-        H.partition(1, granule)  # residual-norm segmentation identical to the N-GPU runs
+        H, b_own = whole_hierarchy(ctx, cfg)
+        if ws == 1:
+            H.partition(1, pr.level_grid(cfg)[2])  # residual-norm segmentation as in the N-GPU runs
+        scaling = "weak" if ws > 1 else "strong"
+        run_info["parallelism"] = f"replicas x{ws}" if ws > 1 else "single GPU"
     ctx.sync()
     setup_s = time.perf_counter() - t0
-    m = cfg.m
-    b_own = np.ascontiguousarray(b[lo_row * m:hi_row * m])
-    n_own = b_own.size
-    bv = Vector(ctx, b_own)
-    xv = Vector(ctx, n_own)
-    k = cfg.k
+    dev = torch.tensor([H.device_bytes / 1e9], device="cuda")
+    if ws > 1:
+        gathered = [torch.zeros_like(dev) for _ in range(ws)]
+        dist.all_gather(gathered, dev)
+        run_info["rank_device_gb"] = [round(float(g.item()), 1) for g in gathered]
+    else:
+        run_info["rank_device_gb"] = [round(float(dev.item()), 1)]
+    run_info["setup_s"] = round(setup_s, 2)
 
+    m, k = cfg.m, cfg.k
+    n_own = b_own.size
+    bv, xv = Vector(ctx, b_own), Vector(ctx, n_own)
     for _ in range(max(args.warmup, 3)):
         H.v_cycle(k, k, bv, xv)
     torch.cuda.synchronize()
@@ -421,41 +640,21 @@ def run_ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_per = ms / args.steps
-    rate = (1 if scaling == "strong" else ws) * args.steps / (ms / 1e3)
+    mult = ws if scaling == "weak" else 1
+    rate = mult * args.steps / (ms / 1e3)
     cycle_bytes = H.cycle_bytes(k, k)
+    if ws > 1 and scaling == "strong":  # every rank's share of the cycle's bytes
+        cb = torch.tensor([float(cycle_bytes)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(cb)
+        cycle_bytes = int(cb.item())
     peak, peak_kind = hbm_peak()
-    eff_gbs = (1 if scaling == "strong" else ws) * cycle_bytes / (ms_per / 1e3) / 1e9
+    eff_gbs = mult * cycle_bytes / (ms_per / 1e3) / 1e9
+    if ws == 1 and cfg.name in CYCLE_BYTES and CYCLE_BYTES[cfg.name] != cycle_bytes:
+        run_info["cycle_bytes_table_mismatch"] = {"table": CYCLE_BYTES[cfg.name], "device": cycle_bytes}
 
-    # ---- dominant kernel: finest-level residual pass r = b - A x (2k+1 per cycle)
-    Af, _, _ = H.level(H.levels - 1)
-    rv = Vector(ctx, n_own)
-    reps = 20
-    residual(Af, bv, xv, rv)
-    torch.cuda.synchronize()
-    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    k0.record(stream)
-    for _ in range(reps):
-        residual(Af, bv, xv, rv)
-    k1.record(stream)
-    torch.cuda.synchronize()
-    kern_ms = k0.elapsed_time(k1) / reps
-    inf = Af.info()
-    kern_bytes = inf["pass_bytes"] + 24 * n_own
-    achieved = kern_bytes / (kern_ms / 1e3) / 1e9
-    try:
-        rpeak = read_peak_gbs()
-    except Exception:
-        rpeak = None
-    traffic = None
-    tfile = os.path.join(ROOT, "profiles", "latest_traffic.json")
-    if os.path.exists(tfile):
-        try:
-            with open(tfile) as f:
-                traffic = json.load(f).get("residual_dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    roof = residual_roofline(ctx, stream, H, bv, xv, n_own, m)
 
-    # ---- e2e through the public C ABI with pinned host buffers
+    # ---- e2e through the public C ABI (bmg_vcycle_host) with pinned host buffers
     hb = torch.from_numpy(b_own).pin_memory()
     hx = torch.zeros(n_own, dtype=torch.float64).pin_memory()
     for _ in range(2):
@@ -474,54 +673,54 @@ def run_ours(args, cfg):
         t = torch.tensor([e2e_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    e2e_rate = (1 if scaling == "strong" else ws) * args.steps / (e2e_ms / 1e3)
+    e2e_rate = mult * args.steps / (e2e_ms / 1e3)
+    del hb, hx
 
     extra = None
+    parity = None
+    cpu = None
     if rank == 0 and ws == 1:
         extra = {}
-        try:
-            extra["C1"] = measure_c1(ctx, stream, args.steps, with_cpu=not args.no_cpu_baseline)
-        except Exception as e:  # secondary lines never fail the headline run
-            extra["C1"] = {"error": f"{type(e).__name__}: {e}"}
-        try:  # the same hierarchy on 8 right-hand sides per cycle (bmg_vcycle_batch)
-            extra["C2x8"] = measure_batch(ctx, stream, H, b_own, k, 8, args.steps)
-        except Exception as e:
-            extra["C2x8"] = {"error": f"{type(e).__name__}: {e}"}
-        if not args.no_c4 or not args.no_quarter:
-            # the large lines: free the headline hierarchy first
-            del H, dA, dT, bv, xv, rv
-            ctx.sync()
-        if not args.no_quarter:
-            # C3 and C5 do not fit one GPU; their shapes (C3: nested FSAI, m = 21, 25-pt,
-            # V(4,4), 5 levels; C5: m = 15, 6 levels) at a quarter of the rows do
-            for key, c in (("C3@512", pr.CONFIGS["C3"].scaled(512)), ("C5@1024", pr.CONFIGS["C5"].scaled(1024))):
+        if not args.no_batch:
+            try:  # the same hierarchy on 4 right-hand sides per cycle (bmg_vcycle_batch)
+                extra[f"{cfg.name}x4"] = measure_batch(ctx, stream, H, b_own, k, 4, max(args.steps // 2, 3), cfg.name)
+            except Exception as e:
+                extra[f"{cfg.name}x4"] = {"error": f"{type(e).__name__}: {e}"}
+        del H, bv, xv
+        ctx.sync()
+        torch.cuda.empty_cache()
+        if not args.no_parity and cfg.name in PARITY_CASE:
+            parity = parity_check(ctx, PARITY_CASE[cfg.name])
+        if not args.no_cpu_baseline:
+            threads = os.cpu_count() or 1
+            s = oracle_sample(cfg, 2, 1, threads, single_core=not args.no_single_core)
+            cpu = {"value": s["value"], "unit": "V-cycles/s", "cores": threads, "kind": "port",
+                   "sample": sample_text(s, threads, cfg)}
+            if "single_core" in s:
+                cpu["single_core"] = {"value": s["single_core"]["value"], "unit": "V-cycles/s", "cores": 1,
+                                      "sample": "1 V-cycle of the same sample on one thread, scaled the same way "
+                                                "(the reference is single-threaded, SURVEY.md §0.1)"}
+        if not args.no_extra:
+            try:
+                extra["C1"] = measure_c1(ctx, stream, args.steps, with_cpu=not args.no_cpu_baseline)
+            except Exception as e:  # secondary lines never fail the headline run
+                extra["C1"] = {"error": f"{type(e).__name__}: {e}"}
+            others = [("C2", pr.CONFIGS["C2"], 8, True, "C2")]
+            others += [("C3@512", pr.CONFIGS["C3"].scaled(512), 0, False, None),
+                       ("C5@1024", pr.CONFIGS["C5"].scaled(1024), 0, False, None)]
+            if cfg.name != "C4":
+                others.append(("C4", pr.CONFIGS["C4"], 4, False, None))
+            for key, c, batch, with_cpu, par in others:
+                if c.name == cfg.name:
+                    continue
                 try:
-                    extra[key] = measure_hierarchy(ctx, stream, c, min(args.steps, 10))
-                    extra[key]["note"] = "reduced size: a quarter of the named config's fine rows, same shape"
+                    extra[key] = measure_extra(ctx, stream, c, min(args.steps, 10), batch,
+                                               with_cpu=with_cpu and not args.no_cpu_baseline, parity=par)
+                    if "@" in key:
+                        extra[key]["note"] = "reduced size: a quarter of the named config's fine rows, same shape"
                 except Exception as e:
                     extra[key] = {"error": f"{type(e).__name__}: {e}"}
-        if not args.no_c4:
-            try:
-                free = torch.cuda.mem_get_info()[0]
-                if free < 125e9:
-                    extra["C4"] = {"skipped": f"needs ~115 GB free, {free / 1e9:.0f} GB available"}
-                else:
-                    extra["C4"] = measure_hierarchy(ctx, stream, pr.CONFIGS["C4"], min(args.steps, 10), batch=4)
-            except Exception as e:
-                extra["C4"] = {"error": f"{type(e).__name__}: {e}"}
-
-    # ---- CPU baseline (rank 0, N = 1 only): bounded oracle sample
-    cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        threads = os.cpu_count() or 1
-        one = [] if not args.no_single_core else None
-        crate, csetup, cdt = oracle_vcycles(cfg, 2, 0, threads, one)
-        cpu = {"value": crate, "unit": "V-cycles/s", "cores": threads, "kind": "port",
-               "sample": f"2 V-cycles of the C++ oracle (reference restatement) on {cfg.name} after "
-                         f"{csetup:.0f}s untimed setup, {threads} OpenMP threads, CPU {cpu_info()}"}
-        if one:
-            cpu["single_core"] = {"value": one[0], "unit": "V-cycles/s", "cores": 1,
-                                  "sample": f"1 V-cycle of the oracle on one thread ({cfg.name}, same hierarchy)"}
+                torch.cuda.empty_cache()
 
     if rank == 0:
         line = {
@@ -536,26 +735,20 @@ def run_ours(args, cfg):
             "scaling": scaling,
             "vs_baseline": None,
             "dtype": "f64",
-            "data": "synthetic (BASELINE.md §3 generator, seed 0; random-init hierarchy built on the device)",
-            "config": {"workload": f"{cfg.name}: {cfg.n}^{cfg.dim} patches, m={cfg.m}, {cfg.levels} levels, "
-                                   f"V({k},{k}), {cfg.fsai} block-FSAI t_max=1",
-                       "parallelism": mode,
-                       "l2": "inputs larger than L2 (>= 14 GB streamed per cycle)",
-                       "setup_s": round(setup_s, 2)},
+            "data": "synthetic (BASELINE.md §3 generator bmggen/, seed 0; hierarchy built on the device)",
+            "config": config_dict(cfg),
+            "run": run_info,
             "effective_gbs": eff_gbs,
             "cycle_bytes": cycle_bytes,
             "frac_of_roofline_cycle": eff_gbs / peak,
-            "roofline": {"bound": "hbm", "kernel": "bsr_stream_kernel<10,10,1,EpiResidual> (finest A, r = b - A x)",
-                         "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "frac_of_nominal_8000": achieved / 8000.0,
-                         "read_peak_gbs": rpeak, "frac_of_read_peak": (achieved / rpeak) if rpeak else None,
-                         "bytes_per_launch": kern_bytes, "ms_per_launch": kern_ms},
+            "roofline": roof,
             "clocks": clocks,
             "e2e": {"value": e2e_rate, "unit": "V-cycles/s", "h2d_bytes_per_step": 2 * 8 * n_own,
-                    "d2h_bytes_per_step": 8 * n_own},
+                    "d2h_bytes_per_step": 8 * n_own, "path": "bmg_vcycle_host (C ABI), pinned host b and x"},
             "gpu_launches": launches,
         }
+        if parity is not None:
+            line["parity"] = parity
         if cpu is not None:
             line["cpu_baseline"] = cpu
         if extra is not None:
@@ -565,42 +758,19 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
 
 
-def measure_batch(ctx, stream, H, b, k, K, steps, name="C2"):
-    """K independent right-hand sides per cycle, interleaved per scalar row: one
-    stream of every matrix serves all K (each RHS bitwise the single cycle)."""
-    import torch
-
-    from paper_2509_06744_b200 import Vector
-    B = np.stack([np.roll(b, 7 * v) for v in range(K)], axis=1).ravel().copy()
-    bv, xv = Vector(ctx, B), Vector(ctx, B.size)
-    for _ in range(3):
-        H.v_cycle_batch(k, k, K, bv, xv)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(steps):
-        H.v_cycle_batch(k, k, K, bv, xv)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / steps
-    by = H.cycle_bytes(k, k, K)
-    return {"workload": f"{name} hierarchy, {K} right-hand sides per V({k},{k}) cycle (bmg_vcycle_batch)",
-            "value": K * 1e3 / ms, "unit": "right-hand-side V-cycles/s", "ms_per_batch": ms,
-            "batch_bytes": by, "effective_gbs": by / ms / 1e6}
-
-
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C4")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of row strips")
-    ap.add_argument("--no-c4", action="store_true", help="skip the extra C4 (largest single-GPU config) line")
+    ap.add_argument("--no-extra", action="store_true", help="skip the extra config lines (C1, C2, C3/C5 shapes)")
+    ap.add_argument("--no-batch", action="store_true", help="skip the 4-right-hand-side line")
+    ap.add_argument("--no-parity", action="store_true", help="skip the solve-to-1e-8 parity check")
     ap.add_argument("--no-single-core", action="store_true", help="skip the 1-thread oracle cycle")
-    ap.add_argument("--no-quarter", action="store_true", help="skip the quarter-size C3 / C5 shape lines")
     args = ap.parse_args()
     from paper_2509_06744_b200 import problems as pr
 

@@ -283,3 +283,84 @@ def fd_biharmonic(n_grid: int, levels: int) -> FdProblem:
         b[r] = acc
     transfers = [fd_prolongation(n_grid >> (levels - 1 - l)) for l in range(1, levels)]
     return FdProblem(A, transfers, b, ref, mass, h)
+
+
+# ---------------------------------------------------------------------------
+# per-rank memory plan of the distributed setup (bmg_dist_plan strips), from the
+# structure alone: no matrix is generated.  Upper bounds, printed by bench.py and
+# tools/dist_memory_plan.py so a C3 / C5 run is sized before it starts.
+def level_offsets(cfg: Config):
+    """Per level (coarsest first) the block-column offsets an interior row of A_l
+    holds: S_p = L_D^p couples offsets with |o|_1 <= p; Galerkin P^T A P (P row i:
+    parents(i) + {-1,0,1}^d) maps a fine offset o of a child with parity x to
+    floor((x + o) / 2) + {-2..2}^d on the coarse grid.  Rows near the boundary hold
+    the subset that stays on the grid (or fewer): the counts are upper bounds."""
+    import itertools
+    d = cfg.dim
+    rng = range(-cfg.power, cfg.power + 1)
+    fine = {o for o in itertools.product(rng, repeat=d) if sum(abs(v) for v in o) <= cfg.power}
+    sets = [fine]
+    for _ in range(cfg.levels - 1):
+        cur = sets[-1]
+        base = {tuple((x[k] + o[k]) // 2 for k in range(d)) for o in cur for x in itertools.product((0, 1), repeat=d)}
+        nxt = {tuple(b[k] + e[k] for k in range(d)) for b in base for e in itertools.product(range(-2, 3), repeat=d)}
+        sets.append(nxt)
+    return sets[::-1]
+
+
+def _count_rows(offsets, n, dim, lo_g, hi_g):
+    """sum over grid rows with outermost index in [lo_g, hi_g) of the offsets that
+    stay on the n^dim grid"""
+    tot = 0
+    for o in offsets:
+        inner = 1
+        for k in range(dim - 1):
+            inner *= max(0, n - abs(o[k]))
+        oz = o[dim - 1]
+        lo, hi = max(lo_g, -oz, 0), min(hi_g, n - oz, n)
+        tot += inner * max(0, hi - lo)
+    return tot
+
+
+def memory_plan(cfg: Config, world: int, agglomerate: int = 1, params=None):
+    """Per-rank device bytes (upper bounds) of the partitioned hierarchy built by
+    bmg_hier_setup_dist: own rows of A_l (padded 16-byte blocks + int32 column),
+    the FSAI chain and its transposes (t_max = 1: <= 2 blocks per row per factor),
+    P_l / R_l, six work vectors over the extended window, and on rank 0 the
+    agglomerated levels plus the packed coarse inverse; `peak` adds the setup's
+    transient extended strip of A and the 4 GB Galerkin chunk.  Returns a list of
+    dicts (one per rank) in GB."""
+    from .api import dist_plan
+    ns, nbr, gran, rad = level_grid(cfg)
+    L = cfg.levels
+    offs = level_offsets(cfg)
+    bounds, elo, ehi, _ = dist_plan(nbr, gran, rad, world, agglomerate, params)
+    m, d = cfg.m, cfg.dim
+    blk = 8 * (m * m + (m * m) % 2) + 4
+    nfac = 2 * (cfg.nest + 1)  # forward factors and their transposes
+    agg = max(1, min(agglomerate, L - 1))
+    out = []
+    for r in range(world):
+        steady = peak_extra = 0
+        for l in range(L):
+            n = ns[l]
+            whole = l < agg
+            if whole and r != 0:
+                continue
+            lo, hi = (0, nbr[l]) if whole else (int(bounds[l, r]), int(bounds[l, r + 1]))
+            elo_, ehi_ = (0, nbr[l]) if whole else (int(elo[l, r]), int(ehi[l, r]))
+            g = gran[l]
+            if l == 0:  # dense coarse level: packed lower 64x64 tiles of the inverse
+                n0 = nbr[0] * m
+                nt = (n0 + 63) // 64
+                steady += nt * (nt + 1) // 2 * 64 * 64 * 8 + nt * nt * 64 * 8
+                peak_extra = max(peak_extra, 8 * n0 * n0 - nt * (nt + 1) // 2 * 64 * 64 * 8)
+                continue
+            a_own = _count_rows(offs[l], n, d, lo // g, -(-hi // g)) * blk
+            a_ext = _count_rows(offs[l], n, d, elo_ // g, -(-ehi_ // g)) * blk
+            steady += a_own + nfac * 2 * (hi - lo) * blk
+            steady += 2 * (hi - lo) * 3 ** d * blk          # P_l rows and their share of R_l
+            steady += 6 * (ehi_ - elo_) * m * 8             # work vectors over the window
+            peak_extra = max(peak_extra, a_ext + (4 << 30))
+        out.append({"rank": r, "steady_gb": steady / 1e9, "peak_gb": (steady + peak_extra) / 1e9})
+    return out

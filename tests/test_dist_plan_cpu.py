@@ -53,3 +53,38 @@ def test_plan_rejects_bad_input():
         dist_plan([4], [2], [1], 2)
     with pytest.raises(InvalidArgument):
         dist_plan([4, 16], [2, 4], [1, 1], 0)
+
+
+@pytest.mark.parametrize("name,n,levels", [("C5", 32, 3), ("C4", 8, 3), ("C3", 16, 3)])
+def test_structural_offsets_bound_the_galerkin_levels(name, n, levels):
+    # problems.level_offsets (the memory plan's structure) against the oracle's
+    # Galerkin operators: every row holds at most the offsets on the grid, and
+    # interior-dominated levels match exactly
+    from oracle import pyoracle as O
+    cfg = pr.CONFIGS[name].scaled(n, levels)
+    A, T, _ = pr.make_problem(cfg)
+    Ac = O.Mat(A)
+    ns, nbr, gran, _ = pr.level_grid(cfg)
+    offs = pr.level_offsets(cfg)
+    mats = [None] * levels
+    mats[-1] = Ac
+    for l in range(levels - 1, 0, -1):
+        mats[l - 1] = O.galerkin(mats[l], O.Mat(T[l - 1]))
+    for l in range(levels):
+        actual = mats[l].info()["nnzb"]
+        bound = pr._count_rows(offs[l], ns[l], cfg.dim, 0, ns[l])
+        assert actual <= bound, (l, actual, bound)
+        if l == levels - 1:
+            assert actual == bound  # the fine stencil itself
+
+
+def test_memory_plan_fits_c3_c5_from_four_gpus():
+    # BASELINE C3 / C5 do not fit one B200; from 4 ranks (coarsest two levels on
+    # rank 0) every rank's setup peak stays under the 180 GB of HBM
+    for name in ("C3", "C5"):
+        cfg = pr.CONFIGS[name]
+        assert max(p["peak_gb"] for p in pr.memory_plan(cfg, 1, 2)) > 180
+        for world in (4, 8):
+            plan = pr.memory_plan(cfg, world, 2)
+            assert len(plan) == world
+            assert max(p["peak_gb"] for p in plan) < 180, (name, world, plan)
