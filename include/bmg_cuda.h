@@ -119,6 +119,12 @@ int bmg_bsr_destroy(bmg_bsr* a);
  * streaming pass (nnzb * (8 m_r m_c + 4)) */
 int bmg_bsr_info(const bmg_bsr* a, int* nbr, int* nbc, int64_t* nnzb, int* dim_r, int* dim_c,
                  int64_t* device_bytes, int64_t* pass_bytes);
+/* symmetric-half streaming (hierarchy setup builds it for every smoothed level's A
+ * that is exactly symmetric and keeps it where it measured faster): whether the
+ * residual / spmv passes of `a` run on the lower triangle (bitwise the same
+ * results), the algorithmic bytes of one such pass, and the measured pass times
+ * (ms) of both forms (0 when not measured) */
+int bmg_bsr_sym_info(const bmg_bsr* a, int* half, int64_t* pass_bytes, double* half_ms, double* full_ms);
 int bmg_bsr_download(const bmg_bsr* a, int64_t* row_ptr, int32_t* col_idx, double* vals);
 /* device-built transpose (values transposed per block) */
 int bmg_bsr_transpose(const bmg_bsr* a, bmg_bsr** out);
@@ -202,6 +208,9 @@ int bmg_hier_level(const bmg_hier* h, int level, const bmg_bsr** a, const bmg_bs
 /* algorithmic HBM bytes of one V(k_pre,k_post) cycle on the finest level */
 int bmg_hier_cycle_bytes(const bmg_hier* h, int k_pre, int k_post, int64_t* bytes);
 int bmg_hier_cycle_bytes_batch(const bmg_hier* h, int k_pre, int k_post, int nrhs, int64_t* bytes);
+/* the same cycle with every A pass counted at full storage (both halves, as the
+ * reference stores them) -- the byte model of the reference's own algorithm */
+int bmg_hier_cycle_bytes_ref(const bmg_hier* h, int k_pre, int k_post, int64_t* bytes);
 /* 1 (default) = replay each cycle from a captured CUDA graph */
 int bmg_hier_use_graph(bmg_hier* h, int on);
 int bmg_vcycle(bmg_hier* h, int k_pre, int k_post, const bmg_vec* b, bmg_vec* x);

@@ -162,6 +162,13 @@ class BlockSparseMatrix:
         return dict(nbr=a.value, nbc=b.value, nnzb=nnzb.value, dim_r=d.value, dim_c=e.value,
                     device_bytes=dev.value, pass_bytes=pb.value)
 
+    def sym_info(self) -> dict:
+        """Symmetric-half streaming of this matrix (bmg_bsr_sym_info)."""
+        h, pb = C.c_int(), C.c_int64()
+        t1, t0 = C.c_double(), C.c_double()
+        check(lib().bmg_bsr_sym_info(self.h, C.byref(h), C.byref(pb), C.byref(t1), C.byref(t0)))
+        return dict(half=bool(h.value), pass_bytes=pb.value, half_ms=t1.value, full_ms=t0.value)
+
     def download(self, row_sizes, col_sizes, symmetric=False) -> HostBsr:
         inf = self.info()
         rp = np.zeros(inf["nbr"] + 1, np.int64)
@@ -453,6 +460,12 @@ class Hierarchy:
     def cycle_bytes(self, k_pre, k_post, nrhs: int = 1) -> int:
         out = C.c_int64()
         check(lib().bmg_hier_cycle_bytes_batch(self.h, k_pre, k_post, nrhs, C.byref(out)))
+        return out.value
+
+    def cycle_bytes_ref(self, k_pre, k_post) -> int:
+        """cycle_bytes with the A passes at full storage (the reference's algorithm)."""
+        out = C.c_int64()
+        check(lib().bmg_hier_cycle_bytes_ref(self.h, k_pre, k_post, C.byref(out)))
         return out.value
 
     def partition(self, world: int, granule, agglomerate: int = 1, rank: int = -1):

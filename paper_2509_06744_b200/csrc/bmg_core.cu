@@ -232,7 +232,8 @@ int64_t Bsr::pass_bytes() const {
 int64_t Bsr::device_bytes() const {
   return (int64_t)(row_ptr.bytes() + col.bytes() + vals.bytes() + voff.bytes() + d_roff.bytes() +
                    d_coff.bytes() + d_rsz.bytes() + d_csz.bytes() + plan.chunks.bytes() +
-                   plan.cta_chunk.bytes());
+                   plan.cta_chunk.bytes()) +
+         (half ? half->bytes() : 0);
 }
 
 static bool stream_supported(int mr, int mc) {
@@ -300,6 +301,26 @@ static int stream_occupancy(size_t smem) {
   int occ = 0;
   BMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kern::kThreads, smem));
   return std::max(occ, 1);
+}
+
+template <int MR>
+static int sym_occupancy(size_t smem) {
+  auto kfn = kern::bsr_stream_kernel<MR, MR, 1, kern::EpiStore, false, true>;
+  stream_attrs(kfn, 1);
+  int occ = 0;
+  BMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kern::kThreads, smem));
+  return std::max(occ, 1);
+}
+static int sym_occupancy_for(int mr, size_t smem) {
+  switch (mr) {
+    case 3: return sym_occupancy<3>(smem);
+    case 6: return sym_occupancy<6>(smem);
+    case 10: return sym_occupancy<10>(smem);
+    case 15: return sym_occupancy<15>(smem);
+    case 20: return sym_occupancy<20>(smem);
+    case 21: return sym_occupancy<21>(smem);
+  }
+  return 1;
 }
 
 template <int MR, int MC>
@@ -408,7 +429,7 @@ static BatchChoice batch_choice(int mr, int K) {
 // rows [row0, row1) only when row1 > 0 (a row-range plan over the whole matrix's
 // storage: chunk descriptors keep absolute block and row indices)
 static void build_plan_into(const Bsr& a, Plan& P, int K, int mr, int bs, bool var = false, int row0 = 0,
-                            int row1 = 0) {
+                            int row1 = 0, bool sym = false) {
   P = Plan();
   if (row1 <= 0) row1 = a.nbr;
   if (!stream_supported(mr, mr) || a.nbr == 0 || row1 <= row0) return;
@@ -432,8 +453,9 @@ static void build_plan_into(const Bsr& a, Plan& P, int K, int mr, int bs, bool v
   // bsr_stream_kernel's SKEW layout (m = 20, K = 1, uniform): block pitch bs + 2 in shared memory
   const int spitch = (K == 1 && mr == 20 && !var) ? bs + 2 : bs;
   const size_t smem0 = P.u ? kern::BatchSmem(bs, P.cb_max, mr, mr, K, P.stages).total
-                           : kern::SmemLayout(spitch, P.cb_max, P.cb_max + 2, mr, P.stages, K).total;
-  const int occ = P.u ? batch_occupancy_for(mr, smem0, K, P.u) : occupancy_for(mr, mr, smem0, K);
+                           : kern::SmemLayout(spitch, P.cb_max, P.cb_max + 2, mr, P.stages, K, sym).total;
+  const int occ = P.u ? batch_occupancy_for(mr, smem0, K, P.u)
+                      : (sym ? sym_occupancy_for(mr, smem0) : occupancy_for(mr, mr, smem0, K));
   const int64_t gmax = (int64_t)a.ctx->sms * occ;
   const int64_t nnzb_range = a.h_row_ptr[row1] - a.h_row_ptr[row0];
   const int64_t per = std::max<int64_t>(1, (nnzb_range + gmax - 1) / gmax);
@@ -471,10 +493,12 @@ static void build_plan_into(const Bsr& a, Plan& P, int K, int mr, int bs, bool v
   P.nctas = (int)cta.size() - 1;
   P.nchunks = (int)chunks.size();
   P.smem = P.u ? kern::BatchSmem(bs, P.cb_max, mr, mr, K, P.stages).total
-               : kern::SmemLayout(spitch, P.cb_max, P.rmax, mr, P.stages, K).total;
+               : kern::SmemLayout(spitch, P.cb_max, P.rmax, mr, P.stages, K, sym).total;
   if (P.smem > 227 * 1024) fail(BMG_EINVAL, "plan: chunk does not fit in shared memory");
   if (P.u)  // sets the shared-memory attributes
     batch_occupancy_for(mr, P.smem, K, P.u);
+  else if (sym)
+    sym_occupancy_for(mr, P.smem);
   else
     occupancy_for(mr, mr, P.smem, K);
   P.chunks.alloc(chunks.size());
@@ -816,15 +840,24 @@ static bool pdl_enabled() {
   return on;
 }
 
-template <int MR, int MC, int K, class Epi, bool VAR = false>
-static void launch_stream_plan(const Bsr& a, const Plan& P, const double* x, Epi epi);
+template <int MR, int MC, int K, class Epi, bool VAR = false, bool SYM = false>
+static void launch_stream_plan(const Bsr& a, const Plan& P, const double* x, Epi epi, const SymHalf* sh = nullptr);
 template <int MR, int MC, int K, class Epi, bool VAR = false>
 static void launch_stream_t(const Bsr& a, const double* x, Epi epi) {
   launch_stream_plan<MR, MC, K, Epi, VAR>(a, plan_for(a, K), x, epi);
 }
-template <int MR, int MC, int K, class Epi, bool VAR>
-static void launch_stream_plan(const Bsr& a, const Plan& P, const double* x, Epi epi) {
+template <int MR, int MC, int K, class Epi, bool VAR, bool SYM>
+static void launch_stream_plan(const Bsr& a, const Plan& P, const double* x, Epi epi, const SymHalf* sh) {
   kern::StreamArgs s;
+  if constexpr (SYM) {
+    static const int colmap = [] {
+      const char* e = std::getenv("BMG_SYM_COLMAP");
+      return e ? std::atoi(e) : 0;
+    }();
+    s.brow = sh->brow.p;
+    s.colpart = sh->colpart.p;
+    s.colmap = colmap;
+  }
   s.vals = VAR ? a.pvals.p : a.vals.p;
   s.col = a.col.p;
   s.row_ptr = a.row_ptr.p;
@@ -844,7 +877,7 @@ static void launch_stream_plan(const Bsr& a, const Plan& P, const double* x, Epi
   s.l2hint = l2_hint_for(a);
   // one attribute per template instantiation (covers the largest plan)
   static const bool attr_set = [] {  // thread-safe one-time init (contexts may live on several threads)
-    stream_attrs(kern::bsr_stream_kernel<MR, MC, K, Epi, VAR>, K);
+    stream_attrs(kern::bsr_stream_kernel<MR, MC, K, Epi, VAR, SYM>, K);
     return true;
   }();
   (void)attr_set;
@@ -858,9 +891,46 @@ static void launch_stream_plan(const Bsr& a, const Plan& P, const double* x, Epi
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  BMG_CUDA(cudaLaunchKernelEx(&cfg, kern::bsr_stream_kernel<MR, MC, K, Epi, VAR>, s, epi));
+  BMG_CUDA(cudaLaunchKernelEx(&cfg, kern::bsr_stream_kernel<MR, MC, K, Epi, VAR, SYM>, s, epi));
   a.ctx->count();
   BMG_LAUNCHED(a.ctx->stream, "bsr_stream_kernel");
+}
+
+// A SYM pass: the lower triangle streamed (row sums to sbuf, transposed products
+// to colpart), then the merge adds the upper contributions and runs the epilogue.
+template <int MR, class Epi>
+static void launch_sym(const Bsr& a, const double* x, Epi epi) {
+  const SymHalf& H = *a.half;
+  const Bsr& low = *H.low;
+  launch_stream_plan<MR, MR, 1, kern::EpiStore, false, true>(low, low.plan, x, kern::EpiStore{H.sbuf.p}, &H);
+  const int64_t n = (int64_t)a.nbr * MR;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)a.ctx->sms * 16)));
+  cfg.blockDim = dim3(256);
+  cfg.stream = a.ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  BMG_CUDA(cudaLaunchKernelEx(&cfg, kern::sym_merge_kernel<MR, Epi>, (const int64_t*)H.up_ptr.p,
+                              (const int32_t*)H.up_slot.p, (const double*)H.colpart.p, (const double*)H.sbuf.p, n,
+                              epi));
+  a.ctx->count();
+  BMG_LAUNCHED(a.ctx->stream, "sym_merge_kernel");
+}
+template <class Epi>
+static bool try_launch_sym(const Bsr& a, const double* x, Epi epi, int nrhs) {
+  if (nrhs != 1 || !a.half) return false;
+  switch (a.mr) {
+    case 3: launch_sym<3>(a, x, epi); return true;
+    case 6: launch_sym<6>(a, x, epi); return true;
+    case 10: launch_sym<10>(a, x, epi); return true;
+    case 15: launch_sym<15>(a, x, epi); return true;
+    case 20: launch_sym<20>(a, x, epi); return true;
+    case 21: launch_sym<21>(a, x, epi); return true;
+  }
+  return false;
 }
 
 template <int MR, int K, int U, class Epi, bool XL>
@@ -994,9 +1064,201 @@ void residual_rows(const Bsr& a, const Plan& P, const double* b, const double* x
   fail(BMG_EINVAL, "residual_rows: streamed block sizes only");
 }
 
-void spmv(const Bsr& a, const double* x, double* y, int nrhs) { launch(a, x, kern::EpiStore{y}, nrhs); }
+void spmv(const Bsr& a, const double* x, double* y, int nrhs) {
+  if (try_launch_sym(a, x, kern::EpiStore{y}, nrhs)) return;
+  launch(a, x, kern::EpiStore{y}, nrhs);
+}
 void residual(const Bsr& a, const double* b, const double* x, double* r, int nrhs) {
+  if (try_launch_sym(a, x, kern::EpiResidual{b, r}, nrhs)) return;
   launch(a, x, kern::EpiResidual{b, r}, nrhs);
+}
+
+// ---- symmetric-half form ----------------------------------------------------------
+namespace kern {
+// flag = 1 if some stored off-diagonal block differs bitwise from the transpose of
+// its mirror block (warp per block)
+__global__ void sym_check_kernel(const double* __restrict__ vals, const int64_t* __restrict__ mirror, int64_t nnzb,
+                                 int m, int bs, int* __restrict__ flag) {
+  const int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (p >= nnzb) return;
+  const int64_t q = mirror[p];
+  const unsigned long long* A = reinterpret_cast<const unsigned long long*>(vals + p * bs);
+  const unsigned long long* B = reinterpret_cast<const unsigned long long*>(vals + q * bs);
+  for (int e = lane; e < m * m; e += 32) {
+    const int r = e / m, c = e - r * m;
+    if (A[r * m + c] != B[c * m + r]) atomicOr(flag, 1);
+  }
+}
+// low block q <- block src[q] (bs doubles each)
+__global__ void gather_blocks_kernel(const double* __restrict__ vals, const int64_t* __restrict__ src, int64_t nq,
+                                     int bs, double* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nq * bs; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = e / bs;
+    out[e] = vals[src[q] * bs + (e - q * bs)];
+  }
+}
+}  // namespace kern
+
+int64_t SymHalf::bytes() const {
+  return (int64_t)(low ? low->device_bytes() : 0) + (int64_t)(brow.bytes() + up_ptr.bytes() + up_slot.bytes() +
+                                                              colpart.bytes() + sbuf.bytes());
+}
+
+int64_t sym_pass_bytes(const Bsr& a) {
+  if (!a.half) return a.pass_bytes();
+  const Bsr& low = *a.half->low;
+  const int64_t nup = a.nnzb - low.nnzb;
+  const int64_t n = a.dim_r, m = a.mr;
+  // phase 1: lower blocks + column and row indices, transposed products written,
+  // row sums written; merge: row sums, partials and slots read
+  return low.nnzb * (8 * (int64_t)a.mr * a.mc + 8) + nup * m * 8 + 8 * n + 8 * n + nup * (m * 8 + 4) +
+         8 * ((int64_t)a.nbr + 1);
+}
+
+// BMG_SYM_HALF: 0 off, 1 always, unset: measured choice per matrix
+static int sym_mode() {
+  static const int v = [] {
+    const char* e = std::getenv("BMG_SYM_HALF");
+    return !e ? -1 : (e[0] == '0' ? 0 : 1);
+  }();
+  return v;
+}
+
+// Both forms give bitwise the same result; which one streams faster depends on
+// the block size and row length (m = 20: the half form saves ~1/3 of the pass
+// time; m = 10: its column dots cost what the halved bytes save).  Each is
+// timed on this matrix (3 passes after a warm one) and the faster one kept.
+// `next` (the level's G, whose pass follows every residual in the cycle) is
+// timed behind each form, so the choice includes how the pass overlaps its
+// successor under programmatic dependent launch.
+static bool sym_faster(const Bsr& a, const Bsr* next) {
+  Ctx* ctx = a.ctx;
+  const int64_t n = std::max<int64_t>(a.dim_r, 1);
+  DBuf<double> x(n), b(n), r(n), w(n);
+  BMG_CUDA(cudaMemsetAsync(x.p, 0, x.bytes(), ctx->stream));
+  BMG_CUDA(cudaMemsetAsync(b.p, 0, b.bytes(), ctx->stream));
+  cudaEvent_t e[3];
+  for (auto& v : e) BMG_CUDA(cudaEventCreate(&v));
+  auto tail = [&] {
+    if (next && next->dim_c == a.dim_r && next->dim_r <= n) launch(*next, r.p, kern::EpiStore{w.p}, 1);
+  };
+  auto sym_pass = [&] {
+    try_launch_sym(a, x.p, kern::EpiResidual{b.p, r.p}, 1);
+    tail();
+  };
+  auto full_pass = [&] {
+    launch(a, x.p, kern::EpiResidual{b.p, r.p}, 1);
+    tail();
+  };
+  float t_sym = 0.f, t_full = 0.f;
+  for (int rep = 0; rep < 2; ++rep) {  // warm both, then time both
+    BMG_CUDA(cudaEventRecord(e[0], ctx->stream));
+    for (int k = 0; k < 3; ++k) sym_pass();
+    BMG_CUDA(cudaEventRecord(e[1], ctx->stream));
+    for (int k = 0; k < 3; ++k) full_pass();
+    BMG_CUDA(cudaEventRecord(e[2], ctx->stream));
+    BMG_CUDA(cudaEventSynchronize(e[2]));
+    BMG_CUDA(cudaEventElapsedTime(&t_sym, e[0], e[1]));
+    BMG_CUDA(cudaEventElapsedTime(&t_full, e[1], e[2]));
+  }
+  for (auto& v : e) cudaEventDestroy(v);
+  a.sym_ms = t_sym / 3.0;
+  a.full_ms = t_full / 3.0;
+  // small passes (C2's levels, < 0.5 ms) measured slower inside whole cycles with
+  // the half form even where the pair above was faster (one more launch per pass,
+  // less overlap of consecutive passes): full storage there
+  return a.full_ms >= 0.5 && t_sym < 0.95f * t_full;
+}
+
+bool ensure_sym_half(const Bsr& a, const Bsr* next) {
+  const bool off = sym_mode() == 0;
+  if (a.half_state != 0) return a.half_state > 0;
+  a.half_state = -1;
+  if (off || !a.sym || !a.uniform || a.mr != a.mc || a.nbr != a.nbc || a.nnzb == 0 || !stream_supported(a.mr, a.mc))
+    return false;
+  Ctx* ctx = a.ctx;
+  const int m = a.mr;
+  const auto& rp = a.h_row_ptr;
+  const auto& cl = a.h_col;
+  // structural mirror of every block; structurally unsymmetric -> no half form
+  std::vector<int64_t> mirror(a.nnzb);
+  for (int i = 0; i < a.nbr; ++i)
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+      const int j = cl[p];
+      auto b = cl.begin() + rp[j], e = cl.begin() + rp[j + 1];
+      auto it = std::lower_bound(b, e, i);
+      if (it == e || *it != i) return false;
+      mirror[p] = rp[j] + (it - b);
+    }
+  {
+    DBuf<int64_t> dm(a.nnzb);
+    DBuf<int> flag(1);
+    BMG_CUDA(cudaMemcpyAsync(dm.p, mirror.data(), a.nnzb * 8, cudaMemcpyHostToDevice, ctx->stream));
+    BMG_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), ctx->stream));
+    kern::sym_check_kernel<<<(unsigned)((a.nnzb * 32 + 255) / 256), 256, 0, ctx->stream>>>(a.vals.p, dm.p, a.nnzb, m,
+                                                                                          a.bs, flag.p);
+    ctx->count();
+    BMG_CUDA(cudaGetLastError());
+    int h = 0;
+    BMG_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (h) return false;  // not exactly symmetric: keep full storage
+  }
+  // lower triangle: structure, block ids, rows
+  std::vector<int64_t> lrp(a.nbr + 1, 0), lid(a.nnzb, -1), src;
+  std::vector<int32_t> lcol, lrow;
+  src.reserve(a.nnzb / 2 + a.nbr);
+  for (int i = 0; i < a.nbr; ++i) {
+    for (int64_t p = rp[i]; p < rp[i + 1] && cl[p] <= i; ++p) {
+      lid[p] = (int64_t)src.size();
+      src.push_back(p);
+      lcol.push_back(cl[p]);
+      lrow.push_back(i);
+    }
+    lrp[i + 1] = (int64_t)src.size();
+  }
+  const int64_t nlow = (int64_t)src.size();
+  if (nlow >= ((int64_t)1 << 31)) return false;
+  // upper blocks of row i (ascending j > i): the lower block (j, i) holding them
+  std::vector<int64_t> uptr(a.nbr + 1, 0);
+  std::vector<int32_t> uslot;
+  uslot.reserve(a.nnzb - nlow);
+  for (int i = 0; i < a.nbr; ++i) {
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p)
+      if (cl[p] > i) uslot.push_back((int32_t)lid[mirror[p]]);
+    uptr[i + 1] = (int64_t)uslot.size();
+  }
+  auto H = std::make_unique<SymHalf>();
+  H->low = make_bsr_structure(ctx, a.nbr, a.rsz.data(), a.nbc, a.csz.data(), std::move(lrp), std::move(lcol), false);
+  // the SYM kernel's plan (its shared memory carries the row indices too)
+  build_plan_into(*H->low, H->low->plan, 1, m, a.bs, false, 0, 0, true);
+  {
+    DBuf<int64_t> dsrc(nlow);
+    BMG_CUDA(cudaMemcpyAsync(dsrc.p, src.data(), nlow * 8, cudaMemcpyHostToDevice, ctx->stream));
+    kern::gather_blocks_kernel<<<grid_for(nlow * a.bs), 256, 0, ctx->stream>>>(a.vals.p, dsrc.p, nlow, a.bs,
+                                                                              H->low->vals.p);
+    ctx->count();
+    BMG_CUDA(cudaGetLastError());
+    BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  H->brow.alloc(nlow + 8);
+  BMG_CUDA(cudaMemset(H->brow.p, 0, (nlow + 8) * 4));
+  BMG_CUDA(cudaMemcpy(H->brow.p, lrow.data(), nlow * 4, cudaMemcpyHostToDevice));
+  H->up_ptr.alloc(a.nbr + 1);
+  BMG_CUDA(cudaMemcpy(H->up_ptr.p, uptr.data(), (a.nbr + 1) * 8, cudaMemcpyHostToDevice));
+  H->up_slot.alloc(std::max<size_t>(uslot.size(), 1));
+  if (!uslot.empty()) BMG_CUDA(cudaMemcpy(H->up_slot.p, uslot.data(), uslot.size() * 4, cudaMemcpyHostToDevice));
+  H->colpart.alloc((size_t)nlow * m);
+  H->sbuf.alloc(std::max<int64_t>(a.dim_r, 1));
+  a.half = std::move(H);
+  a.half_state = 1;
+  if (sym_mode() < 0 && !sym_faster(a, next)) {
+    a.half.reset();
+    a.half_state = -1;
+    return false;
+  }
+  return true;
 }
 void prolong_add(const Bsr& a, const double* e, double* x, int nrhs) { launch(a, e, kern::EpiAdd{x}, nrhs); }
 void gt_cheb(const Bsr& gt, const double* w, double* p, double* x, double mu2, double dmu,
@@ -1082,6 +1344,15 @@ int bmg_bsr_info(const bmg_bsr* ah, int* nbr, int* nbc, int64_t* nnzb, int* dim_
     if (dim_c) *dim_c = a->dim_c;
     if (device_bytes) *device_bytes = a->device_bytes();
     if (pass_bytes) *pass_bytes = a->pass_bytes();
+  });
+}
+int bmg_bsr_sym_info(const bmg_bsr* ah, int* half, int64_t* pass_bytes, double* half_ms, double* full_ms) {
+  return guard([&] {
+    const Bsr* a = reinterpret_cast<const Bsr*>(ah);
+    if (half) *half = a->half ? 1 : 0;
+    if (pass_bytes) *pass_bytes = a->half ? sym_pass_bytes(*a) : a->pass_bytes();
+    if (half_ms) *half_ms = a->sym_ms;
+    if (full_ms) *full_ms = a->full_ms;
   });
 }
 int bmg_bsr_download(const bmg_bsr* ah, int64_t* row_ptr, int32_t* col_idx, double* vals) {

@@ -208,6 +208,21 @@ namespace bmg {
 // process-unique object ids (graph cache keys must not alias a freed object's address)
 uint64_t next_object_uid();
 
+// Symmetric-half streaming of an exactly symmetric uniform A (bsr_stream.cuh SYM):
+// the lower triangle as its own BSR (diagonal included, same padded blocks), the
+// row of every lower block, and for every row i the lower blocks (j, i), j > i
+// ascending, whose transposed products complete y_i.  colpart / sbuf are the
+// pass's scratch (one stream per matrix at a time, like the context's vectors).
+struct SymHalf {
+  std::unique_ptr<Bsr> low;
+  DBuf<int32_t> brow;     // [nnzb_low + 8]
+  DBuf<int64_t> up_ptr;   // [nbr + 1]
+  DBuf<int32_t> up_slot;  // [nnzb - nnzb_low]: lower-block ids
+  DBuf<double> colpart;   // [nnzb_low * m]
+  DBuf<double> sbuf;      // [dim]
+  int64_t bytes() const;
+};
+
 struct Bsr {
   CtxRef ctx;
   mutable std::atomic<int> refs{1};  // the creator's reference + hierarchies holding it
@@ -236,9 +251,21 @@ struct Bsr {
   mutable int pbs = 0;
   mutable std::unique_ptr<Plan> pplan[4];
   std::unique_ptr<Bsr> tcache;  // device transpose (spmv_t)
+  // symmetric-half form (ensure_sym_half); state 0 untried, 1 built, -1 not applicable
+  mutable std::unique_ptr<SymHalf> half;
+  mutable int half_state = 0;
+  mutable double sym_ms = 0.0, full_ms = 0.0;  // the measured choice (ensure_sym_half)
   int64_t pass_bytes() const;
   int64_t device_bytes() const;
 };
+// Builds a.half when a is square, uniform, streamed, flagged symmetric and its
+// stored blocks are exactly (bitwise) symmetric and the half form measured
+// faster (BMG_SYM_HALF=1 forces it, 0 disables it); true if a.half is usable.
+// Outside graph capture.
+// `next`: the pass that follows the residual in the cycle (timed with it), or null
+bool ensure_sym_half(const Bsr& a, const Bsr* next = nullptr);
+// algorithmic bytes of one SYM residual pass (both kernels)
+int64_t sym_pass_bytes(const Bsr& a);
 
 // Device view of a block layout for the setup kernels: uniform layouts address
 // block q at q * bs with m_r x m_c blocks; variable layouts through per-block

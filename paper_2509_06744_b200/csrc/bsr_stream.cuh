@@ -188,6 +188,12 @@ struct StreamArgs {
   const int* rsz = nullptr;
   int64_t xlen = 0;
   int l2hint = 1;  // matrix stream with the L2 evict-first policy
+  // SYM kernels (lower triangle of an exactly symmetric A): row index of every
+  // streamed block (bulk-copied beside the column indices) and the output of the
+  // transposed products A_ij^T x_i, MC doubles per block at the block's index
+  const int32_t* brow = nullptr;
+  double* colpart = nullptr;
+  int colmap = 0;  // SYM column items: 0 block-major, 1 block-fastest tiles (BMG_SYM_COLMAP)
 };
 
 // column-index slots per stage: cb_max + 8, rounded to 16 bytes (bulk-copy
@@ -195,8 +201,8 @@ struct StreamArgs {
 __host__ __device__ inline int stage_cols_of(int cb_max) { return (cb_max + 8 + 3) & ~3; }
 
 struct SmemLayout {
-  uint32_t vals, cols, part, carry, bars, total;
-  __host__ __device__ SmemLayout(int bs, int cb_max, int rmax, int mr, int kStages, int nrhs = 1) {
+  uint32_t vals, cols, rows, part, carry, bars, total;
+  __host__ __device__ SmemLayout(int bs, int cb_max, int rmax, int mr, int kStages, int nrhs = 1, bool sym = false) {
     uint32_t o = 0;
     auto al = [](uint32_t v, uint32_t a) { return (v + a - 1) / a * a; };
     (void)rmax;
@@ -204,6 +210,8 @@ struct SmemLayout {
     o += al((uint32_t)kStages * cb_max * bs * 8, 128);
     cols = o;
     o += al((uint32_t)kStages * stage_cols_of(cb_max) * 4, 128);
+    rows = o;  // block row indices (SYM)
+    if (sym) o += al((uint32_t)kStages * stage_cols_of(cb_max) * 4, 128);
     part = o;  // double-buffered partial sums
     o += al((uint32_t)2 * cb_max * mr * (nrhs > 1 ? nrhs + 1 : 1) * 8, 16);
     carry = o;  // double-buffered row carry
@@ -219,8 +227,16 @@ struct SmemLayout {
 // VAR: a variable layout whose blocks are stored padded to MR x MC with zeros; the
 // zero padding adds exact zeros to every fma chain, so each real entry keeps the
 // oracle's arithmetic order; padded rows are computed and never stored.
-template <int MR, int MC, int K, class Epi, bool VAR = false>
+// SYM: the streamed matrix is the lower triangle (diagonal included) of an exactly
+// symmetric A.  Besides the row dots, every off-diagonal block (i, j) computes the
+// transposed product A_ij^T x_i -- the contribution of the unstored block (j, i)
+// to row j -- as column dots over the staged block (fma chain over the block's
+// rows ascending: the same chain as the row dot of the stored transpose) and
+// writes it to colpart; the row sums (lower blocks only) go to the epilogue, and
+// sym_merge_kernel adds the upper contributions in ascending column order.
+template <int MR, int MC, int K, class Epi, bool VAR = false, bool SYM = false>
 __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi epi) {
+  static_assert(!SYM || (K == 1 && !VAR && MR == MC), "SYM streams uniform square blocks, one RHS");
   extern __shared__ __align__(128) unsigned char smem[];
   const int kStages = s.stages;
   // SKEW (m = 20): blocks land in shared memory at a pitch of bs + 2 doubles (one
@@ -229,11 +245,12 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
   // same banks (2-way conflicts on every 16-byte load, 2.5e8 per C4 coarse pass)
   constexpr bool SKEW = (MR == 20 && MC == 20 && K == 1 && !VAR);
   const int pitch = SKEW ? s.bs + 2 : s.bs;
-  const SmemLayout L(pitch, s.cb_max, s.rmax, MR, kStages, K);
+  const SmemLayout L(pitch, s.cb_max, s.rmax, MR, kStages, K, SYM);
   // partials of one (block, row) item for K > 1 sit at stride K + 1 (bank spread)
   constexpr int KP = K > 1 ? K + 1 : 1;
   double* vals_s = reinterpret_cast<double*>(smem + L.vals);
   int* cols_s = reinterpret_cast<int*>(smem + L.cols);
+  int* rows_s = reinterpret_cast<int*>(smem + L.rows);
   double* part_s = reinterpret_cast<double*>(smem + L.part);
   double* carry_s = reinterpret_cast<double*>(smem + L.carry);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
@@ -273,7 +290,8 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
         const int cl = d.x & ~3;
         const int ch = (d.x + d.y + 3) & ~3;
         const uint32_t cbytes = (uint32_t)(ch - cl) * 4u;
-        mbar_arrive_expect_tx(&full[st], vbytes + cbytes);
+        mbar_arrive_expect_tx(&full[st], vbytes + (SYM ? 2 : 1) * cbytes);
+        if constexpr (SYM) bulk_stream(rows_s + st * stage_cols, s.brow + cl, cbytes, &full[st], s.l2hint, pol);
         if constexpr (SKEW) {
           for (int b = 0; b < d.y; ++b)
             bulk_stream(vals_s + (size_t)st * stage_vals + b * pitch, s.vals + (int64_t)(d.x + b) * s.bs,
@@ -421,6 +439,67 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
       }
       part[b * MR + r] = t;
     }
+    if constexpr (SYM) {  // transposed products of the off-diagonal blocks
+      // an item is CPT adjacent columns of one block: x_i is loaded once for them
+      // and even block sizes read two columns per 16-byte shared-memory load
+      constexpr int CPT = (MC % 2 == 0) ? 2 : ((MC % 3 == 0) ? 3 : 1);
+      constexpr int NCG = MC / CPT;
+      // items run block-fastest within tiles of BB blocks, so the lanes of one
+      // shared-memory wavefront read the same column group of different blocks,
+      // whose pitch spreads them over distinct banks (16-byte loads: m = 20 pitch
+      // 402 -> 2 doubles apart, 8 blocks; m = 10 / 6: 4 apart, 4 blocks x 2
+      // groups; 8-byte loads, m = 15 / 21: 8 blocks x 2 groups, even + odd)
+      constexpr int BB = (MC == 10 || MC == 6) ? 4 : 8;
+      const int* rs = rows_s + st * stage_cols + (d.x & 3);
+      const bool tiled = s.colmap != 0;
+      const int citems = tiled ? ((d.y + BB - 1) / BB) * BB * NCG : d.y * NCG;
+      for (int item = tid; item < citems; item += kConsumers) {
+        int b, c0;
+        if (tiled) {
+          const int tile = item / (BB * NCG);
+          const int k = item - tile * BB * NCG;
+          b = tile * BB + (k % BB);
+          c0 = (k / BB) * CPT;
+          if (b >= d.y) continue;
+        } else {
+          b = item / NCG;
+          c0 = (item - b * NCG) * CPT;
+        }
+        const int i = rs[b];
+        if (cs[b] == i) continue;  // the diagonal block's row dots are complete
+        const double* __restrict__ xi = s.x + (int64_t)i * MR;
+        double xv[MR];
+        if constexpr (MR % 2 == 0) {
+#pragma unroll
+          for (int q = 0; q < MR / 2; ++q) {
+            const double2 t2 = __ldg(reinterpret_cast<const double2*>(xi) + q);
+            xv[2 * q] = t2.x;
+            xv[2 * q + 1] = t2.y;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < MR; ++q) xv[q] = __ldg(xi + q);
+        }
+        const double* a = vs + b * pitch + c0;
+        double t[CPT];
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) t[q] = 0.0;
+#pragma unroll
+        for (int r = 0; r < MR; ++r) {
+          if constexpr (CPT == 2) {
+            const double2 a2 = *reinterpret_cast<const double2*>(a + r * MC);
+            t[0] = __fma_rn(a2.x, xv[r], t[0]);
+            t[1] = __fma_rn(a2.y, xv[r], t[1]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < CPT; ++q) t[q] = __fma_rn(a[r * MC + q], xv[r], t[q]);
+          }
+        }
+        double* out = s.colpart + (int64_t)(d.x + b) * MC + c0;
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) out[q] = t[q];
+      }
+    }
     consumer_bar();
     if (tid == 0) mbar_arrive(&empty[st]);
 
@@ -453,6 +532,42 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
       else if (real)
         epi.store(oi, acc, pre);
     }
+  }
+}
+
+// Second half of a SYM pass: y_i = S_i + sum over the upper blocks (i, j), j > i
+// ascending, of the transposed products A_ji^T x_j left in colpart by the
+// blocks (j, i) -- the reference's row sum continued in its column order
+// (kernels.cpp:39-47: blocks ascending, y += block * x_j), so r = b - A x comes
+// out bitwise equal to the full-storage pass.  One thread per scalar row; the
+// slots and partials of eight upper blocks are loaded before they are added.
+template <int MR, class Epi>
+__global__ void __launch_bounds__(256) sym_merge_kernel(const int64_t* __restrict__ up_ptr,
+                                                        const int32_t* __restrict__ up_slot,
+                                                        const double* __restrict__ colpart,
+                                                        const double* __restrict__ S, int64_t n, Epi epi) {
+  pdl_launch_dependents();
+  pdl_wait();
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / MR;
+    const int r = (int)(e - i * MR);
+    const typename Epi::Pre pre = epi.load(e);
+    double y = S[e];
+    const int64_t u0 = __ldg(up_ptr + i), u1 = __ldg(up_ptr + i + 1);
+    int64_t u = u0;
+    constexpr int U = 8;  // partials in flight per thread (coarse 3-D rows hold ~230 upper blocks)
+    for (; u + U <= u1; u += U) {
+      int sl[U];
+      double c[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) sl[q] = __ldg(up_slot + u + q);
+#pragma unroll
+      for (int q = 0; q < U; ++q) c[q] = __ldg(colpart + (int64_t)sl[q] * MR + r);
+#pragma unroll
+      for (int q = 0; q < U; ++q) y = __dadd_rn(y, c[q]);
+    }
+    for (; u < u1; ++u) y = __dadd_rn(y, __ldg(colpart + (int64_t)__ldg(up_slot + u) * MR + r));
+    epi.store(e, y, pre);
   }
 }
 

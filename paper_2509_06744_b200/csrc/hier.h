@@ -101,6 +101,7 @@ struct Part {
 
 struct LevelStats {  // global byte model inputs (bmg_hier_cycle_bytes)
   int64_t n = 0, a_pass = 0, m_pass = 0, r_pass = 0, p_pass = 0;
+  int64_t a_pass_ref = 0;  // full-storage A pass (the reference's storage; 0: = a_pass)
 };
 
 struct GraphKey {

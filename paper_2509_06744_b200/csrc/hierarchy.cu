@@ -398,7 +398,8 @@ static void record_stats(Hier& h) {
     LevelStats& s = h.stats[l];
     const PLevel& L = p.lv[l];
     s.n = L.A->dim_r;
-    s.a_pass = L.A->pass_bytes();
+    s.a_pass = L.A->half ? sym_pass_bytes(*L.A) : L.A->pass_bytes();
+    s.a_pass_ref = L.A->pass_bytes();
     if (l >= 1) {
       for (auto& f : L.M->fwd) s.m_pass += f->pass_bytes();
       for (auto& f : L.M->bwd) s.m_pass += f->pass_bytes();
@@ -452,6 +453,9 @@ static void finish_whole(Hier& h, int cap) {
     }
   }
   coarse_factor(h, p);
+  // symmetric-half streaming of every smoothed level's A (bitwise the same passes,
+  // about half the bytes; kept full when A is not exactly symmetric)
+  for (int l = 1; l < L; ++l) ensure_sym_half(*p.lv[l].A, p.lv[l].M->fwd.front().get());
   record_stats(h);
 }
 
@@ -822,17 +826,24 @@ int bmg_hier_cycle_bytes(const bmg_hier* hh, int kpre, int kpost, int64_t* bytes
 }
 
 // algorithmic bytes of one (batched) cycle: every matrix streamed once, vector
-// traffic per right-hand side
+// traffic per right-hand side; `ref`: A passes at full storage (the reference's)
+static int64_t cycle_bytes(const Hier* h, int kpre, int kpost, int nrhs, bool ref);
 int bmg_hier_cycle_bytes_batch(const bmg_hier* hh, int kpre, int kpost, int nrhs, int64_t* bytes) {
-  return guard([&] {
-    const Hier* h = H_(hh);
+  return guard([&] { *bytes = cycle_bytes(H_(hh), kpre, kpost, nrhs, false); });
+}
+int bmg_hier_cycle_bytes_ref(const bmg_hier* hh, int kpre, int kpost, int64_t* bytes) {
+  return guard([&] { *bytes = cycle_bytes(H_(hh), kpre, kpost, 1, true); });
+}
+static int64_t cycle_bytes(const Hier* h, int kpre, int kpost, int nrhs, bool ref) {
+  {
     const int64_t K = std::max(1, nrhs);
     int64_t tot = 0;
     const int top = h->finest();
     for (int l = 1; l <= top; ++l) {
       const LevelStats& s = h->stats[l];
       const int64_t n = s.n * K, nc = h->stats[l - 1].n * K;
-      const int64_t apass = s.a_pass + 24 * n;  // x, b read; r write
+      const int64_t a_bytes = (ref && s.a_pass_ref) ? s.a_pass_ref : (nrhs > 1 && s.a_pass_ref ? s.a_pass_ref : s.a_pass);
+      const int64_t apass = a_bytes + 24 * n;  // x, b read; r write
       const int64_t gvec = 16 * n + 40 * n;     // G: r, w; G^T+cheb: w, p rw, x rw
       const int steps = kpre + kpost;
       int64_t lvl = steps * (apass + s.m_pass + gvec);
@@ -850,8 +861,8 @@ int bmg_hier_cycle_bytes_batch(const bmg_hier* hh, int kpre, int kpost, int nrhs
       const int64_t one = nt * (nt + 1) / 2 * 64 * 64 * 8 + (16 * h->n0 + 2 * nt * nt * 64 * 8) * K;
       tot += tri ? 2 * one : one;
     }
-    *bytes = tot;
-  });
+    return tot;
+  }
 }
 
 int bmg_hier_use_graph(bmg_hier* hh, int on) {

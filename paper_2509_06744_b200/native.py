@@ -103,6 +103,7 @@ _SIGS = {
     "bmg_bsr_create": (_I, [_P, _I, _PI32, _I, _PI32, _PI64, _PI32, _PD, _I, _PP]),
     "bmg_bsr_destroy": (_I, [_P]),
     "bmg_bsr_info": (_I, [_P, C.POINTER(_I), C.POINTER(_I), _PI64, C.POINTER(_I), C.POINTER(_I), _PI64, _PI64]),
+    "bmg_bsr_sym_info": (_I, [_P, C.POINTER(_I), _PI64, _PD, _PD]),
     "bmg_bsr_download": (_I, [_P, _PI64, _PI32, _PD]),
     "bmg_bsr_transpose": (_I, [_P, _PP]),
     "bmg_vec_create": (_I, [_P, _I64, _PP]),
@@ -143,6 +144,7 @@ _SIGS = {
     "bmg_hier_level": (_I, [_P, _I, _PP, _PP, _PP]),
     "bmg_hier_cycle_bytes": (_I, [_P, _I, _I, _PI64]),
     "bmg_hier_cycle_bytes_batch": (_I, [_P, _I, _I, _I, _PI64]),
+    "bmg_hier_cycle_bytes_ref": (_I, [_P, _I, _I, _PI64]),
     "bmg_vcycle_batch": (_I, [_P, _I, _I, _I, _P, _P]),
     "bmg_vcycle_batch_host": (_I, [_P, _I, _I, _I, _PD, _PD]),
     "bmg_hier_use_graph": (_I, [_P, _I]),
