@@ -41,3 +41,15 @@ def test_c2_full_size_matches_oracle(ctx):
     assert np.all(np.abs(rho_g[big] / rho_o[big] - 1) <= 1e-10), np.abs(rho_g[big] / rho_o[big] - 1).max()
     xg = xv.download()
     assert np.linalg.norm(xg - x_o) <= 1e-10 * np.linalg.norm(x_o)
+
+
+def test_c2_full_solve_to_1e8_matches_oracle_fixture(ctx):
+    # the headline criterion on the whole C2 configuration: device setup and the
+    # stop-on-tolerance loop to ||r|| / ||r0|| < 1e-8 against the oracle's run of the
+    # same (tests/golden/solve_C2.json, ~45 min of oracle time on 8 host threads):
+    # Galerkin A_l and FSAI factors bitwise, beta 1e-10, every rho_n within 1e-10,
+    # equal iteration counts
+    from tests.test_gpu_shapes import run_case
+
+    it, dmax = run_case(ctx, "C2")
+    assert it > 100 and dmax <= 1e-10
