@@ -235,7 +235,7 @@ def oracle_sample(cfg, steps, warmup, threads, single_core=False):
     A, T, b = pr.make_problem(scfg)
     t0 = time.perf_counter()
     oh = O.Hierarchy(O.Mat(A), [O.Mat(p) for p in T], t_max=1, tau=1.0, nest=scfg.nest,
-                     fsai_kind=0 if scfg.fsai == "static" else 3, coarse_dim_cap=1 << 30, probe=False)
+                     fsai_kind=0 if scfg.fsai == "static" else 3, coarse_dim_cap=1 << 30, probe=False, consume=True)
     setup_s = time.perf_counter() - t0
     del A, T
     n0 = oh.A(0).info()["dim_r"]

@@ -1203,13 +1203,13 @@ static double lanczos_lambda_max(const Mat& a, const Nested& f, int iters, doubl
 }
 
 // setup: multilevel.cpp:36-75
-static Hier setup(const Mat& a_finest, std::vector<Mat> transfers, int t_max, double tau, int nest,
+static Hier setup(Mat a_finest, std::vector<Mat> transfers, int t_max, double tau, int nest,
                   int fsai_kind, int lanczos_iters, double safety, uint64_t seed, int cap,
                   bool probe, int kind, double omega, double fraction) {
   Hier h;
   const int depth = (int)transfers.size();
   h.levels.resize(depth + 1);
-  h.levels[depth].A = a_finest;
+  h.levels[depth].A = std::move(a_finest);
   for (int l = depth; l >= 1; --l) {
     h.levels[l].P = std::move(transfers[l - 1]);
     h.levels[l - 1].A = galerkin(h.levels[l].A, h.levels[l].P);
@@ -1549,14 +1549,23 @@ int orc_poly_eval(int kind, int degree, double alpha, double beta, double t, dou
 }
 double orc_fourth_kind_mu(int n) { return fourth_kind_mu(n); }
 
+static bool g_consume = false;
+int orc_set_consume(int on) {
+  g_consume = on != 0;
+  return 0;
+}
 int orc_setup(const orc_mat* a_finest, int ntransfers, const orc_mat* const* transfers, int t_max,
               double tau, int nest, int fsai_kind, int lanczos_iters, double lanczos_safety,
               uint64_t seed, int coarse_dim_cap, int smallest_ritz_probe, int smoother_kind,
               double richardson_omega, double first_kind_fraction, orc_hier** out) {
   return guard([&] {
+    // consume mode (orc_set_consume): the inputs are moved into the hierarchy and
+    // left empty, so a large config (C4: 20 GB of A, 21 GB of P) is not held twice
     std::vector<Mat> tr;
-    for (int i = 0; i < ntransfers; ++i) tr.push_back(transfers[i]->m);
-    *out = new orc_hier{setup(a_finest->m, std::move(tr), t_max, tau, nest, fsai_kind,
+    for (int i = 0; i < ntransfers; ++i)
+      tr.push_back(g_consume ? std::move(const_cast<orc_mat*>(transfers[i])->m) : transfers[i]->m);
+    Mat a = g_consume ? std::move(const_cast<orc_mat*>(a_finest)->m) : a_finest->m;
+    *out = new orc_hier{setup(std::move(a), std::move(tr), t_max, tau, nest, fsai_kind,
                               lanczos_iters, lanczos_safety, seed, coarse_dim_cap,
                               smallest_ritz_probe != 0, smoother_kind, richardson_omega,
                               first_kind_fraction)};

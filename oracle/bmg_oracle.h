@@ -108,6 +108,8 @@ double orc_fourth_kind_mu(int n);
 /* transfers[l-1] prolongates level l-1 to level l; levels = ntransfers + 1.
  * fsai_kind: 3 = nested_build(t_max, tau, nest) as reference setup();
  *            0 = static lower(P(A)) per level (lower-level API, config 1)     */
+/* 1: orc_setup moves its input matrices into the hierarchy (they are left empty) */
+int orc_set_consume(int on);
 int orc_setup(const orc_mat* a_finest, int ntransfers, const orc_mat* const* transfers,
               int t_max, double tau, int nest, int fsai_kind, int lanczos_iters,
               double lanczos_safety, uint64_t seed, int coarse_dim_cap, int smallest_ritz_probe,

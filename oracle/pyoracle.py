@@ -58,6 +58,7 @@ _SIGS = {
     "orc_smoother_apply_diag": (_I, [_I, _PD, _I, _D, _D, _D, _I, _PD, _PD]),
     "orc_poly_eval": (_I, [_I, _I, _D, _D, _D, _PD]),
     "orc_fourth_kind_mu": (_D, [_I]),
+    "orc_set_consume": (_I, [_I]),
     "orc_setup": (_I, [_P, _I, _PP, _I, _D, _I, _I, _I, _D, _U64, _I, _I, _I, _D, _D, _PP]),
     "orc_hier_destroy": (None, [_P]),
     "orc_hier_levels": (_I, [_P]),
@@ -336,12 +337,18 @@ FIRST_T, FOURTH_W, SCALED_FIRST, SCALED_FOURTH = 0, 1, 2, 3
 class Hierarchy:
     def __init__(self, a, transfers, t_max=1, tau=1.0, nest=0, fsai_kind=3, lanczos_iters=100,
                  lanczos_safety=1.01, seed=42, coarse_dim_cap=5000, probe=True, smoother_kind=2,
-                 richardson_omega=1.0, first_kind_fraction=1.0 / 30.0):
+                 richardson_omega=1.0, first_kind_fraction=1.0 / 30.0, consume=False):
+        """consume=True moves a and the transfers into the hierarchy (they are
+        left empty): large configs are not held twice in host memory."""
         arr = (C.c_void_p * max(len(transfers), 1))(*[t.h.value for t in transfers])
         h = C.c_void_p()
-        check(lib().orc_setup(a.h, len(transfers), arr, t_max, tau, nest, fsai_kind, lanczos_iters,
-                              lanczos_safety, seed, coarse_dim_cap, 1 if probe else 0, smoother_kind,
-                              richardson_omega, first_kind_fraction, C.byref(h)))
+        lib().orc_set_consume(1 if consume else 0)
+        try:
+            check(lib().orc_setup(a.h, len(transfers), arr, t_max, tau, nest, fsai_kind, lanczos_iters,
+                                  lanczos_safety, seed, coarse_dim_cap, 1 if probe else 0, smoother_kind,
+                                  richardson_omega, first_kind_fraction, C.byref(h)))
+        finally:
+            lib().orc_set_consume(0)
         self.h = h
         self.sizes = [a.row_sizes] + []
         self._transfers = transfers
