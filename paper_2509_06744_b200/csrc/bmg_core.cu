@@ -253,7 +253,7 @@ static int ring_stages() {
 // several CTAs fit per SM.  Caps measured on B200 (tools/kernel_sweep.py, residual
 // pass on each config family's fine operator): 24 KB for m = 10 and 20, 32 KB for
 // m = 15 and 21.  BMG_CHUNK_KB overrides the cap for every m.
-static int chunk_blocks(int mr, int bs, int K = 1) {
+static int chunk_blocks(int mr, int bs, int K = 1, bool sym = false) {
   static int env_cap = [] {
     const char* e = std::getenv("BMG_CHUNK_KB");
     if (!e) return 0;
@@ -268,6 +268,10 @@ static int chunk_blocks(int mr, int bs, int K = 1) {
   // the coarse levels' 285 / 462-block rows gain most)
   int kb = (mr == 15 || mr == 21 || mr == 20) ? 32 : 24;
   if (K > 1 && mr == 20) kb = 48;
+  // the half-storage pass (twice the consumer work per staged block) on m = 20: 11
+  // blocks per chunk, still 3 CTAs per SM (C4 fine residual + G pair 2.50 -> 2.42 ms;
+  // 40 KB drops to 2 CTAs: 2.68)
+  if (sym && mr == 20) kb = 36;
   if (K == 8 && mr == 10) kb = 16;
   const int cap = env_cap ? env_cap : kb * 1024;
   // small blocks: several phase-A items per consumer thread, so a chunk still
@@ -442,7 +446,7 @@ static void build_plan_into(const Bsr& a, Plan& P, int K, int mr, int bs, bool v
     P.xl = bc.xl;
     P.cb_max = std::min(32, bc.cb > 0 ? bc.cb : std::max(1, kern::kConsumers / (mr * P.u)));
   } else {
-    P.cb_max = chunk_blocks(mr, bs, K);
+    P.cb_max = chunk_blocks(mr, bs, K, sym);
   }
   const auto& rp = a.h_row_ptr;
   // chunk list per CTA range
