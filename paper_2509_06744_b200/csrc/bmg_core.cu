@@ -845,21 +845,22 @@ static bool pdl_enabled() {
 }
 
 template <int MR, int MC, int K, class Epi, bool VAR = false, bool SYM = false>
-static void launch_stream_plan(const Bsr& a, const Plan& P, const double* x, Epi epi, const SymHalf* sh = nullptr);
+static void launch_stream_plan(const Bsr& a, const Plan& P, const double* x, Epi epi, const SymArgs* sa = nullptr);
 template <int MR, int MC, int K, class Epi, bool VAR = false>
 static void launch_stream_t(const Bsr& a, const double* x, Epi epi) {
   launch_stream_plan<MR, MC, K, Epi, VAR>(a, plan_for(a, K), x, epi);
 }
 template <int MR, int MC, int K, class Epi, bool VAR, bool SYM>
-static void launch_stream_plan(const Bsr& a, const Plan& P, const double* x, Epi epi, const SymHalf* sh) {
+static void launch_stream_plan(const Bsr& a, const Plan& P, const double* x, Epi epi, const SymArgs* sa) {
   kern::StreamArgs s;
   if constexpr (SYM) {
     static const int colmap = [] {
       const char* e = std::getenv("BMG_SYM_COLMAP");
       return e ? std::atoi(e) : 0;
     }();
-    s.brow = sh->brow.p;
-    s.colpart = sh->colpart.p;
+    s.brow = sa->brow;
+    s.colpart = sa->colpart;
+    s.sym_lo = sa->sym_lo;
     s.colmap = colmap;
   }
   s.vals = VAR ? a.pvals.p : a.vals.p;
@@ -903,25 +904,31 @@ static void launch_stream_plan(const Bsr& a, const Plan& P, const double* x, Epi
 // A SYM pass: the lower triangle streamed (row sums to sbuf, transposed products
 // to colpart), then the merge adds the upper contributions and runs the epilogue.
 template <int MR, class Epi>
-static void launch_sym(const Bsr& a, const double* x, Epi epi) {
-  const SymHalf& H = *a.half;
-  const Bsr& low = *H.low;
-  launch_stream_plan<MR, MR, 1, kern::EpiStore, false, true>(low, low.plan, x, kern::EpiStore{H.sbuf.p}, &H);
-  const int64_t n = (int64_t)a.nbr * MR;
+static void launch_merge(Ctx* ctx, int64_t nrows, const int64_t* up_ptr, const int32_t* up_slot, const double* colpart,
+                         const double* S, Epi epi, double* tbuf, int64_t tsplit_rows) {
+  const int64_t n = nrows * MR;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)a.ctx->sms * 16)));
+  cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)ctx->sms * 16)));
   cfg.blockDim = dim3(256);
-  cfg.stream = a.ctx->stream;
+  cfg.stream = ctx->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  BMG_CUDA(cudaLaunchKernelEx(&cfg, kern::sym_merge_kernel<MR, Epi>, (const int64_t*)H.up_ptr.p,
-                              (const int32_t*)H.up_slot.p, (const double*)H.colpart.p, (const double*)H.sbuf.p, n,
-                              epi));
-  a.ctx->count();
-  BMG_LAUNCHED(a.ctx->stream, "sym_merge_kernel");
+  BMG_CUDA(cudaLaunchKernelEx(&cfg, kern::sym_merge_kernel<MR, Epi>, up_ptr, up_slot, colpart, S, n, epi, tbuf,
+                              tsplit_rows * MR));
+  ctx->count();
+  BMG_LAUNCHED(ctx->stream, "sym_merge_kernel");
+}
+
+template <int MR, class Epi>
+static void launch_sym(const Bsr& a, const double* x, Epi epi) {
+  const SymHalf& H = *a.half;
+  const Bsr& low = *H.low;
+  const SymArgs sa{H.brow.p, H.colpart.p, 0};
+  launch_stream_plan<MR, MR, 1, kern::EpiStore, false, true>(low, low.plan, x, kern::EpiStore{H.sbuf.p}, &sa);
+  launch_merge<MR>(a.ctx, a.nbr, H.up_ptr.p, H.up_slot.p, H.colpart.p, H.sbuf.p, epi, nullptr, a.nbr);
 }
 template <class Epi>
 static bool try_launch_sym(const Bsr& a, const double* x, Epi epi, int nrhs) {
@@ -1075,6 +1082,54 @@ void spmv(const Bsr& a, const double* x, double* y, int nrhs) {
 void residual(const Bsr& a, const double* b, const double* x, double* r, int nrhs) {
   if (try_launch_sym(a, x, kern::EpiResidual{b, r}, nrhs)) return;
   launch(a, x, kern::EpiResidual{b, r}, nrhs);
+}
+
+void build_sym_plan(Bsr& low) {
+  if (!low.uniform || low.mr != low.mc || !stream_supported(low.mr, low.mc)) fail(BMG_EINVAL, "sym plan: streamed uniform blocks only");
+  build_plan_into(low, low.plan, 1, low.mr, low.bs, false, 0, 0, true);
+}
+
+void sym_phase1(const Bsr& low, const SymArgs& sa, const double* x, double* S) {
+  if (low.nbr == 0) return;
+  const kern::EpiStore epi{S};
+  switch (low.mr) {
+    case 3: return launch_stream_plan<3, 3, 1, kern::EpiStore, false, true>(low, low.plan, x, epi, &sa);
+    case 6: return launch_stream_plan<6, 6, 1, kern::EpiStore, false, true>(low, low.plan, x, epi, &sa);
+    case 10: return launch_stream_plan<10, 10, 1, kern::EpiStore, false, true>(low, low.plan, x, epi, &sa);
+    case 15: return launch_stream_plan<15, 15, 1, kern::EpiStore, false, true>(low, low.plan, x, epi, &sa);
+    case 20: return launch_stream_plan<20, 20, 1, kern::EpiStore, false, true>(low, low.plan, x, epi, &sa);
+    case 21: return launch_stream_plan<21, 21, 1, kern::EpiStore, false, true>(low, low.plan, x, epi, &sa);
+  }
+  fail(BMG_EINVAL, "sym_phase1: streamed block sizes only");
+}
+
+void sym_merge(Ctx* ctx, int m, int64_t nrows, const int64_t* up_ptr, const int32_t* up_slot, const double* colpart,
+               const double* S, const double* b, double* r, double* tbuf, int64_t tsplit_rows) {
+  if (nrows <= 0) return;
+  const kern::EpiResidual epi{b, r};
+  switch (m) {
+    case 3: return launch_merge<3>(ctx, nrows, up_ptr, up_slot, colpart, S, epi, tbuf, tsplit_rows);
+    case 6: return launch_merge<6>(ctx, nrows, up_ptr, up_slot, colpart, S, epi, tbuf, tsplit_rows);
+    case 10: return launch_merge<10>(ctx, nrows, up_ptr, up_slot, colpart, S, epi, tbuf, tsplit_rows);
+    case 15: return launch_merge<15>(ctx, nrows, up_ptr, up_slot, colpart, S, epi, tbuf, tsplit_rows);
+    case 20: return launch_merge<20>(ctx, nrows, up_ptr, up_slot, colpart, S, epi, tbuf, tsplit_rows);
+    case 21: return launch_merge<21>(ctx, nrows, up_ptr, up_slot, colpart, S, epi, tbuf, tsplit_rows);
+  }
+  fail(BMG_EINVAL, "sym_merge: streamed block sizes only");
+}
+
+void residual_from(const Bsr& tail, const double* t, const double* b, const double* x, double* r) {
+  if (tail.nbr == 0) return;
+  const kern::EpiResidualFrom epi{t, b, r};
+  switch (tail.mr) {
+    case 3: return launch_stream_plan<3, 3, 1>(tail, tail.plan, x, epi);
+    case 6: return launch_stream_plan<6, 6, 1>(tail, tail.plan, x, epi);
+    case 10: return launch_stream_plan<10, 10, 1>(tail, tail.plan, x, epi);
+    case 15: return launch_stream_plan<15, 15, 1>(tail, tail.plan, x, epi);
+    case 20: return launch_stream_plan<20, 20, 1>(tail, tail.plan, x, epi);
+    case 21: return launch_stream_plan<21, 21, 1>(tail, tail.plan, x, epi);
+  }
+  fail(BMG_EINVAL, "residual_from: streamed block sizes only");
 }
 
 // ---- symmetric-half form ----------------------------------------------------------

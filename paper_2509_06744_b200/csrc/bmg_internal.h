@@ -213,6 +213,13 @@ uint64_t next_object_uid();
 // row of every lower block, and for every row i the lower blocks (j, i), j > i
 // ascending, whose transposed products complete y_i.  colpart / sbuf are the
 // pass's scratch (one stream per matrix at a time, like the context's vectors).
+// what a SYM streaming pass needs besides the matrix (bsr_stream.cuh StreamArgs)
+struct SymArgs {
+  const int32_t* brow;  // per streamed block: the x segment of its row (vector-local block index)
+  double* colpart;      // transposed products, m doubles per streamed block
+  int sym_lo;           // blocks in columns below this have no stored mirror (row dots only)
+};
+
 struct SymHalf {
   std::unique_ptr<Bsr> low;
   DBuf<int32_t> brow;     // [nnzb_low + 8]
@@ -266,6 +273,16 @@ struct Bsr {
 bool ensure_sym_half(const Bsr& a, const Bsr* next = nullptr);
 // algorithmic bytes of one SYM residual pass (both kernels)
 int64_t sym_pass_bytes(const Bsr& a);
+// the pieces of a half-storage pass on a partitioned level (vcycle.cu sym_residual_pass):
+// phase 1 over a lower-part slice (row sums to S), the merge of the in-rank upper
+// contributions (r = b - y, or the partial sum to tbuf from scalar row
+// tsplit_rows * m on), and the tail over the blocks past the rank's own columns
+void sym_phase1(const Bsr& low, const SymArgs& sa, const double* x, double* S);
+void sym_merge(Ctx* ctx, int m, int64_t nrows, const int64_t* up_ptr, const int32_t* up_slot, const double* colpart,
+               const double* S, const double* b, double* r, double* tbuf, int64_t tsplit_rows);
+void residual_from(const Bsr& tail, const double* t, const double* b, const double* x, double* r);
+// the plan of a lower-part slice for the SYM kernel (shared memory carries the row indices)
+void build_sym_plan(Bsr& low);
 
 // Device view of a block layout for the setup kernels: uniform layouts address
 // block q at q * bs with m_r x m_c blocks; variable layouts through per-block

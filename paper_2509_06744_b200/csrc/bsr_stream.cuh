@@ -130,6 +130,7 @@ __device__ __forceinline__ void consumer_bar() {
 struct EpiStore {
   double* y;
   struct Pre {};
+  __device__ __forceinline__ double init(int64_t) const { return 0.0; }
   __device__ __forceinline__ Pre load(int64_t) const { return {}; }
   __device__ __forceinline__ void store(int64_t i, double v, const Pre&) const { y[i] = v; }
 };
@@ -139,6 +140,7 @@ struct EpiResidual {  // r = b - A x
   struct Pre {
     double b;
   };
+  __device__ __forceinline__ double init(int64_t) const { return 0.0; }
   __device__ __forceinline__ Pre load(int64_t i) const { return {__ldg(b + i)}; }
   __device__ __forceinline__ void store(int64_t i, double v, const Pre& p) const { r[i] = __dsub_rn(p.b, v); }
 };
@@ -147,6 +149,7 @@ struct EpiAdd {  // x += P e
   struct Pre {
     double x;
   };
+  __device__ __forceinline__ double init(int64_t) const { return 0.0; }
   __device__ __forceinline__ Pre load(int64_t i) const { return {x[i]}; }
   __device__ __forceinline__ void store(int64_t i, double v, const Pre& p) const { x[i] = __dadd_rn(p.x, v); }
 };
@@ -159,6 +162,7 @@ struct EpiCheb {
   struct Pre {
     double p, x;
   };
+  __device__ __forceinline__ double init(int64_t) const { return 0.0; }
   __device__ __forceinline__ Pre load(int64_t i) const {
     return {first ? 0.0 : p[i], xzero ? 0.0 : x[i]};
   }
@@ -168,6 +172,21 @@ struct EpiCheb {
     const double inc = __dmul_rn(dmu, pn);
     x[i] = xzero ? inc : __dadd_rn(q.x, inc);
   }
+};
+
+// r = b - (t + A x): the row sum continues from t (a partial sum of the same row's
+// earlier blocks, in column order) -- the last segment of a half-storage pass on a
+// partitioned level, whose blocks past the rank's own columns come last in the row
+struct EpiResidualFrom {
+  const double* t;
+  const double* b;
+  double* r;
+  struct Pre {
+    double b;
+  };
+  __device__ __forceinline__ double init(int64_t i) const { return t[i]; }
+  __device__ __forceinline__ Pre load(int64_t i) const { return {__ldg(b + i)}; }
+  __device__ __forceinline__ void store(int64_t i, double v, const Pre& p) const { r[i] = __dsub_rn(p.b, v); }
 };
 
 struct StreamArgs {
@@ -194,6 +213,8 @@ struct StreamArgs {
   const int32_t* brow = nullptr;
   double* colpart = nullptr;
   int colmap = 0;  // SYM column items: 0 block-major, 1 block-fastest tiles (BMG_SYM_COLMAP)
+  int sym_lo = 0;  // SYM: blocks in columns below this one (a partitioned level's lower halo)
+                   // have no stored mirror here: row dots only
 };
 
 // column-index slots per stage: cb_max + 8, rounded to 16 bytes (bulk-copy
@@ -466,7 +487,7 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
           c0 = (item - b * NCG) * CPT;
         }
         const int i = rs[b];
-        if (cs[b] == i) continue;  // the diagonal block's row dots are complete
+        if (cs[b] == i || cs[b] < s.sym_lo) continue;  // diagonal / lower-halo block: row dots only
         const double* __restrict__ xi = s.x + (int64_t)i * MR;
         double xv[MR];
         if constexpr (MR % 2 == 0) {
@@ -524,7 +545,7 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
       }
       const int lo = (int)(max(rlo, (int64_t)d.x) - d.x);
       const int hi = (int)(min(rhi, (int64_t)(d.x + d.y)) - d.x);
-      double acc = (rr == 0 && cin) ? carry_in[rv] : 0.0;
+      double acc = (rr == 0 && cin) ? carry_in[rv] : epi.init(oi);
       const int r = rv / K, v = rv - (rv / K) * K;
       for (int b = lo; b < hi; ++b) acc = __dadd_rn(acc, part[(b * MR + r) * KP + v]);
       if (rr == nrows - 1 && cout)
@@ -541,11 +562,14 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
 // (kernels.cpp:39-47: blocks ascending, y += block * x_j), so r = b - A x comes
 // out bitwise equal to the full-storage pass.  One thread per scalar row; the
 // slots and partials of eight upper blocks are loaded before they are added.
+// Scalar rows from tsplit on are written to tbuf instead (partitioned levels: a
+// tail pass adds the row's blocks beyond the rank's own columns).
 template <int MR, class Epi>
 __global__ void __launch_bounds__(256) sym_merge_kernel(const int64_t* __restrict__ up_ptr,
                                                         const int32_t* __restrict__ up_slot,
                                                         const double* __restrict__ colpart,
-                                                        const double* __restrict__ S, int64_t n, Epi epi) {
+                                                        const double* __restrict__ S, int64_t n, Epi epi,
+                                                        double* __restrict__ tbuf, int64_t tsplit) {
   pdl_launch_dependents();
   pdl_wait();
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
@@ -567,7 +591,10 @@ __global__ void __launch_bounds__(256) sym_merge_kernel(const int64_t* __restric
       for (int q = 0; q < U; ++q) y = __dadd_rn(y, c[q]);
     }
     for (; u < u1; ++u) y = __dadd_rn(y, __ldg(colpart + (int64_t)__ldg(up_slot + u) * MR + r));
-    epi.store(e, y, pre);
+    if (e >= tsplit)
+      tbuf[e - tsplit] = y;  // rows continued by a tail pass (EpiResidualFrom)
+    else
+      epi.store(e, y, pre);
   }
 }
 

@@ -761,9 +761,12 @@ static std::unique_ptr<Hier> dist_setup(Ctx* ctx, const DistPlan& P, int rank, s
     BMG_CUDA(cudaStreamSynchronize(ctx->stream));
     h->n0 = n0;
   }
+  // half-storage A on the large partitioned levels (after the distributed Lanczos,
+  // the setup's last full-storage A passes)
+  build_level_psym(*h);
   // global byte-model inputs: sum of own-row pass bytes over ranks
   {
-    std::vector<int64_t> st((size_t)5 * L, 0);
+    std::vector<int64_t> st((size_t)6 * L, 0);
     for (Part& p : h->parts)
       for (int l = 0; l < L; ++l) {
         PLevel& d = p.lv[l];
@@ -773,12 +776,13 @@ static std::unique_ptr<Hier> dist_setup(Ctx* ctx, const DistPlan& P, int rank, s
           return b;
         };
         if (!d.active()) continue;
-        st[5 * l + 0] += d.n_own();
-        st[5 * l + 1] += pb(d.sA);
-        for (auto& f : d.sF) st[5 * l + 2] += pb(f);
-        for (auto& f : d.sB) st[5 * l + 2] += pb(f);
-        st[5 * l + 3] += pb(d.sR);
-        st[5 * l + 4] += pb(d.sP);
+        st[6 * l + 0] += d.n_own();
+        st[6 * l + 1] += d.psym ? d.psym->pass_bytes : pb(d.sA);
+        for (auto& f : d.sF) st[6 * l + 2] += pb(f);
+        for (auto& f : d.sB) st[6 * l + 2] += pb(f);
+        st[6 * l + 3] += pb(d.sR);
+        st[6 * l + 4] += pb(d.sP);
+        st[6 * l + 5] += pb(d.sA);
       }
     if (!h->emulated && world > 1) {
       DBuf<int64_t> d(st.size());
@@ -789,11 +793,12 @@ static std::unique_ptr<Hier> dist_setup(Ctx* ctx, const DistPlan& P, int rank, s
     }
     h->stats.assign(L, LevelStats());
     for (int l = 0; l < L; ++l) {
-      h->stats[l].n = st[5 * l + 0];
-      h->stats[l].a_pass = st[5 * l + 1];
-      h->stats[l].m_pass = st[5 * l + 2];
-      h->stats[l].r_pass = st[5 * l + 3];
-      h->stats[l].p_pass = st[5 * l + 4];
+      h->stats[l].n = st[6 * l + 0];
+      h->stats[l].a_pass = st[6 * l + 1];
+      h->stats[l].m_pass = st[6 * l + 2];
+      h->stats[l].r_pass = st[6 * l + 3];
+      h->stats[l].p_pass = st[6 * l + 4];
+      h->stats[l].a_pass_ref = st[6 * l + 5];
     }
   }
   BMG_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -67,6 +67,28 @@ struct SplitMat {
   }
 };
 
+// Half-storage A on one rank's share of a partitioned level (vcycle.cu
+// sym_residual_pass): the rows' blocks up to the diagonal -- those in the lower halo
+// (columns below the own ones: row dots only, their mirrors live on another rank)
+// and the in-rank lower triangle (row dots + transposed products) -- streamed as two
+// slices (rows that read the lower halo first); the in-rank upper blocks come from
+// the transposed products in column order (merge); blocks past the own columns
+// (upper halo) finish the last rows in a tail pass.  Every row's sum keeps the
+// reference's column order, so the pass is bitwise the full-storage one.
+struct PSym {
+  std::unique_ptr<Bsr> low_bnd, low_int;  // rows [0, k1), [k1, n) of the lower part
+  int k1 = 0, n = 0, m = 0, oc0 = 0;      // oc0: the first own column in the window
+  int64_t nlow_bnd = 0;                   // lower blocks of low_bnd (colpart / brow offset of low_int)
+  DBuf<int32_t> brow;                     // per lower block: window block index of its row
+  int64_t brow_int_off = 0;               // low_int's entries start here (16-byte aligned)
+  DBuf<int64_t> up_ptr;                   // [n + 1]
+  DBuf<int32_t> up_slot;                  // in-rank upper blocks (ascending columns) -> lower block ids
+  DBuf<double> colpart, sbuf, tbuf;
+  std::unique_ptr<Bsr> tail;              // rows [t0, n): blocks past the own columns
+  int t0 = 0;
+  int64_t pass_bytes = 0;                 // algorithmic bytes of one pass (matrix + scratch)
+};
+
 struct PLevel {  // one (virtual) rank's share of one level
   int lo = 0, hi = 0;    // own block rows
   int wlo = 0, whi = 0;  // vector window (block rows)
@@ -78,6 +100,7 @@ struct PLevel {  // one (virtual) rank's share of one level
   std::unique_ptr<Bsr> A_own, R_own, P_own;
   std::unique_ptr<Fsai> M_own;
   SplitMat sA, sR, sP;                 // the matrices as launched
+  std::unique_ptr<PSym> psym;          // half-storage A (partitioned levels; whole ones use Bsr::half)
   std::vector<SplitMat> sF, sB;        // FSAI chain factors and their transposes
   SmootherSpec spec;  // Level::smoother (multilevel.hpp:25)
   DBuf<double> v[VNUM];
@@ -145,6 +168,7 @@ struct Hier {
   int granule_top = 1;                        // block rows per norm segment (top level)
   int64_t n0 = 0;
   std::vector<LevelStats> stats;
+  std::vector<char> psym_on;  // per level: partitioned A passes in half storage (build_level_psym)
   bool use_graph = true;
   struct Captured {
     cudaGraphExec_t exec;
@@ -223,6 +247,9 @@ void measure_rates(Hier& h, const Bsr& mass, const double* b, const double* u, i
                    double tol, int max_iter, double* l2_sq, double* energy_sq, double* resid, int* iters,
                    int* status, int* blowup, double* rates);
 void alloc_vectors(Hier& h, PLevel& L, bool top);
+// half-storage A on every eligible partitioned level of h (after the parts are built
+// and the setup's own A passes are done); consistent over all ranks
+void build_level_psym(Hier& h);
 std::unique_ptr<Bsr> slice_rows(const Bsr& g, int lo, int hi, int col_lo, int ncols);
 SplitMat split_rows(const Bsr& g, int lo, int hi, int wlo, int nwin, int own_lo, int own_hi);
 

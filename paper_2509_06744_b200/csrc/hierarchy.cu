@@ -82,6 +82,28 @@ __global__ void copy_rows_kernel(const double* __restrict__ a, int64_t ld, int64
     for (int c = threadIdx.x; c < ncols; c += blockDim.x) out[r * ncols + c] = c < ld ? a[r * ld + c] : 0.0;
 }
 
+// block q <- the block at src[q] (bs doubles), sources anywhere on the device
+__global__ void gather_ptr_kernel(const unsigned long long* __restrict__ src, int64_t nq, int bs,
+                                  double* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nq * bs; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = e / bs;
+    out[e] = reinterpret_cast<const double*>(src[q])[e - q * bs];
+  }
+}
+// flag = 1 if a block differs bitwise from the transpose of its mirror (pairs a[k], b[k])
+__global__ void mirror_check_kernel(const unsigned long long* __restrict__ a, const unsigned long long* __restrict__ b,
+                                    int64_t npairs, int m, int* __restrict__ flag) {
+  const int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (k >= npairs) return;
+  const unsigned long long* A = reinterpret_cast<const unsigned long long*>(a[k]);
+  const unsigned long long* B = reinterpret_cast<const unsigned long long*>(b[k]);
+  for (int e = lane; e < m * m; e += 32) {
+    const int r = e / m, c = e - r * m;
+    if (A[r * m + c] != B[c * m + r]) atomicOr(flag, 1);
+  }
+}
+
 }  // namespace kern
 
 // BMG_SETUP_TIMING=1: per-phase wall time of the setup on stderr (device synced)
@@ -525,6 +547,204 @@ SplitMat split_rows(const Bsr& g, int lo, int hi, int wlo, int nwin, int own_lo,
   return sm;
 }
 
+// ---- half-storage A on partitioned levels (hier.h PSym) -----------------------------
+// One rank's share: the SplitMat's slices hold its own rows [0, n) (level rows
+// lo + i) with columns in the vector window; own columns are [oc0, oc1).  nullptr
+// when the in-rank blocks are not exactly symmetric.
+static std::unique_ptr<PSym> build_psym(Ctx* ctx, const SplitMat& sA, int n, int oc0, int oc1, int m) {
+  struct Blk {
+    int col;
+    const double* v;
+  };
+  std::vector<std::vector<Blk>> rows(n);
+  int nwin = 0;
+  for (const Slice& sl : sA.s) {
+    const Bsr& a = *sl.m;
+    if (!a.uniform || a.mr != m || a.mc != m) return nullptr;
+    nwin = a.nbc;
+    for (int rr = 0; rr < a.nbr; ++rr)
+      for (int64_t q = a.h_row_ptr[rr]; q < a.h_row_ptr[rr + 1]; ++q)
+        rows[sl.row0 + rr].push_back({a.h_col[q], a.vals.p + q * a.bs});
+  }
+  auto P = std::make_unique<PSym>();
+  P->n = n;
+  P->m = m;
+  P->oc0 = oc0;
+  // rows that read the lower halo come first (phase 1 waits for the exchange there)
+  int k1 = 0;
+  for (int i = 0; i < n; ++i)
+    if (!rows[i].empty() && rows[i].front().col < oc0) k1 = i + 1;
+  P->k1 = k1;
+  int t0 = n;
+  for (int i = n - 1; i >= 0; --i)
+    if (!rows[i].empty() && rows[i].back().col >= oc1) t0 = i;
+  P->t0 = t0;
+  // the lower part (columns <= the diagonal's), boundary rows first
+  std::vector<int64_t> rp_b(1, 0), rp_i(1, 0), rp_t(1, 0);
+  std::vector<int32_t> col_b, col_i, col_t, brow;
+  std::vector<unsigned long long> src_low, src_tail;
+  std::vector<std::vector<std::pair<int, int64_t>>> low_of(n);  // (column, lower block id) per row
+  int64_t nlow = 0;
+  for (int i = 0; i < n; ++i) {
+    const int dc = i + oc0;
+    for (const Blk& b : rows[i]) {
+      if (b.col > dc) continue;
+      (i < k1 ? col_b : col_i).push_back(b.col);
+      src_low.push_back((unsigned long long)b.v);
+      brow.push_back(dc);
+      low_of[i].push_back({b.col, nlow++});
+    }
+    (i < k1 ? rp_b : rp_i).push_back((int64_t)(i < k1 ? col_b.size() : col_i.size()));
+    if (i >= t0) {
+      for (const Blk& b : rows[i])
+        if (b.col >= oc1) {
+          col_t.push_back(b.col);
+          src_tail.push_back((unsigned long long)b.v);
+        }
+      rp_t.push_back((int64_t)col_t.size());
+    }
+  }
+  P->nlow_bnd = (int64_t)col_b.size();
+  // in-rank upper blocks of every row: the lower block (j, i) holding their products
+  std::vector<int64_t> uptr(n + 1, 0);
+  std::vector<int32_t> uslot;
+  std::vector<unsigned long long> pa, pb;  // (upper block, its mirror) for the exact-symmetry check
+  for (int i = 0; i < n; ++i) {
+    const int dc = i + oc0;
+    for (const Blk& b : rows[i]) {
+      if (b.col <= dc || b.col >= oc1) continue;
+      const int j = b.col - oc0;
+      const auto& lj = low_of[j];
+      auto it = std::lower_bound(lj.begin(), lj.end(), std::make_pair(dc, (int64_t)-1));
+      if (it == lj.end() || it->first != dc) return nullptr;  // structurally unsymmetric
+      uslot.push_back((int32_t)it->second);
+      pa.push_back((unsigned long long)b.v);
+      pb.push_back(src_low[it->second]);
+    }
+    uptr[i + 1] = (int64_t)uslot.size();
+  }
+  if (nlow >= ((int64_t)1 << 31)) return nullptr;
+  {  // the half form is kept beside the full-storage slices (batched cycles use those):
+     // only where it fits with 2 GB to spare (C5 on 4 GPUs: rank 0 skips the levels
+     // that would not fit; every rank then keeps full storage there)
+    const int bs_ = (m * m + 1) & ~1;
+    const int64_t need = (nlow + (int64_t)src_tail.size()) * (int64_t)bs_ * 8 + nlow * (int64_t)m * 8 +
+                         2 * (int64_t)n * m * 8 + ((int64_t)2 << 30);
+    size_t fr = 0, tot = 0;
+    BMG_CUDA(cudaMemGetInfo(&fr, &tot));
+    if ((int64_t)fr < need) return nullptr;
+  }
+  if (!pa.empty()) {
+    DBuf<unsigned long long> da(pa.size()), db(pb.size());
+    DBuf<int> flag(1);
+    BMG_CUDA(cudaMemcpy(da.p, pa.data(), pa.size() * 8, cudaMemcpyHostToDevice));
+    BMG_CUDA(cudaMemcpy(db.p, pb.data(), pb.size() * 8, cudaMemcpyHostToDevice));
+    BMG_CUDA(cudaMemset(flag.p, 0, sizeof(int)));
+    kern::mirror_check_kernel<<<(unsigned)((pa.size() * 32 + 255) / 256), 256, 0, ctx->stream>>>(
+        da.p, db.p, (int64_t)pa.size(), m, flag.p);
+    ctx->count();
+    BMG_CUDA(cudaGetLastError());
+    int h = 0;
+    BMG_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (h) return nullptr;
+  }
+  const int bs = (m * m + 1) & ~1;
+  auto make = [&](int nr, std::vector<int64_t> rp, std::vector<int32_t> cl,
+                  const unsigned long long* src, int64_t nb, bool sym) -> std::unique_ptr<Bsr> {
+    if (nr == 0) return nullptr;
+    std::vector<int> rsz(nr, m), csz(nwin, m);
+    auto a = make_bsr_structure(ctx, nr, rsz.data(), nwin, csz.data(), std::move(rp), std::move(cl), false);
+    if (nb > 0) {
+      DBuf<unsigned long long> d(nb);
+      BMG_CUDA(cudaMemcpy(d.p, src, nb * 8, cudaMemcpyHostToDevice));
+      kern::gather_ptr_kernel<<<grid1d(nb * bs), 256, 0, ctx->stream>>>(d.p, nb, bs, a->vals.p);
+      ctx->count();
+      BMG_CUDA(cudaGetLastError());
+      BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    if (sym) build_sym_plan(*a);
+    return a;
+  };
+  P->low_bnd = make(k1, std::move(rp_b), std::move(col_b), src_low.data(), P->nlow_bnd, true);
+  P->low_int = make(n - k1, std::move(rp_i), std::move(col_i), src_low.data() + P->nlow_bnd, nlow - P->nlow_bnd,
+                    true);
+  P->tail = make(n - t0, std::move(rp_t), std::move(col_t), src_tail.data(), (int64_t)src_tail.size(), false);
+  // the interior slice's rows start 16-byte aligned (its bulk copies read from there)
+  P->brow_int_off = (P->nlow_bnd + 3) & ~(int64_t)3;
+  const int64_t nint = nlow - P->nlow_bnd;
+  P->brow.alloc(P->brow_int_off + nint + 8);
+  BMG_CUDA(cudaMemset(P->brow.p, 0, (P->brow_int_off + nint + 8) * 4));
+  if (P->nlow_bnd) BMG_CUDA(cudaMemcpy(P->brow.p, brow.data(), P->nlow_bnd * 4, cudaMemcpyHostToDevice));
+  if (nint)
+    BMG_CUDA(cudaMemcpy(P->brow.p + P->brow_int_off, brow.data() + P->nlow_bnd, nint * 4, cudaMemcpyHostToDevice));
+  P->up_ptr.alloc(n + 1);
+  BMG_CUDA(cudaMemcpy(P->up_ptr.p, uptr.data(), (n + 1) * 8, cudaMemcpyHostToDevice));
+  P->up_slot.alloc(std::max<size_t>(uslot.size(), 1));
+  if (!uslot.empty()) BMG_CUDA(cudaMemcpy(P->up_slot.p, uslot.data(), uslot.size() * 4, cudaMemcpyHostToDevice));
+  P->colpart.alloc(std::max<int64_t>(nlow, 1) * m);
+  P->sbuf.alloc(std::max<int64_t>((int64_t)n * m, 1));
+  P->tbuf.alloc(std::max<int64_t>((int64_t)(n - t0) * m, 1));
+  const int64_t nup = (int64_t)uslot.size(), ntail = (int64_t)src_tail.size();
+  P->pass_bytes = nlow * (8 * (int64_t)m * m + 8) + nup * (16 * (int64_t)m + 4) + 16 * (int64_t)n * m +
+                  8 * ((int64_t)n + 1) + ntail * (8 * (int64_t)m * m + 4) + 16 * (int64_t)(n - t0) * m;
+  return P;
+}
+
+void build_level_psym(Hier& h) {
+  static const int mode = [] {
+    const char* e = std::getenv("BMG_SYM_HALF");
+    return !e ? -1 : (e[0] == '0' ? 0 : 1);
+  }();
+  if (h.whole() || mode == 0) return;
+  Ctx* ctx = h.ctx;
+  const bool nccl = !h.emulated && h.world > 1;
+  auto reduce = [&](std::vector<int64_t>& v, ROp op) {
+    if (!nccl) return;
+    DBuf<int64_t> d(v.size());
+    BMG_CUDA(cudaMemcpy(d.p, v.data(), v.size() * 8, cudaMemcpyHostToDevice));
+    ctx->comm->allreduce(d.p, d.p, v.size(), DType::I64, op, ctx->stream);
+    BMG_CUDA(cudaMemcpyAsync(v.data(), d.p, v.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+  };
+  const int L = h.finest() + 1;
+  h.psym_on.assign(L, 0);
+  // eligibility from the whole level's full-storage bytes (same on every rank): the
+  // half form measured faster on the m >= 15 operators of C3 / C4 / C5 with passes of
+  // >= 0.5 ms (hierarchy.cu ensure_sym_half); BMG_SYM_HALF=1 forces every level
+  std::vector<int64_t> bytes(L, 0);
+  for (Part& p : h.parts)
+    for (int l = 1; l < L; ++l)
+      if (p.lv[l].active() && !p.lv[l].sA.s.empty() && p.lv[l].lo >= 0)
+        for (const Slice& sl : p.lv[l].sA.s) bytes[l] += sl.m->pass_bytes();
+  reduce(bytes, ROp::Sum);
+  std::vector<int64_t> bad(L, 0);  // any rank unable -> full storage everywhere
+  for (int l = 1; l < L; ++l) {
+    const bool partitioned = h.bounds[l].size() > 2 && h.bounds[l][1] < h.nbr[l];  // not held whole by rank 0
+    const int ml = h.msz[l];
+    const bool streamed = ml == 3 || ml == 6 || ml == 10 || ml == 15 || ml == 20 || ml == 21;
+    const bool eligible = streamed && (mode == 1 || (ml >= 15 && bytes[l] >= (int64_t)3e9));
+    if (!partitioned || !eligible) {
+      bad[l] = 1;
+      continue;
+    }
+    for (Part& p : h.parts) {
+      PLevel& d = p.lv[l];
+      if (!d.active()) continue;
+      d.psym = build_psym(ctx, d.sA, d.hi - d.lo, d.lo - d.wlo, d.hi - d.wlo, d.m);
+      if (!d.psym) bad[l] = 1;
+    }
+  }
+  reduce(bad, ROp::Max);
+  for (int l = 1; l < L; ++l) {
+    const bool ok = bad[l] == 0;
+    h.psym_on[l] = ok ? 1 : 0;
+    if (!ok)
+      for (Part& p : h.parts) p.lv[l].psym.reset();
+  }
+  BMG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
 // Split the (identically built) whole hierarchy into row strips.  rank < 0:
 // every virtual rank in this process (emulation); else only this rank's share
 // and the context's NCCL communicator moves the halos.
@@ -628,6 +848,7 @@ static void partition(Hier& h, int world, int rank, const int32_t* granule, int 
     BMG_CUDA(cudaEventCreateWithFlags(&h.ev_fork, cudaEventDisableTiming));
     BMG_CUDA(cudaEventCreateWithFlags(&h.ev_join, cudaEventDisableTiming));
   }
+  build_level_psym(h);
 }
 
 }  // namespace bmg

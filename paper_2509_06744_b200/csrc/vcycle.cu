@@ -221,6 +221,52 @@ void exchange(Hier& h, int l, Which w) {
   comm.group_end();
 }
 
+// r = b - A x on a partitioned level in half storage (hier.h PSym): the exchange of x
+// forks onto the comm stream while the rows that do not read the lower halo run
+// phase 1; then the boundary rows' phase 1, the merge of the in-rank upper
+// contributions (rows before t0 finish there) and the tail over the upper-halo
+// blocks.  gb / gr give a part's own-row b and r, gx its window x.
+template <class GB, class GX, class GR>
+static void sym_residual_pass(Hier& h, int l, Which xin, GB gb, GX gx, GR gr) {
+  Ctx* ctx = h.ctx;
+  BMG_CUDA(cudaEventRecord(h.ev_fork, ctx->stream));
+  BMG_CUDA(cudaStreamWaitEvent(h.comm, h.ev_fork, 0));
+  cudaStream_t main = ctx->stream;
+  ctx->stream = h.comm;
+  try {
+    exchange(h, l, xin);
+  } catch (...) {
+    ctx->stream = main;
+    throw;
+  }
+  ctx->stream = main;
+  BMG_CUDA(cudaEventRecord(h.ev_join, h.comm));
+  for (int phase = 0; phase < 2; ++phase) {
+    if (phase == 1) BMG_CUDA(cudaStreamWaitEvent(ctx->stream, h.ev_join, 0));
+    for (Part& p : h.parts) {
+      PLevel& L = p.lv[l];
+      if (!L.active() || !L.psym) continue;
+      PSym& S = *L.psym;
+      const double* x = gx(p, L);
+      const int m = S.m;
+      if (phase == 0) {
+        if (S.low_int)
+          sym_phase1(*S.low_int, SymArgs{S.brow.p + S.brow_int_off, S.colpart.p + S.nlow_bnd * m, S.oc0}, x,
+                     S.sbuf.p + (int64_t)S.k1 * m);
+        continue;
+      }
+      if (S.low_bnd) sym_phase1(*S.low_bnd, SymArgs{S.brow.p, S.colpart.p, S.oc0}, x, S.sbuf.p);
+      const double* b = gb(p, L);
+      double* r = gr(p, L);
+      sym_merge(ctx, m, S.n, S.up_ptr.p, S.up_slot.p, S.colpart.p, S.sbuf.p, b, r, S.tbuf.p, S.t0);
+      if (S.tail) residual_from(*S.tail, S.tbuf.p, b + (int64_t)S.t0 * m, x, r + (int64_t)S.t0 * m);
+    }
+  }
+}
+static bool level_psym(const Hier& h, int l) {
+  return h.nrhs == 1 && !h.whole() && l < (int)h.psym_on.size() && h.psym_on[l];
+}
+
 // ============================================================================ V-cycle
 // one smoother application (apply_smoother, chebyshev.hpp:117-129) on level l, all parts
 static void smooth(Hier& h, int l, int k, bool xzero) {
@@ -246,6 +292,12 @@ static void smooth(Hier& h, int l, int k, bool xzero) {
     } else if (s == 0 && h.skip_top_res && l == h.cycle_top()) {
       src = VR;  // computed by the host-buffer slices (run_vcycle_hostio); pre-smoothing only
       h.skip_top_res = false;
+    } else if (level_psym(h, l)) {
+      sym_residual_pass(
+          h, l, VX, [&](Part& p, PLevel& L) { return vec(h, p, l, VB) + L.off(); },
+          [&](Part& p, PLevel&) { return vec(h, p, l, VX); },
+          [&](Part& p, PLevel& L) { return vec(h, p, l, VR) + L.off(); });
+      src = VR;
     } else {
       run_pass(h, l, VX, l, [&](Part& p) { return &p.lv[l].sA; },
                [&](Part& p, PLevel& L, const Slice& sl) {
@@ -329,7 +381,12 @@ static void enqueue_vcycle(Hier& h, int kpre, int kpost) {
         if (p.lv[l].active()) fill(h.ctx, vec(h, p, l, VX) + p.lv[l].off(), p.lv[l].n_own(), 0.0);
       r = VB;
     }
-    if (r == VR) {
+    if (r == VR && level_psym(h, l)) {
+      sym_residual_pass(
+          h, l, VX, [&](Part& p, PLevel& L) { return vec(h, p, l, VB) + L.off(); },
+          [&](Part& p, PLevel&) { return vec(h, p, l, VX); },
+          [&](Part& p, PLevel& L) { return vec(h, p, l, VR) + L.off(); });
+    } else if (r == VR) {
       run_pass(h, l, VX, l, [&](Part& p) { return &p.lv[l].sA; },
                [&](Part& p, PLevel& L, const Slice& sl) {
                  const int64_t o = L.off() + L.sc(sl.row0);
@@ -751,6 +808,12 @@ void finest_residual(Hier& h, const double* b, double* x, double* rtmp) {
   h.user_b = b;
   h.user_x = x;
   stage_in(h, b, x);
+  if (level_psym(h, top)) {
+    sym_residual_pass(
+        h, top, VX, [&](Part&, PLevel& L) { return L.v[VB].p + L.off(); }, [&](Part&, PLevel& L) { return L.v[VX].p; },
+        [&](Part&, PLevel& L) { return L.v[VR].p + L.off(); });
+    return;
+  }
   run_pass(h, top, VX, top, [&](Part& p) { return &p.lv[top].sA; },
            [&](Part& p, PLevel& L, const Slice& sl) {
              const int64_t o = L.off() + L.sc(sl.row0);

@@ -341,7 +341,7 @@ def memory_plan(cfg: Config, world: int, agglomerate: int = 1, params=None):
     agg = max(1, min(agglomerate, L - 1))
     out = []
     for r in range(world):
-        steady = peak_extra = 0
+        steady = peak_extra = half_extra = 0
         for l in range(L):
             n = ns[l]
             whole = l < agg
@@ -358,9 +358,14 @@ def memory_plan(cfg: Config, world: int, agglomerate: int = 1, params=None):
                 continue
             a_own = _count_rows(offs[l], n, d, lo // g, -(-hi // g)) * blk
             a_ext = _count_rows(offs[l], n, d, elo_ // g, -(-ehi_ // g)) * blk
+            if not whole and m >= 15 and _count_rows(offs[l], n, d, 0, n) * blk >= 3e9:
+                # the half form of A beside the full one (hierarchy.cu build_level_psym;
+                # built only where it fits, else the level keeps full storage)
+                half_extra += a_own // 2 + (hi - lo) * m * 8 * (len(offs[l]) // 2 + 2)
             steady += a_own + nfac * 2 * (hi - lo) * blk
             steady += 2 * (hi - lo) * 3 ** d * blk          # P_l rows and their share of R_l
             steady += 6 * (ehi_ - elo_) * m * 8             # work vectors over the window
             peak_extra = max(peak_extra, a_ext + (4 << 30))
-        out.append({"rank": r, "steady_gb": steady / 1e9, "peak_gb": (steady + peak_extra) / 1e9})
+        out.append({"rank": r, "steady_gb": steady / 1e9, "peak_gb": (steady + peak_extra) / 1e9,
+                    "half_storage_gb": half_extra / 1e9})
     return out

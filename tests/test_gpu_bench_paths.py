@@ -2,6 +2,7 @@
 device's, and the N > 1 branch (distributed setup + partition-invariance check)
 through the loopback transport -- each rank a host thread with its own context,
 the same Comm calls NCCL serves on a multi-GPU node."""
+import os
 import threading
 
 import numpy as np
@@ -75,6 +76,8 @@ def test_bench_distributed_branch_c5_shape_world4(ctx):
     def rank(c, r, all_min):
         assert bench.invariance_check(c, cfg.scaled(128), world, r, agg, all_min)
         H, b_own = bench.partitioned_hierarchy(c, cfg, world, r, agg)
+        if os.environ.get("BMG_SYM_HALF") == "1":  # (test_gpu_sym_partitioned.py) the half form is on
+            assert H.cycle_bytes(cfg.k, cfg.k) < H.cycle_bytes_ref(cfg.k, cfg.k)
         x = Vector(c, b_own.size)
         hist, it, _ = H.solve(cfg.k, cfg.k, Vector(c, b_own), x, 1e-8, 8)
         lo = H.part_info(cfg.levels - 1, r)[0]

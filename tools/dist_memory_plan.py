@@ -14,5 +14,7 @@ for name in sys.argv[1:] or ["C2", "C4", "C3", "C5"]:
         plan = pr.memory_plan(cfg, world, AGG[name])
         worst = max(plan, key=lambda p: p["peak_gb"])
         fits = "fits" if worst["peak_gb"] < 180 else "does not fit"
+        half = max(p["steady_gb"] + p["half_storage_gb"] for p in plan)
         print(f"{name} x{world}: steady max {max(p['steady_gb'] for p in plan):6.1f} GB, "
-              f"setup peak max {worst['peak_gb']:6.1f} GB (rank {worst['rank']}) -> {fits} in 180 GB")
+              f"setup peak max {worst['peak_gb']:6.1f} GB (rank {worst['rank']}) -> {fits} in 180 GB; "
+              f"with the half-storage A of the large levels: steady max {half:6.1f} GB")
