@@ -262,6 +262,41 @@ def oracle_sample(cfg, steps, warmup, threads, single_core=False):
     return out
 
 
+# the reference's own sources (oracle/_ref, built against oracle/eigen_shim): a small
+# same-shape sample, since they are single-threaded and the stand-in's dense
+# primitives are not vectorised
+REF_BUILD_SAMPLE = {"C4": ("C4", 8, 3), "C2": ("C2", 32, 3), "C3": ("C3", 32, 3), "C5": ("C5", 32, 4)}
+
+
+def reference_build_sample(cfg, steps=2):
+    """V-cycles of THE REFERENCE ITSELF (oracle/_ref/libblockmg_ref.so) on a small
+    hierarchy of cfg's shape, one thread, scaled to cfg by algorithmic bytes."""
+    from oracle import pyref as R
+    from paper_2509_06744_b200 import problems as pr
+
+    if not R.available() or cfg.name not in REF_BUILD_SAMPLE:
+        return None
+    name, n, levels = REF_BUILD_SAMPLE[cfg.name]
+    scfg = pr.CONFIGS[name].scaled(n, levels)
+    A, T, b = pr.make_problem(scfg)
+    t0 = time.perf_counter()
+    rh = R.Hierarchy(R.Mat(A), [R.Mat(p) for p in T], t_max=1, tau=1.0, nest=scfg.nest, coarse_dim_cap=1 << 30)
+    setup_s = time.perf_counter() - t0
+    sample_bytes = cycle_bytes_model(oracle_levels(rh, scfg.m), scfg.k, scfg.k, rh.A(0).info()["dim_r"])
+    x = rh.v_cycle(scfg.k, scfg.k, b, np.zeros_like(b))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        x = rh.v_cycle(scfg.k, scfg.k, b, x)
+    rate = steps / (time.perf_counter() - t0)
+    full = CYCLE_BYTES.get(cfg.name)
+    return {"value": rate * sample_bytes / full if full else None, "unit": "V-cycles/s", "cores": 1,
+            "kind": "reference",
+            "sample": f"{steps} V-cycles of the reference's own sources (oracle/_ref: proj/src/*.cpp compiled in "
+                      f"place against oracle/eigen_shim, Eigen3 being absent; single-threaded as the reference is, "
+                      f"dense primitives not vectorised) on {scfg.name} after {setup_s:.1f} s setup; measured "
+                      f"{rate:.4g} cycles/s, {sample_bytes / 1e9:.3f} GB per cycle, scaled to {cfg.name} by bytes"}
+
+
 def sample_text(s, threads, cfg):
     if s["sample"] == cfg.name:
         return (f"{s['steps']} V-cycles of the C++ oracle (reference restatement; the reference needs Eigen3, "
@@ -293,6 +328,12 @@ def run_reference(args, cfg):
                          "sample": sample_text(s, threads, cfg)},
         "e2e": {"value": s["value"], "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    try:  # the reference's own sources on one thread, reported beside the (faster) 16-thread port
+        rb = reference_build_sample(cfg)
+        if rb is not None:
+            line["cpu_baseline"]["reference_build"] = rb
+    except Exception as e:
+        line["cpu_baseline"]["reference_build"] = {"error": f"{type(e).__name__}: {e}"}
     print(json.dumps(line), flush=True)
 
 
@@ -718,6 +759,12 @@ def run_ours(args, cfg):
                 cpu["single_core"] = {"value": s["single_core"]["value"], "unit": "V-cycles/s", "cores": 1,
                                       "sample": "1 V-cycle of the same sample on one thread, scaled the same way "
                                                 "(the reference is single-threaded, SURVEY.md §0.1)"}
+            try:
+                rb = reference_build_sample(cfg)
+                if rb is not None:
+                    cpu["reference_build"] = rb
+            except Exception as e:
+                cpu["reference_build"] = {"error": f"{type(e).__name__}: {e}"}
         if not args.no_extra:
             try:
                 extra["C1"] = measure_c1(ctx, stream, args.steps, with_cpu=not args.no_cpu_baseline)

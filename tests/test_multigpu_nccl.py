@@ -1,8 +1,7 @@
 """Multi-GPU path over real NCCL (skipped with fewer than 2 GPUs): bench.py under
 torchrun partitions C2 into row strips (distributed setup, NCCL halos, coarsest
 level on rank 0) and itself checks the partitioned cycle bitwise against the
-1-GPU cycle before timing; a failure there shows up as a replica fallback in
-config.parallelism."""
+1-GPU cycle before timing; a failure there fails the run (no replica fallback)."""
 import json
 import os
 import subprocess
@@ -31,11 +30,12 @@ def test_bench_row_strips_over_nccl(n):
         pytest.skip(f"needs {n} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "bench.py"), "--gpus", str(n),
-           "--steps", "3", "--warmup", "3", "--no-c4", "--no-quarter", "--no-cpu-baseline"]
+           "--steps", "3", "--warmup", "3", "--config", "C2", "--no-extra", "--no-cpu-baseline", "--no-parity"]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-4000:]
     line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["n_gpus"] == n
-    assert line["config"]["parallelism"].startswith(f"row strips x{n}"), line["config"]["parallelism"]
-    assert "verified bitwise" in line["config"]["parallelism"]
+    assert line["run"]["parallelism"].startswith(f"row strips x{n}"), line["run"]["parallelism"]
+    assert "verified bitwise" in line["run"]["parallelism"]
+    assert len(line["run"]["rank_device_gb"]) == n
     assert line["value"] > 0
