@@ -6,9 +6,13 @@
 // tests/, __graft_entry__.smoke() and bench.py's CPU-baseline legs.  The product
 // (paper_2509_06744_b200/libbmgcuda.so) never links or calls it.
 //
-// Parity: the reference is unbuildable here (Eigen3 absent) and
-// ships no golden vectors; the restatement is pinned against the reference's own
-// known-answer/property tests (tests/test_oracle_pins.py).
+// Parity: pinned to the reference run here.  The reference's own build needs Eigen3
+// (absent), so its unmodified sources are compiled in place against
+// oracle/eigen_shim into oracle/_ref/libblockmg_ref.so (same C API,
+// ref_driver.cpp) and compared with this file BITWISE
+// (tests/test_reference_build.py, tools/reference_vs_fixtures.py); it is also
+// pinned against the reference's own known-answer/property tests
+// (tests/test_oracle_pins.py).
 //
 // Arithmetic conventions (the reference's Eigen kernels have an unspecified
 // inner summation order, so the oracle fixes one and the CUDA kernels mirror it

@@ -7,11 +7,18 @@
  * cpu_baseline / --impl reference legs may load it, and only as the checker or
  * the CPU baseline.  The product (libbmgcuda.so) never links or calls it.
  *
- * Parity status: the reference cannot be compiled here (Eigen3 and vendor/ are
- * absent), and it ships no golden vectors.  The
- * restatement is pinned against every known-answer and property test the
- * reference holds for this path (tests/test_oracle_pins.py citing
- * proj/tests/ sources  line by line).
+ * Parity status: PINNED TO THE REFERENCE RUN HERE.  The reference's own build needs
+ * Eigen3 (absent, no network), so `make -C oracle ref` compiles its unmodified
+ * sources where they lie against oracle/eigen_shim (a from-scratch stand-in for
+ * the Eigen API subset they use, fixing the summation order inside a dense
+ * primitive to the one documented in bmg_oracle.cpp) into
+ * oracle/_ref/libblockmg_ref.so, which exports THIS SAME API (ref_driver.cpp).
+ * tests/test_reference_build.py compares the two libraries bitwise: kernels,
+ * FSAI builds, smoothers, Lanczos, setup and solves on the C2/C3/C4/C5 shapes,
+ * measure_rates, fd_biharmonic; tools/reference_vs_fixtures.py checks the
+ * reference against the committed solve fixtures.  It is also pinned against
+ * every known-answer and property test the reference holds for this path
+ * (tests/test_oracle_pins.py citing proj/tests/ sources line by line).
  *
  * Handles are opaque; every entry returns 0 on success or a negative status
  * (see ORC_E*), with the message available from orc_last_error().
