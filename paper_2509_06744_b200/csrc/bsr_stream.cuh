@@ -255,8 +255,26 @@ struct SmemLayout {
 // rows ascending: the same chain as the row dot of the stored transpose) and
 // writes it to colpart; the row sums (lower blocks only) go to the epilogue, and
 // sym_merge_kernel adds the upper contributions in ascending column order.
+#ifndef BMG_SYM_CPT1_MASK
+#define BMG_SYM_CPT1_MASK 0
+#endif
+// columns per SYM column item (bit m of BMG_SYM_CPT1_MASK: one column per item)
+constexpr int sym_cpt(int mc) {
+  return ((BMG_SYM_CPT1_MASK >> mc) & 1) ? 1 : (mc % 2 == 0) ? 2 : ((mc % 3 == 0) ? 3 : 1);
+}
+// Register budget.  Blocks of m >= 15 stream 24-36 KB chunks through a two-stage ring,
+// so shared memory holds 3 CTAs per SM whatever the registers; telling ptxas so
+// (65536 / (3 x 288) = 75 registers instead of the 47-56 it settles on unasked) lets
+// it issue a whole item's x gathers before the first fma of the chain instead of
+// trickling them in between the dependent fmas (SASS: 12 + 8 loads hoisted instead
+// of 5 + 4 in the m = 15 half-storage kernel).  Measured on whole cycles: C5 shape
+// 14.4 -> 16.1 V-cycles/s, C3 shape 16.1 -> 16.5, C4 20.0 -> 20.5.  m <= 10 keeps the
+// default: 4 CTAs of its smaller chunks fit and need <= 56 registers (C2 474 -> 462
+// with the 3-CTA budget).
+// (0 = no hint)  Batched kernels (K > 1) keep the default too.
+constexpr int stream_min_blocks(int mr, int k) { return (mr >= 15 && k == 1) ? 3 : 0; }
 template <int MR, int MC, int K, class Epi, bool VAR = false, bool SYM = false>
-__global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi epi) {
+__global__ void __launch_bounds__(kThreads, stream_min_blocks(MR, K)) bsr_stream_kernel(StreamArgs s, Epi epi) {
   static_assert(!SYM || (K == 1 && !VAR && MR == MC), "SYM streams uniform square blocks, one RHS");
   extern __shared__ __align__(128) unsigned char smem[];
   const int kStages = s.stages;
@@ -463,7 +481,7 @@ __global__ void __launch_bounds__(kThreads) bsr_stream_kernel(StreamArgs s, Epi 
     if constexpr (SYM) {  // transposed products of the off-diagonal blocks
       // an item is CPT adjacent columns of one block: x_i is loaded once for them
       // and even block sizes read two columns per 16-byte shared-memory load
-      constexpr int CPT = (MC % 2 == 0) ? 2 : ((MC % 3 == 0) ? 3 : 1);
+      constexpr int CPT = sym_cpt(MC);
       constexpr int NCG = MC / CPT;
       // items run block-fastest within tiles of BB blocks, so the lanes of one
       // shared-memory wavefront read the same column group of different blocks,

@@ -15,7 +15,10 @@ import bench  # noqa: E402
 from paper_2509_06744_b200 import Context, Vector, residual  # noqa: E402
 from paper_2509_06744_b200 import problems as pr  # noqa: E402
 
-cfg = pr.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "C4"]
+_arg = sys.argv[1] if len(sys.argv) > 1 else "C4"  # NAME or NAME@N (same shape on an N-per-side grid)
+cfg = pr.CONFIGS[_arg.split("@")[0]]
+if "@" in _arg:
+    cfg = cfg.scaled(int(_arg.split("@")[1]))
 ctx = Context(0)
 stream = torch.cuda.current_stream()
 ctx.set_stream(stream.cuda_stream)
