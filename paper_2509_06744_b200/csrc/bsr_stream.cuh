@@ -491,10 +491,13 @@ __global__ void __launch_bounds__(kThreads, stream_min_blocks(MR, K)) bsr_stream
       constexpr int BB = (MC == 10 || MC == 6) ? 4 : 8;
       const int* rs = rows_s + st * stage_cols + (d.x & 3);
       const bool tiled = s.colmap != 0;
-      const int citems = tiled ? ((d.y + BB - 1) / BB) * BB * NCG : d.y * NCG;
+      // colmap 2: only the chunk's full tiles run block-fastest, the remaining blocks
+      // block-major (a partial tile leaves most lanes of its wavefronts idle)
+      const int ntiled = !tiled ? 0 : (s.colmap == 2 ? (d.y / BB) * BB : ((d.y + BB - 1) / BB) * BB) * NCG;
+      const int citems = !tiled ? d.y * NCG : (s.colmap == 2 ? d.y * NCG : ntiled);
       for (int item = tid; item < citems; item += kConsumers) {
         int b, c0;
-        if (tiled) {
+        if (item < ntiled) {
           const int tile = item / (BB * NCG);
           const int k = item - tile * BB * NCG;
           b = tile * BB + (k % BB);
