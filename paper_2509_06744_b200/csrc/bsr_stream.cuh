@@ -212,7 +212,8 @@ struct StreamArgs {
   // transposed products A_ij^T x_i, MC doubles per block at the block's index
   const int32_t* brow = nullptr;
   double* colpart = nullptr;
-  int colmap = 0;  // SYM column items: 0 block-major, 1 block-fastest tiles (BMG_SYM_COLMAP)
+  int colmap = 2;  // SYM column items: 0 block-major, 1 block-fastest tiles, 2 block-fastest full tiles +
+                   // block-major remainder (BMG_SYM_COLMAP; 2 measured best)
   int sym_lo = 0;  // SYM: blocks in columns below this one (a partitioned level's lower halo)
                    // have no stored mirror here: row dots only
 };
