@@ -1062,6 +1062,27 @@ std::unique_ptr<Plan> plan_rows(const Bsr& a, int row0, int row1) {
   if (p->nctas == 0) return nullptr;
   return p;
 }
+// row-range plan over the lower triangle of a half-storage A (rows [row0, row1):
+// their blocks reach columns <= the row, so the range reads x rows < row1 only)
+std::unique_ptr<Plan> plan_rows_sym(const Bsr& low, int row0, int row1) {
+  if (!low.uniform || low.mr != low.mc || !stream_supported(low.mr, low.mc)) return nullptr;
+  auto p = std::make_unique<Plan>();
+  build_plan_into(low, *p, 1, low.mr, low.bs, false, row0, row1, true);
+  if (p->nctas == 0) return nullptr;
+  return p;
+}
+void sym_phase1_rows(const Bsr& low, const Plan& P, const SymArgs& sa, const double* x, double* S) {
+  const kern::EpiStore epi{S};
+  switch (low.mr) {
+    case 3: return launch_stream_plan<3, 3, 1, kern::EpiStore, false, true>(low, P, x, epi, &sa);
+    case 6: return launch_stream_plan<6, 6, 1, kern::EpiStore, false, true>(low, P, x, epi, &sa);
+    case 10: return launch_stream_plan<10, 10, 1, kern::EpiStore, false, true>(low, P, x, epi, &sa);
+    case 15: return launch_stream_plan<15, 15, 1, kern::EpiStore, false, true>(low, P, x, epi, &sa);
+    case 20: return launch_stream_plan<20, 20, 1, kern::EpiStore, false, true>(low, P, x, epi, &sa);
+    case 21: return launch_stream_plan<21, 21, 1, kern::EpiStore, false, true>(low, P, x, epi, &sa);
+  }
+  fail(BMG_EINVAL, "sym_phase1_rows: streamed block sizes only");
+}
 void residual_rows(const Bsr& a, const Plan& P, const double* b, const double* x, double* r) {
   const kern::EpiResidual epi{b, r};
   switch (a.mr) {

@@ -340,6 +340,10 @@ const Plan& plan_for(const Bsr& a, int nrhs);
 // a single-RHS plan over block rows [row0, row1) of a uniform streamed matrix (no
 // data copy; outputs land at their absolute rows); nullptr if not streamable
 std::unique_ptr<Plan> plan_rows(const Bsr& a, int row0, int row1);
+// the same over the lower triangle of a half-storage A, and its phase 1 (row and
+// transposed products of the rows' blocks; the merge follows once every range ran)
+std::unique_ptr<Plan> plan_rows_sym(const Bsr& low, int row0, int row1);
+void sym_phase1_rows(const Bsr& low, const Plan& P, const SymArgs& sa, const double* x, double* S);
 // r = b - A x on the rows of a plan_rows plan
 void residual_rows(const Bsr& a, const Plan& P, const double* b, const double* x, double* r);
 // whether a variable layout runs on the streaming kernel through padded blocks

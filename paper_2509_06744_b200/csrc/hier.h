@@ -144,6 +144,8 @@ struct GraphKey {
 // reads have landed, so the upload overlaps the first pass.
 struct HostIo {
   std::vector<std::unique_ptr<Plan>> plans;  // row-range plans of the finest A
+  std::vector<std::unique_ptr<Plan>> sym_plans;  // ... of its lower triangle (half-storage A)
+  cudaEvent_t ev_b = nullptr;                // b landed (half-storage path)
   std::vector<int> row0, row1, need;         // slice rows; last slice whose x it reads
   cudaStream_t cs = nullptr;
   cudaEvent_t fork = nullptr;
@@ -151,6 +153,7 @@ struct HostIo {
   ~HostIo() {
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
     if (fork) cudaEventDestroy(fork);
+    if (ev_b) cudaEventDestroy(ev_b);
     if (cs) cudaStreamDestroy(cs);
   }
 };

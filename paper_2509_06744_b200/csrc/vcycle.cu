@@ -601,8 +601,19 @@ bool run_vcycle_hostio(Hier& h, int kpre, int kpost, const double* hb, double* h
       while (t + 1 < S && io->need[s] >= io->row1[t]) ++t;
       io->need[s] = t;
     }
+    if (A.half) {  // half-storage A: the same row ranges over its lower triangle
+      for (int s = 0; s < S; ++s) {
+        auto pl = plan_rows_sym(*A.half->low, io->row0[s], io->row1[s]);
+        if (!pl) {
+          io->sym_plans.clear();
+          break;
+        }
+        io->sym_plans.push_back(std::move(pl));
+      }
+    }
     BMG_CUDA(cudaStreamCreateWithFlags(&io->cs, cudaStreamNonBlocking));
     BMG_CUDA(cudaEventCreateWithFlags(&io->fork, cudaEventDisableTiming));
+    BMG_CUDA(cudaEventCreateWithFlags(&io->ev_b, cudaEventDisableTiming));
     io->ev.resize(S, nullptr);
     for (auto& e : io->ev) BMG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     h.hio = std::move(io);
@@ -622,17 +633,38 @@ bool run_vcycle_hostio(Hier& h, int kpre, int kpost, const double* hb, double* h
       BMG_CUDA(cudaEventRecord(io.fork, ctx->own));
       BMG_CUDA(cudaStreamWaitEvent(io.cs, io.fork, 0));
       const int S = (int)io.plans.size();
-      for (int s = 0; s < S; ++s) {
-        const int64_t o = (int64_t)io.row0[s] * m, len = (int64_t)(io.row1[s] - io.row0[s]) * m;
-        BMG_CUDA(cudaMemcpyAsync(h.io_b.p + o, hb + o, len * 8, cudaMemcpyHostToDevice, io.cs));
-        BMG_CUDA(cudaMemcpyAsync(h.io_x.p + o, hx + o, len * 8, cudaMemcpyHostToDevice, io.cs));
-        BMG_CUDA(cudaEventRecord(io.ev[s], io.cs));
+      if (A.half && (int)io.sym_plans.size() == S) {
+        // half-storage A: a row range of the lower triangle reads x up to its own
+        // rows only, so phase 1 follows the x slices as they land; b is needed by the
+        // merge alone and arrives under phase 1
+        const SymHalf& H = *A.half;
+        for (int s = 0; s < S; ++s) {
+          const int64_t o = (int64_t)io.row0[s] * m, len = (int64_t)(io.row1[s] - io.row0[s]) * m;
+          BMG_CUDA(cudaMemcpyAsync(h.io_x.p + o, hx + o, len * 8, cudaMemcpyHostToDevice, io.cs));
+          BMG_CUDA(cudaEventRecord(io.ev[s], io.cs));
+        }
+        BMG_CUDA(cudaMemcpyAsync(h.io_b.p, hb, n * 8, cudaMemcpyHostToDevice, io.cs));
+        BMG_CUDA(cudaEventRecord(io.ev_b, io.cs));
+        const SymArgs sa{H.brow.p, H.colpart.p, 0};
+        for (int s = 0; s < S; ++s) {
+          BMG_CUDA(cudaStreamWaitEvent(ctx->own, io.ev[s], 0));
+          sym_phase1_rows(*H.low, *io.sym_plans[s], sa, h.io_x.p, H.sbuf.p);
+        }
+        BMG_CUDA(cudaStreamWaitEvent(ctx->own, io.ev_b, 0));  // joins the copy stream
+        sym_merge(ctx, m, A.nbr, H.up_ptr.p, H.up_slot.p, H.colpart.p, H.sbuf.p, h.io_b.p, r, nullptr, A.nbr);
+      } else {
+        for (int s = 0; s < S; ++s) {
+          const int64_t o = (int64_t)io.row0[s] * m, len = (int64_t)(io.row1[s] - io.row0[s]) * m;
+          BMG_CUDA(cudaMemcpyAsync(h.io_b.p + o, hb + o, len * 8, cudaMemcpyHostToDevice, io.cs));
+          BMG_CUDA(cudaMemcpyAsync(h.io_x.p + o, hx + o, len * 8, cudaMemcpyHostToDevice, io.cs));
+          BMG_CUDA(cudaEventRecord(io.ev[s], io.cs));
+        }
+        for (int s = 0; s < S; ++s) {
+          BMG_CUDA(cudaStreamWaitEvent(ctx->own, io.ev[io.need[s]], 0));
+          residual_rows(A, *io.plans[s], h.io_b.p, h.io_x.p, r);
+        }
+        BMG_CUDA(cudaStreamWaitEvent(ctx->own, io.ev[S - 1], 0));  // join the copy stream
       }
-      for (int s = 0; s < S; ++s) {
-        BMG_CUDA(cudaStreamWaitEvent(ctx->own, io.ev[io.need[s]], 0));
-        residual_rows(A, *io.plans[s], h.io_b.p, h.io_x.p, r);
-      }
-      BMG_CUDA(cudaStreamWaitEvent(ctx->own, io.ev[S - 1], 0));  // join the copy stream
       h.user_b = h.io_b.p;
       h.user_x = h.io_x.p;
       h.skip_top_res = true;
