@@ -251,6 +251,13 @@ int bmg_measure_rates(bmg_hier* h, const bmg_bsr* mass, const bmg_vec* b, const 
  * bitwise equal to the unpartitioned cycle. */
 int bmg_nccl_unique_id(unsigned char* id128);
 int bmg_ctx_create_nccl(int device, int rank, int world, const unsigned char* id128, bmg_ctx** out);
+/* Transport self-test (no reference counterpart; diagnostic): the halo-exchange
+ * pattern of the partitioned V-cycle -- a grouped send + recv of `count` doubles on a
+ * side stream forked from and joined to the context's stream, captured in a CUDA
+ * graph where the transport allows it and replayed `reps` times -- with this rank as
+ * its own peer, plus a sum all-reduce.  *mismatches = entries that did not arrive.
+ * Lets one GPU drive the real NCCL point-to-point path (world = 1). */
+int bmg_ctx_transport_selftest(bmg_ctx* ctx, int64_t count, int reps, int64_t* mismatches);
 /* Loopback transport: `world` ranks as host threads of ONE process, each with
  * its own context on the same device; sends and receives are matched in-process
  * (host-side waits only).  Runs the exact NCCL code path where one GPU exists. */

@@ -117,6 +117,14 @@ class Context:
         check(lib().bmg_nccl_unique_id(buf))
         return buf.raw
 
+    def transport_selftest(self, count: int = 1 << 16, reps: int = 3) -> int:
+        """bmg_ctx_transport_selftest: the halo-exchange pattern with this rank as
+        its own peer (captured where the transport allows) + an all-reduce;
+        returns the number of mismatching entries."""
+        bad = C.c_int64()
+        check(lib().bmg_ctx_transport_selftest(self.h, count, reps, C.byref(bad)))
+        return int(bad.value)
+
     def set_stream(self, stream_ptr: int | None):
         check(lib().bmg_ctx_set_stream(self.h, C.c_void_p(stream_ptr or 0)))
 

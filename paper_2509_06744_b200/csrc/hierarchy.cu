@@ -1220,6 +1220,86 @@ int bmg_ctx_create_nccl(int device, int rank, int world, const unsigned char* id
   });
 }
 
+int bmg_ctx_transport_selftest(bmg_ctx* c, int64_t count, int reps, int64_t* mismatches) {
+  return guard([&] {
+    Ctx* ctx = reinterpret_cast<Ctx*>(c);
+    if (!ctx || !ctx->comm) fail(BMG_EINVAL, "transport selftest: the context has no transport");
+    if (count < 1 || reps < 1) fail(BMG_EINVAL, "transport selftest: count and reps must be >= 1");
+    ctx->activate();
+    Comm& comm = *ctx->comm;
+    const int self = ctx->rank;
+    DBuf<double> src, dst, red;
+    src.alloc((size_t)count);
+    dst.alloc((size_t)count);
+    red.alloc(2);
+    std::vector<double> hsrc((size_t)count);
+    for (int64_t i = 0; i < count; ++i) hsrc[(size_t)i] = 1.0 + (double)(i % 1021) * 0.5;
+    BMG_CUDA(cudaMemcpy(src.p, hsrc.data(), (size_t)count * 8, cudaMemcpyHostToDevice));
+    cudaStream_t side;
+    cudaEvent_t fork, join;
+    BMG_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    BMG_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    BMG_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    cudaStream_t main = ctx->stream ? ctx->stream : ctx->own;
+    auto exchange_once = [&] {  // the shape of vcycle.cu exchange(): fork, grouped send/recv, join
+      BMG_CUDA(cudaEventRecord(fork, main));
+      BMG_CUDA(cudaStreamWaitEvent(side, fork, 0));
+      comm.group_start();
+      comm.send(src.p, (size_t)count, DType::F64, self, side);
+      comm.recv(dst.p, (size_t)count, DType::F64, self, side);
+      comm.group_end();
+      BMG_CUDA(cudaEventRecord(join, side));
+      BMG_CUDA(cudaStreamWaitEvent(main, join, 0));
+    };
+    int64_t bad = 0;
+    auto check = [&] {
+      std::vector<double> h((size_t)count);
+      BMG_CUDA(cudaMemcpyAsync(h.data(), dst.p, (size_t)count * 8, cudaMemcpyDeviceToHost, main));
+      BMG_CUDA(cudaStreamSynchronize(main));
+      for (int64_t i = 0; i < count; ++i)
+        if (h[(size_t)i] != hsrc[(size_t)i]) ++bad;
+      BMG_CUDA(cudaMemsetAsync(dst.p, 0, (size_t)count * 8, main));
+    };
+    if (comm.capturable()) {
+      cudaGraph_t g = nullptr;
+      cudaGraphExec_t ex = nullptr;
+      BMG_CUDA(cudaStreamBeginCapture(main, cudaStreamCaptureModeThreadLocal));
+      try {
+        exchange_once();
+      } catch (...) {
+        cudaStreamEndCapture(main, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      BMG_CUDA(cudaStreamEndCapture(main, &g));
+      BMG_CUDA(cudaGraphInstantiate(&ex, g, 0));
+      cudaGraphDestroy(g);
+      for (int r = 0; r < reps; ++r) {
+        BMG_CUDA(cudaGraphLaunch(ex, main));
+        check();
+      }
+      cudaGraphExecDestroy(ex);
+    } else {
+      for (int r = 0; r < reps; ++r) {
+        exchange_once();
+        check();
+      }
+    }
+    // sum all-reduce of {1, rank}: world and world (world - 1) / 2
+    const double in[2] = {1.0, (double)ctx->rank};
+    double out[2] = {0.0, 0.0};
+    BMG_CUDA(cudaMemcpyAsync(red.p, in, 16, cudaMemcpyHostToDevice, main));
+    comm.allreduce(red.p, red.p, 2, DType::F64, ROp::Sum, main);
+    BMG_CUDA(cudaMemcpyAsync(out, red.p, 16, cudaMemcpyDeviceToHost, main));
+    BMG_CUDA(cudaStreamSynchronize(main));
+    if (out[0] != (double)ctx->world || out[1] != 0.5 * ctx->world * (ctx->world - 1)) ++bad;
+    cudaEventDestroy(fork);
+    cudaEventDestroy(join);
+    cudaStreamDestroy(side);
+    *mismatches = bad;
+  });
+}
+
 int bmg_nccl_unique_id(unsigned char* id128) {
   return guard([&] { nccl_unique_id(id128); });
 }

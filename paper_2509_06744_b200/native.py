@@ -157,6 +157,7 @@ _SIGS = {
     "bmg_time_residual": (_I, [_P, _P, _P, _P, _I, _PD]),
     "bmg_nccl_unique_id": (_I, [C.c_char_p]),
     "bmg_ctx_create_nccl": (_I, [_I, _I, _I, C.c_char_p, _PP]),
+    "bmg_ctx_transport_selftest": (_I, [_P, C.c_int64, _I, C.POINTER(C.c_int64)]),
     "bmg_loopback_create": (_I, [_I, _PP]),
     "bmg_loopback_destroy": (_I, [_P]),
     "bmg_ctx_create_loopback": (_I, [_I, _P, _I, _PP]),

@@ -95,6 +95,43 @@ def test_dist_setup_world1_plain_context(ctx):
     assert np.array_equal(x1.download(), x2.download())
 
 
+def test_dist_setup_world1_over_real_nccl():
+    """One GPU is enough for a world of one: the context's transport is the real
+    NcclComm (ncclGetUniqueId and ncclCommInitRank called from libbmgcuda.so,
+    ncclAllReduce in the distributed Lanczos and the residual norms, captured
+    V-cycle graphs with a capturable transport).  Bitwise the plain context."""
+    from paper_2509_06744_b200 import Context
+
+    cfg, params = _cfg("c5_m15")
+    uid = Context.nccl_unique_id()
+    assert isinstance(uid, (bytes, bytearray)) and len(uid) == 128
+    nctx = Context(0, nccl=(0, 1, uid))
+    pctx = Context(0)
+    hw, b = _whole(pctx, cfg, params)
+    A, T, b_own, plan = pr.dist_inputs(cfg, 1, 0, 1, params)
+    _, _, gran, rad = pr.level_grid(cfg)
+    hd = Hierarchy.setup_dist(nctx, BlockSparseMatrix(nctx, A), [BlockSparseMatrix(nctx, p) for p in T], gran, rad, 1,
+                              params)
+    for l in range(1, cfg.levels):
+        assert hw.beta(l) == hd.beta(l)
+    x1, x2 = Vector(pctx, b.size), Vector(nctx, b.size)
+    h1, i1, _ = hw.solve(3, 3, Vector(pctx, b), x1, 1e-8, 5)
+    h2, i2, _ = hd.solve(3, 3, Vector(nctx, b), x2, 1e-8, 5)
+    assert i1 == i2 and np.array_equal(h1, h2)
+    assert np.array_equal(x1.download(), x2.download())
+
+
+def test_nccl_point_to_point_pattern_in_a_captured_graph():
+    """The exchange pattern of the partitioned cycle (grouped ncclSend / ncclRecv on a
+    forked stream, inside a captured graph, replayed) over the real NCCL transport,
+    this rank being its own peer -- what one GPU can drive of the multi-GPU path."""
+    from paper_2509_06744_b200 import Context
+
+    nctx = Context(0, nccl=(0, 1, Context.nccl_unique_id()))
+    for count in (1, 4096, 1 << 20):
+        assert nctx.transport_selftest(count, 3) == 0
+
+
 def test_dist_setup_rejects_underestimated_radius(ctx):
     cfg, params = _cfg("c2_like")
     A, T, _, _ = pr.dist_inputs(cfg, 1, 0, 1, params)
