@@ -271,7 +271,8 @@ static int chunk_blocks(int mr, int bs, int K = 1, bool sym = false) {
   // the half-storage pass (twice the consumer work per staged block) on m = 20: 11
   // blocks per chunk, still 3 CTAs per SM (C4 fine residual + G pair 2.50 -> 2.42 ms;
   // 40 KB drops to 2 CTAs: 2.68)
-  if (sym && mr == 20) kb = 36;
+  // m = 21 likewise: 10 blocks per chunk (C3 shape 17.79 -> 17.94 V-cycles/s)
+  if (sym && (mr == 20 || mr == 21)) kb = 36;
   if (K == 8 && mr == 10) kb = 16;
   const int cap = env_cap ? env_cap : kb * 1024;
   // small blocks: several phase-A items per consumer thread, so a chunk still
