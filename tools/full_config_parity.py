@@ -18,7 +18,9 @@ from paper_2509_06744_b200 import problems as pr  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "C4"
 cycles = int(sys.argv[2]) if len(sys.argv) > 2 else 6
-cfg = pr.CONFIGS[name]
+cfg = pr.CONFIGS[name.split("@")[0]]
+if "@" in name:  # the same shape on an N-per-side grid (e.g. C5@1024: a quarter of C5's rows)
+    cfg = cfg.scaled(int(name.split("@")[1]))
 O.set_threads(os.cpu_count() or 1)
 A, T, b = pr.make_problem(cfg)
 oA, oT = O.Mat(A), [O.Mat(p) for p in T]
