@@ -283,7 +283,8 @@ static int chunk_blocks(int mr, int bs, int K = 1, bool sym = false) {
   }();
   const int per_thread = mr >= 10 ? 1 : (env_items ? env_items : 3);  // measured: m = 3 3.1 -> 4.2, m = 6 5.9 -> 6.1 TB/s
   // m = 15 takes 16 lanes per block in bsr_stream_kernel (bank-conflict-free rows)
-  const int lanes = (K == 1 && mr == 15) ? 16 : mr;
+  // ... and m = 21 takes 22 (PAD21)
+  const int lanes = (K == 1 && mr == 15) ? 16 : ((BMG_PAD21 && K == 1 && mr == 21) ? 22 : mr);
   const int by_items = std::max(1, per_thread * kern::kConsumers / lanes);
   const int by_bytes = std::max(1, cap / (bs * 8));
   return std::min(by_items, by_bytes);
@@ -456,7 +457,7 @@ static void build_plan_into(const Bsr& a, Plan& P, int K, int mr, int bs, bool v
   int rmax = 1;
   // first pass with a provisional rmax to size smem and query occupancy
   // bsr_stream_kernel's SKEW layout (m = 20, K = 1, uniform): block pitch bs + 2 in shared memory
-  const int spitch = (K == 1 && mr == 20 && !var) ? bs + 2 : bs;
+  const int spitch = (K == 1 && mr == 20 && !var) ? bs + 2 : ((BMG_PAD21 && K == 1 && mr == 21 && !var) ? bs + 4 : bs);
   const size_t smem0 = P.u ? kern::BatchSmem(bs, P.cb_max, mr, mr, K, P.stages).total
                            : kern::SmemLayout(spitch, P.cb_max, P.cb_max + 2, mr, P.stages, K, sym).total;
   const int occ = P.u ? batch_occupancy_for(mr, smem0, K, P.u)

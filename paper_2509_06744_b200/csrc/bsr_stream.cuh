@@ -256,6 +256,9 @@ struct SmemLayout {
 // rows ascending: the same chain as the row dot of the stored transpose) and
 // writes it to colpart; the row sums (lower blocks only) go to the epilogue, and
 // sym_merge_kernel adds the upper contributions in ascending column order.
+#ifndef BMG_PAD21
+#define BMG_PAD21 1  // m = 21: 22 lanes per block at a shared-memory pitch of bs + 4 (bmg_core.cu follows it)
+#endif
 #ifndef BMG_SYM_CPT1_MASK
 #define BMG_SYM_CPT1_MASK 0
 #endif
@@ -284,7 +287,15 @@ __global__ void __launch_bounds__(kThreads, stream_min_blocks(MR, K)) bsr_stream
   // blocks: the 160-byte row pitch alone maps rows r and r + 4 of a block to the
   // same banks (2-way conflicts on every 16-byte load, 2.5e8 per C4 coarse pass)
   constexpr bool SKEW = (MR == 20 && MC == 20 && K == 1 && !VAR);
-  const int pitch = SKEW ? s.bs + 2 : s.bs;
+  // PAD21 (m = 21): 22 lanes per block (one idle) and a pitch of bs + 4 = 446 doubles
+  // (one bulk copy per block).  8-byte loads are served per half-warp; with 21 lanes
+  // per block at the packed pitch the half-warps that straddle two blocks hit three
+  // bank pairs twice (1.64x the wavefronts of the row items, ~52 M per C3-shape
+  // pass).  Lane g of a chunk reads double offset 446 j + 21 r + q with g = 22 j + r:
+  // 13 (446 j + 21 r) = 6 j + r = g (mod 16), so any 16 consecutive lanes cover the
+  // 16 bank pairs once.
+  constexpr bool PAD21 = BMG_PAD21 && (MR == 21 && MC == 21 && K == 1 && !VAR);
+  const int pitch = SKEW ? s.bs + 2 : (PAD21 ? s.bs + 4 : s.bs);
   const SmemLayout L(pitch, s.cb_max, s.rmax, MR, kStages, K, SYM);
   // partials of one (block, row) item for K > 1 sit at stride K + 1 (bank spread)
   constexpr int KP = K > 1 ? K + 1 : 1;
@@ -332,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, stream_min_blocks(MR, K)) bsr_stream
         const uint32_t cbytes = (uint32_t)(ch - cl) * 4u;
         mbar_arrive_expect_tx(&full[st], vbytes + (SYM ? 2 : 1) * cbytes);
         if constexpr (SYM) bulk_stream(rows_s + st * stage_cols, s.brow + cl, cbytes, &full[st], s.l2hint, pol);
-        if constexpr (SKEW) {
+        if constexpr (SKEW || PAD21) {
           for (int b = 0; b < d.y; ++b)
             bulk_stream(vals_s + (size_t)st * stage_vals + b * pitch, s.vals + (int64_t)(d.x + b) * s.bs,
                         (uint32_t)s.bs * 8u, &full[st], s.l2hint, pol);
@@ -428,12 +439,12 @@ __global__ void __launch_bounds__(kThreads, stream_min_blocks(MR, K)) bsr_stream
     // of 8-byte loads -- reads the 15 rows of one block: the 120-byte row pitch
     // spreads them over distinct bank pairs, while two blocks in one half-warp collide
     constexpr bool HALF = (MR == 15 && MC == 15 && K == 1 && !VAR);
-    constexpr int LPB = HALF ? 16 : MR;
+    constexpr int LPB = HALF ? 16 : (PAD21 ? 22 : MR);
     const int items = K > 1 ? 0 : d.y * LPB;
     for (int item = tid; item < items; item += kConsumers) {
       int b = item / LPB;
       int r = item - b * LPB;
-      if (HALF && r >= MR) continue;
+      if ((HALF || PAD21) && r >= MR) continue;
       if constexpr (SKEW) {  // pairs of blocks: quarter k of a pair = rows 4k..4k+3 of both
         const int pair = item / (2 * MR);
         if (2 * pair + 1 < d.y) {
