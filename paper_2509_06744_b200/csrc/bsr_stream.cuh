@@ -21,7 +21,12 @@
 //     nothing is re-read (DRAM bytes = algorithmic bytes under ncu).
 //   * m = 20: blocks are copied one by one to a shared-memory pitch of bs + 2
 //     doubles and quarter-warps span two blocks (SKEW), which removes the bank
-//     conflicts of the 160-byte row pitch.
+//     conflicts of the 160-byte row pitch.  m = 21: a pitch of bs + 4 doubles and
+//     22 lanes per block (PAD21), m = 15: 16 lanes per block (HALF): every
+//     half-warp of 8-byte loads covers the 16 bank pairs once.
+//   * m >= 15 kernels carry a 3-CTA register budget (stream_min_blocks): their
+//     chunks fill shared memory at 3 CTAs per SM anyway, and with 72 registers
+//     ptxas issues an item's x gathers before the first fma of its chain.
 //   * Consumers (8 warps) compute per-(block, scalar row) dot products from
 //     shared memory against x gathered through L1/L2 (phase A), release the
 //     stage, then sum each row's partials in ascending block order and run the
